@@ -1,0 +1,4 @@
+#pragma once
+// Reference-named header (proj/core/include/chainhull/datasets.hpp); the
+// whole drop-in API lives in chainhull/api.hpp.
+#include "chainhull/api.hpp"

@@ -1,0 +1,168 @@
+/* chgpu.h — C ABI of the B200-native CudaChain hull path.
+ *
+ * This is the drop-in boundary under the reference's C++ entry point
+ * chainhull::convex_hull (reference: proj/core/include/chainhull/
+ * pipeline.hpp:55, implemented in proj/core/src/pipeline.cpp:25-106).
+ * The C++ shim in paper_1508_05488_b200/cpp/ re-exports the reference's
+ * own API (the headers under include/chainhull/) on top of these entry points, and the
+ * Python mirror (paper_1508_05488_b200/__init__.py) binds them with ctypes.
+ * Signatures carry plain pointers and sizes only.
+ *
+ * Points are interleaved float64 pairs, byte-identical to
+ * chainhull::Point2 (sizeof 16, alignof 8: geometry.hpp:8-15).
+ *
+ * Errors: every entry point returns a chgpu_status. The C++ shim maps
+ * CHGPU_EMPTY -> chainhull::EmptyInput, CHGPU_DEGENERATE ->
+ * chainhull::DegenerateInput, CHGPU_INVALID_ARG -> std::invalid_argument,
+ * on exactly the branches where the reference throws them
+ * (pipeline.cpp:27, :58-59, spa.cpp:112-113, polygon.cpp:26-27,
+ * melkman.cpp:44-47). chgpu_last_error() gives the message.
+ *
+ * Threading: a context owns one CUDA stream, a device workspace and pinned
+ * staging buffers. Calls on one context must be serialised by the caller;
+ * distinct contexts may be used concurrently (the reference promises
+ * reentrancy, pipeline.hpp:53).
+ */
+#ifndef CHGPU_H
+#define CHGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CHGPU_OK = 0,
+  CHGPU_EMPTY = 1,       /* EmptyInput (pipeline.cpp:27, extremes.cpp:29) */
+  CHGPU_DEGENERATE = 2,  /* DegenerateInput (pipeline.cpp:58, polygon.cpp:26, melkman.cpp:44) */
+  CHGPU_INVALID_ARG = 3, /* std::invalid_argument (spa.cpp:112, region_less/sort_region) */
+  CHGPU_CUDA_ERR = 4,    /* CUDA runtime failure; see chgpu_last_error */
+  CHGPU_NO_DEVICE = 5,   /* no CUDA device: the product never falls back to the CPU */
+  CHGPU_TOO_LARGE = 6    /* n >= 2^32 points in one call (shard the input) */
+} chgpu_status;
+
+/* Layout-identical to chainhull::StageStats (pipeline.hpp:30-42). */
+typedef struct {
+  size_t n_input;
+  size_t n_after_round1;
+  size_t n_after_spa;
+  size_t n_hull;
+  double t_extremes_ms;
+  double t_classify_ms;
+  double t_partition_ms; /* 0: the partition is fused into the classify kernel */
+  double t_sort_ms;
+  double t_spa_ms;
+  double t_melkman_ms;
+  double t_total_ms;
+} chgpu_stats;
+
+/* Diagnostics of the last chgpu_hull* call (parity taps). */
+typedef struct {
+  double quad[8];           /* left, bottom, right, top (extremes.hpp:22-27) */
+  size_t frame_size;        /* frame_vertices(quad).size() (extremes.cpp:49-57) */
+  size_t region_counts[5];  /* Interior, LL, LR, UR, UL after classify */
+  size_t kept_counts[4];    /* per-region SPA survivors (0 on the degenerate branch) */
+  int degenerate_branch;    /* 1 when pipeline.cpp:53-71 was taken */
+  int sort_passes;          /* radix passes actually executed */
+  size_t tie_runs;          /* equal-primary runs fixed up after the radix sort */
+  int launches;             /* kernels launched by this call */
+  int pad_;
+  /* Device time per stage from CUDA events on the context stream. */
+  double t_h2d_ms;          /* host->device copy of the input (0 for device input) */
+  double t_k1_ms;           /* extremes kernels (overlapping the copy for host input) */
+  double t_k2_ms;           /* classify + compaction kernel */
+  double t_hist_ms;         /* digit histogram + scan */
+  double t_passes_ms;       /* all onesweep passes (sort_passes launches) */
+  double t_ties_ms;         /* tie-run detect + fix */
+  double t_spa_kernel_ms;   /* SPA scan + chain compaction */
+  double t_d2h_ms;          /* chains device->host */
+  double t_host_ms;         /* host assemble + Melkman */
+} chgpu_diag;
+
+typedef struct chgpu_ctx chgpu_ctx;
+
+/* Context lifecycle. device < 0 selects the current device. */
+int chgpu_ctx_create(int device, chgpu_ctx** out);
+void chgpu_ctx_destroy(chgpu_ctx* ctx);
+const char* chgpu_last_error(const chgpu_ctx* ctx);
+/* The CUDA stream the context launches on (a cudaStream_t). */
+void* chgpu_ctx_stream(chgpu_ctx* ctx);
+/* Pre-size the workspace for n points (optional; grows on demand). */
+int chgpu_reserve(chgpu_ctx* ctx, size_t n);
+
+/* convex_hull (pipeline.hpp:55) over HOST points xy[2n]. On CHGPU_OK
+ * *hull_xy points at 2*(*n_hull) doubles owned by ctx, valid until the next
+ * call on ctx. Hull is canonical: CCW, starting at the lexicographic
+ * minimum, strict (melkman.hpp:10-16). stats/diag may be NULL. */
+int chgpu_hull(chgpu_ctx* ctx, const double* xy, size_t n, size_t chunk_count,
+               int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+               chgpu_stats* stats, chgpu_diag* diag);
+
+/* Same, with xy already resident in device memory (16-byte aligned). */
+int chgpu_hull_device(chgpu_ctx* ctx, const double* d_xy, size_t n, size_t chunk_count,
+                      int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+                      chgpu_stats* stats, chgpu_diag* diag);
+
+/* ---- stage taps (the reference stage API, used by the C++ shim) -------- */
+
+/* find_extremes (extremes.hpp:32): quad_out = left, bottom, right, top. */
+int chgpu_find_extremes(chgpu_ctx* ctx, const double* xy, size_t n, double* quad_out);
+
+/* classify (classify.hpp:55-58): labels[i] in {0..4}; counts[5]. */
+int chgpu_classify(chgpu_ctx* ctx, const double* xy, size_t n, const double* quad,
+                   uint8_t* labels, size_t* counts);
+
+/* discard_round1 (classify.hpp:64): survivors grouped LL|LR|UR|UL into
+ * out_xy (capacity n points), out_labels; counts[5] (Interior = 0). */
+int chgpu_discard_round1(chgpu_ctx* ctx, const double* xy, const uint8_t* labels, size_t n,
+                         double* out_xy, uint8_t* out_labels, size_t* counts);
+
+/* sort_region (spa.hpp:43) in place on a host segment; region 1..4. */
+int chgpu_sort_region(chgpu_ctx* ctx, int region, double* xy, size_t m);
+
+/* spa_filter (spa.hpp:77) over a sorted host segment; anchors = first,
+ * last; out capacity m points. */
+int chgpu_spa_filter(chgpu_ctx* ctx, int region, const double* xy, size_t m,
+                     const double* anchors, size_t chunk_count, double* out, size_t* n_out);
+
+/* ---- host finisher (C++; identical semantics to the reference) --------- */
+
+/* assemble_polygon (polygon.hpp:25): chains = the 4 kept chains
+ * concatenated, kept_counts[4]; out capacity sum + 4. */
+int chgpu_assemble_polygon(const double* chains, const size_t* kept_counts, const double* quad,
+                           double* out, size_t* n_out);
+/* melkman (melkman.hpp:29); out capacity n. */
+int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out);
+/* canonicalize_ring (melkman.hpp:20), in place. */
+void chgpu_canonicalize_ring(double* ring, size_t n);
+/* hull_oracle (pipeline.hpp:62): host reference hull; out capacity n. */
+int chgpu_hull_oracle(const double* xy, size_t n, double* out, size_t* n_out);
+
+/* ---- data plumbing ------------------------------------------------------ */
+
+/* generate (datasets.hpp:35): bit-identical to the reference's
+ * mt19937_64-based generator. dist follows datasets.hpp:13-21. */
+int chgpu_generate(int dist, size_t n, uint64_t seed, double* out_xy);
+
+/* ---- sharded path (multi-GPU, one rank per GPU) ------------------------- */
+
+/* Local extremes of a device-resident shard with global tie-break indices:
+ * quad_out[8], idx_out[4] = base_index + local index of each corner. */
+int chgpu_shard_extremes(chgpu_ctx* ctx, const double* d_xy, size_t n, uint64_t base_index,
+                         double* quad_out, uint64_t* idx_out);
+/* Fold of per-rank candidates in rank order (extremes.cpp:39-46 semantics
+ * with lowest global index on ties): quads[8*k], idxs[4*k] -> quad_out. */
+void chgpu_fold_extremes(const double* quads, const uint64_t* idxs, size_t k, double* quad_out);
+/* Round-1 discard, region sort and SPA of a device-resident shard against
+ * a GIVEN (global) quad. Chains (host, owned by ctx until the next call)
+ * are the kept points of the 4 regions concatenated; kept_counts[4]. */
+int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
+                       size_t chunk_count, const double** chains_xy, size_t* kept_counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHGPU_H */

@@ -1,0 +1,224 @@
+// Device-side building blocks shared by the hull kernels.
+//
+// Arithmetic contract (reference geometry.hpp:22-35): the orientation
+// predicate is evaluated as (b.x-a.x)*(p.y-a.y) - (b.y-a.y)*(p.x-a.x) with
+// every operation individually rounded (no FMA). All .cu files are built
+// with -fmad=false AND the predicate spells the roundings out with
+// __dmul_rn/__dsub_rn, so contraction cannot creep back in.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace chgpu {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+// ---------------------------------------------------------------- geometry
+
+// cross(a, b, p) with a precomputed edge (ex, ey) = (b.x - a.x, b.y - a.y).
+// Precomputing the edge is exact: it is the same rounded subtraction the
+// reference performs per call.
+__device__ __forceinline__ double cross_edge(double ax, double ay, double ex, double ey,
+                                             double px, double py) {
+  return __dsub_rn(__dmul_rn(ex, __dsub_rn(py, ay)), __dmul_rn(ey, __dsub_rn(px, ax)));
+}
+
+// Lexicographic orders (geometry.hpp:39-44).
+__device__ __forceinline__ bool less_xy(double ax, double ay, double bx, double by) {
+  return ax < bx || (ax == bx && ay < by);
+}
+__device__ __forceinline__ bool less_yx(double ax, double ay, double bx, double by) {
+  return ay < by || (ay == by && ax < bx);
+}
+
+// ---------------------------------------------------------------- key codec
+//
+// Sort records are (k, v) pairs of 64-bit words. k is the region's primary
+// coordinate and v its secondary, each mapped by an order-preserving
+// bijection of the double's bits (descending orders use the complement),
+// so ascending unsigned order on (k, v) is exactly region_less
+// (spa.cpp:38-52):
+//   region 1 LL: k = ord(x),  v = ~ord(y)   x asc,  ties y desc
+//   region 2 LR: k = ord(y),  v = ord(x)    y asc,  ties x asc
+//   region 3 UR: k = ~ord(x), v = ord(y)    x desc, ties y asc
+//   region 4 UL: k = ~ord(y), v = ~ord(x)   y desc, ties x desc
+//   mode 0 LEX : k = ord(x),  v = ord(y)    less_xy (degenerate branch)
+// Both maps are bijective, so the point is recovered bit-exactly
+// (including the sign of zero). -0.0 and +0.0 are adjacent in k-order and
+// are merged into one tie run by prim_eq() below, restoring the
+// reference's `==` tie semantics.
+
+__host__ __device__ __forceinline__ u64 dbits(double d) {
+#ifdef __CUDA_ARCH__
+  return (u64)__double_as_longlong(d);
+#else
+  u64 u;
+  __builtin_memcpy(&u, &d, 8);
+  return u;
+#endif
+}
+__host__ __device__ __forceinline__ double bitsd(u64 u) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)u);
+#else
+  double d;
+  __builtin_memcpy(&d, &u, 8);
+  return d;
+#endif
+}
+__host__ __device__ __forceinline__ u64 ord_enc(double d) {
+  const u64 b = dbits(d);
+  return b ^ ((u64)((long long)b >> 63) | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double ord_dec(u64 u) {
+  return bitsd(u ^ ((u >> 63) ? 0x8000000000000000ull : 0xFFFFFFFFFFFFFFFFull));
+}
+
+// Region codes: 0 = LEX (degenerate branch), 1..4 = LL, LR, UR, UL.
+__host__ __device__ __forceinline__ void encode_point(int region, double x, double y, u64& k,
+                                                      u64& v) {
+  switch (region) {
+    case 1: k = ord_enc(x); v = ~ord_enc(y); break;
+    case 2: k = ord_enc(y); v = ord_enc(x); break;
+    case 3: k = ~ord_enc(x); v = ord_enc(y); break;
+    case 4: k = ~ord_enc(y); v = ~ord_enc(x); break;
+    default: k = ord_enc(x); v = ord_enc(y); break;
+  }
+}
+__host__ __device__ __forceinline__ void decode_point(int region, u64 k, u64 v, double& x,
+                                                      double& y) {
+  switch (region) {
+    case 1: x = ord_dec(k); y = ord_dec(~v); break;
+    case 2: y = ord_dec(k); x = ord_dec(v); break;
+    case 3: x = ord_dec(~k); y = ord_dec(v); break;
+    case 4: y = ord_dec(~k); x = ord_dec(~v); break;
+    default: x = ord_dec(k); y = ord_dec(v); break;
+  }
+}
+// The primary coordinate as a double (for == tie tests).
+__host__ __device__ __forceinline__ double primary_of(int region, u64 k) {
+  return (region == 3 || region == 4) ? ord_dec(~k) : ord_dec(k);
+}
+// The SPA guarded coordinate (spa.cpp:86-88) is always the secondary.
+__host__ __device__ __forceinline__ double guarded_of(int region, u64 v) {
+  return (region == 1 || region == 4) ? ord_dec(~v) : ord_dec(v);
+}
+// Primary equality under IEEE == (merges -0.0 and +0.0).
+__host__ __device__ __forceinline__ bool prim_eq(int region, u64 a, u64 b) {
+  return a == b || primary_of(region, a) == primary_of(region, b);
+}
+
+// ---------------------------------------------------------------- look-back
+//
+// Decoupled look-back status words: [tag:30 | flag:2 | value:32]. The tag
+// identifies the launch that wrote the word, so status arrays never need
+// clearing between launches (a stale word from any earlier launch carries
+// a different tag and reads as "not ready").
+enum : u32 { kFlagNone = 0, kFlagAgg = 1, kFlagPrefix = 2 };
+
+__device__ __forceinline__ u64 make_status(u32 tag, u32 flag, u32 value) {
+  return ((u64)(tag & 0x3FFFFFFFu) << 34) | ((u64)flag << 32) | (u64)value;
+}
+__device__ __forceinline__ u32 status_flag(u64 w, u32 tag) {
+  return ((u32)(w >> 34) == (tag & 0x3FFFFFFFu)) ? (u32)((w >> 32) & 3u) : 0u;
+}
+__device__ __forceinline__ void store_status(u64* p, u64 w) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ u64 load_status(const u64* p) {
+  u64 w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+// Warp-cooperative look-back over a status column (stride between
+// consecutive tiles). Returns the exclusive prefix for `tile`, given that
+// tile `first` (the chain's first tile) publishes a prefix directly.
+// Every lane returns the same value.
+__device__ __forceinline__ u32 warp_lookback(const u64* col, size_t stride, int tile, int first,
+                                             u32 tag) {
+  const int lane = threadIdx.x & 31;
+  u32 excl = 0;
+  int base = tile - 1;
+  while (true) {
+    const int j = base - lane;
+    u32 flag = kFlagPrefix, val = 0;
+    if (j >= first) {
+      u64 w;
+      do {
+        w = load_status(col + (size_t)j * stride);
+        flag = status_flag(w, tag);
+      } while (flag == kFlagNone);
+      val = (u32)w;
+    }
+    const unsigned pmask = __ballot_sync(0xffffffffu, flag == kFlagPrefix);
+    const int stop = pmask ? (__ffs(pmask) - 1) : 32;  // nearest predecessor holding a prefix
+    u32 contrib = (lane <= stop) ? val : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+    excl += contrib;
+    if (pmask) break;
+    base -= 32;
+  }
+  return excl;
+}
+
+// ---------------------------------------------------------------- loads
+
+__device__ __forceinline__ double2 ldg_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- shared structs
+
+// Device-resident result of the extremes reduction, consumed by the
+// classify kernel without a host round trip.
+struct QuadInfo {
+  double q[8];       // left.x, left.y, bottom.x, bottom.y, right.x, right.y, top.x, top.y
+  u64 idx[4];        // index of each corner (earliest among == ties)
+  u32 frame_size;    // frame_vertices(quad).size()
+  u32 degenerate;    // frame_size <= 2
+};
+
+// One extremes candidate per corner: the point and its index.
+struct Cand {
+  double x, y;
+  u64 i;
+};
+struct QuadCand {
+  Cand c[4];
+};
+
+// Sort segment descriptor (one region, or one long tie run).
+struct SegDesc {
+  u64 src_off;     // element offset of the segment in the pass's source array
+  u64 dst_off;     // element offset in the destination array
+  u32 len;         // elements
+  u32 tile_begin;  // first global tile of the segment
+  int region;      // key codec region (0 = LEX)
+  int pad;
+};
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kDigits = 256;
+constexpr int kPasses = 8;
+
+constexpr int kK2Threads = 256;
+constexpr int kK2Items = 8;
+constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
+
+}  // namespace chgpu

@@ -1,0 +1,26 @@
+// Host finisher (see finisher.cpp).
+#pragma once
+
+#include <stddef.h>
+
+#include <vector>
+
+namespace chgpu {
+namespace host {
+
+struct Pt {
+  double x, y;
+};
+
+enum { kOk = 0, kEmpty = 1, kDegenerate = 2, kInvalid = 3 };
+
+int assemble_ring(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
+                  std::vector<Pt>& ring);
+void canonicalize(Pt* ring, size_t n);
+int melkman(const Pt* poly, size_t n, std::vector<Pt>& hull);
+int monotone_chain(const Pt* sorted_unique, size_t n, std::vector<Pt>& hull);
+int sorted_hull(const Pt* pts, size_t n, std::vector<Pt>& hull);
+void insert_sorted_unique(std::vector<Pt>& sorted, const Pt& p);
+
+}  // namespace host
+}  // namespace chgpu

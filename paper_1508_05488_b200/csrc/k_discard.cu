@@ -1,0 +1,399 @@
+// K1 (extreme quad) and K2 (classify + round-1 discard + 4-way compaction).
+//
+// K1 follows find_extremes/fold (reference extremes.cpp:12-47): four
+// lexicographic min/max reductions with the earliest index winning among
+// ==-equal points. It streams the input once (16 B/point).
+//
+// K2 fuses classify_point (classify.hpp:42-48), the per-region counting of
+// classify (classify.cpp:9-33) and discard_round1's partition
+// (classify.cpp:40-87) into one pass: every point is read once, labelled in
+// registers, and survivors are written straight into per-region output
+// streams as sort-ready (k, v) records (chgpu_internal.cuh key codec).
+// Stream offsets come from a single-pass decoupled look-back with four
+// independent chains (one per region). Interior points are never written.
+
+#include "chgpu_internal.cuh"
+#include "kernels.h"
+
+namespace chgpu {
+
+// ------------------------------------------------------------------ K1
+
+__device__ __forceinline__ bool beats_left(const Cand& a, const Cand& b) {
+  if (less_xy(a.x, a.y, b.x, b.y)) return true;
+  if (less_xy(b.x, b.y, a.x, a.y)) return false;
+  return a.i < b.i;
+}
+__device__ __forceinline__ bool beats_bottom(const Cand& a, const Cand& b) {
+  if (less_yx(a.x, a.y, b.x, b.y)) return true;
+  if (less_yx(b.x, b.y, a.x, a.y)) return false;
+  return a.i < b.i;
+}
+__device__ __forceinline__ bool beats_right(const Cand& a, const Cand& b) {
+  if (less_xy(b.x, b.y, a.x, a.y)) return true;
+  if (less_xy(a.x, a.y, b.x, b.y)) return false;
+  return a.i < b.i;
+}
+__device__ __forceinline__ bool beats_top(const Cand& a, const Cand& b) {
+  if (less_yx(b.x, b.y, a.x, a.y)) return true;
+  if (less_yx(a.x, a.y, b.x, b.y)) return false;
+  return a.i < b.i;
+}
+
+// Candidates with i == ~0 are empty and lose to everything.
+__device__ __forceinline__ void merge_quad(QuadCand& acc, const QuadCand& o) {
+  if (o.c[0].i != ~0ull && (acc.c[0].i == ~0ull || beats_left(o.c[0], acc.c[0]))) acc.c[0] = o.c[0];
+  if (o.c[1].i != ~0ull && (acc.c[1].i == ~0ull || beats_bottom(o.c[1], acc.c[1]))) acc.c[1] = o.c[1];
+  if (o.c[2].i != ~0ull && (acc.c[2].i == ~0ull || beats_right(o.c[2], acc.c[2]))) acc.c[2] = o.c[2];
+  if (o.c[3].i != ~0ull && (acc.c[3].i == ~0ull || beats_top(o.c[3], acc.c[3]))) acc.c[3] = o.c[3];
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
+  Cand r;
+  r.x = __shfl_down_sync(0xffffffffu, c.x, src);
+  r.y = __shfl_down_sync(0xffffffffu, c.y, src);
+  r.i = __shfl_down_sync(0xffffffffu, c.i, src);
+  return r;
+}
+
+// Folds one point visited in increasing index order: strict comparisons
+// keep the earliest of ==-equal points, exactly like fold() (:12-17).
+__device__ __forceinline__ void fold_point(QuadCand& a, double x, double y, u64 i) {
+  if (a.c[0].i == ~0ull) {
+    a.c[0] = a.c[1] = a.c[2] = a.c[3] = Cand{x, y, i};
+    return;
+  }
+  if (less_xy(x, y, a.c[0].x, a.c[0].y)) a.c[0] = Cand{x, y, i};
+  if (less_yx(x, y, a.c[1].x, a.c[1].y)) a.c[1] = Cand{x, y, i};
+  if (less_xy(a.c[2].x, a.c[2].y, x, y)) a.c[2] = Cand{x, y, i};
+  if (less_yx(a.c[3].x, a.c[3].y, x, y)) a.c[3] = Cand{x, y, i};
+}
+
+constexpr int kK1Threads = 256;
+constexpr int kK1Unroll = 4;
+
+// Grid-stride pass: thread t visits t, t+T, t+2T, ... in increasing order,
+// so its running fold is the sequential fold of its subsequence.
+__global__ __launch_bounds__(kK1Threads) void k_extremes_partial(const double2* __restrict__ pts,
+                                                                 u64 n, u64 base_index,
+                                                                 QuadCand* __restrict__ partials) {
+  QuadCand acc;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc.c[c] = Cand{0.0, 0.0, ~0ull};
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
+    double2 p[kK1Unroll];
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
+  }
+  for (; i < n; i += stride) {
+    const double2 p = ldg_stream(pts + i);
+    fold_point(acc, p.x, p.y, base_index + i);
+  }
+  // Warp then block combine; ties fall back to the index so the result is
+  // independent of the combine order.
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    QuadCand other;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) other.c[c] = shfl_cand(acc.c[c], o);
+    merge_quad(acc, other);
+  }
+  __shared__ QuadCand warp_acc[kK1Threads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) warp_acc[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kK1Threads / 32; ++w) merge_quad(acc, warp_acc[w]);
+    partials[blockIdx.x] = acc;
+  }
+}
+
+__global__ void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
+                                 QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
+  QuadCand acc;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc.c[c] = Cand{0.0, 0.0, ~0ull};
+  for (int p = threadIdx.x; p < nparts; p += blockDim.x) merge_quad(acc, partials[p]);
+  __shared__ QuadCand sacc[256];
+  sacc[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < (int)blockDim.x; ++t) merge_quad(acc, sacc[t]);
+    if (raw_out) *raw_out = acc;
+    if (out) {
+      QuadInfo qi;
+      for (int c = 0; c < 4; ++c) {
+        qi.q[2 * c] = acc.c[c].x;
+        qi.q[2 * c + 1] = acc.c[c].y;
+        qi.idx[c] = acc.c[c].i;
+      }
+      // frame_vertices (extremes.cpp:49-57)
+      double fx[4], fy[4];
+      int k = 0;
+      for (int c = 0; c < 4; ++c) {
+        const double x = qi.q[2 * c], y = qi.q[2 * c + 1];
+        if (k == 0 || !(fx[k - 1] == x && fy[k - 1] == y)) {
+          fx[k] = x;
+          fy[k] = y;
+          ++k;
+        }
+      }
+      if (k > 1 && fx[0] == fx[k - 1] && fy[0] == fy[k - 1]) --k;
+      qi.frame_size = (u32)k;
+      qi.degenerate = k <= 2 ? 1u : 0u;
+      *out = qi;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K2
+
+// classify_point (classify.hpp:42-48): the first CCW quad edge the point is
+// strictly right of, else Interior.
+struct QuadEdges {
+  double ax[4], ay[4], ex[4], ey[4];
+};
+
+__device__ __forceinline__ int classify(const QuadEdges& e, double px, double py) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (cross_edge(e.ax[c], e.ay[c], e.ex[c], e.ey[c], px, py) < 0.0) return c + 1;
+  }
+  return 0;
+}
+
+// Two-ended stream layout: streams 1 and 2 share kbuf[0, ncap) growing
+// from both ends, streams 3 and 4 share kbuf[ncap, 2*ncap).
+__device__ __forceinline__ u64 stream_slot(int s, u64 pos, u64 ncap) {
+  switch (s) {
+    case 1: return pos;
+    case 2: return ncap - 1 - pos;
+    case 3: return ncap + pos;
+    default: return 2 * ncap - 1 - pos;
+  }
+}
+
+template <bool kGivenLabels>
+__global__ __launch_bounds__(kK2Threads) void k_classify_compact(
+    const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
+    const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
+    u64* __restrict__ vbuf, u64 ncap, u64* __restrict__ status, u32 tag,
+    u32* __restrict__ tile_ctr, u32 num_tiles, u32* __restrict__ counts_out) {
+  __shared__ u32 s_tile;
+  __shared__ u32 s_warp_cnt[kK2Threads / 32][4];
+  __shared__ u32 s_excl[4];
+  __shared__ QuadEdges s_edges;
+  __shared__ int s_lex;
+
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(tile_ctr, 1u);
+    const QuadInfo qi = *qinfo;
+    for (int c = 0; c < 4; ++c) {
+      const int d = (c + 1) & 3;
+      s_edges.ax[c] = qi.q[2 * c];
+      s_edges.ay[c] = qi.q[2 * c + 1];
+      s_edges.ex[c] = __dsub_rn(qi.q[2 * d], qi.q[2 * c]);
+      s_edges.ey[c] = __dsub_rn(qi.q[2 * d + 1], qi.q[2 * c + 1]);
+    }
+    // Degenerate frame: survivors all go to stream 1 in lexicographic
+    // encoding for the hull_oracle-style finish (pipeline.cpp:53-71).
+    s_lex = force_lex || (!kGivenLabels && qi.degenerate);
+  }
+  __syncthreads();
+  const u32 tile = s_tile;
+  const bool lex = s_lex != 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u64 tile_base = (u64)tile * kK2Tile;
+
+  int reg[kK2Items];
+  double px[kK2Items], py[kK2Items];
+  u32 rank[kK2Items];
+  u32 run[4] = {0, 0, 0, 0};  // warp-uniform running counts per stream
+  const QuadEdges e = s_edges;
+
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + warp * 32 + lane;
+    reg[j] = 0;
+    px[j] = py[j] = 0.0;
+    if (idx < n) {
+      const double2 p = ldg_stream(pts + idx);
+      px[j] = p.x;
+      py[j] = p.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + warp * 32 + lane;
+    if (idx < n) {
+      int r = kGivenLabels ? (int)given_labels[idx] : classify(e, px[j], py[j]);
+      if (lex && r != 0) r = 1;
+      reg[j] = r;
+    }
+    rank[j] = 0;
+#pragma unroll
+    for (int s = 1; s <= 4; ++s) {
+      const unsigned m = __ballot_sync(0xffffffffu, reg[j] == s);
+      if (reg[j] == s) rank[j] = run[s - 1] + __popc(m & lanemask_lt());
+      run[s - 1] += __popc(m);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) s_warp_cnt[warp][s] = run[s];
+  }
+  __syncthreads();
+
+  // Warp s (s < 4) owns stream s+1: block-exclusive scan over warps, then
+  // the look-back for this tile.
+  if (warp < 4) {
+    const int s = warp;
+    u32 agg = 0;
+    if (lane == 0) {
+      for (int w = 0; w < kK2Threads / 32; ++w) {
+        const u32 c = s_warp_cnt[w][s];
+        s_warp_cnt[w][s] = agg;
+        agg += c;
+      }
+    }
+    agg = __shfl_sync(0xffffffffu, agg, 0);
+    u64* col = status + s;
+    u32 excl = 0;
+    if (tile == 0) {
+      if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, agg));
+    } else {
+      if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagAgg, agg));
+      excl = warp_lookback(col, 4, (int)tile, 0, tag);
+      if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagPrefix, excl + agg));
+    }
+    if (lane == 0) {
+      s_excl[s] = excl;
+      if (tile == num_tiles - 1) counts_out[s + 1] = excl + agg;
+    }
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const int s = reg[j];
+    if (s != 0) {
+      const u64 pos = (u64)s_excl[s - 1] + s_warp_cnt[warp][s - 1] + rank[j];
+      const u64 slot = stream_slot(s, pos, ncap);
+      u64 k, v;
+      encode_point(lex ? 0 : s, px[j], py[j], k, v);
+      kbuf[slot] = k;
+      vbuf[slot] = v;
+    }
+  }
+}
+
+// Labels only (the classify() stage tap, classify.cpp:9-33).
+__global__ void k_classify_labels(const double2* __restrict__ pts, u64 n,
+                                  const QuadInfo* __restrict__ qinfo,
+                                  unsigned char* __restrict__ labels,
+                                  unsigned long long* __restrict__ counts) {
+  __shared__ QuadEdges s_edges;
+  __shared__ unsigned long long s_cnt[5];
+  if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    const QuadInfo qi = *qinfo;
+    for (int c = 0; c < 4; ++c) {
+      const int d = (c + 1) & 3;
+      s_edges.ax[c] = qi.q[2 * c];
+      s_edges.ay[c] = qi.q[2 * c + 1];
+      s_edges.ex[c] = __dsub_rn(qi.q[2 * d], qi.q[2 * c]);
+      s_edges.ey[c] = __dsub_rn(qi.q[2 * d + 1], qi.q[2 * c + 1]);
+    }
+  }
+  __syncthreads();
+  const QuadEdges e = s_edges;
+  u32 local[5] = {0, 0, 0, 0, 0};
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const double2 p = ldg_stream(pts + i);
+    const int r = classify(e, p.x, p.y);
+    labels[i] = (unsigned char)r;
+    ++local[r];
+  }
+  for (int r = 0; r < 5; ++r) {
+    u32 c = local[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_cnt[r], (unsigned long long)c);
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------ launchers
+
+void launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
+                             int blocks, cudaStream_t st) {
+  k_extremes_partial<<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials);
+}
+
+void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
+                           QuadCand* raw_out, cudaStream_t st) {
+  k_extremes_final<<<1, 256, 0, st>>>(partials, nparts, out, raw_out);
+}
+
+void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
+                             const unsigned char* given_labels, int force_lex, u64* kbuf,
+                             u64* vbuf, u64 ncap, u64* status, u32 tag, u32* tile_ctr,
+                             u32* counts_out, cudaStream_t st) {
+  const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
+  if (tiles == 0) return;
+  if (given_labels)
+    k_classify_compact<true><<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, given_labels, force_lex,
+                                                           kbuf, vbuf, ncap, status, tag, tile_ctr,
+                                                           tiles, counts_out);
+  else
+    k_classify_compact<false><<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, nullptr, force_lex,
+                                                            kbuf, vbuf, ncap, status, tag,
+                                                            tile_ctr, tiles, counts_out);
+}
+
+void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
+                            unsigned char* labels, unsigned long long* counts, int blocks,
+                            cudaStream_t st) {
+  k_classify_labels<<<blocks, 256, 0, st>>>(pts, n, qinfo, labels, counts);
+}
+
+}  // namespace chgpu
+
+namespace chgpu {
+
+// Stage-tap helpers: raw points <-> sort records for one region codec.
+__global__ void k_encode(const double2* __restrict__ pts, u64 n, int region, u64* __restrict__ k,
+                         u64* __restrict__ v) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const double2 p = pts[i];
+    encode_point(region, p.x, p.y, k[i], v[i]);
+  }
+}
+
+__global__ void k_decode(const u64* __restrict__ k, const u64* __restrict__ v, u64 n, int region,
+                         double2* __restrict__ out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    double x, y;
+    decode_point(region, k[i], v[i], x, y);
+    out[i] = make_double2(x, y);
+  }
+}
+
+void launch_encode(const double2* pts, u64 n, int region, u64* k, u64* v, cudaStream_t st) {
+  if (!n) return;
+  const u64 blocks = (n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16;
+  k_encode<<<(unsigned)blocks, 256, 0, st>>>(pts, n, region, k, v);
+}
+
+void launch_decode(const u64* k, const u64* v, u64 n, int region, double2* out, cudaStream_t st) {
+  if (!n) return;
+  const u64 blocks = (n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16;
+  k_decode<<<(unsigned)blocks, 256, 0, st>>>(k, v, n, region, out);
+}
+
+}  // namespace chgpu

@@ -1,0 +1,267 @@
+// K4 + K5: SPA second-round discard and chain compaction.
+//
+// spa_filter (reference spa.cpp:109-163) scans each chunk of a sorted
+// region sequentially with a running threshold t that only moves when a
+// point is kept. Since a kept point always satisfies g <= t (LL/UL) or
+// g >= t (LR/UR), t after any step equals the running min (resp. max) of
+// the chunk's seed and every guarded value seen so far, whether kept or
+// not. The filter is therefore an exclusive segmented prefix-min/max:
+//   keep(i)  <=>  !steps_back(g_i, op(seed_c, g_begin .. g_{i-1}))
+// with seed_0 = guarded(anchors.first) (:130-132) and seed_c = the op's
+// identity for c > 0, which keeps every later chunk's first point (:134-138).
+// One CTA owns one chunk: a block-wide scan per 4096-record tile with the
+// carry in registers. Kept records are then compacted, stably and in
+// region order, into decoded points with a decoupled look-back over chunks
+// (the serial compaction of spa.cpp:158-161).
+
+#include <math.h>
+
+#include "chgpu_internal.cuh"
+#include "kernels.h"
+
+namespace chgpu {
+
+constexpr int kSpaThreads = 256;
+constexpr int kSpaItems = 16;
+constexpr int kSpaTile = kSpaThreads * kSpaItems;
+
+__device__ __forceinline__ double op_ext(bool is_min, double a, double b) {
+  return is_min ? (b < a ? b : a) : (b > a ? b : a);
+}
+__device__ __forceinline__ bool steps_back(bool is_min, double g, double t) {
+  return is_min ? (g > t) : (g < t);  // spa.cpp:92-105
+}
+
+// Block-wide exclusive scan with op_ext; returns the exclusive value for
+// this thread and the block aggregate in *agg.
+__device__ __forceinline__ double block_excl_ext(bool is_min, double x, double ident, double* sw,
+                                                 double* agg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = op_ext(is_min, y, incl);
+  }
+  double excl_w = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl_w = ident;
+  if (lane == 31) sw[warp] = incl;
+  __syncthreads();
+  double pre = ident;
+  for (int w = 0; w < warp; ++w) pre = op_ext(is_min, pre, sw[w]);
+  double tot = ident;
+  for (int w = 0; w < kSpaThreads / 32; ++w) tot = op_ext(is_min, tot, sw[w]);
+  *agg = tot;
+  __syncthreads();
+  return op_ext(is_min, pre, excl_w);
+}
+
+__device__ __forceinline__ u32 block_excl_sum(u32 x, u32* sw, u32* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) sw[warp] = incl;
+  __syncthreads();
+  u32 pre = 0, tot = 0;
+  for (int w = 0; w < kSpaThreads / 32; ++w) {
+    if (w < warp) pre += sw[w];
+    tot += sw[w];
+  }
+  *total = tot;
+  __syncthreads();
+  return pre + incl - x;
+}
+
+__global__ __launch_bounds__(kSpaThreads) void k_spa(const u64* __restrict__ k,
+                                                     const u64* __restrict__ v, SpaPlan plan,
+                                                     unsigned char* __restrict__ flags,
+                                                     double2* __restrict__ kept_out,
+                                                     unsigned long long* __restrict__ kept_counts,
+                                                     u64* __restrict__ status, u32 tag,
+                                                     u32* __restrict__ chunk_ctr) {
+  __shared__ double sg[kSpaTile + kSpaTile / 16];
+  __shared__ double swd[kSpaThreads / 32];
+  __shared__ u32 swu[kSpaThreads / 32];
+  __shared__ u32 s_chunk, s_excl;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) s_chunk = atomicAdd(chunk_ctr, 1u);
+  __syncthreads();
+  const u32 chunk = s_chunk;
+  int r = 0;
+  while (r < 3 && chunk >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const u64 c = chunk - plan.chunk_begin[r];
+  const u64 begin = plan.off[r] + c * plan.chunk_size[r];
+  const u64 len = min((u64)plan.chunk_size[r], (u64)plan.m[r] - c * plan.chunk_size[r]);
+  const bool is_min = (region == 1 || region == 4);
+  const double ident = is_min ? INFINITY : -INFINITY;
+  double carry = (c == 0) ? plan.seed[r] : ident;
+
+  // Pass A: keep flags.
+  u32 kept = 0;
+  for (u64 t0 = 0; t0 < len; t0 += kSpaTile) {
+    const u32 cnt = (u32)min((u64)kSpaTile, len - t0);
+    for (u32 i = tid; i < cnt; i += kSpaThreads) sg[i + (i >> 4)] = guarded_of(region, v[begin + t0 + i]);
+    __syncthreads();
+    double g[kSpaItems];
+    double agg = ident;
+#pragma unroll
+    for (int j = 0; j < kSpaItems; ++j) {
+      const u32 i = tid * kSpaItems + j;
+      g[j] = i < cnt ? sg[i + (i >> 4)] : ident;
+      agg = op_ext(is_min, agg, g[j]);
+    }
+    double tile_agg;
+    const double excl = block_excl_ext(is_min, agg, ident, swd, &tile_agg);
+    double t = op_ext(is_min, carry, excl);
+    unsigned char f[kSpaItems];
+#pragma unroll
+    for (int j = 0; j < kSpaItems; ++j) {
+      const u32 i = tid * kSpaItems + j;
+      f[j] = 0;
+      if (i < cnt) {
+        f[j] = steps_back(is_min, g[j], t) ? 0 : 1;
+        kept += f[j];
+        t = op_ext(is_min, t, g[j]);
+      }
+    }
+    // Flags go out through shared memory as coalesced bytes.
+    __syncthreads();
+    unsigned char* sf = reinterpret_cast<unsigned char*>(sg);
+#pragma unroll
+    for (int j = 0; j < kSpaItems; ++j) sf[tid * kSpaItems + j] = f[j];
+    __syncthreads();
+    for (u32 i = tid; i < cnt; i += kSpaThreads) flags[begin + t0 + i] = sf[i];
+    carry = op_ext(is_min, carry, tile_agg);
+    __syncthreads();
+  }
+  u32 chunk_kept;
+  block_excl_sum(kept, swu, &chunk_kept);
+
+  // Look-back over chunks in (region, chunk) order.
+  if (tid < 32) {
+    u32 excl = 0;
+    if (chunk == 0) {
+      if (tid == 0) store_status(status, make_status(tag, kFlagPrefix, chunk_kept));
+    } else {
+      if (tid == 0) store_status(status + chunk, make_status(tag, kFlagAgg, chunk_kept));
+      excl = warp_lookback(status, 1, (int)chunk, 0, tag);
+      if (tid == 0) store_status(status + chunk, make_status(tag, kFlagPrefix, excl + chunk_kept));
+    }
+    if (tid == 0) {
+      s_excl = excl;
+      if (chunk_kept) atomicAdd(&kept_counts[r], (unsigned long long)chunk_kept);
+    }
+  }
+  __syncthreads();
+
+  // Pass B: stable scatter of the kept records as decoded points.
+  u32 out = s_excl;
+  for (u64 t0 = 0; t0 < len; t0 += kSpaTile) {
+    const u32 cnt = (u32)min((u64)kSpaTile, len - t0);
+    unsigned char f[kSpaItems];
+    u32 mine = 0;
+#pragma unroll
+    for (int j = 0; j < kSpaItems; ++j) {
+      const u32 i = tid * kSpaItems + j;
+      f[j] = i < cnt ? flags[begin + t0 + i] : 0;
+      mine += f[j];
+    }
+    u32 tile_kept;
+    u32 pos = out + block_excl_sum(mine, swu, &tile_kept);
+#pragma unroll
+    for (int j = 0; j < kSpaItems; ++j) {
+      if (f[j]) {
+        const u64 a = begin + t0 + tid * kSpaItems + j;
+        double x, y;
+        decode_point(region, k[a], v[a], x, y);
+        kept_out[pos++] = make_double2(x, y);
+      }
+    }
+    out += tile_kept;
+  }
+}
+
+// Degenerate branch: unique over the lexicographically sorted survivors
+// (oracle.cpp:16-17 std::sort + std::unique), compacted in order.
+__global__ __launch_bounds__(kSpaThreads) void k_unique(const u64* __restrict__ k,
+                                                        const u64* __restrict__ v, u64 n,
+                                                        double2* __restrict__ out,
+                                                        u64* __restrict__ status, u32 tag,
+                                                        u32* __restrict__ tile_ctr,
+                                                        unsigned long long* __restrict__ total) {
+  __shared__ u32 swu[kSpaThreads / 32];
+  __shared__ u32 s_tile, s_excl;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const u32 tile = s_tile;
+  const u64 t0 = (u64)tile * kSpaTile;
+  unsigned char f[kSpaItems];
+  u32 mine = 0;
+#pragma unroll
+  for (int j = 0; j < kSpaItems; ++j) {
+    const u64 i = t0 + tid * kSpaItems + j;
+    f[j] = 0;
+    if (i < n) {
+      if (i == 0) {
+        f[j] = 1;
+      } else {
+        double x0, y0, x1, y1;
+        decode_point(0, k[i - 1], v[i - 1], x0, y0);
+        decode_point(0, k[i], v[i], x1, y1);
+        f[j] = (x0 == x1 && y0 == y1) ? 0 : 1;
+      }
+    }
+    mine += f[j];
+  }
+  u32 tile_cnt;
+  const u32 lpos = block_excl_sum(mine, swu, &tile_cnt);
+  if (tid < 32) {
+    u32 excl = 0;
+    if (tile == 0) {
+      if (tid == 0) store_status(status, make_status(tag, kFlagPrefix, tile_cnt));
+    } else {
+      if (tid == 0) store_status(status + tile, make_status(tag, kFlagAgg, tile_cnt));
+      excl = warp_lookback(status, 1, (int)tile, 0, tag);
+      if (tid == 0) store_status(status + tile, make_status(tag, kFlagPrefix, excl + tile_cnt));
+    }
+    if (tid == 0) {
+      s_excl = excl;
+      if (tile_cnt) atomicAdd(total, (unsigned long long)tile_cnt);
+    }
+  }
+  __syncthreads();
+  u32 pos = s_excl + lpos;
+#pragma unroll
+  for (int j = 0; j < kSpaItems; ++j) {
+    if (f[j]) {
+      const u64 i = t0 + tid * kSpaItems + j;
+      double x, y;
+      decode_point(0, k[i], v[i], x, y);
+      out[pos++] = make_double2(x, y);
+    }
+  }
+}
+
+void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
+                double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,
+                u32* chunk_ctr, cudaStream_t st) {
+  if (plan.total_chunks == 0) return;
+  k_spa<<<plan.total_chunks, kSpaThreads, 0, st>>>(k, v, plan, flags, kept_out, kept_counts,
+                                                    status, tag, chunk_ctr);
+}
+
+void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
+                   u32* tile_ctr, unsigned long long* total, cudaStream_t st) {
+  const u64 tiles = (n + kSpaTile - 1) / kSpaTile;
+  if (tiles == 0) return;
+  k_unique<<<(unsigned)tiles, kSpaThreads, 0, st>>>(k, v, n, out, status, tag, tile_ctr, total);
+}
+
+}  // namespace chgpu

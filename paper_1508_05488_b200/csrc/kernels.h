@@ -1,0 +1,60 @@
+// Host-callable launchers for the hull kernels (internal to libchgpu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "chgpu_internal.cuh"
+
+namespace chgpu {
+
+struct SpaPlan {
+  u64 off[4];         // region offset in the sorted array
+  u64 m[4];           // region size
+  u64 chunk_size[4];  // ceil(m / chunk_count)            (spa.cpp:121)
+  u32 chunk_begin[4]; // prefix of per-region chunk counts (spa.cpp:122)
+  u32 total_chunks;
+  double seed[4];     // guarded(anchors.first)           (spa.cpp:130-132)
+};
+
+// K1
+void launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
+                             int blocks, cudaStream_t st);
+void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, QuadCand* raw_out,
+                           cudaStream_t st);
+// K2
+void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
+                             const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
+                             u64 ncap, u64* status, u32 tag, u32* tile_ctr, u32* counts_out,
+                             cudaStream_t st);
+void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
+                            unsigned char* labels, unsigned long long* counts, int blocks,
+                            cudaStream_t st);
+// K3
+void launch_hist(const u64* kin, const u64* vin, const SegDesc* segs, int nseg, u32 total_tiles,
+                 int from_v, int use_src, u32* hist, cudaStream_t st);
+void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, u32* digit_excl,
+                      u32* needed_mask, cudaStream_t st);
+void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
+                     int nseg, u32 total_tiles, int use_src, int from_v, const u32* digit_excl,
+                     int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st);
+void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
+                     int nseg, u32 total_tiles, int use_src, cudaStream_t st);
+void launch_tie_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, u64* starts,
+                       u32* nstarts, u32 cap, cudaStream_t st);
+void launch_tie_fix(u64* k, u64* v, const SegDesc* segs, const u64* starts, u32 nstarts,
+                    void* long_runs, u32* nlong, cudaStream_t st);
+size_t tie_run_record_bytes();
+// K4/K5
+void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
+                double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,
+                u32* chunk_ctr, cudaStream_t st);
+void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
+                   u32* tile_ctr, unsigned long long* total, cudaStream_t st);
+
+}  // namespace chgpu
+
+namespace chgpu {
+void launch_encode(const double2* pts, u64 n, int region, u64* k, u64* v, cudaStream_t st);
+void launch_decode(const u64* k, const u64* v, u64 n, int region, double2* out, cudaStream_t st);
+}  // namespace chgpu

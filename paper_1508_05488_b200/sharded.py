@@ -1,0 +1,152 @@
+"""Multi-GPU hull: one rank per GPU, the point set sharded by contiguous
+index ranges. Scaling is by sharding, with two tiny
+exchanges over torch.distributed (NCCL on GPUs, gloo in the CPU tests):
+
+1. all-gather of each rank's 4 extreme candidates (point + global index),
+   folded in rank order with the lexicographic rules and lowest-global-index
+   ties (reference extremes.cpp:39-46 semantics), so every rank holds the
+   quad find_extremes would return on the whole set;
+2. each rank runs round-1 discard, region sort and SPA of its shard against
+   that global quad (every dropped point lies inside the global quad or
+   inside a triangle of kept points and global anchors, so no hull vertex is
+   lost), then the chains are gathered on rank 0, which finishes with the
+   single-GPU pipeline over (union of chains) + frame: the hull of the union
+   is the hull of the whole set.
+
+The per-rank compute is behind `ShardOps` so the exchange logic is tested
+with the gloo backend on CPU (tests/test_sharded.py) and runs the sm_100a
+kernels through the C ABI on GPUs (GpuShardOps).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def frame_vertices(quad: np.ndarray) -> np.ndarray:
+    """extremes.cpp:49-57."""
+    ring = []
+    for p in np.asarray(quad, np.float64).reshape(4, 2):
+        if not ring or not (ring[-1][0] == p[0] and ring[-1][1] == p[1]):
+            ring.append(p)
+    if len(ring) > 1 and ring[0][0] == ring[-1][0] and ring[0][1] == ring[-1][1]:
+        ring.pop()
+    return np.array(ring, np.float64).reshape(-1, 2)
+
+
+def _less_xy(a, b):
+    return a[0] < b[0] or (a[0] == b[0] and a[1] < b[1])
+
+
+def _less_yx(a, b):
+    return a[1] < b[1] or (a[1] == b[1] and a[0] < b[0])
+
+
+def fold_extremes(quads: np.ndarray, idxs: np.ndarray) -> np.ndarray:
+    """Rank-ordered fold of per-rank corner candidates; ties -> lowest global
+    index (the earliest point, as the reference's sequential fold keeps)."""
+    quads = np.asarray(quads, np.float64).reshape(-1, 4, 2)
+    idxs = np.asarray(idxs, np.int64).reshape(-1, 4)
+    best = [None] * 4
+    for r in range(len(quads)):
+        for c in range(4):
+            cand = (quads[r, c], int(idxs[r, c]))
+            if best[c] is None:
+                best[c] = cand
+                continue
+            a, b = cand[0], best[c][0]
+            if c == 0:
+                win, lose = _less_xy(a, b), _less_xy(b, a)
+            elif c == 1:
+                win, lose = _less_yx(a, b), _less_yx(b, a)
+            elif c == 2:
+                win, lose = _less_xy(b, a), _less_xy(a, b)
+            else:
+                win, lose = _less_yx(b, a), _less_yx(a, b)
+            if win or (not lose and cand[1] < best[c][1]):
+                best[c] = cand
+    return np.array([b[0] for b in best], np.float64)
+
+
+class ShardOps:
+    """Per-rank compute used by sharded_convex_hull."""
+
+    def extremes(self):  # -> (quad (4, 2), global indices (4,))
+        raise NotImplementedError
+
+    def chains(self, quad: np.ndarray, chunk_count: int):  # -> (k, 2) kept points
+        raise NotImplementedError
+
+    def finish(self, points: np.ndarray, chunk_count: int) -> np.ndarray:  # -> hull vertices
+        raise NotImplementedError
+
+
+class GpuShardOps(ShardOps):
+    """sm_100a kernels through the C ABI; `points` is a CUDA float64 (n, 2)
+    tensor holding this rank's shard, `base_index` its global offset."""
+
+    def __init__(self, ctx, points: torch.Tensor, base_index: int):
+        self.ctx, self.t, self.base = ctx, points, int(base_index)
+
+    def extremes(self):
+        q, idx = self.ctx.shard_extremes(self.t.data_ptr(), self.t.shape[0], self.base)
+        return q.reshape(4, 2), idx.astype(np.int64)
+
+    def chains(self, quad, chunk_count):
+        pts, _ = self.ctx.shard_chains(self.t.data_ptr(), self.t.shape[0], quad, chunk_count)
+        return pts
+
+    def finish(self, points, chunk_count):
+        from . import PipelineConfig
+        return self.ctx.convex_hull(points, PipelineConfig(chunk_count=chunk_count)).hull.vertices
+
+
+def _device_for(group) -> torch.device:
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
+    """Returns the global hull on rank 0 (None elsewhere)."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = _device_for(group)
+
+    # exchange 1: extreme candidates (8 coords + 4 indices; indices < 2^53
+    # travel exactly as float64)
+    q, idx = ops.extremes()
+    mine = torch.tensor(np.concatenate([np.asarray(q, np.float64).reshape(8),
+                                        np.asarray(idx, np.float64)]), dtype=torch.float64,
+                        device=dev)
+    allq = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allq, mine, group=group)
+    arr = torch.stack(allq).cpu().numpy()
+    quad = fold_extremes(arr[:, :8], arr[:, 8:].astype(np.int64))
+
+    # per-rank discard + sort + SPA against the global quad
+    ch = np.ascontiguousarray(ops.chains(quad, chunk_count), np.float64).reshape(-1, 2)
+
+    # exchange 2: chains to rank 0 (sizes first, then padded payloads)
+    cnt = torch.tensor([len(ch)], dtype=torch.int64, device=dev)
+    counts = [torch.empty_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    width = max(max(counts), 1)
+    buf = torch.zeros((width, 2), dtype=torch.float64, device=dev)
+    if len(ch):
+        buf[: len(ch)] = torch.from_numpy(ch).to(dev)
+    gathered = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+    if dist.get_backend(group) == "nccl":
+        # NCCL gather: emulate with all_gather (the payload is tiny)
+        tmp = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(tmp, buf, group=group)
+        gathered = tmp if rank == 0 else None
+    else:
+        dist.gather(buf, gathered, dst=0, group=group)
+    if rank != 0:
+        return None
+    parts = [g[:c].cpu().numpy() for g, c in zip(gathered, counts)]
+    union = np.concatenate(parts + [frame_vertices(quad)], axis=0)
+    return ops.finish(union, chunk_count)

@@ -1,0 +1,93 @@
+"""CPU: the C-ABI library loads, exports every symbol include/chgpu.h
+declares, and its host-side parts (finisher, generator, error mapping) agree
+with the reference's known answers. No GPU compute is called here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import kats
+from conftest import ROOT, load_golden, sha
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "chgpu.h")).read()
+    return sorted(set(re.findall(r"\b(chgpu_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(product):
+    lib = product.load_library()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/chgpu.h but not exported"
+
+
+def test_no_device_fails_loudly(product):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(product.Error):
+        product.Context()
+
+
+def test_host_melkman_kats(product):
+    for poly, want in kats.MELKMAN:
+        if want is None:
+            with pytest.raises(product.DegenerateInput):
+                product.melkman(poly)
+        else:
+            assert product.melkman(poly).tolist() == want
+
+
+def test_host_assemble_kats(product):
+    for quad, chains, want in kats.ASSEMBLE:
+        flat = [p for c in chains for p in c]
+        counts = [len(c) for c in chains]
+        if want is None:
+            with pytest.raises(product.DegenerateInput):
+                product.assemble_polygon(np.array(flat).reshape(-1, 2), counts, quad)
+        else:
+            got = product.assemble_polygon(np.array(flat, np.float64).reshape(-1, 2), counts, quad)
+            assert got.tolist() == want
+
+
+def test_host_hull_oracle_and_canonicalize(product):
+    for pts, want in kats.ORACLE:
+        assert product.hull_oracle(pts).tolist() == want
+    with pytest.raises(product.EmptyInput):
+        product.hull_oracle(np.empty((0, 2)))
+    ring = product.canonicalize_ring([[4, 4], [0, 4], [0, 0], [4, 0]])   # melkman_test.cpp:66-71
+    assert ring.tolist() == [[0, 0], [4, 0], [4, 4], [0, 4]]
+
+
+def test_product_generator_bit_identical(product):
+    """chgpu_generate == the reference generate() (hashes from the reference)."""
+    for case in load_golden("pipeline_sweep.json"):
+        pts = product.generate(case["dist"], case["n"], case["seed"])
+        assert sha(pts) == case["input_sha"], (case["dist"], case["n"], case["seed"])
+    for case in load_golden("big.json"):
+        if case["n"] <= 4_000_000:
+            assert sha(product.generate(case["dist"], case["n"], case["seed"])) == case["input_sha"]
+    with pytest.raises(ValueError):
+        product.generate("uniform_square", 0, 1)
+
+
+def test_host_finisher_matches_oracle_random_polygons(product, oracle):
+    """acceptance.cpp:281-300 (criterion 7) style: melkman on radial polygons."""
+    rng = np.random.default_rng(777)
+    for _ in range(100):
+        k = int(rng.integers(3, 400))
+        pts = rng.random((k, 2))
+        c = pts.mean(axis=0)
+        ring = pts[np.argsort(np.arctan2(pts[:, 1] - c[1], pts[:, 0] - c[0]))]
+        st, want = oracle.melkman(ring)
+        assert st == 0
+        assert np.array_equal(product.melkman(ring), want)
+        assert np.array_equal(product.hull_oracle(ring), oracle.hull_oracle(ring)[1])
+
+
+def test_stats_struct_layout(product):
+    assert C.sizeof(product._Stats) == 4 * 8 + 7 * 8
