@@ -201,15 +201,23 @@ struct QuadCand {
   Cand c[4];
 };
 
-// Sort segment descriptor (one region, or one long tie run).
+// Sort segment descriptor (one region, or one long group of a region).
 struct SegDesc {
   u64 src_off;     // element offset of the segment in the pass's source array
   u64 dst_off;     // element offset in the destination array
   u32 len;         // elements
   u32 tile_begin;  // first global tile of the segment
   int region;      // key codec region (0 = LEX)
-  int pad;
+  int qbits;       // quantizer width (digit mode kDigitQ)
+  double qlo;      // quantizer: q = clamp((primary - qlo) * qscale, 0, qmax)
+  double qscale;
+  double qmax;     // 2^qbits - 1
 };
+
+// Digit sources of a radix pass.
+enum : int { kDigitK = 0, kDigitV = 1, kDigitQ = 2 };
+// Group equality of the in-place fix-up.
+enum : int { kEqQ = 0, kEqPrim = 1 };
 
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;

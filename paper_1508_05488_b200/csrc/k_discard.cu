@@ -118,11 +118,20 @@ __global__ void k_extremes_final(const QuadCand* __restrict__ partials, int npar
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc.c[c] = Cand{0.0, 0.0, ~0ull};
   for (int p = threadIdx.x; p < nparts; p += blockDim.x) merge_quad(acc, partials[p]);
-  __shared__ QuadCand sacc[256];
-  sacc[threadIdx.x] = acc;
+  // Tree combine: warp shuffles, then the 8 warp results (order-free: ties
+  // fall back to the global index).
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    QuadCand other;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) other.c[c] = shfl_cand(acc.c[c], o);
+    merge_quad(acc, other);
+  }
+  __shared__ QuadCand sacc[8];
+  if ((threadIdx.x & 31) == 0) sacc[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int t = 1; t < (int)blockDim.x; ++t) merge_quad(acc, sacc[t]);
+    for (int t = 1; t < (int)(blockDim.x >> 5); ++t) merge_quad(acc, sacc[t]);
     if (raw_out) *raw_out = acc;
     if (out) {
       QuadInfo qi;

@@ -1,17 +1,26 @@
 // K3: region sort. Replaces sort_region's per-region std::sort
-// (reference spa.cpp:59-81) with a segmented onesweep LSD radix sort.
+// (reference spa.cpp:59-81).
 //
-// * Records are (k, v) 64-bit pairs (chgpu_internal.cuh codec); ascending
-//   (k, v) order is region_less (spa.cpp:38-52).
-// * All four regions sort in the same launches: each region is a segment,
-//   tiles never straddle segments, and each (segment, digit) bin has its own
-//   decoupled look-back chain, so one pass moves every region at once.
-// * One histogram pass computes the digit counts of all 8 digit positions;
-//   positions where every segment has a single populated bin are skipped.
-// * LSD on k alone leaves equal-primary runs in input order; k_tie_detect /
-//   k_tie_fix then order each run by v (short runs in shared memory, long
-//   runs through the same onesweep engine keyed on v). prim_eq merges -0.0
-//   and +0.0 into one run, which is exactly the reference's `==` tie.
+// Records are (k, v) 64-bit pairs (chgpu_internal.cuh codec): ascending
+// (k, v) with -0.0/+0.0 merged is region_less (spa.cpp:38-52). The sort
+// runs in two phases, both over all four regions at once (one segment per
+// region, tiles never straddle segments, one decoupled look-back chain per
+// (segment, digit)):
+//
+//  1. Bucket phase: a segmented onesweep LSD radix sort keyed on
+//     q = quantize(primary) with 24 or 32 bits, a monotone map of the
+//     region's primary coordinate onto [0, 2^bits) (monotone because
+//     subtraction, multiplication by a positive constant, clamping and
+//     truncation are all monotone in IEEE round-to-nearest). It moves each
+//     record to its final bucket in 3-4 passes instead of the 8 a 64-bit
+//     key needs.
+//  2. Group phase: runs of equal q (a few percent of records for smooth
+//     inputs) are ordered by the full key (kc, v) in place: a thread per
+//     run up to 16 records, a block-wide bitonic sort up to 2048, and the
+//     same onesweep engine keyed on k then v beyond that.
+//
+// Every launch uses (segment, bin) tagged look-back words, so the status
+// array never needs clearing.
 
 #include "chgpu_internal.cuh"
 #include "kernels.h"
@@ -27,14 +36,40 @@ __device__ __forceinline__ int find_segment(const SegDesc* segs, int nseg, u32 t
   return lo;
 }
 
+// Monotone quantizer of the primary coordinate (see header comment).
+__device__ __forceinline__ u32 quantize(const SegDesc& s, u64 k) {
+  const double p = primary_of(s.region, k);
+  const double qmax = s.qmax;
+  double t = __dmul_rn(__dsub_rn(p, s.qlo), s.qscale);
+  t = fmin(fmax(t, 0.0), qmax);
+  const u32 q = (u32)__double2ull_rz(t);
+  return (s.region == 3 || s.region == 4) ? (u32)((u64)qmax - q) : q;
+}
+
+// -0.0 as primary compares like +0.0: map its code onto +0.0's.
+__device__ __forceinline__ u64 canon_k(int region, u64 k) {
+  const bool desc = (region == 3 || region == 4);
+  const u64 neg0 = desc ? ~0x7FFFFFFFFFFFFFFFull : 0x7FFFFFFFFFFFFFFFull;
+  const u64 pos0 = desc ? ~0x8000000000000000ull : 0x8000000000000000ull;
+  return k == neg0 ? pos0 : k;
+}
+
+template <int kMode>
+__device__ __forceinline__ u32 digit_of(const SegDesc& s, u64 k, u64 v, int pass) {
+  if (kMode == kDigitQ) return (quantize(s, k) >> (8 * pass)) & 0xFFu;
+  if (kMode == kDigitV) return (u32)(v >> (8 * pass)) & 0xFFu;
+  return (u32)(k >> (8 * pass)) & 0xFFu;
+}
+
 // ------------------------------------------------------------------ histogram
 
 constexpr int kHistThreads = 256;
 
+template <int kMode>
 __global__ __launch_bounds__(kHistThreads) void k_hist(const u64* __restrict__ kin,
                                                        const u64* __restrict__ vin,
                                                        const SegDesc* __restrict__ segs, int nseg,
-                                                       u32 total_tiles, int from_v, int use_src,
+                                                       u32 total_tiles, int npasses, int use_src,
                                                        u32* __restrict__ hist) {
   __shared__ u32 sh[kPasses][kDigits];
   const u32 per = (total_tiles + gridDim.x - 1) / gridDim.x;
@@ -43,11 +78,9 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const u64* __restrict__ k
   if (t0 >= t1) return;
   for (int i = threadIdx.x; i < kPasses * kDigits; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
-  const u64* src = from_v ? vin : kin;
   int seg = find_segment(segs, nseg, t0);
   for (u32 t = t0; t < t1; ++t) {
     while (seg + 1 < nseg && segs[seg + 1].tile_begin <= t) {
-      // flush the finished segment
       __syncthreads();
       for (int i = threadIdx.x; i < kPasses * kDigits; i += blockDim.x) {
         const u32 c = (&sh[0][0])[i];
@@ -64,9 +97,15 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const u64* __restrict__ k
     const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
     const u64 base = (use_src ? sd.src_off : sd.dst_off) + e0;
     for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const u64 key = src[base + i];
-#pragma unroll
-      for (int p = 0; p < kPasses; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 0xFF], 1u);
+      const u64 k = kMode == kDigitV ? 0 : kin[base + i];
+      const u64 v = kMode == kDigitV ? vin[base + i] : 0;
+      if (kMode == kDigitQ) {
+        const u32 q = quantize(sd, k);
+        for (int p = 0; p < npasses; ++p) atomicAdd(&sh[p][(q >> (8 * p)) & 0xFF], 1u);
+      } else {
+        const u64 key = kMode == kDigitV ? v : k;
+        for (int p = 0; p < npasses; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 0xFF], 1u);
+      }
     }
   }
   __syncthreads();
@@ -79,8 +118,9 @@ __global__ __launch_bounds__(kHistThreads) void k_hist(const u64* __restrict__ k
 // One block per (segment, pass): exclusive digit prefix and the
 // "this pass moves something" mask.
 __global__ void k_hist_scan(const u32* __restrict__ hist, const SegDesc* __restrict__ segs,
-                            u32* __restrict__ digit_excl, u32* __restrict__ needed_mask) {
+                            int npasses, u32* __restrict__ digit_excl, u32* __restrict__ needed_mask) {
   const int seg = blockIdx.x / kPasses, pass = blockIdx.x % kPasses;
+  if (pass >= npasses) return;
   const u32* h = hist + ((size_t)seg * kPasses + pass) * kDigits;
   u32* out = digit_excl + ((size_t)seg * kPasses + pass) * kDigits;
   __shared__ u32 s[kDigits];
@@ -92,7 +132,6 @@ __global__ void k_hist_scan(const u32* __restrict__ hist, const SegDesc* __restr
   if (c == segs[seg].len) s_trivial = 1;  // every record has the same digit
   s[b] = c;
   __syncthreads();
-  // Hillis-Steele inclusive scan over 256 bins.
   for (int o = 1; o < kDigits; o <<= 1) {
     const u32 add = b >= o ? s[b - o] : 0u;
     __syncthreads();
@@ -105,7 +144,7 @@ __global__ void k_hist_scan(const u32* __restrict__ hist, const SegDesc* __restr
 
 // ------------------------------------------------------------------ onesweep pass
 
-template <bool kFromV>
+template <int kMode>
 __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
@@ -135,7 +174,6 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
   const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
   const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
   const u64 src = (use_src ? sd.src_off : sd.dst_off) + e0;
-  const int shift = 8 * pass;
 
   u64 kk[kSortItems], vv[kSortItems];
   u32 rank[kSortItems];
@@ -150,11 +188,13 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
   }
   // Warp-local multisplit: items are ranked in (warp, item, lane) order,
   // which is the input order inside the tile, so the pass is stable.
+  unsigned char dg[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
     const bool valid = li < cnt;
-    const u32 d = (u32)(((kFromV ? vv[j] : kk[j]) >> shift) & 0xFF);
+    const u32 d = digit_of<kMode>(sd, kk[j], vv[j], pass);
+    dg[j] = (unsigned char)d;
     const u32 key = valid ? d : (0x100u | (u32)lane);
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
@@ -177,7 +217,6 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
     whist[w][b] = tile_cnt;
     tile_cnt += c;
   }
-  // Block exclusive scan of tile_cnt over bins.
   u32 incl = tile_cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -221,7 +260,7 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
   for (int j = 0; j < kSortItems; ++j) {
     const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
     if (li < cnt) {
-      const u32 d = (u32)(((kFromV ? vv[j] : kk[j]) >> shift) & 0xFF);
+      const u32 d = dg[j];
       lpos[j] = bin_excl[d] + whist[warp][d] + rank[j];
       stage[lpos[j]] = kk[j];
       sdig[lpos[j]] = (unsigned char)d;
@@ -240,7 +279,7 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
 }
 
 // Moves segments between layouts without reordering (used when every
-// digit pass is trivial, and to return tie runs after an odd pass count).
+// digit pass is trivial, and to return runs after an odd pass count).
 __global__ void k_seg_copy(const u64* __restrict__ kin, const u64* __restrict__ vin,
                            u64* __restrict__ kout, u64* __restrict__ vout,
                            const SegDesc* __restrict__ segs, int nseg, int use_src) {
@@ -257,19 +296,25 @@ __global__ void k_seg_copy(const u64* __restrict__ kin, const u64* __restrict__ 
   }
 }
 
-// ------------------------------------------------------------------ tie runs
+// ------------------------------------------------------------------ groups
 
-struct TieRun {
-  u64 start;
-  u32 len;
-  int region;
-};
+// Group = maximal run (length >= 2) of records that compare equal under
+//   kEqQ:    equal quantized primary (bucket-phase leftovers), or
+//   kEqPrim: ==-equal primary (after a full sort on k).
+// Both are then ordered by (canon_k, v), which is region_less.
+__device__ __forceinline__ bool group_eq(int eqmode, const SegDesc& s, u64 a, u64 b) {
+  return eqmode == kEqQ ? quantize(s, a) == quantize(s, b) : prim_eq(s.region, a, b);
+}
 
-// Marks the start of every maximal run (length >= 2) of ==-equal primaries
-// inside a segment. One block per 4096-element tile of the region layout.
-__global__ void k_tie_detect(const u64* __restrict__ k, const SegDesc* __restrict__ segs,
-                             int nseg, u64* __restrict__ starts, u32* __restrict__ nstarts,
-                             u32 cap) {
+__device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u64 kb, u64 vb) {
+  const u64 ca = canon_k(region, ka), cb = canon_k(region, kb);
+  return ca < cb || (ca == cb && va < vb);
+}
+
+// Marks the start of every group. One block per 4096-record tile.
+__global__ void k_group_detect(const u64* __restrict__ k, const SegDesc* __restrict__ segs,
+                               int nseg, int eqmode, u64* __restrict__ starts,
+                               u32* __restrict__ nstarts, u32 cap) {
   const u32 tile = blockIdx.x;
   const int s = find_segment(segs, nseg, tile);
   const SegDesc sd = segs[s];
@@ -280,67 +325,90 @@ __global__ void k_tie_detect(const u64* __restrict__ k, const SegDesc* __restric
     const u64 pos = e0 + i;  // position inside the segment
     if (pos + 1 >= sd.len) continue;
     const u64 a = sd.dst_off + pos;
-    if (!prim_eq(sd.region, k[a], k[a + 1])) continue;
-    if (pos > 0 && prim_eq(sd.region, k[a - 1], k[a])) continue;  // not the first of its run
+    if (!group_eq(eqmode, sd, k[a], k[a + 1])) continue;
+    if (pos > 0 && group_eq(eqmode, sd, k[a - 1], k[a])) continue;  // not the first of its run
     const u32 slot = atomicAdd(nstarts, 1u);
     if (slot < cap) starts[slot] = ((u64)s << 40) | pos;
   }
 }
 
-constexpr int kTieSmem = 2048;
+struct GroupRun {
+  u64 start;  // absolute record index
+  u32 len;
+  int seg;
+};
 
-// Orders each run by v. Runs up to kTieSmem records are bitonic-sorted in
-// shared memory; longer runs are handed back for the onesweep engine.
-__global__ __launch_bounds__(256) void k_tie_fix(u64* __restrict__ k, u64* __restrict__ v,
-                                                 const SegDesc* __restrict__ segs,
-                                                 const u64* __restrict__ starts, u32 nstarts,
-                                                 TieRun* __restrict__ long_runs,
-                                                 u32* __restrict__ nlong) {
-  __shared__ u64 sk[kTieSmem], sv[kTieSmem];
-  __shared__ u32 s_len;
-  for (u32 r = blockIdx.x; r < nstarts; r += gridDim.x) {
+constexpr int kSmallGroup = 16;
+constexpr int kMediumGroup = 2048;
+
+// One thread per group: measures it, insertion-sorts it in registers when
+// it holds at most kSmallGroup records, else queues it as medium.
+__global__ void k_group_fix_small(u64* __restrict__ k, u64* __restrict__ v,
+                                  const SegDesc* __restrict__ segs, int eqmode,
+                                  const u64* __restrict__ starts, u32 nstarts,
+                                  GroupRun* __restrict__ medium, u32* __restrict__ nmedium) {
+  for (u32 r = blockIdx.x * blockDim.x + threadIdx.x; r < nstarts; r += gridDim.x * blockDim.x) {
     const u64 code = starts[r];
     const int s = (int)(code >> 40);
     const u64 pos = code & ((1ull << 40) - 1);
     const SegDesc sd = segs[s];
     const u64 a = sd.dst_off + pos;
     const u64 k0 = k[a];
-    // Run length: first index past the run, found 256 at a time.
-    if (threadIdx.x == 0) s_len = 0;
-    __syncthreads();
-    u64 probe = 1;
-    while (true) {
-      const u64 q = probe + threadIdx.x;
-      const bool stop = (pos + q >= sd.len) || !prim_eq(sd.region, k0, k[a + q]);
-      const unsigned m = __ballot_sync(0xffffffffu, stop);
-      __shared__ u32 s_stop[8];
-      if ((threadIdx.x & 31) == 0) s_stop[threadIdx.x >> 5] = m ? (u32)(__ffs(m) - 1) : 0xFFFFFFFFu;
-      __syncthreads();
-      u32 found = 0xFFFFFFFFu;
-      for (int w = 0; w < 8; ++w)
-        if (s_stop[w] != 0xFFFFFFFFu) { found = w * 32 + s_stop[w]; break; }
-      __syncthreads();
-      if (found != 0xFFFFFFFFu) {
-        if (threadIdx.x == 0) s_len = (u32)(probe + found);
-        break;
-      }
-      probe += blockDim.x;
+    u32 len = 1;
+    while (pos + len < sd.len && group_eq(eqmode, sd, k0, k[a + len])) {
+      ++len;
+      if (len > kSmallGroup) break;
     }
-    __syncthreads();
-    const u32 len = s_len;
-    if (len > kTieSmem) {
-      if (threadIdx.x == 0) {
-        const u32 slot = atomicAdd(nlong, 1u);
-        long_runs[slot] = TieRun{a, len, sd.region};
-      }
-      __syncthreads();
+    if (len > kSmallGroup) {
+      while (pos + len < sd.len && group_eq(eqmode, sd, k0, k[a + len])) ++len;
+      const u32 slot = atomicAdd(nmedium, 1u);
+      medium[slot] = GroupRun{a, len, s};
       continue;
     }
+    u64 gk[kSmallGroup], gv[kSmallGroup];
+    for (u32 i = 0; i < len; ++i) {
+      u64 kx = k[a + i], vx = v[a + i];
+      u32 j = i;
+      while (j > 0 && rec_less(sd.region, kx, vx, gk[j - 1], gv[j - 1])) {
+        gk[j] = gk[j - 1];
+        gv[j] = gv[j - 1];
+        --j;
+      }
+      gk[j] = kx;
+      gv[j] = vx;
+    }
+    for (u32 i = 0; i < len; ++i) {
+      k[a + i] = gk[i];
+      v[a + i] = gv[i];
+    }
+  }
+}
+
+// One block per medium group: bitonic sort in shared memory; groups longer
+// than kMediumGroup are handed back for the onesweep engine.
+__global__ __launch_bounds__(256) void k_group_fix_medium(u64* __restrict__ k, u64* __restrict__ v,
+                                                          const SegDesc* __restrict__ segs,
+                                                          const GroupRun* __restrict__ medium,
+                                                          u32 nmedium, GroupRun* __restrict__ longr,
+                                                          u32* __restrict__ nlong) {
+  __shared__ u64 sk[kMediumGroup], sv[kMediumGroup], sc[kMediumGroup];
+  for (u32 r = blockIdx.x; r < nmedium; r += gridDim.x) {
+    const GroupRun g = medium[r];
+    if (g.len > kMediumGroup) {
+      if (threadIdx.x == 0) longr[atomicAdd(nlong, 1u)] = g;
+      continue;
+    }
+    const int region = segs[g.seg].region;
     u32 P = 1;
-    while (P < len) P <<= 1;
+    while (P < g.len) P <<= 1;
     for (u32 i = threadIdx.x; i < P; i += blockDim.x) {
-      sk[i] = i < len ? k[a + i] : ~0ull;
-      sv[i] = i < len ? v[a + i] : ~0ull;
+      if (i < g.len) {
+        sk[i] = k[g.start + i];
+        sv[i] = v[g.start + i];
+        sc[i] = canon_k(region, sk[i]);
+      } else {
+        sk[i] = sv[i] = sc[i] = ~0ull;
+      }
     }
     __syncthreads();
     for (u32 size = 2; size <= P; size <<= 1) {
@@ -349,19 +417,20 @@ __global__ __launch_bounds__(256) void k_tie_fix(u64* __restrict__ k, u64* __res
           const u32 jx = i ^ stride;
           if (jx > i) {
             const bool up = (i & size) == 0;
-            const bool gt = sv[i] > sv[jx] || (sv[i] == sv[jx] && sk[i] > sk[jx]);
+            const bool gt = sc[i] > sc[jx] || (sc[i] == sc[jx] && sv[i] > sv[jx]);
             if (gt == up) {
-              const u64 tk = sk[i]; sk[i] = sk[jx]; sk[jx] = tk;
-              const u64 tv = sv[i]; sv[i] = sv[jx]; sv[jx] = tv;
+              u64 t = sk[i]; sk[i] = sk[jx]; sk[jx] = t;
+              t = sv[i]; sv[i] = sv[jx]; sv[jx] = t;
+              t = sc[i]; sc[i] = sc[jx]; sc[jx] = t;
             }
           }
         }
         __syncthreads();
       }
     }
-    for (u32 i = threadIdx.x; i < len; i += blockDim.x) {
-      k[a + i] = sk[i];
-      v[a + i] = sv[i];
+    for (u32 i = threadIdx.x; i < g.len; i += blockDim.x) {
+      k[g.start + i] = sk[i];
+      v[g.start + i] = sv[i];
     }
     __syncthreads();
   }
@@ -370,29 +439,47 @@ __global__ __launch_bounds__(256) void k_tie_fix(u64* __restrict__ k, u64* __res
 // ------------------------------------------------------------------ launchers
 
 void launch_hist(const u64* kin, const u64* vin, const SegDesc* segs, int nseg, u32 total_tiles,
-                 int from_v, int use_src, u32* hist, cudaStream_t st) {
+                 int mode, int npasses, int use_src, u32* hist, cudaStream_t st) {
   if (total_tiles == 0) return;
   const int blocks = (int)min(total_tiles, 148u * 4u);
-  k_hist<<<blocks, kHistThreads, 0, st>>>(kin, vin, segs, nseg, total_tiles, from_v, use_src, hist);
+  switch (mode) {
+    case kDigitQ:
+      k_hist<kDigitQ><<<blocks, kHistThreads, 0, st>>>(kin, vin, segs, nseg, total_tiles, npasses,
+                                                       use_src, hist);
+      break;
+    case kDigitV:
+      k_hist<kDigitV><<<blocks, kHistThreads, 0, st>>>(kin, vin, segs, nseg, total_tiles, npasses,
+                                                       use_src, hist);
+      break;
+    default:
+      k_hist<kDigitK><<<blocks, kHistThreads, 0, st>>>(kin, vin, segs, nseg, total_tiles, npasses,
+                                                       use_src, hist);
+  }
 }
 
-void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, u32* digit_excl,
+void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, int npasses, u32* digit_excl,
                       u32* needed_mask, cudaStream_t st) {
   if (nseg == 0) return;
-  k_hist_scan<<<nseg * kPasses, kDigits, 0, st>>>(hist, segs, digit_excl, needed_mask);
+  k_hist_scan<<<nseg * kPasses, kDigits, 0, st>>>(hist, segs, npasses, digit_excl, needed_mask);
 }
 
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
-                     int nseg, u32 total_tiles, int use_src, int from_v, const u32* digit_excl,
+                     int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
                      int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st) {
   if (total_tiles == 0) return;
-  if (from_v)
-    k_onesweep<true><<<total_tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, segs, nseg, use_src,
-                                                           digit_excl, pass, status, tag, tile_ctr);
-  else
-    k_onesweep<false><<<total_tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, segs, nseg,
-                                                            use_src, digit_excl, pass, status, tag,
-                                                            tile_ctr);
+  switch (mode) {
+    case kDigitQ:
+      k_onesweep<kDigitQ><<<total_tiles, kSortThreads, 0, st>>>(
+          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      break;
+    case kDigitV:
+      k_onesweep<kDigitV><<<total_tiles, kSortThreads, 0, st>>>(
+          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      break;
+    default:
+      k_onesweep<kDigitK><<<total_tiles, kSortThreads, 0, st>>>(
+          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+  }
 }
 
 void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
@@ -401,19 +488,28 @@ void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const
   k_seg_copy<<<total_tiles, 256, 0, st>>>(kin, vin, kout, vout, segs, nseg, use_src);
 }
 
-void launch_tie_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, u64* starts,
-                       u32* nstarts, u32 cap, cudaStream_t st) {
+void launch_group_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
+                         u64* starts, u32* nstarts, u32 cap, cudaStream_t st) {
   if (total_tiles == 0) return;
-  k_tie_detect<<<total_tiles, 256, 0, st>>>(k, segs, nseg, starts, nstarts, cap);
+  k_group_detect<<<total_tiles, 256, 0, st>>>(k, segs, nseg, eqmode, starts, nstarts, cap);
 }
 
-void launch_tie_fix(u64* k, u64* v, const SegDesc* segs, const u64* starts, u32 nstarts,
-                    void* long_runs, u32* nlong, cudaStream_t st) {
+void launch_group_fix_small(u64* k, u64* v, const SegDesc* segs, int eqmode, const u64* starts,
+                            u32 nstarts, void* medium, u32* nmedium, cudaStream_t st) {
   if (nstarts == 0) return;
-  const u32 blocks = nstarts < 148u * 8u ? nstarts : 148u * 8u;
-  k_tie_fix<<<blocks, 256, 0, st>>>(k, v, segs, starts, nstarts, (TieRun*)long_runs, nlong);
+  const u32 blocks = min((nstarts + 127) / 128, 148u * 16u);
+  k_group_fix_small<<<blocks, 128, 0, st>>>(k, v, segs, eqmode, starts, nstarts,
+                                            (GroupRun*)medium, nmedium);
 }
 
-size_t tie_run_record_bytes() { return sizeof(TieRun); }
+void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium, u32 nmedium,
+                             void* longr, u32* nlong, cudaStream_t st) {
+  if (nmedium == 0) return;
+  const u32 blocks = min(nmedium, 148u * 4u);
+  k_group_fix_medium<<<blocks, 256, 0, st>>>(k, v, segs, (const GroupRun*)medium, nmedium,
+                                             (GroupRun*)longr, nlong);
+}
+
+size_t group_run_bytes() { return sizeof(GroupRun); }
 
 }  // namespace chgpu

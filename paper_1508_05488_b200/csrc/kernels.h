@@ -32,19 +32,21 @@ void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             cudaStream_t st);
 // K3
 void launch_hist(const u64* kin, const u64* vin, const SegDesc* segs, int nseg, u32 total_tiles,
-                 int from_v, int use_src, u32* hist, cudaStream_t st);
-void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, u32* digit_excl,
+                 int mode, int npasses, int use_src, u32* hist, cudaStream_t st);
+void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, int npasses, u32* digit_excl,
                       u32* needed_mask, cudaStream_t st);
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
-                     int nseg, u32 total_tiles, int use_src, int from_v, const u32* digit_excl,
+                     int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
                      int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st);
 void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, cudaStream_t st);
-void launch_tie_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, u64* starts,
-                       u32* nstarts, u32 cap, cudaStream_t st);
-void launch_tie_fix(u64* k, u64* v, const SegDesc* segs, const u64* starts, u32 nstarts,
-                    void* long_runs, u32* nlong, cudaStream_t st);
-size_t tie_run_record_bytes();
+void launch_group_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
+                         u64* starts, u32* nstarts, u32 cap, cudaStream_t st);
+void launch_group_fix_small(u64* k, u64* v, const SegDesc* segs, int eqmode, const u64* starts,
+                            u32 nstarts, void* medium, u32* nmedium, cudaStream_t st);
+void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium, u32 nmedium,
+                             void* longr, u32* nlong, cudaStream_t st);
+size_t group_run_bytes();
 // K4/K5
 void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
                 double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,

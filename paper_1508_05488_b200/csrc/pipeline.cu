@@ -2,16 +2,17 @@
 //
 // Mirrors convex_hull (reference pipeline.cpp:25-106) stage for stage:
 //   K1 extremes -> frame -> K2 classify+discard -> [degenerate branch]
-//   -> K3 region sort (+ tie runs) -> K4/K5 SPA + chain compaction
-//   -> D2H chains -> host assemble + Melkman (finisher.cpp).
+//   -> K3 region sort (bucket passes + group fix-up) -> K4/K5 SPA + chain
+//   compaction -> D2H chains -> host assemble + Melkman (finisher.cpp).
 // Host syncs happen only where the host must size the next launch: after
 // K2 (region counts), after the histogram (which digit passes move data),
-// after the tie scan, and after the SPA (how many chain points to copy).
+// after the group scan, and after the SPA (how many chain points to copy).
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,21 +30,7 @@ namespace {
 constexpr int kMaxPartials = 148 * 8 * 16;
 constexpr int kPartialBlocks = 148 * 8;
 constexpr size_t kH2DChunk = size_t(1) << 21;  // points per staged copy (32 MB)
-
-// Counter slots (u32) cleared once per call.
-enum Ctr : int {
-  kCtrK2 = 0,
-  kCtrPass = 1,       // 8 slots: region sort passes
-  kCtrLongPass = 9,   // 8 slots: tie-run passes
-  kCtrSpa = 17,
-  kCtrUnique = 18,
-  kCtrMask = 19,
-  kCtrMaskLong = 20,
-  kCtrNStarts = 21,
-  kCtrNLong = 22,
-  kCtrCounts = 24,    // 5 slots: K2 stream counts
-  kCtrSlots = 64
-};
+constexpr int kCtrSlots = 256;                 // u32 counters, cleared once per call
 
 struct Pinned {
   QuadInfo qi;
@@ -75,15 +62,17 @@ struct chgpu_ctx {
   u64* d_va = nullptr;          // cap
   unsigned char* d_flags = nullptr;  // cap
   double2* d_kept = nullptr;    // cap
-  u64* d_status = nullptr;      // status words
+  u64* d_status = nullptr;      // look-back status words
   size_t status_words = 0;
-  u64* d_tie_starts = nullptr;  // cap/2+16
-  void* d_long_runs = nullptr;  // cap/2049+16 records
+  u64* d_starts = nullptr;      // group starts (cap/2+16)
+  void* d_medium = nullptr;     // medium groups (cap/2+16)
+  void* d_long = nullptr;       // long groups (cap/2049+16)
 
   QuadCand* d_partials = nullptr;
   QuadInfo* d_qinfo = nullptr;
   QuadCand* d_rawquad = nullptr;
   u32* d_ctr = nullptr;
+  int ctr_used = 0;
   unsigned long long* d_u64 = nullptr;  // [0..3] kept counts, [4] unique total, [5..9] label counts
   u32* d_hist = nullptr;
   u32* d_digit_excl = nullptr;
@@ -109,18 +98,29 @@ u32 next_tag(chgpu_ctx* c) {
   return c->tag;
 }
 
-#define CK(call)                                                          \
-  do {                                                                    \
-    cudaError_t e_ = (call);                                              \
-    if (e_ != cudaSuccess) {                                              \
-      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);      \
-      return CHGPU_CUDA_ERR;                                              \
-    }                                                                     \
+#define CK(call)                                                     \
+  do {                                                               \
+    cudaError_t e_ = (call);                                         \
+    if (e_ != cudaSuccess) {                                         \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return CHGPU_CUDA_ERR;                                         \
+    }                                                                \
+  } while (0)
+
+#define TRY(expr)               \
+  do {                          \
+    if (int e_ = (expr)) return e_; \
   } while (0)
 
 int fail(chgpu_ctx* ctx, int code, const char* msg) {
   ctx->err = msg;
   return code;
+}
+
+// A fresh zeroed device counter for this call.
+int take_ctr(chgpu_ctx* ctx) {
+  if (ctx->ctr_used >= kCtrSlots) return kCtrSlots - 1;  // never reached for sane inputs
+  return ctx->ctr_used++;
 }
 
 void free_ws(chgpu_ctx* c) {
@@ -132,15 +132,16 @@ void free_ws(chgpu_ctx* c) {
   cudaFree(c->d_flags);
   cudaFree(c->d_kept);
   cudaFree(c->d_status);
-  cudaFree(c->d_tie_starts);
-  cudaFree(c->d_long_runs);
+  cudaFree(c->d_starts);
+  cudaFree(c->d_medium);
+  cudaFree(c->d_long);
   c->d_pts = nullptr;
   c->d_kbuf = c->d_vbuf = c->d_ka = c->d_va = nullptr;
   c->d_flags = nullptr;
   c->d_kept = nullptr;
   c->d_status = nullptr;
-  c->d_tie_starts = nullptr;
-  c->d_long_runs = nullptr;
+  c->d_starts = nullptr;
+  c->d_medium = c->d_long = nullptr;
   c->cap = 0;
 }
 
@@ -187,14 +188,24 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
   ctx->status_words = std::max(cap + 4096, (cap / kSortTile + 4096) * (size_t)kDigits);
   CK(cudaMalloc(&ctx->d_status, ctx->status_words * sizeof(u64)));
   CK(cudaMemset(ctx->d_status, 0, ctx->status_words * sizeof(u64)));
-  CK(cudaMalloc(&ctx->d_tie_starts, (cap / 2 + 16) * sizeof(u64)));
-  CK(cudaMalloc(&ctx->d_long_runs, (cap / 2049 + 16) * tie_run_record_bytes()));
+  CK(cudaMalloc(&ctx->d_starts, (cap / 2 + 16) * sizeof(u64)));
+  CK(cudaMalloc(&ctx->d_medium, (cap / 2 + 16) * group_run_bytes()));
+  CK(cudaMalloc(&ctx->d_long, (cap / 2049 + 16) * group_run_bytes()));
   ctx->cap = cap;
   return CHGPU_OK;
 }
 
 int sync(chgpu_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->st));
+  return CHGPU_OK;
+}
+
+// Reads one device counter (synchronising the stream).
+int read_ctr(chgpu_ctx* ctx, int slot, u32* out) {
+  CK(cudaMemcpyAsync(&ctx->h->ctr[slot], ctx->d_ctr + slot, sizeof(u32), cudaMemcpyDeviceToHost,
+                     ctx->st));
+  TRY(sync(ctx));
+  *out = ctx->h->ctr[slot];
   return CHGPU_OK;
 }
 
@@ -208,40 +219,70 @@ u32 plan_tiles(SegDesc* segs, int nseg) {
   return t;
 }
 
-// Segmented LSD radix sort of (k, v) records.
-// First executed pass reads (ksrc, vsrc) at src_off; passes alternate
-// between (kA, vA) and (kB, vB) at dst_off. *in_a reports where the result
-// landed. from_v selects v as the key (tie runs), k riding along.
+SegDesc make_seg(u64 src, u64 dst, u64 len, int region) {
+  SegDesc s{};
+  s.src_off = src;
+  s.dst_off = dst;
+  s.len = (u32)len;
+  s.region = region;
+  return s;
+}
+
+// Quantizer over the primary range [lo, hi] of a region (chgpu_internal.cuh).
+void set_quantizer(SegDesc& s, double lo, double hi, int bits) {
+  s.qbits = bits;
+  s.qmax = std::ldexp(1.0, bits) - 1.0;
+  s.qlo = lo;
+  const double span = hi - lo;
+  double scale = (span > 0.0) ? s.qmax / span : 0.0;
+  if (!std::isfinite(scale)) scale = 0.0;
+  s.qscale = scale;
+}
+
+// Primary range of each region between its anchors (exact arithmetic puts
+// every region survivor inside it; rounding stragglers clamp).
+void region_range(const double* q, int region, double* lo, double* hi) {
+  switch (region) {
+    case 1: *lo = q[0]; *hi = q[2]; break;  // LL: x in [left.x, bottom.x]
+    case 2: *lo = q[3]; *hi = q[5]; break;  // LR: y in [bottom.y, right.y]
+    case 3: *lo = q[6]; *hi = q[4]; break;  // UR: x in [top.x, right.x]
+    case 4: *lo = q[1]; *hi = q[7]; break;  // UL: y in [left.y, top.y]
+    default: *lo = q[0]; *hi = q[4]; break; // LEX: x in [left.x, right.x]
+  }
+}
+
+// Segmented LSD radix sort of (k, v) records over the segments in
+// ctx->h_segs. The first executed pass reads (ksrc, vsrc) at src_off;
+// passes alternate between (kA, vA) and (kB, vB) at dst_off. *in_a tells
+// where the result landed.
 int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* kA, u64* vA,
-               u64* kB, u64* vB, int from_v, int ctr_base, int mask_slot, bool* in_a,
-               int* passes_run, bool timed = false) {
+               u64* kB, u64* vB, int mode, int npasses, bool* in_a, int* passes_run,
+               bool timed = false) {
   const u32 tiles = plan_tiles(ctx->h_segs, nseg);
   *passes_run = 0;
   *in_a = true;
   if (tiles == 0) return CHGPU_OK;
+  const int mask_slot = take_ctr(ctx);
   CK(cudaMemcpyAsync(ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc), cudaMemcpyHostToDevice,
                      ctx->st));
   CK(cudaMemsetAsync(ctx->d_hist, 0, (size_t)nseg * kPasses * kDigits * sizeof(u32), ctx->st));
-  launch_hist(ksrc, vsrc, ctx->d_segs, nseg, tiles, from_v, 1, ctx->d_hist, ctx->st);
-  launch_hist_scan(ctx->d_hist, ctx->d_segs, nseg, ctx->d_digit_excl, ctx->d_ctr + mask_slot,
-                   ctx->st);
+  launch_hist(ksrc, vsrc, ctx->d_segs, nseg, tiles, mode, npasses, 1, ctx->d_hist, ctx->st);
+  launch_hist_scan(ctx->d_hist, ctx->d_segs, nseg, npasses, ctx->d_digit_excl,
+                   ctx->d_ctr + mask_slot, ctx->st);
   ctx->launches += 2;
   if (timed) CK(cudaEventRecord(ctx->ev[3], ctx->st));
-  CK(cudaMemcpyAsync(&ctx->h->ctr[mask_slot], ctx->d_ctr + mask_slot, sizeof(u32),
-                     cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
-  const u32 mask = ctx->h->ctr[mask_slot];
+  u32 mask = 0;
+  TRY(read_ctr(ctx, mask_slot, &mask));
   const u64* kin = ksrc;
   const u64* vin = vsrc;
   int use_src = 1, done = 0;
   if (timed) CK(cudaEventRecord(ctx->ev[4], ctx->st));
-  for (int p = 0; p < kPasses; ++p) {
+  for (int p = 0; p < npasses; ++p) {
     if (!(mask & (1u << p))) continue;
     u64* ko = (done % 2 == 0) ? kA : kB;
     u64* vo = (done % 2 == 0) ? vA : vB;
-    launch_onesweep(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, from_v,
-                    ctx->d_digit_excl, p, ctx->d_status, next_tag(ctx), ctx->d_ctr + ctr_base + p,
-                    ctx->st);
+    launch_onesweep(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode, ctx->d_digit_excl,
+                    p, ctx->d_status, next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->st);
     kin = ko;
     vin = vo;
     use_src = 0;
@@ -263,65 +304,189 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
   return CHGPU_OK;
 }
 
-// Orders every equal-primary run of the sorted region layout by v.
-int fix_ties(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, size_t* nruns) {
+struct Run {
+  u64 start;
+  u32 len;
+  int seg;
+};
+
+// Orders every group of the sorted layout (segments in ctx->h_segs, at
+// dst_off of (kF, vF)) by (canon k, v), in place. eqmode kEqQ: groups of
+// equal quantized primary; kEqPrim: groups of ==-equal primary.
+int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int eqmode,
+               size_t* ngroups, int depth = 0) {
   const u32 tiles = plan_tiles(ctx->h_segs, nseg);
-  *nruns = 0;
   if (tiles == 0) return CHGPU_OK;
   const u32 cap = (u32)(ctx->cap / 2 + 16);
+  const int s_starts = take_ctr(ctx), s_medium = take_ctr(ctx), s_long = take_ctr(ctx);
   CK(cudaMemcpyAsync(ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc), cudaMemcpyHostToDevice,
                      ctx->st));
-  launch_tie_detect(kF, ctx->d_segs, nseg, tiles, ctx->d_tie_starts, ctx->d_ctr + kCtrNStarts, cap,
-                    ctx->st);
+  launch_group_detect(kF, ctx->d_segs, nseg, tiles, eqmode, ctx->d_starts, ctx->d_ctr + s_starts,
+                      cap, ctx->st);
   ++ctx->launches;
-  CK(cudaMemcpyAsync(&ctx->h->ctr[kCtrNStarts], ctx->d_ctr + kCtrNStarts, sizeof(u32),
-                     cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
-  const u32 nstarts = std::min(ctx->h->ctr[kCtrNStarts], cap);
-  *nruns = nstarts;
+  u32 nstarts = 0;
+  TRY(read_ctr(ctx, s_starts, &nstarts));
+  nstarts = std::min(nstarts, cap);
+  if (ngroups) *ngroups += nstarts;
   if (nstarts == 0) return CHGPU_OK;
-  launch_tie_fix(kF, vF, ctx->d_segs, ctx->d_tie_starts, nstarts, ctx->d_long_runs,
-                 ctx->d_ctr + kCtrNLong, ctx->st);
+  launch_group_fix_small(kF, vF, ctx->d_segs, eqmode, ctx->d_starts, nstarts, ctx->d_medium,
+                         ctx->d_ctr + s_medium, ctx->st);
   ++ctx->launches;
-  CK(cudaMemcpyAsync(&ctx->h->ctr[kCtrNLong], ctx->d_ctr + kCtrNLong, sizeof(u32),
-                     cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
-  const u32 nlong = ctx->h->ctr[kCtrNLong];
+  u32 nmedium = 0;
+  TRY(read_ctr(ctx, s_medium, &nmedium));
+  if (nmedium == 0) return CHGPU_OK;
+  launch_group_fix_medium(kF, vF, ctx->d_segs, ctx->d_medium, nmedium, ctx->d_long,
+                          ctx->d_ctr + s_long, ctx->st);
+  ++ctx->launches;
+  u32 nlong = 0;
+  TRY(read_ctr(ctx, s_long, &nlong));
   if (nlong == 0) return CHGPU_OK;
 
-  // Long runs: sort each by v with the onesweep engine, in place.
-  struct Run {
-    u64 start;
-    u32 len;
-    int region;
-  };
+  // Long groups: full sort of each group with the onesweep engine.
   std::vector<Run> runs(nlong);
-  CK(cudaMemcpyAsync(runs.data(), ctx->d_long_runs, nlong * sizeof(Run), cudaMemcpyDeviceToHost,
+  CK(cudaMemcpyAsync(runs.data(), ctx->d_long, nlong * sizeof(Run), cudaMemcpyDeviceToHost,
                      ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
+  std::vector<int> regions(nseg);
+  for (int s = 0; s < nseg; ++s) regions[s] = ctx->h_segs[s].region;
   std::sort(runs.begin(), runs.end(), [](const Run& a, const Run& b) { return a.start < b.start; });
-  if (int e = ensure_segs(ctx, nlong)) return e;
-  for (u32 i = 0; i < nlong; ++i) {
-    ctx->h_segs[i] = SegDesc{runs[i].start, runs[i].start, runs[i].len, 0, runs[i].region, 0};
-  }
+  TRY(ensure_segs(ctx, nlong));
+  for (u32 i = 0; i < nlong; ++i)
+    ctx->h_segs[i] = make_seg(runs[i].start, runs[i].start, runs[i].len, regions[runs[i].seg]);
   bool in_a = true;
   int passes = 0;
   // A = scratch, B = F: an even pass count ends back in F.
-  if (int e = radix_sort(ctx, (int)nlong, kF, vF, kS, vS, kF, vF, 1, kCtrLongPass, kCtrMaskLong,
-                         &in_a, &passes))
-    return e;
+  const int mode = (eqmode == kEqQ) ? kDigitK : kDigitV;
+  TRY(radix_sort(ctx, (int)nlong, kF, vF, kS, vS, kF, vF, mode, kPasses, &in_a, &passes));
   if (passes % 2 == 1) {
-    const u32 tiles2 = plan_tiles(ctx->h_segs, (int)nlong);
-    launch_seg_copy(kS, vS, kF, vF, ctx->d_segs, (int)nlong, tiles2, 0, ctx->st);
+    const u32 t2 = plan_tiles(ctx->h_segs, (int)nlong);
+    launch_seg_copy(kS, vS, kF, vF, ctx->d_segs, (int)nlong, t2, 0, ctx->st);
     ++ctx->launches;
   }
   CK(cudaGetLastError());
+  // After a full sort on k, ==-equal primaries still need their v order.
+  if (eqmode == kEqQ && depth == 0) {
+    for (u32 i = 0; i < nlong; ++i)
+      ctx->h_segs[i] = make_seg(runs[i].start, runs[i].start, runs[i].len, regions[runs[i].seg]);
+    TRY(fix_groups(ctx, (int)nlong, kF, vF, kS, vS, kEqPrim, nullptr, depth + 1));
+  }
   return CHGPU_OK;
 }
 
-// Core of chgpu_hull / chgpu_hull_device. pts_dev must already hold the
-// input unless h_src != nullptr (then the copy is staged here, overlapped
-// with K1 on a second stream).
+// Sorts the nseg segments in ctx->h_segs (src layout in kbuf/vbuf) into
+// region order. Bucket phase keyed on the quantized primary when qbits > 0,
+// else a full LSD on k; then the in-place group fix-up.
+struct Sorted {
+  u64 *kF, *vF, *kS, *vS;
+  int passes;
+  size_t groups;
+};
+
+int sort_segments(chgpu_ctx* ctx, int nseg, int qbits, bool timed, Sorted* out) {
+  std::vector<SegDesc> segs(ctx->h_segs, ctx->h_segs + nseg);
+  bool in_a = true;
+  int passes = 0;
+  const int mode = qbits ? kDigitQ : kDigitK;
+  const int npasses = qbits ? qbits / 8 : kPasses;
+  TRY(radix_sort(ctx, nseg, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
+                 ctx->d_vbuf, mode, npasses, &in_a, &passes, timed));
+  out->kF = in_a ? ctx->d_ka : ctx->d_kbuf;
+  out->vF = in_a ? ctx->d_va : ctx->d_vbuf;
+  out->kS = in_a ? ctx->d_kbuf : ctx->d_ka;
+  out->vS = in_a ? ctx->d_vbuf : ctx->d_va;
+  out->passes = passes;
+  out->groups = 0;
+  for (int s = 0; s < nseg; ++s) {
+    ctx->h_segs[s] = segs[s];
+    ctx->h_segs[s].src_off = segs[s].dst_off;
+  }
+  TRY(fix_groups(ctx, nseg, out->kF, out->vF, out->kS, out->vS, qbits ? kEqQ : kEqPrim,
+                 &out->groups));
+  return CHGPU_OK;
+}
+
+// Region segments of the K2 two-ended layout, with quantizers.
+int plan_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, int* qbits) {
+  TRY(ensure_segs(ctx, 4));
+  const u64 cap = ctx->cap;
+  const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
+  const u64 mmax = std::max(std::max(m[0], m[1]), std::max(m[2], m[3]));
+  *qbits = mmax <= (u64(1) << 22) ? 24 : 32;
+  u64 dst = 0;
+  for (int s = 0; s < 4; ++s) {
+    ctx->h_segs[s] = make_seg(src_off[s], dst, m[s], s + 1);
+    double lo, hi;
+    region_range(quad, s + 1, &lo, &hi);
+    set_quantizer(ctx->h_segs[s], lo, hi, *qbits);
+    dst += m[s];
+  }
+  return CHGPU_OK;
+}
+
+SpaPlan make_spa_plan(const u64 m[4], size_t chunk_count, const double* quad) {
+  SpaPlan plan{};
+  u32 chunks = 0;
+  u64 off = 0;
+  for (int r = 0; r < 4; ++r) {
+    plan.off[r] = off;
+    plan.m[r] = m[r];
+    plan.chunk_begin[r] = chunks;
+    const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;  // spa.cpp:121
+    plan.chunk_size[r] = cs;
+    if (m[r]) chunks += (u32)((m[r] + cs - 1) / cs);                   // spa.cpp:122
+    off += m[r];
+    // guarded(region, anchors.first): LL left.y, LR bottom.x, UR right.y, UL top.x
+    plan.seed[r] = (r == 0 || r == 2) ? quad[2 * r + 1] : quad[2 * r];
+  }
+  plan.total_chunks = chunks;
+  return plan;
+}
+
+// Degenerate-branch survivors: one LEX segment, sorted, unique-compacted
+// into d_kept; returns the unique count.
+int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* nuniq, int* passes,
+                            size_t* groups) {
+  TRY(ensure_segs(ctx, 1));
+  ctx->h_segs[0] = make_seg(0, 0, s1, 0);
+  double lo, hi;
+  region_range(quad, 0, &lo, &hi);
+  const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
+  set_quantizer(ctx->h_segs[0], lo, hi, qbits);
+  Sorted so{};
+  TRY(sort_segments(ctx, 1, qbits, false, &so));
+  *passes = so.passes;
+  *groups = so.groups;
+  const int slot = take_ctr(ctx);
+  launch_unique(so.kF, so.vF, s1, ctx->d_kept, ctx->d_status, next_tag(ctx), ctx->d_ctr + slot,
+                ctx->d_u64 + 4, ctx->st);
+  if (s1) ++ctx->launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 4, sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, ctx->st));
+  TRY(sync(ctx));
+  *nuniq = (size_t)ctx->h->uniq;
+  return CHGPU_OK;
+}
+
+void frame_of(const double* quad, Pt* fr, int* nf) {
+  *nf = 0;
+  for (int c = 0; c < 4; ++c) {
+    const Pt p{quad[2 * c], quad[2 * c + 1]};
+    if (*nf == 0 || !(fr[*nf - 1].x == p.x && fr[*nf - 1].y == p.y)) fr[(*nf)++] = p;
+  }
+  if (*nf > 1 && fr[0].x == fr[*nf - 1].x && fr[0].y == fr[*nf - 1].y) --*nf;
+}
+
+int begin_call(chgpu_ctx* ctx) {
+  ctx->launches = 0;
+  ctx->ctr_used = 0;
+  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
+  CK(cudaMemsetAsync(ctx->d_u64, 0, 16 * sizeof(unsigned long long), ctx->st));
+  return CHGPU_OK;
+}
+
+// Core of chgpu_hull / chgpu_hull_device. h_src != nullptr: the input is on
+// the host and is staged in chunks on a copy stream, overlapped with K1.
 int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, size_t n,
                  size_t chunk_count, int fallback, const double** hull_xy, size_t* n_hull,
                  chgpu_stats* stats, chgpu_diag* diag) {
@@ -330,13 +495,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   chgpu_diag D{};
   S.n_input = n;
   cudaStream_t st = ctx->st;
-  ctx->launches = 0;
-
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), st));
-  CK(cudaMemsetAsync(ctx->d_u64, 0, 16 * sizeof(unsigned long long), st));
+  TRY(begin_call(ctx));
   CK(cudaEventRecord(ctx->ev[0], st));
 
-  // ---- K1: extremes (extremes.cpp:28-47), overlapped with the H2D copy.
+  // ---- K1: extremes (extremes.cpp:28-47).
   int nparts = 0;
   if (h_src) {
     const size_t nchunks = (n + kH2DChunk - 1) / kH2DChunk;
@@ -370,27 +532,28 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   const double2* pts = h_src ? ctx->d_pts : pts_dev;
   launch_extremes_final(ctx->d_partials, nparts, ctx->d_qinfo, nullptr, st);
   CK(cudaEventRecord(ctx->ev[1], st));
-  ctx->launches += 2;  // final + K2 below
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87).
+  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  ctx->ctr_used += 5;
   launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
-                          ctx->cap, ctx->d_status, next_tag(ctx), ctx->d_ctr + kCtrK2,
-                          ctx->d_ctr + kCtrCounts, st);
+                          ctx->cap, ctx->d_status, next_tag(ctx), ctx->d_ctr + k2_slot,
+                          ctx->d_ctr + cnt_slot, st);
+  ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ctx->h->ctr[kCtrCounts], ctx->d_ctr + kCtrCounts, 5 * sizeof(u32),
+  CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
 
   const QuadInfo qi = ctx->h->qi;
   u64 m[4];
-  for (int s = 0; s < 4; ++s) m[s] = ctx->h->ctr[kCtrCounts + 1 + s];
+  for (int s = 0; s < 4; ++s) m[s] = ctx->h->ctr[cnt_slot + 1 + s];
   const u64 s1 = m[0] + m[1] + m[2] + m[3];
   std::memcpy(D.quad, qi.q, sizeof D.quad);
   D.frame_size = qi.frame_size;
   S.n_after_round1 = s1 + qi.frame_size;  // pipeline.cpp:51
-
   const Pt* corners = reinterpret_cast<const Pt*>(qi.q);
   double t_sort_ms = 0, t_spa_ms = 0;
   auto t_fin0 = std::chrono::steady_clock::now();
@@ -403,105 +566,45 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     if (!fallback) return fail(ctx, CHGPU_DEGENERATE, "convex_hull: degenerate extreme quadrilateral");
     S.n_after_spa = S.n_after_round1;
     // GPU lexicographic sort + unique of the survivors (oracle.cpp:16-17).
-    if (int e = ensure_segs(ctx, 1)) return e;
-    ctx->h_segs[0] = SegDesc{0, 0, (u32)s1, 0, 0, 0};
-    bool in_a = true;
-    int passes = 0;
-    if (int e = radix_sort(ctx, 1, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                           ctx->d_vbuf, 0, kCtrPass, kCtrMask, &in_a, &passes))
-      return e;
-    D.sort_passes = passes;
-    u64* kF = in_a ? ctx->d_ka : ctx->d_kbuf;
-    u64* vF = in_a ? ctx->d_va : ctx->d_vbuf;
-    u64* kS = in_a ? ctx->d_kbuf : ctx->d_ka;
-    u64* vS = in_a ? ctx->d_vbuf : ctx->d_va;
-    ctx->h_segs[0] = SegDesc{0, 0, (u32)s1, 0, 0, 0};
-    if (int e = fix_ties(ctx, 1, kF, vF, kS, vS, &D.tie_runs)) return e;
-    ++ctx->launches;
-    launch_unique(kF, vF, s1, ctx->d_kept, ctx->d_status, next_tag(ctx), ctx->d_ctr + kCtrUnique,
-                  ctx->d_u64 + 4, st);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 4, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    if (int e = sync(ctx)) return e;
-    const size_t nu = (size_t)ctx->h->uniq;
-    if (int e = ensure_host_out(ctx, nu + 4)) return e;
+    size_t nu = 0;
+    TRY(sorted_unique_survivors(ctx, s1, qi.q, &nu, &D.sort_passes, &D.tie_runs));
+    TRY(ensure_host_out(ctx, nu + 4));
     CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, nu * sizeof(double2), cudaMemcpyDeviceToHost, st));
-    if (int e = sync(ctx)) return e;
+    TRY(sync(ctx));
     t_fin0 = std::chrono::steady_clock::now();
     const Pt* up = reinterpret_cast<const Pt*>(ctx->h_out);
     ctx->chains.assign(up, up + nu);
     // frame_vertices(quad) joins the survivors (pipeline.cpp:63-64).
     Pt fr[4];
     int nf = 0;
-    for (int c = 0; c < 4; ++c) {
-      const Pt p = corners[c];
-      if (nf == 0 || !(fr[nf - 1].x == p.x && fr[nf - 1].y == p.y)) fr[nf++] = p;
-    }
-    if (nf > 1 && fr[0].x == fr[nf - 1].x && fr[0].y == fr[nf - 1].y) --nf;
+    frame_of(qi.q, fr, &nf);
     for (int f = 0; f < nf; ++f) chgpu::host::insert_sorted_unique(ctx->chains, fr[f]);
     chgpu::host::monotone_chain(ctx->chains.data(), ctx->chains.size(), ctx->hull);
   } else {
     for (int s = 0; s < 4; ++s) D.region_counts[s + 1] = m[s];
     D.region_counts[0] = n - s1;
     // ---- K3: region sort (spa.cpp:59-81).
-    if (int e = ensure_segs(ctx, 4)) return e;
-    const u64 cap = ctx->cap;
-    const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
-    u64 dst = 0;
-    for (int s = 0; s < 4; ++s) {
-      ctx->h_segs[s] = SegDesc{src_off[s], dst, (u32)m[s], 0, s + 1, 0};
-      dst += m[s];
-    }
-    bool in_a = true;
-    int passes = 0;
-    if (int e = radix_sort(ctx, 4, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                           ctx->d_vbuf, 0, kCtrPass, kCtrMask, &in_a, &passes, true))
-      return e;
-    D.sort_passes = passes;
-    const bool sort_timed = plan_tiles(ctx->h_segs, 4) > 0;
-    u64* kF = in_a ? ctx->d_ka : ctx->d_kbuf;
-    u64* vF = in_a ? ctx->d_va : ctx->d_vbuf;
-    u64* kS = in_a ? ctx->d_kbuf : ctx->d_ka;
-    u64* vS = in_a ? ctx->d_vbuf : ctx->d_va;
-    dst = 0;
-    for (int s = 0; s < 4; ++s) {
-      ctx->h_segs[s] = SegDesc{dst, dst, (u32)m[s], 0, s + 1, 0};
-      dst += m[s];
-    }
-    if (int e = fix_ties(ctx, 4, kF, vF, kS, vS, &D.tie_runs)) return e;
+    int qbits = 0;
+    TRY(plan_regions(ctx, m, qi.q, &qbits));
+    Sorted so{};
+    TRY(sort_segments(ctx, 4, qbits, true, &so));
+    D.sort_passes = so.passes;
+    D.tie_runs = so.groups;
+    const bool sort_timed = s1 > 0;
     CK(cudaEventRecord(ctx->ev[6], st));
 
     // ---- K4/K5: SPA (spa.cpp:109-163). chunk_count == 0 raises here, on
     // the non-degenerate branch only, exactly like the reference.
     if (chunk_count == 0) return fail(ctx, CHGPU_INVALID_ARG, "spa_filter: chunk_count must be >= 1");
-    SpaPlan plan{};
-    u32 chunks = 0;
-    u64 off = 0;
-    for (int r = 0; r < 4; ++r) {
-      plan.off[r] = off;
-      plan.m[r] = m[r];
-      plan.chunk_begin[r] = chunks;
-      if (m[r]) {
-        const u64 cs = (m[r] + chunk_count - 1) / chunk_count;
-        plan.chunk_size[r] = cs;
-        chunks += (u32)((m[r] + cs - 1) / cs);
-      } else {
-        plan.chunk_size[r] = 1;
-      }
-      off += m[r];
-      // guarded(region, anchors.first): LL left.y, LR bottom.x, UR right.y, UL top.x
-      plan.seed[r] = (r == 0 || r == 2) ? qi.q[2 * r + 1] : qi.q[2 * r];
-    }
-    plan.total_chunks = chunks;
-    launch_spa(kF, vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status, next_tag(ctx),
-               ctx->d_ctr + kCtrSpa, st);
+    const SpaPlan plan = make_spa_plan(m, chunk_count, qi.q);
+    launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
+               next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
     if (plan.total_chunks) ++ctx->launches;
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[8], st));
     CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
-    if (int e = sync(ctx)) return e;
+    TRY(sync(ctx));
     size_t kept_counts[4], kept = 0;
     for (int r = 0; r < 4; ++r) {
       kept_counts[r] = (size_t)ctx->h->kept[r];
@@ -520,11 +623,11 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
 
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
-    if (int e = ensure_host_out(ctx, kept + 4)) return e;
+    TRY(ensure_host_out(ctx, kept + 4));
     CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, kept * sizeof(double2), cudaMemcpyDeviceToHost,
                        st));
     CK(cudaEventRecord(ctx->ev[9], st));
-    if (int e = sync(ctx)) return e;
+    TRY(sync(ctx));
     D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
     const auto t_host0 = std::chrono::steady_clock::now();
     const int a = chgpu::host::assemble_ring(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
@@ -532,7 +635,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     if (a) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon: fewer than 3 distinct vertices");
     const int mk = chgpu::host::melkman(ctx->ring.data(), ctx->ring.size(), ctx->hull);
     if (mk) return fail(ctx, CHGPU_DEGENERATE, "melkman: degenerate polygon");
-    D.t_host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    D.t_host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
   }
   const auto t_end = std::chrono::steady_clock::now();
 
@@ -553,6 +657,25 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   *n_hull = ctx->hull.size();
   if (stats) *stats = S;
   if (diag) *diag = D;
+  return CHGPU_OK;
+}
+
+int upload_points(chgpu_ctx* ctx, const double* xy, size_t n) {
+  TRY(ensure_cap(ctx, n));
+  CK(cudaMemcpyAsync(ctx->d_pts, xy, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->st));
+  return CHGPU_OK;
+}
+
+int upload_quad(chgpu_ctx* ctx, const double* quad) {
+  QuadInfo qi{};
+  std::memcpy(qi.q, quad, sizeof qi.q);
+  Pt fr[4];
+  int nf = 0;
+  frame_of(quad, fr, &nf);
+  qi.frame_size = (u32)nf;
+  qi.degenerate = nf <= 2;
+  ctx->h->qi = qi;
+  CK(cudaMemcpyAsync(ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo), cudaMemcpyHostToDevice, ctx->st));
   return CHGPU_OK;
 }
 
@@ -637,7 +760,7 @@ int chgpu_hull(chgpu_ctx* ctx, const double* xy, size_t n, size_t chunk_count,
   if (n == 0) return fail(ctx, CHGPU_EMPTY, "convex_hull: no points");
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "more than 2^32-1 points per call");
   cudaSetDevice(ctx->device);
-  if (int e = ensure_cap(ctx, n)) return e;
+  TRY(ensure_cap(ctx, n));
   return run_pipeline(ctx, xy, nullptr, n, chunk_count, degenerate_fallback, hull_xy, n_hull, stats,
                       diag);
 }
@@ -651,47 +774,24 @@ int chgpu_hull_device(chgpu_ctx* ctx, const double* d_xy, size_t n, size_t chunk
   if (reinterpret_cast<uintptr_t>(d_xy) % 16 != 0)
     return fail(ctx, CHGPU_INVALID_ARG, "device input must be 16-byte aligned");
   cudaSetDevice(ctx->device);
-  if (int e = ensure_cap(ctx, n)) return e;
+  TRY(ensure_cap(ctx, n));
   return run_pipeline(ctx, nullptr, reinterpret_cast<const double2*>(d_xy), n, chunk_count,
                       degenerate_fallback, hull_xy, n_hull, stats, diag);
 }
 
 // ---------------------------------------------------------------- stage taps
 
-static int upload_points(chgpu_ctx* ctx, const double* xy, size_t n) {
-  if (int e = ensure_cap(ctx, n)) return e;
-  CK(cudaMemcpyAsync(ctx->d_pts, xy, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->st));
-  return CHGPU_OK;
-}
-
-static int upload_quad(chgpu_ctx* ctx, const double* quad) {
-  QuadInfo qi{};
-  std::memcpy(qi.q, quad, sizeof qi.q);
-  Pt fr[4];
-  int nf = 0;
-  for (int c = 0; c < 4; ++c) {
-    const Pt p{quad[2 * c], quad[2 * c + 1]};
-    if (nf == 0 || !(fr[nf - 1].x == p.x && fr[nf - 1].y == p.y)) fr[nf++] = p;
-  }
-  if (nf > 1 && fr[0].x == fr[nf - 1].x && fr[0].y == fr[nf - 1].y) --nf;
-  qi.frame_size = (u32)nf;
-  qi.degenerate = nf <= 2;
-  ctx->h->qi = qi;
-  CK(cudaMemcpyAsync(ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo), cudaMemcpyHostToDevice, ctx->st));
-  return CHGPU_OK;
-}
-
 int chgpu_find_extremes(chgpu_ctx* ctx, const double* xy, size_t n, double* quad_out) {
   if (n == 0) return fail(ctx, CHGPU_EMPTY, "find_extremes: no points");
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "too many points");
   cudaSetDevice(ctx->device);
-  if (int e = upload_points(ctx, xy, n)) return e;
+  TRY(upload_points(ctx, xy, n));
   const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
   launch_extremes_partial(ctx->d_pts, n, 0, ctx->d_partials, blocks, ctx->st);
   launch_extremes_final(ctx->d_partials, blocks, ctx->d_qinfo, nullptr, ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   std::memcpy(quad_out, ctx->h->qi.q, 8 * sizeof(double));
   return CHGPU_OK;
 }
@@ -701,8 +801,8 @@ int chgpu_classify(chgpu_ctx* ctx, const double* xy, size_t n, const double* qua
   for (int r = 0; r < 5; ++r) counts[r] = 0;
   if (n == 0) return CHGPU_OK;
   cudaSetDevice(ctx->device);
-  if (int e = upload_points(ctx, xy, n)) return e;
-  if (int e = upload_quad(ctx, quad)) return e;
+  TRY(upload_points(ctx, xy, n));
+  TRY(upload_quad(ctx, quad));
   CK(cudaMemsetAsync(ctx->d_u64 + 5, 0, 5 * sizeof(unsigned long long), ctx->st));
   const int blocks = (int)std::min<size_t>(148 * 8, (n + 255) / 256);
   launch_classify_labels(ctx->d_pts, n, ctx->d_qinfo, ctx->d_flags, ctx->d_u64 + 5, blocks, ctx->st);
@@ -710,7 +810,7 @@ int chgpu_classify(chgpu_ctx* ctx, const double* xy, size_t n, const double* qua
   CK(cudaMemcpyAsync(labels, ctx->d_flags, n, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaMemcpyAsync(ctx->h->counts5, ctx->d_u64 + 5, 5 * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   for (int r = 0; r < 5; ++r) counts[r] = (size_t)ctx->h->counts5[r];
   return CHGPU_OK;
 }
@@ -721,20 +821,22 @@ int chgpu_discard_round1(chgpu_ctx* ctx, const double* xy, const uint8_t* labels
   if (n == 0) return CHGPU_OK;
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "too many points");
   cudaSetDevice(ctx->device);
-  if (int e = upload_points(ctx, xy, n)) return e;
+  TRY(upload_points(ctx, xy, n));
   CK(cudaMemcpyAsync(ctx->d_flags, labels, n, cudaMemcpyHostToDevice, ctx->st));
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
+  TRY(begin_call(ctx));
+  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  ctx->ctr_used += 5;
   launch_classify_compact(ctx->d_pts, (u32)n, ctx->d_qinfo, ctx->d_flags, 0, ctx->d_kbuf,
                           ctx->d_vbuf, ctx->cap, ctx->d_status, next_tag(ctx),
-                          ctx->d_ctr + kCtrK2, ctx->d_ctr + kCtrCounts, ctx->st);
+                          ctx->d_ctr + k2_slot, ctx->d_ctr + cnt_slot, ctx->st);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(&ctx->h->ctr[kCtrCounts], ctx->d_ctr + kCtrCounts, 5 * sizeof(u32),
+  CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   const u64 cap = ctx->cap;
   u64 m[4], s1 = 0;
   for (int s = 0; s < 4; ++s) {
-    m[s] = ctx->h->ctr[kCtrCounts + 1 + s];
+    m[s] = ctx->h->ctr[cnt_slot + 1 + s];
     s1 += m[s];
   }
   // Decode each stream on the device into contiguous block order.
@@ -747,7 +849,7 @@ int chgpu_discard_round1(chgpu_ctx* ctx, const double* xy, const uint8_t* labels
   }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out_xy, ctx->d_kept, s1 * sizeof(double2), cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   dst = 0;
   for (int s = 0; s < 4; ++s) {
     std::memset(out_labels + dst, s + 1, m[s]);
@@ -764,24 +866,15 @@ int chgpu_sort_region(chgpu_ctx* ctx, int region, double* xy, size_t m) {
   if (m <= 1) return CHGPU_OK;
   if (m >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "too many points");
   cudaSetDevice(ctx->device);
-  if (int e = upload_points(ctx, xy, m)) return e;
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
+  TRY(upload_points(ctx, xy, m));
+  TRY(begin_call(ctx));
   launch_encode(ctx->d_pts, m, region, ctx->d_kbuf, ctx->d_vbuf, ctx->st);
-  if (int e = ensure_segs(ctx, 1)) return e;
-  ctx->h_segs[0] = SegDesc{0, 0, (u32)m, 0, region, 0};
-  bool in_a = true;
-  int passes = 0;
-  if (int e = radix_sort(ctx, 1, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                         ctx->d_vbuf, 0, kCtrPass, kCtrMask, &in_a, &passes))
-    return e;
-  u64* kF = in_a ? ctx->d_ka : ctx->d_kbuf;
-  u64* vF = in_a ? ctx->d_va : ctx->d_vbuf;
-  u64* kS = in_a ? ctx->d_kbuf : ctx->d_ka;
-  u64* vS = in_a ? ctx->d_vbuf : ctx->d_va;
-  ctx->h_segs[0] = SegDesc{0, 0, (u32)m, 0, region, 0};
-  size_t runs = 0;
-  if (int e = fix_ties(ctx, 1, kF, vF, kS, vS, &runs)) return e;
-  launch_decode(kF, vF, m, region, ctx->d_kept, ctx->st);
+  // No quad here: a full 64-bit LSD on k, then the ==-primary fix-up.
+  TRY(ensure_segs(ctx, 1));
+  ctx->h_segs[0] = make_seg(0, 0, m, region);
+  Sorted so{};
+  TRY(sort_segments(ctx, 1, 0, false, &so));
+  launch_decode(so.kF, so.vF, m, region, ctx->d_kept, ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(xy, ctx->d_kept, m * sizeof(double2), cudaMemcpyDeviceToHost, ctx->st));
   return sync(ctx);
@@ -800,9 +893,8 @@ int chgpu_spa_filter(chgpu_ctx* ctx, int region, const double* xy, size_t m, con
   }
   if (m >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "too many points");
   cudaSetDevice(ctx->device);
-  if (int e = upload_points(ctx, xy, m)) return e;
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
-  CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), ctx->st));
+  TRY(upload_points(ctx, xy, m));
+  TRY(begin_call(ctx));
   launch_encode(ctx->d_pts, m, region, ctx->d_ka, ctx->d_va, ctx->st);
   SpaPlan plan{};
   const int r = region - 1;
@@ -816,14 +908,14 @@ int chgpu_spa_filter(chgpu_ctx* ctx, int region, const double* xy, size_t m, con
   plan.total_chunks = (u32)((m + cs - 1) / cs);
   plan.seed[r] = (region == 1 || region == 3) ? anchors[1] : anchors[0];
   launch_spa(ctx->d_ka, ctx->d_va, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
-             next_tag(ctx), ctx->d_ctr + kCtrSpa, ctx->st);
+             next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   const size_t k = (size_t)ctx->h->kept[r];
   CK(cudaMemcpyAsync(out, ctx->d_kept, k * sizeof(double2), cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   *n_out = k;
   return CHGPU_OK;
 }
@@ -841,7 +933,7 @@ int chgpu_shard_extremes(chgpu_ctx* ctx, const double* d_xy, size_t n, uint64_t 
   CK(cudaGetLastError());
   QuadCand qc;
   CK(cudaMemcpyAsync(&qc, ctx->d_rawquad, sizeof qc, cudaMemcpyDeviceToHost, ctx->st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   for (int c = 0; c < 4; ++c) {
     quad_out[2 * c] = qc.c[c].x;
     quad_out[2 * c + 1] = qc.c[c].y;
@@ -888,98 +980,51 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
   if (n == 0) return CHGPU_OK;
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "shard too large");
   cudaSetDevice(ctx->device);
-  if (int e = ensure_cap(ctx, n)) return e;
+  TRY(ensure_cap(ctx, n));
   cudaStream_t st = ctx->st;
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), st));
-  CK(cudaMemsetAsync(ctx->d_u64, 0, 16 * sizeof(unsigned long long), st));
-  if (int e = upload_quad(ctx, quad)) return e;
+  TRY(begin_call(ctx));
+  TRY(upload_quad(ctx, quad));
   const bool degenerate = ctx->h->qi.degenerate != 0;
+  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  ctx->ctr_used += 5;
   launch_classify_compact(reinterpret_cast<const double2*>(d_xy), (u32)n, ctx->d_qinfo, nullptr,
                           degenerate ? 1 : 0, ctx->d_kbuf, ctx->d_vbuf, ctx->cap, ctx->d_status,
-                          next_tag(ctx), ctx->d_ctr + kCtrK2, ctx->d_ctr + kCtrCounts, st);
+                          next_tag(ctx), ctx->d_ctr + k2_slot, ctx->d_ctr + cnt_slot, st);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(&ctx->h->ctr[kCtrCounts], ctx->d_ctr + kCtrCounts, 5 * sizeof(u32),
+  CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   u64 m[4], s1 = 0;
   for (int s = 0; s < 4; ++s) {
-    m[s] = ctx->h->ctr[kCtrCounts + 1 + s];
+    m[s] = ctx->h->ctr[cnt_slot + 1 + s];
     s1 += m[s];
   }
-  const u64 cap = ctx->cap;
-  if (int e = ensure_segs(ctx, 4)) return e;
   if (degenerate) {
     // Survivors go back sorted and unique; the merge re-runs the
     // degenerate branch on their union.
-    ctx->h_segs[0] = SegDesc{0, 0, (u32)s1, 0, 0, 0};
-    bool in_a = true;
+    size_t nu = 0, groups = 0;
     int passes = 0;
-    if (int e = radix_sort(ctx, 1, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                           ctx->d_vbuf, 0, kCtrPass, kCtrMask, &in_a, &passes))
-      return e;
-    u64* kF = in_a ? ctx->d_ka : ctx->d_kbuf;
-    u64* vF = in_a ? ctx->d_va : ctx->d_vbuf;
-    u64* kS = in_a ? ctx->d_kbuf : ctx->d_ka;
-    u64* vS = in_a ? ctx->d_vbuf : ctx->d_va;
-    ctx->h_segs[0] = SegDesc{0, 0, (u32)s1, 0, 0, 0};
-    size_t runs = 0;
-    if (int e = fix_ties(ctx, 1, kF, vF, kS, vS, &runs)) return e;
-    launch_unique(kF, vF, s1, ctx->d_kept, ctx->d_status, next_tag(ctx), ctx->d_ctr + kCtrUnique,
-                  ctx->d_u64 + 4, st);
-    CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 4, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    if (int e = sync(ctx)) return e;
-    kept_counts[0] = (size_t)ctx->h->uniq;
+    TRY(sorted_unique_survivors(ctx, s1, quad, &nu, &passes, &groups));
+    kept_counts[0] = nu;
   } else {
     if (chunk_count == 0) return fail(ctx, CHGPU_INVALID_ARG, "spa_filter: chunk_count must be >= 1");
-    const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
-    u64 dst = 0;
-    for (int s = 0; s < 4; ++s) {
-      ctx->h_segs[s] = SegDesc{src_off[s], dst, (u32)m[s], 0, s + 1, 0};
-      dst += m[s];
-    }
-    bool in_a = true;
-    int passes = 0;
-    if (int e = radix_sort(ctx, 4, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                           ctx->d_vbuf, 0, kCtrPass, kCtrMask, &in_a, &passes))
-      return e;
-    u64* kF = in_a ? ctx->d_ka : ctx->d_kbuf;
-    u64* vF = in_a ? ctx->d_va : ctx->d_vbuf;
-    u64* kS = in_a ? ctx->d_kbuf : ctx->d_ka;
-    u64* vS = in_a ? ctx->d_vbuf : ctx->d_va;
-    dst = 0;
-    for (int s = 0; s < 4; ++s) {
-      ctx->h_segs[s] = SegDesc{dst, dst, (u32)m[s], 0, s + 1, 0};
-      dst += m[s];
-    }
-    size_t runs = 0;
-    if (int e = fix_ties(ctx, 4, kF, vF, kS, vS, &runs)) return e;
-    SpaPlan plan{};
-    u32 chunks = 0;
-    u64 off = 0;
-    for (int r = 0; r < 4; ++r) {
-      plan.off[r] = off;
-      plan.m[r] = m[r];
-      plan.chunk_begin[r] = chunks;
-      const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;
-      plan.chunk_size[r] = cs;
-      if (m[r]) chunks += (u32)((m[r] + cs - 1) / cs);
-      off += m[r];
-      plan.seed[r] = (r == 0 || r == 2) ? quad[2 * r + 1] : quad[2 * r];
-    }
-    plan.total_chunks = chunks;
-    launch_spa(kF, vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status, next_tag(ctx),
-               ctx->d_ctr + kCtrSpa, st);
+    int qbits = 0;
+    TRY(plan_regions(ctx, m, quad, &qbits));
+    Sorted so{};
+    TRY(sort_segments(ctx, 4, qbits, false, &so));
+    const SpaPlan plan = make_spa_plan(m, chunk_count, quad);
+    launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
+               next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
-    if (int e = sync(ctx)) return e;
+    TRY(sync(ctx));
     for (int r = 0; r < 4; ++r) kept_counts[r] = (size_t)ctx->h->kept[r];
   }
   const size_t total = kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3];
-  if (int e = ensure_host_out(ctx, total + 4)) return e;
+  TRY(ensure_host_out(ctx, total + 4));
   CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, total * sizeof(double2), cudaMemcpyDeviceToHost, st));
-  if (int e = sync(ctx)) return e;
+  TRY(sync(ctx));
   *chains_xy = reinterpret_cast<const double*>(ctx->h_out);
   return CHGPU_OK;
 }
