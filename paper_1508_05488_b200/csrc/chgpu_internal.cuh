@@ -220,8 +220,8 @@ enum : int { kDigitK = 0, kDigitV = 1, kDigitQ = 2 };
 enum : int { kEqQ = 0, kEqPrim = 1 };
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortItems = 12;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 3072
 constexpr int kDigits = 256;
 constexpr int kPasses = 8;
 

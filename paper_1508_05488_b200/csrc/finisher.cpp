@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 
 namespace chgpu {
 namespace host {
@@ -60,13 +61,33 @@ void canonicalize(Pt* ring, size_t n) {
   std::rotate(ring, ring + lo, ring + n);
 }
 
+namespace {
+
+// Per-thread scratch that only ever grows: the finisher runs once per hull
+// call, and re-allocating (and page-faulting) megabytes each time costs more
+// than the scan itself.
+struct Scratch {
+  std::unique_ptr<Pt[]> buf;
+  size_t cap = 0;
+  Pt* get(size_t n) {
+    if (n > cap) {
+      cap = n + n / 2;
+      buf.reset(new Pt[cap]);
+    }
+    return buf.get();
+  }
+};
+
+}  // namespace
+
 int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
   // melkman.cpp:20-25: consecutive duplicates (and a closing repeat) go.
-  std::vector<Pt> ring;
-  ring.reserve(n_in);
-  for (size_t i = 0; i < n_in; ++i) push_distinct(ring, poly[i]);
-  if (ring.size() > 1 && same(ring.front(), ring.back())) ring.pop_back();
-  const size_t n = ring.size();
+  thread_local Scratch ring_s, deque_s;
+  Pt* ring = ring_s.get(n_in + 1);
+  size_t n = 0;
+  for (size_t i = 0; i < n_in; ++i)
+    if (n == 0 || !same(ring[n - 1], poly[i])) ring[n++] = poly[i];
+  if (n > 1 && same(ring[0], ring[n - 1])) --n;
 
   // melkman.cpp:30-47: absorb the leading collinear run; remember its two
   // extreme endpoints (lo, hi) and the last vertex visited.
@@ -86,7 +107,7 @@ int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
   if (i >= n) return kDegenerate;
 
   // melkman.cpp:52-60: seed triangle; the deque lives in buf[head, tail).
-  std::vector<Pt> buf(2 * n + 8);
+  Pt* buf = deque_s.get(2 * n + 8);
   size_t head = n + 4, tail = head;
   const Pt w = ring[i];
   const Pt second = last;
@@ -107,7 +128,7 @@ int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
     while (tail - head >= 2 && turn(v, buf[head], buf[head + 1]) != kLeft) ++head;
     buf[--head] = v;
   }
-  hull.assign(buf.begin() + head, buf.begin() + (tail - 1));  // ends coincide (:83)
+  hull.assign(buf + head, buf + (tail - 1));  // ends coincide (:83)
   canonicalize(hull.data(), hull.size());
   return kOk;
 }

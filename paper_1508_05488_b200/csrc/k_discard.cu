@@ -12,6 +12,8 @@
 // Stream offsets come from a single-pass decoupled look-back with four
 // independent chains (one per region). Interior points are never written.
 
+#include <algorithm>
+
 #include "chgpu_internal.cuh"
 #include "kernels.h"
 
@@ -186,20 +188,38 @@ __device__ __forceinline__ u64 stream_slot(int s, u64 pos, u64 ncap) {
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int bytes = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Persistent CTAs, double-buffered: while a tile is classified and its
+// survivors scattered, the next tile streams into shared memory with
+// cp.async (no registers held by in-flight loads). Tiles are claimed in
+// increasing order by running CTAs, which keeps the look-back deadlock-free.
 template <bool kGivenLabels>
-__global__ __launch_bounds__(kK2Threads) void k_classify_compact(
+__global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u64 ncap, u64* __restrict__ status, u32 tag,
     u32* __restrict__ tile_ctr, u32 num_tiles, u32* __restrict__ counts_out) {
-  __shared__ u32 s_tile;
+  extern __shared__ __align__(16) double2 sbuf[];  // [2][kK2Tile]
+  __shared__ u32 s_tile[2];
   __shared__ u32 s_warp_cnt[kK2Threads / 32][4];
   __shared__ u32 s_excl[4];
   __shared__ QuadEdges s_edges;
   __shared__ int s_lex;
 
-  if (threadIdx.x == 0) {
-    s_tile = atomicAdd(tile_ctr, 1u);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    s_tile[0] = atomicAdd(tile_ctr, 1u);
     const QuadInfo qi = *qinfo;
     for (int c = 0; c < 4; ++c) {
       const int d = (c + 1) & 3;
@@ -213,91 +233,119 @@ __global__ __launch_bounds__(kK2Threads) void k_classify_compact(
     s_lex = force_lex || (!kGivenLabels && qi.degenerate);
   }
   __syncthreads();
-  const u32 tile = s_tile;
   const bool lex = s_lex != 0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const u64 tile_base = (u64)tile * kK2Tile;
 
-  int reg[kK2Items];
-  double px[kK2Items], py[kK2Items];
-  u32 rank[kK2Items];
-  u32 run[4] = {0, 0, 0, 0};  // warp-uniform running counts per stream
-  const QuadEdges e = s_edges;
-
+  auto issue = [&](int stage, u32 t) {
+    const u64 base = (u64)t * kK2Tile;
+    double2* dst = sbuf + stage * kK2Tile;
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
-    const u64 idx = tile_base + (u64)j * kK2Threads + warp * 32 + lane;
-    reg[j] = 0;
-    px[j] = py[j] = 0.0;
-    if (idx < n) {
-      const double2 p = ldg_stream(pts + idx);
-      px[j] = p.x;
-      py[j] = p.y;
+    for (int j = 0; j < kK2Items; ++j) {
+      const u64 idx = base + (u64)j * kK2Threads + tid;
+      const bool ok = idx < n;
+      cp_async16(dst + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
     }
-  }
+  };
+  if (s_tile[0] < num_tiles) issue(0, s_tile[0]);
+  cp_async_commit();
+
+  int stage = 0;
+  while (true) {
+    const u32 tile = s_tile[stage];
+    if (tile >= num_tiles) break;
+    if (tid == 0) s_tile[stage ^ 1] = atomicAdd(tile_ctr, 1u);
+    __syncthreads();  // next tile id visible; previous use of sbuf[stage^1] finished
+    const u32 nt = s_tile[stage ^ 1];
+    if (nt < num_tiles) issue(stage ^ 1, nt);
+    cp_async_commit();
+    cp_async_wait<1>();  // this thread's copies of the current tile have landed
+
+    const double2* sb = sbuf + stage * kK2Tile;
+    const u64 tile_base = (u64)tile * kK2Tile;
+    int reg[kK2Items];
+    u32 rank[kK2Items];
+    u32 run[4] = {0, 0, 0, 0};  // warp-uniform running counts per stream
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
-    const u64 idx = tile_base + (u64)j * kK2Threads + warp * 32 + lane;
-    if (idx < n) {
-      int r = kGivenLabels ? (int)given_labels[idx] : classify(e, px[j], py[j]);
-      if (lex && r != 0) r = 1;
+    for (int j = 0; j < kK2Items; ++j) {
+      const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+      int r = 0;
+      if (idx < n) {
+        if (kGivenLabels) {
+          r = (int)given_labels[idx];
+        } else {
+          const double2 p = sb[j * kK2Threads + tid];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (cross_edge(s_edges.ax[c], s_edges.ay[c], s_edges.ex[c], s_edges.ey[c], p.x, p.y) <
+                0.0) {
+              r = c + 1;
+              break;
+            }
+          }
+        }
+        if (lex && r != 0) r = 1;
+      }
       reg[j] = r;
-    }
-    rank[j] = 0;
+      u32 rk = 0;
 #pragma unroll
-    for (int s = 1; s <= 4; ++s) {
-      const unsigned m = __ballot_sync(0xffffffffu, reg[j] == s);
-      if (reg[j] == s) rank[j] = run[s - 1] + __popc(m & lanemask_lt());
-      run[s - 1] += __popc(m);
+      for (int s = 1; s <= 4; ++s) {
+        const unsigned m = __ballot_sync(0xffffffffu, r == s);
+        rk = (r == s) ? run[s - 1] + __popc(m & lanemask_lt()) : rk;
+        run[s - 1] += __popc(m);
+      }
+      rank[j] = rk;
     }
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) s_warp_cnt[warp][s] = run[s];
-  }
-  __syncthreads();
-
-  // Warp s (s < 4) owns stream s+1: block-exclusive scan over warps, then
-  // the look-back for this tile.
-  if (warp < 4) {
-    const int s = warp;
-    u32 agg = 0;
     if (lane == 0) {
-      for (int w = 0; w < kK2Threads / 32; ++w) {
-        const u32 c = s_warp_cnt[w][s];
-        s_warp_cnt[w][s] = agg;
-        agg += c;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) s_warp_cnt[warp][s] = run[s];
+    }
+    __syncthreads();
+
+    // Warp s (s < 4) owns stream s+1: block-exclusive scan over warps, then
+    // the look-back for this tile.
+    if (warp < 4) {
+      const int s = warp;
+      u32 agg = 0;
+      if (lane == 0) {
+        for (int w = 0; w < kK2Threads / 32; ++w) {
+          const u32 c = s_warp_cnt[w][s];
+          s_warp_cnt[w][s] = agg;
+          agg += c;
+        }
+      }
+      agg = __shfl_sync(0xffffffffu, agg, 0);
+      u64* col = status + s;
+      u32 excl = 0;
+      if (tile == 0) {
+        if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, agg));
+      } else {
+        if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagAgg, agg));
+        excl = warp_lookback(col, 4, (int)tile, 0, tag);
+        if (lane == 0)
+          store_status(col + (size_t)tile * 4, make_status(tag, kFlagPrefix, excl + agg));
+      }
+      if (lane == 0) {
+        s_excl[s] = excl;
+        if (tile == num_tiles - 1) counts_out[s + 1] = excl + agg;
       }
     }
-    agg = __shfl_sync(0xffffffffu, agg, 0);
-    u64* col = status + s;
-    u32 excl = 0;
-    if (tile == 0) {
-      if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, agg));
-    } else {
-      if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagAgg, agg));
-      excl = warp_lookback(col, 4, (int)tile, 0, tag);
-      if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagPrefix, excl + agg));
-    }
-    if (lane == 0) {
-      s_excl[s] = excl;
-      if (tile == num_tiles - 1) counts_out[s + 1] = excl + agg;
-    }
-  }
-  __syncthreads();
+    __syncthreads();
 
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
-    const int s = reg[j];
-    if (s != 0) {
-      const u64 pos = (u64)s_excl[s - 1] + s_warp_cnt[warp][s - 1] + rank[j];
-      const u64 slot = stream_slot(s, pos, ncap);
-      u64 k, v;
-      encode_point(lex ? 0 : s, px[j], py[j], k, v);
-      kbuf[slot] = k;
-      vbuf[slot] = v;
+    for (int j = 0; j < kK2Items; ++j) {
+      const int s = reg[j];
+      if (s != 0) {
+        const double2 p = sb[j * kK2Threads + tid];
+        const u64 pos = (u64)s_excl[s - 1] + s_warp_cnt[warp][s - 1] + rank[j];
+        const u64 slot = stream_slot(s, pos, ncap);
+        u64 k, v;
+        encode_point(lex ? 0 : s, p.x, p.y, k, v);
+        kbuf[slot] = k;
+        vbuf[slot] = v;
+      }
     }
+    stage ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 // Labels only (the classify() stage tap, classify.cpp:9-33).
@@ -339,9 +387,21 @@ __global__ void k_classify_labels(const double2* __restrict__ pts, u64 n,
 
 // ------------------------------------------------------------------ launchers
 
-void launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
-                             int blocks, cudaStream_t st) {
+int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
+                            int blocks, cudaStream_t st) {
+  // One resident wave at most: a grid-stride kernel gains nothing from a
+  // second partial wave, it only adds a tail.
+  static int wave = 0;
+  if (!wave) {
+    int occ = 0, sms = 0, dev = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_extremes_partial, kK1Threads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    wave = std::max(1, occ) * std::max(1, sms);
+  }
+  blocks = std::max(1, std::min(blocks, wave));
   k_extremes_partial<<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials);
+  return blocks;
 }
 
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
@@ -355,14 +415,28 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              u32* counts_out, cudaStream_t st) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
+  constexpr size_t smem = 2 * kK2Tile * sizeof(double2);
+  static int occ[2] = {0, 0};
+  static int sms = 0;
+  const int g = given_labels ? 1 : 0;
+  if (!occ[g]) {
+    auto fn = given_labels ? k_classify_compact<true> : k_classify_compact<false>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[g], fn, kK2Threads, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ[g] < 1) occ[g] = 1;
+  }
+  const u32 grid = std::min<u32>(tiles, (u32)(occ[g] * sms));
   if (given_labels)
-    k_classify_compact<true><<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, given_labels, force_lex,
-                                                           kbuf, vbuf, ncap, status, tag, tile_ctr,
-                                                           tiles, counts_out);
+    k_classify_compact<true><<<grid, kK2Threads, smem, st>>>(pts, n, qinfo, given_labels, force_lex,
+                                                             kbuf, vbuf, ncap, status, tag, tile_ctr,
+                                                             tiles, counts_out);
   else
-    k_classify_compact<false><<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, nullptr, force_lex,
-                                                            kbuf, vbuf, ncap, status, tag,
-                                                            tile_ctr, tiles, counts_out);
+    k_classify_compact<false><<<grid, kK2Threads, smem, st>>>(pts, n, qinfo, nullptr, force_lex,
+                                                              kbuf, vbuf, ncap, status, tag,
+                                                              tile_ctr, tiles, counts_out);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

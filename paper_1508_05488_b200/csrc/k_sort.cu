@@ -144,67 +144,87 @@ __global__ void k_hist_scan(const u32* __restrict__ hist, const SegDesc* __restr
 
 // ------------------------------------------------------------------ onesweep pass
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+struct OnesweepSmem {
+  u32 whist[kSortThreads / 32][kDigits];  // per-warp digit counters, then offsets
+  u32 bin_excl[kDigits];                  // tile-local exclusive prefix over digits
+  u64 bin_base[kDigits];                  // global destination base per digit
+  u64 kstage[kSortTile];                  // keys in tile-sorted order
+  u64 vraw[kSortTile];                    // values in load order (cp.async)
+  unsigned short perm[kSortTile];         // tile-sorted position -> load position
+  unsigned char sdig[kSortTile];          // digit of each tile-sorted record
+  u32 wsum[kSortThreads / 32];
+  u32 tile;
+  int seg;
+};
+
+// One LSD pass. Keys stay in registers for the ranking; values travel
+// global -> shared with cp.async and are only touched again by the scatter,
+// so a thread holds kSortItems keys and nothing else across the pass.
 template <int kMode>
-__global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
+__global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
     const u32* __restrict__ digit_excl, int pass, u64* __restrict__ status, u32 tag,
     u32* __restrict__ tile_ctr) {
-  __shared__ u32 whist[kSortThreads / 32][kDigits];
-  __shared__ u32 bin_excl[kDigits];
-  __shared__ u64 bin_base[kDigits];
-  __shared__ u64 stage[kSortTile];
-  __shared__ unsigned char sdig[kSortTile];
-  __shared__ u32 s_tile;
-  __shared__ int s_seg;
-  __shared__ u32 s_wsum[kSortThreads / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     const u32 t = atomicAdd(tile_ctr, 1u);
-    s_tile = t;
-    s_seg = find_segment(segs, nseg, t);
+    S.tile = t;
+    S.seg = find_segment(segs, nseg, t);
   }
-  for (int i = tid; i < (kSortThreads / 32) * kDigits; i += kSortThreads) (&whist[0][0])[i] = 0;
+  for (int i = tid; i < (kSortThreads / 32) * kDigits; i += kSortThreads) (&S.whist[0][0])[i] = 0;
   __syncthreads();
 
-  const u32 tile = s_tile;
-  const int segi = s_seg;
+  const u32 tile = S.tile;
+  const int segi = S.seg;
   const SegDesc sd = segs[segi];
   const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
   const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
   const u64 src = (use_src ? sd.src_off : sd.dst_off) + e0;
+  const u32 wbase = warp * (kSortItems * 32);
 
-  u64 kk[kSortItems], vv[kSortItems];
-  u32 rank[kSortItems];
+  // The digit source word (v for kDigitV, else k) stays in registers; the
+  // other word rides along through shared memory.
+  const u64* rin = kMode == kDigitV ? vin : kin;
+  const u64* oin = kMode == kDigitV ? kin : vin;
+  u64 kk[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
-    kk[j] = vv[j] = 0;
+    const u32 li = wbase + j * 32 + lane;
+    kk[j] = 0;
     if (li < cnt) {
-      kk[j] = kin[src + li];
-      vv[j] = vin[src + li];
+      kk[j] = rin[src + li];
+      cp_async8(&S.vraw[li], oin + src + li);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+
   // Warp-local multisplit: items are ranked in (warp, item, lane) order,
   // which is the input order inside the tile, so the pass is stable.
-  unsigned char dg[kSortItems];
+  u32 code[kSortItems];  // digit | rank << 8
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
+    const u32 li = wbase + j * 32 + lane;
     const bool valid = li < cnt;
-    const u32 d = digit_of<kMode>(sd, kk[j], vv[j], pass);
-    dg[j] = (unsigned char)d;
+    const u32 d = digit_of<kMode>(sd, kk[j], kk[j], pass);
     const u32 key = valid ? d : (0x100u | (u32)lane);
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
     u32 old = 0;
     if (valid && lane == leader) {
-      old = whist[warp][d];
-      whist[warp][d] = old + __popc(peers);
+      old = S.whist[warp][d];
+      S.whist[warp][d] = old + __popc(peers);
     }
     old = __shfl_sync(0xffffffffu, old, leader);
-    rank[j] = old + __popc(peers & lanemask_lt());
+    code[j] = d | ((old + __popc(peers & lanemask_lt())) << 8);
   }
   __syncthreads();
 
@@ -213,8 +233,8 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
   u32 tile_cnt = 0;
 #pragma unroll
   for (int w = 0; w < kSortThreads / 32; ++w) {
-    const u32 c = whist[w][b];
-    whist[w][b] = tile_cnt;
+    const u32 c = S.whist[w][b];
+    S.whist[w][b] = tile_cnt;
     tile_cnt += c;
   }
   u32 incl = tile_cnt;
@@ -223,11 +243,12 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
     const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) s_wsum[warp] = incl;
+  if (lane == 31) S.wsum[warp] = incl;
   __syncthreads();
   u32 wpre = 0;
-  for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
-  bin_excl[b] = wpre + incl - tile_cnt;
+  for (int w = 0; w < warp; ++w) wpre += S.wsum[w];
+  const u32 bexcl = wpre + incl - tile_cnt;
+  S.bin_excl[b] = bexcl;
 
   // Decoupled look-back, one chain per (segment, bin).
   u64* col = status + b;
@@ -250,32 +271,33 @@ __global__ __launch_bounds__(kSortThreads, 2) void k_onesweep(
     }
     store_status(col + (size_t)tile * kDigits, make_status(tag, kFlagPrefix, before + tile_cnt));
   }
-  bin_base[b] = sd.dst_off + digit_excl[((size_t)segi * kPasses + pass) * kDigits + b] + before -
-                bin_excl[b];
+  S.bin_base[b] =
+      sd.dst_off + digit_excl[((size_t)segi * kPasses + pass) * kDigits + b] + before - bexcl;
   __syncthreads();
 
-  // Scatter through shared memory so global writes of a bin are contiguous.
-  u32 lpos[kSortItems];
+  // Tile-sorted staging: keys, load positions and digits.
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
+    const u32 li = wbase + j * 32 + lane;
     if (li < cnt) {
-      const u32 d = dg[j];
-      lpos[j] = bin_excl[d] + whist[warp][d] + rank[j];
-      stage[lpos[j]] = kk[j];
-      sdig[lpos[j]] = (unsigned char)d;
+      const u32 d = code[j] & 0xFF;
+      const u32 lp = S.bin_excl[d] + S.whist[warp][d] + (code[j] >> 8);
+      S.kstage[lp] = kk[j];
+      S.perm[lp] = (unsigned short)li;
+      S.sdig[lp] = (unsigned char)d;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  for (u32 i = tid; i < cnt; i += kSortThreads) kout[bin_base[sdig[i]] + i] = stage[i];
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
-    const u32 li = warp * (kSortItems * 32) + j * 32 + lane;
-    if (li < cnt) stage[lpos[j]] = vv[j];
+  // Scatter: consecutive sorted positions of a digit are consecutive in
+  // global memory, so warps write contiguous runs.
+  u64* rout = kMode == kDigitV ? vout : kout;
+  u64* oout = kMode == kDigitV ? kout : vout;
+  for (u32 i = tid; i < cnt; i += kSortThreads) {
+    const u64 dst = S.bin_base[S.sdig[i]] + i;
+    rout[dst] = S.kstage[i];
+    oout[dst] = S.vraw[S.perm[i]];
   }
-  __syncthreads();
-  for (u32 i = tid; i < cnt; i += kSortThreads) vout[bin_base[sdig[i]] + i] = stage[i];
 }
 
 // Moves segments between layouts without reordering (used when every
@@ -311,27 +333,6 @@ __device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u64 kb, u64
   return ca < cb || (ca == cb && va < vb);
 }
 
-// Marks the start of every group. One block per 4096-record tile.
-__global__ void k_group_detect(const u64* __restrict__ k, const SegDesc* __restrict__ segs,
-                               int nseg, int eqmode, u64* __restrict__ starts,
-                               u32* __restrict__ nstarts, u32 cap) {
-  const u32 tile = blockIdx.x;
-  const int s = find_segment(segs, nseg, tile);
-  const SegDesc sd = segs[s];
-  const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
-  if (e0 >= sd.len) return;
-  const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
-  for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const u64 pos = e0 + i;  // position inside the segment
-    if (pos + 1 >= sd.len) continue;
-    const u64 a = sd.dst_off + pos;
-    if (!group_eq(eqmode, sd, k[a], k[a + 1])) continue;
-    if (pos > 0 && group_eq(eqmode, sd, k[a - 1], k[a])) continue;  // not the first of its run
-    const u32 slot = atomicAdd(nstarts, 1u);
-    if (slot < cap) starts[slot] = ((u64)s << 40) | pos;
-  }
-}
-
 struct GroupRun {
   u64 start;  // absolute record index
   u32 len;
@@ -341,47 +342,75 @@ struct GroupRun {
 constexpr int kSmallGroup = 16;
 constexpr int kMediumGroup = 2048;
 
-// One thread per group: measures it, insertion-sorts it in registers when
-// it holds at most kSmallGroup records, else queues it as medium.
-__global__ void k_group_fix_small(u64* __restrict__ k, u64* __restrict__ v,
-                                  const SegDesc* __restrict__ segs, int eqmode,
-                                  const u64* __restrict__ starts, u32 nstarts,
-                                  GroupRun* __restrict__ medium, u32* __restrict__ nmedium) {
-  for (u32 r = blockIdx.x * blockDim.x + threadIdx.x; r < nstarts; r += gridDim.x * blockDim.x) {
-    const u64 code = starts[r];
-    const int s = (int)(code >> 40);
-    const u64 pos = code & ((1ull << 40) - 1);
-    const SegDesc sd = segs[s];
-    const u64 a = sd.dst_off + pos;
-    const u64 k0 = k[a];
-    u32 len = 1;
-    while (pos + len < sd.len && group_eq(eqmode, sd, k0, k[a + len])) {
+// Group key: equal keys <=> same group (q for kEqQ; canonical k, i.e. the
+// primary under ==, for kEqPrim).
+__device__ __forceinline__ u64 group_key(int eqmode, const SegDesc& s, u64 k) {
+  return eqmode == kEqQ ? (u64)quantize(s, k) : canon_k(s.region, k);
+}
+
+// Detects group starts tile by tile (group keys computed once per record
+// into shared memory) and fixes each group on the spot: the thread owning a
+// group start insertion-sorts it in registers when it holds at most
+// kSmallGroup records, else queues it for k_group_fix_medium.
+__global__ __launch_bounds__(256) void k_group_scan(u64* __restrict__ k, u64* __restrict__ v,
+                                                    const SegDesc* __restrict__ segs, int nseg,
+                                                    int eqmode, GroupRun* __restrict__ medium,
+                                                    u32* __restrict__ nmedium,
+                                                    unsigned long long* __restrict__ ngroups) {
+  __shared__ u64 gk[kSortTile + 2];
+  const u32 tile = blockIdx.x;
+  const int s = find_segment(segs, nseg, tile);
+  const SegDesc sd = segs[s];
+  const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
+  if (e0 >= sd.len) return;
+  const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
+  const u64 base = sd.dst_off + e0;
+  // gk[0] = record e0-1 (if any), gk[1 + i] = record e0+i, gk[cnt+1] = e0+cnt (if any)
+  for (u32 i = threadIdx.x; i < cnt + 2; i += blockDim.x) {
+    const long long pos = (long long)e0 + (long long)i - 1;
+    u64 g = ~0ull;
+    if (pos >= 0 && (u64)pos < sd.len) g = group_key(eqmode, sd, k[sd.dst_off + pos]);
+    gk[i] = g;
+  }
+  __syncthreads();
+  u32 found = 0;
+  for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const u64 pos = e0 + i;
+    if (pos + 1 >= sd.len || gk[i + 1] != gk[i + 2]) continue;
+    if (pos > 0 && gk[i] == gk[i + 1]) continue;  // not the first of its group
+    ++found;
+    const u64 a = base + i;
+    const u64 g0 = gk[i + 1];
+    u32 len = 2;
+    while (pos + len < sd.len && len <= kSmallGroup) {
+      const u64 gn = (i + len + 1 < cnt + 2) ? gk[i + len + 1]
+                                             : group_key(eqmode, sd, k[a + len]);
+      if (gn != g0) break;
       ++len;
-      if (len > kSmallGroup) break;
     }
     if (len > kSmallGroup) {
-      while (pos + len < sd.len && group_eq(eqmode, sd, k0, k[a + len])) ++len;
-      const u32 slot = atomicAdd(nmedium, 1u);
-      medium[slot] = GroupRun{a, len, s};
+      while (pos + len < sd.len && group_key(eqmode, sd, k[a + len]) == g0) ++len;
+      medium[atomicAdd(nmedium, 1u)] = GroupRun{a, len, s};
       continue;
     }
-    u64 gk[kSmallGroup], gv[kSmallGroup];
-    for (u32 i = 0; i < len; ++i) {
-      u64 kx = k[a + i], vx = v[a + i];
-      u32 j = i;
-      while (j > 0 && rec_less(sd.region, kx, vx, gk[j - 1], gv[j - 1])) {
-        gk[j] = gk[j - 1];
-        gv[j] = gv[j - 1];
-        --j;
+    u64 rk[kSmallGroup], rv[kSmallGroup];
+    for (u32 j = 0; j < len; ++j) {
+      const u64 kx = k[a + j], vx = v[a + j];
+      u32 t = j;
+      while (t > 0 && rec_less(sd.region, kx, vx, rk[t - 1], rv[t - 1])) {
+        rk[t] = rk[t - 1];
+        rv[t] = rv[t - 1];
+        --t;
       }
-      gk[j] = kx;
-      gv[j] = vx;
+      rk[t] = kx;
+      rv[t] = vx;
     }
-    for (u32 i = 0; i < len; ++i) {
-      k[a + i] = gk[i];
-      v[a + i] = gv[i];
+    for (u32 j = 0; j < len; ++j) {
+      k[a + j] = rk[j];
+      v[a + j] = rv[j];
     }
   }
+  if (found) atomicAdd(ngroups, (unsigned long long)found);
 }
 
 // One block per medium group: bitonic sort in shared memory; groups longer
@@ -389,9 +418,11 @@ __global__ void k_group_fix_small(u64* __restrict__ k, u64* __restrict__ v,
 __global__ __launch_bounds__(256) void k_group_fix_medium(u64* __restrict__ k, u64* __restrict__ v,
                                                           const SegDesc* __restrict__ segs,
                                                           const GroupRun* __restrict__ medium,
-                                                          u32 nmedium, GroupRun* __restrict__ longr,
+                                                          const u32* __restrict__ nmedium_p,
+                                                          GroupRun* __restrict__ longr,
                                                           u32* __restrict__ nlong) {
   __shared__ u64 sk[kMediumGroup], sv[kMediumGroup], sc[kMediumGroup];
+  const u32 nmedium = *nmedium_p;
   for (u32 r = blockIdx.x; r < nmedium; r += gridDim.x) {
     const GroupRun g = medium[r];
     if (g.len > kMediumGroup) {
@@ -463,22 +494,37 @@ void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, int npasse
   k_hist_scan<<<nseg * kPasses, kDigits, 0, st>>>(hist, segs, npasses, digit_excl, needed_mask);
 }
 
+template <int kMode>
+static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout,
+                            const SegDesc* segs, int nseg, u32 total_tiles, int use_src,
+                            const u32* digit_excl, int pass, u64* status, u32 tag, u32* tile_ctr,
+                            cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_onesweep<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(OnesweepSmem));
+    configured = true;
+  }
+  k_onesweep<kMode><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
+      kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+}
+
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
                      int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st) {
   if (total_tiles == 0) return;
   switch (mode) {
     case kDigitQ:
-      k_onesweep<kDigitQ><<<total_tiles, kSortThreads, 0, st>>>(
-          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      onesweep_launch<kDigitQ>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, status, tag, tile_ctr, st);
       break;
     case kDigitV:
-      k_onesweep<kDigitV><<<total_tiles, kSortThreads, 0, st>>>(
-          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      onesweep_launch<kDigitV>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, status, tag, tile_ctr, st);
       break;
     default:
-      k_onesweep<kDigitK><<<total_tiles, kSortThreads, 0, st>>>(
-          kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      onesweep_launch<kDigitK>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, status, tag, tile_ctr, st);
   }
 }
 
@@ -488,26 +534,17 @@ void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const
   k_seg_copy<<<total_tiles, 256, 0, st>>>(kin, vin, kout, vout, segs, nseg, use_src);
 }
 
-void launch_group_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
-                         u64* starts, u32* nstarts, u32 cap, cudaStream_t st) {
+void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
+                       void* medium, u32* nmedium, unsigned long long* ngroups, cudaStream_t st) {
   if (total_tiles == 0) return;
-  k_group_detect<<<total_tiles, 256, 0, st>>>(k, segs, nseg, eqmode, starts, nstarts, cap);
+  k_group_scan<<<total_tiles, 256, 0, st>>>(k, v, segs, nseg, eqmode, (GroupRun*)medium, nmedium,
+                                            ngroups);
 }
 
-void launch_group_fix_small(u64* k, u64* v, const SegDesc* segs, int eqmode, const u64* starts,
-                            u32 nstarts, void* medium, u32* nmedium, cudaStream_t st) {
-  if (nstarts == 0) return;
-  const u32 blocks = min((nstarts + 127) / 128, 148u * 16u);
-  k_group_fix_small<<<blocks, 128, 0, st>>>(k, v, segs, eqmode, starts, nstarts,
-                                            (GroupRun*)medium, nmedium);
-}
-
-void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium, u32 nmedium,
-                             void* longr, u32* nlong, cudaStream_t st) {
-  if (nmedium == 0) return;
-  const u32 blocks = min(nmedium, 148u * 4u);
-  k_group_fix_medium<<<blocks, 256, 0, st>>>(k, v, segs, (const GroupRun*)medium, nmedium,
-                                             (GroupRun*)longr, nlong);
+void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium,
+                             const u32* nmedium, void* longr, u32* nlong, cudaStream_t st) {
+  k_group_fix_medium<<<148 * 2, 256, 0, st>>>(k, v, segs, (const GroupRun*)medium, nmedium,
+                                              (GroupRun*)longr, nlong);
 }
 
 size_t group_run_bytes() { return sizeof(GroupRun); }

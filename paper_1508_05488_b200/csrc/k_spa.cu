@@ -102,7 +102,10 @@ __global__ __launch_bounds__(kSpaThreads) void k_spa(const u64* __restrict__ k,
   const double ident = is_min ? INFINITY : -INFINITY;
   double carry = (c == 0) ? plan.seed[r] : ident;
 
-  // Pass A: keep flags.
+  // Pass A: keep flags (kept in registers when the chunk is one tile, the
+  // common case; spilled to global memory as bytes otherwise).
+  const bool single = len <= kSpaTile;
+  unsigned char fr[kSpaItems];
   u32 kept = 0;
   for (u64 t0 = 0; t0 < len; t0 += kSpaTile) {
     const u32 cnt = (u32)min((u64)kSpaTile, len - t0);
@@ -130,13 +133,18 @@ __global__ __launch_bounds__(kSpaThreads) void k_spa(const u64* __restrict__ k,
         t = op_ext(is_min, t, g[j]);
       }
     }
-    // Flags go out through shared memory as coalesced bytes.
-    __syncthreads();
-    unsigned char* sf = reinterpret_cast<unsigned char*>(sg);
+    if (single) {
 #pragma unroll
-    for (int j = 0; j < kSpaItems; ++j) sf[tid * kSpaItems + j] = f[j];
-    __syncthreads();
-    for (u32 i = tid; i < cnt; i += kSpaThreads) flags[begin + t0 + i] = sf[i];
+      for (int j = 0; j < kSpaItems; ++j) fr[j] = f[j];
+    } else {
+      // Flags go out through shared memory as coalesced bytes.
+      __syncthreads();
+      unsigned char* sf = reinterpret_cast<unsigned char*>(sg);
+#pragma unroll
+      for (int j = 0; j < kSpaItems; ++j) sf[tid * kSpaItems + j] = f[j];
+      __syncthreads();
+      for (u32 i = tid; i < cnt; i += kSpaThreads) flags[begin + t0 + i] = sf[i];
+    }
     carry = op_ext(is_min, carry, tile_agg);
     __syncthreads();
   }
@@ -169,7 +177,7 @@ __global__ __launch_bounds__(kSpaThreads) void k_spa(const u64* __restrict__ k,
 #pragma unroll
     for (int j = 0; j < kSpaItems; ++j) {
       const u32 i = tid * kSpaItems + j;
-      f[j] = i < cnt ? flags[begin + t0 + i] : 0;
+      f[j] = single ? fr[j] : (i < cnt ? flags[begin + t0 + i] : 0);
       mine += f[j];
     }
     u32 tile_kept;

@@ -18,8 +18,8 @@ struct SpaPlan {
 };
 
 // K1
-void launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
-                             int blocks, cudaStream_t st);
+int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
+                            int blocks, cudaStream_t st);
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, QuadCand* raw_out,
                            cudaStream_t st);
 // K2
@@ -40,12 +40,10 @@ void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const
                      int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st);
 void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, cudaStream_t st);
-void launch_group_detect(const u64* k, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
-                         u64* starts, u32* nstarts, u32 cap, cudaStream_t st);
-void launch_group_fix_small(u64* k, u64* v, const SegDesc* segs, int eqmode, const u64* starts,
-                            u32 nstarts, void* medium, u32* nmedium, cudaStream_t st);
-void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium, u32 nmedium,
-                             void* longr, u32* nlong, cudaStream_t st);
+void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
+                       void* medium, u32* nmedium, unsigned long long* ngroups, cudaStream_t st);
+void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium,
+                             const u32* nmedium, void* longr, u32* nlong, cudaStream_t st);
 size_t group_run_bytes();
 // K4/K5
 void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,

@@ -257,7 +257,7 @@ void region_range(const double* q, int region, double* lo, double* hi) {
 // where the result landed.
 int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* kA, u64* vA,
                u64* kB, u64* vB, int mode, int npasses, bool* in_a, int* passes_run,
-               bool timed = false) {
+               bool timed = false, bool all_passes = false) {
   const u32 tiles = plan_tiles(ctx->h_segs, nseg);
   *passes_run = 0;
   *in_a = true;
@@ -271,8 +271,10 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
                    ctx->d_ctr + mask_slot, ctx->st);
   ctx->launches += 2;
   if (timed) CK(cudaEventRecord(ctx->ev[3], ctx->st));
-  u32 mask = 0;
-  TRY(read_ctr(ctx, mask_slot, &mask));
+  // Bucket passes always move data; a full-key sort skips digit positions
+  // that are constant in every segment (one host round trip).
+  u32 mask = (1u << npasses) - 1;
+  if (!all_passes) TRY(read_ctr(ctx, mask_slot, &mask));
   const u64* kin = ksrc;
   const u64* vin = vsrc;
   int use_src = 1, done = 0;
@@ -310,65 +312,89 @@ struct Run {
   int seg;
 };
 
+// Groups left for the host to resolve after the in-place fix-up.
+struct PendingLong {
+  int slot = -1;
+  int eqmode = 0;
+  int depth = 0;
+  std::vector<int> regions;
+  u64 *kF = nullptr, *vF = nullptr, *kS = nullptr, *vS = nullptr;
+};
+
+int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long);
+
 // Orders every group of the sorted layout (segments in ctx->h_segs, at
 // dst_off of (kF, vF)) by (canon k, v), in place. eqmode kEqQ: groups of
-// equal quantized primary; kEqPrim: groups of ==-equal primary.
+// equal quantized primary; kEqPrim: groups of ==-equal primary. Small and
+// medium groups are fixed on the device without a host round trip; groups
+// longer than a shared-memory sort are recorded in *pend and sorted by
+// resolve_long() (immediately unless `defer`).
 int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int eqmode,
-               size_t* ngroups, int depth = 0) {
+               PendingLong* pend, bool defer, int depth = 0) {
   const u32 tiles = plan_tiles(ctx->h_segs, nseg);
+  pend->slot = -1;
   if (tiles == 0) return CHGPU_OK;
-  const u32 cap = (u32)(ctx->cap / 2 + 16);
-  const int s_starts = take_ctr(ctx), s_medium = take_ctr(ctx), s_long = take_ctr(ctx);
+  const int s_medium = take_ctr(ctx), s_long = take_ctr(ctx);
   CK(cudaMemcpyAsync(ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc), cudaMemcpyHostToDevice,
                      ctx->st));
-  launch_group_detect(kF, ctx->d_segs, nseg, tiles, eqmode, ctx->d_starts, ctx->d_ctr + s_starts,
-                      cap, ctx->st);
-  ++ctx->launches;
-  u32 nstarts = 0;
-  TRY(read_ctr(ctx, s_starts, &nstarts));
-  nstarts = std::min(nstarts, cap);
-  if (ngroups) *ngroups += nstarts;
-  if (nstarts == 0) return CHGPU_OK;
-  launch_group_fix_small(kF, vF, ctx->d_segs, eqmode, ctx->d_starts, nstarts, ctx->d_medium,
-                         ctx->d_ctr + s_medium, ctx->st);
-  ++ctx->launches;
-  u32 nmedium = 0;
-  TRY(read_ctr(ctx, s_medium, &nmedium));
-  if (nmedium == 0) return CHGPU_OK;
-  launch_group_fix_medium(kF, vF, ctx->d_segs, ctx->d_medium, nmedium, ctx->d_long,
+  launch_group_scan(kF, vF, ctx->d_segs, nseg, tiles, eqmode, ctx->d_medium,
+                    ctx->d_ctr + s_medium, ctx->d_u64 + 10, ctx->st);
+  launch_group_fix_medium(kF, vF, ctx->d_segs, ctx->d_medium, ctx->d_ctr + s_medium, ctx->d_long,
                           ctx->d_ctr + s_long, ctx->st);
-  ++ctx->launches;
-  u32 nlong = 0;
-  TRY(read_ctr(ctx, s_long, &nlong));
-  if (nlong == 0) return CHGPU_OK;
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  pend->slot = s_long;
+  pend->eqmode = eqmode;
+  pend->depth = depth;
+  pend->regions.resize(nseg);
+  for (int s = 0; s < nseg; ++s) pend->regions[s] = ctx->h_segs[s].region;
+  pend->kF = kF;
+  pend->vF = vF;
+  pend->kS = kS;
+  pend->vS = vS;
+  if (defer) return CHGPU_OK;
+  bool had = false;
+  return resolve_long(ctx, *pend, &had);
+}
 
-  // Long groups: full sort of each group with the onesweep engine.
+// Long groups: a full sort of each group with the onesweep engine (on k
+// for quantizer groups, then their ==-primary runs on v; on v for
+// ==-primary runs).
+int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long) {
+  *had_long = false;
+  if (p.slot < 0) return CHGPU_OK;
+  u32 nlong = 0;
+  TRY(read_ctr(ctx, p.slot, &nlong));
+  if (nlong == 0) return CHGPU_OK;
+  *had_long = true;
   std::vector<Run> runs(nlong);
   CK(cudaMemcpyAsync(runs.data(), ctx->d_long, nlong * sizeof(Run), cudaMemcpyDeviceToHost,
                      ctx->st));
   TRY(sync(ctx));
-  std::vector<int> regions(nseg);
-  for (int s = 0; s < nseg; ++s) regions[s] = ctx->h_segs[s].region;
   std::sort(runs.begin(), runs.end(), [](const Run& a, const Run& b) { return a.start < b.start; });
   TRY(ensure_segs(ctx, nlong));
-  for (u32 i = 0; i < nlong; ++i)
-    ctx->h_segs[i] = make_seg(runs[i].start, runs[i].start, runs[i].len, regions[runs[i].seg]);
+  auto load_segs = [&]() {
+    for (u32 i = 0; i < nlong; ++i)
+      ctx->h_segs[i] = make_seg(runs[i].start, runs[i].start, runs[i].len, p.regions[runs[i].seg]);
+  };
+  load_segs();
   bool in_a = true;
   int passes = 0;
   // A = scratch, B = F: an even pass count ends back in F.
-  const int mode = (eqmode == kEqQ) ? kDigitK : kDigitV;
-  TRY(radix_sort(ctx, (int)nlong, kF, vF, kS, vS, kF, vF, mode, kPasses, &in_a, &passes));
+  const int mode = (p.eqmode == kEqQ) ? kDigitK : kDigitV;
+  TRY(radix_sort(ctx, (int)nlong, p.kF, p.vF, p.kS, p.vS, p.kF, p.vF, mode, kPasses, &in_a,
+                 &passes));
   if (passes % 2 == 1) {
     const u32 t2 = plan_tiles(ctx->h_segs, (int)nlong);
-    launch_seg_copy(kS, vS, kF, vF, ctx->d_segs, (int)nlong, t2, 0, ctx->st);
+    launch_seg_copy(p.kS, p.vS, p.kF, p.vF, ctx->d_segs, (int)nlong, t2, 0, ctx->st);
     ++ctx->launches;
   }
   CK(cudaGetLastError());
   // After a full sort on k, ==-equal primaries still need their v order.
-  if (eqmode == kEqQ && depth == 0) {
-    for (u32 i = 0; i < nlong; ++i)
-      ctx->h_segs[i] = make_seg(runs[i].start, runs[i].start, runs[i].len, regions[runs[i].seg]);
-    TRY(fix_groups(ctx, (int)nlong, kF, vF, kS, vS, kEqPrim, nullptr, depth + 1));
+  if (p.eqmode == kEqQ && p.depth == 0) {
+    load_segs();
+    PendingLong inner;
+    TRY(fix_groups(ctx, (int)nlong, p.kF, p.vF, p.kS, p.vS, kEqPrim, &inner, false, 1));
   }
   return CHGPU_OK;
 }
@@ -379,29 +405,33 @@ int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int
 struct Sorted {
   u64 *kF, *vF, *kS, *vS;
   int passes;
-  size_t groups;
+  PendingLong pend;  // long groups still to resolve (see fix_groups)
 };
 
-int sort_segments(chgpu_ctx* ctx, int nseg, int qbits, bool timed, Sorted* out) {
+// Sorts the nseg segments in ctx->h_segs (src layout in kbuf/vbuf) into
+// region order. Bucket phase keyed on the quantized primary when qbits > 0
+// (all qbits/8 passes run: no histogram round trip), else a full LSD on k
+// with trivial passes skipped; then the in-place group fix-up. With
+// defer_long the caller must call resolve_long(out->pend) later.
+int sort_segments(chgpu_ctx* ctx, int nseg, int qbits, bool timed, bool defer_long, Sorted* out) {
   std::vector<SegDesc> segs(ctx->h_segs, ctx->h_segs + nseg);
   bool in_a = true;
   int passes = 0;
   const int mode = qbits ? kDigitQ : kDigitK;
   const int npasses = qbits ? qbits / 8 : kPasses;
   TRY(radix_sort(ctx, nseg, ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, ctx->d_kbuf,
-                 ctx->d_vbuf, mode, npasses, &in_a, &passes, timed));
+                 ctx->d_vbuf, mode, npasses, &in_a, &passes, timed, qbits != 0));
   out->kF = in_a ? ctx->d_ka : ctx->d_kbuf;
   out->vF = in_a ? ctx->d_va : ctx->d_vbuf;
   out->kS = in_a ? ctx->d_kbuf : ctx->d_ka;
   out->vS = in_a ? ctx->d_vbuf : ctx->d_va;
   out->passes = passes;
-  out->groups = 0;
   for (int s = 0; s < nseg; ++s) {
     ctx->h_segs[s] = segs[s];
     ctx->h_segs[s].src_off = segs[s].dst_off;
   }
-  TRY(fix_groups(ctx, nseg, out->kF, out->vF, out->kS, out->vS, qbits ? kEqQ : kEqPrim,
-                 &out->groups));
+  TRY(fix_groups(ctx, nseg, out->kF, out->vF, out->kS, out->vS, qbits ? kEqQ : kEqPrim, &out->pend,
+                 defer_long));
   return CHGPU_OK;
 }
 
@@ -453,9 +483,9 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
   const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
   set_quantizer(ctx->h_segs[0], lo, hi, qbits);
   Sorted so{};
-  TRY(sort_segments(ctx, 1, qbits, false, &so));
+  TRY(sort_segments(ctx, 1, qbits, false, false, &so));
   *passes = so.passes;
-  *groups = so.groups;
+  *groups = 0;
   const int slot = take_ctr(ctx);
   launch_unique(so.kF, so.vF, s1, ctx->d_kept, ctx->d_status, next_tag(ctx), ctx->d_ctr + slot,
                 ctx->d_u64 + 4, ctx->st);
@@ -518,15 +548,14 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       CK(cudaEventRecord(ctx->ev_copy[c], ctx->st_copy));
       CK(cudaStreamWaitEvent(st, ctx->ev_copy[c], 0));
       const int blocks = (int)std::min<size_t>(per, (cnt + 255) / 256);
-      launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials + nparts, blocks, st);
-      nparts += blocks;
+      nparts += launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials + nparts,
+                                        blocks, st);
       ++ctx->launches;
     }
     CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
   } else {
     const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
-    launch_extremes_partial(pts_dev, n, 0, ctx->d_partials, blocks, st);
-    nparts = blocks;
+    nparts = launch_extremes_partial(pts_dev, n, 0, ctx->d_partials, blocks, st);
     ++ctx->launches;
   }
   const double2* pts = h_src ? ctx->d_pts : pts_dev;
@@ -587,9 +616,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     int qbits = 0;
     TRY(plan_regions(ctx, m, qi.q, &qbits));
     Sorted so{};
-    TRY(sort_segments(ctx, 4, qbits, true, &so));
+    TRY(sort_segments(ctx, 4, qbits, true, true, &so));
     D.sort_passes = so.passes;
-    D.tie_runs = so.groups;
     const bool sort_timed = s1 > 0;
     CK(cudaEventRecord(ctx->ev[6], st));
 
@@ -597,14 +625,32 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     // the non-degenerate branch only, exactly like the reference.
     if (chunk_count == 0) return fail(ctx, CHGPU_INVALID_ARG, "spa_filter: chunk_count must be >= 1");
     const SpaPlan plan = make_spa_plan(m, chunk_count, qi.q);
-    launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
-               next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
-    if (plan.total_chunks) ++ctx->launches;
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ctx->ev[8], st));
-    CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    TRY(sync(ctx));
+    auto spa_and_read = [&]() -> int {
+      CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), st));
+      launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
+                 next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
+      if (plan.total_chunks) ++ctx->launches;
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ctx->ev[8], st));
+      // kept counts, the group count and the long-group count in one trip
+      CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 10, sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, st));
+      if (so.pend.slot >= 0)
+        CK(cudaMemcpyAsync(&ctx->h->ctr[so.pend.slot], ctx->d_ctr + so.pend.slot, sizeof(u32),
+                           cudaMemcpyDeviceToHost, st));
+      return sync(ctx);
+    };
+    TRY(spa_and_read());
+    D.tie_runs = (size_t)ctx->h->uniq;
+    if (so.pend.slot >= 0 && ctx->h->ctr[so.pend.slot] > 0) {
+      // Rare: groups too long for shared memory. Sort them, then redo the
+      // SPA over the now fully ordered regions.
+      bool had = false;
+      TRY(resolve_long(ctx, so.pend, &had));
+      TRY(spa_and_read());
+    }
     size_t kept_counts[4], kept = 0;
     for (int r = 0; r < 4; ++r) {
       kept_counts[r] = (size_t)ctx->h->kept[r];
@@ -786,8 +832,9 @@ int chgpu_find_extremes(chgpu_ctx* ctx, const double* xy, size_t n, double* quad
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "too many points");
   cudaSetDevice(ctx->device);
   TRY(upload_points(ctx, xy, n));
-  const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
-  launch_extremes_partial(ctx->d_pts, n, 0, ctx->d_partials, blocks, ctx->st);
+  const int blocks = launch_extremes_partial(
+      ctx->d_pts, n, 0, ctx->d_partials, (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256),
+      ctx->st);
   launch_extremes_final(ctx->d_partials, blocks, ctx->d_qinfo, nullptr, ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, ctx->st));
@@ -873,7 +920,7 @@ int chgpu_sort_region(chgpu_ctx* ctx, int region, double* xy, size_t m) {
   TRY(ensure_segs(ctx, 1));
   ctx->h_segs[0] = make_seg(0, 0, m, region);
   Sorted so{};
-  TRY(sort_segments(ctx, 1, 0, false, &so));
+  TRY(sort_segments(ctx, 1, 0, false, false, &so));
   launch_decode(so.kF, so.vF, m, region, ctx->d_kept, ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(xy, ctx->d_kept, m * sizeof(double2), cudaMemcpyDeviceToHost, ctx->st));
@@ -926,9 +973,10 @@ int chgpu_shard_extremes(chgpu_ctx* ctx, const double* d_xy, size_t n, uint64_t 
                          double* quad_out, uint64_t* idx_out) {
   if (n == 0) return fail(ctx, CHGPU_EMPTY, "find_extremes: no points");
   cudaSetDevice(ctx->device);
-  const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
-  launch_extremes_partial(reinterpret_cast<const double2*>(d_xy), n, base_index, ctx->d_partials,
-                          blocks, ctx->st);
+  const int blocks =
+      launch_extremes_partial(reinterpret_cast<const double2*>(d_xy), n, base_index,
+                              ctx->d_partials,
+                              (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256), ctx->st);
   launch_extremes_final(ctx->d_partials, blocks, nullptr, ctx->d_rawquad, ctx->st);
   CK(cudaGetLastError());
   QuadCand qc;
@@ -1011,7 +1059,7 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     int qbits = 0;
     TRY(plan_regions(ctx, m, quad, &qbits));
     Sorted so{};
-    TRY(sort_segments(ctx, 4, qbits, false, &so));
+    TRY(sort_segments(ctx, 4, qbits, false, false, &so));
     const SpaPlan plan = make_spa_plan(m, chunk_count, quad);
     launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
                next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
