@@ -127,6 +127,14 @@ __device__ __forceinline__ u32 status_flag(u64 w, u32 tag) {
 __device__ __forceinline__ void store_status(u64* p, u64 w) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
+__device__ __forceinline__ u64 load_status_acquire(const u64* p) {
+  u64 w;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ u64 load_status(const u64* p) {
   u64 w;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");

@@ -42,12 +42,12 @@ __device__ __forceinline__ bool beats_top(const Cand& a, const Cand& b) {
   return a.i < b.i;
 }
 
-// Candidates with i == ~0 are empty and lose to everything.
+// Empty candidates carry +-inf sentinels (index ~0) and lose to any point.
 __device__ __forceinline__ void merge_quad(QuadCand& acc, const QuadCand& o) {
-  if (o.c[0].i != ~0ull && (acc.c[0].i == ~0ull || beats_left(o.c[0], acc.c[0]))) acc.c[0] = o.c[0];
-  if (o.c[1].i != ~0ull && (acc.c[1].i == ~0ull || beats_bottom(o.c[1], acc.c[1]))) acc.c[1] = o.c[1];
-  if (o.c[2].i != ~0ull && (acc.c[2].i == ~0ull || beats_right(o.c[2], acc.c[2]))) acc.c[2] = o.c[2];
-  if (o.c[3].i != ~0ull && (acc.c[3].i == ~0ull || beats_top(o.c[3], acc.c[3]))) acc.c[3] = o.c[3];
+  if (beats_left(o.c[0], acc.c[0])) acc.c[0] = o.c[0];
+  if (beats_bottom(o.c[1], acc.c[1])) acc.c[1] = o.c[1];
+  if (beats_right(o.c[2], acc.c[2])) acc.c[2] = o.c[2];
+  if (beats_top(o.c[3], acc.c[3])) acc.c[3] = o.c[3];
 }
 
 __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
@@ -60,15 +60,22 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 
 // Folds one point visited in increasing index order: strict comparisons
 // keep the earliest of ==-equal points, exactly like fold() (:12-17).
+// A point strictly inside the running box on a corner's axis cannot win that
+// corner, so each corner costs one compare on the common path; the full
+// lexicographic test only runs on the rare boundary hits. Empty corners
+// hold +-inf sentinels (inputs are finite), so no emptiness test is needed.
 __device__ __forceinline__ void fold_point(QuadCand& a, double x, double y, u64 i) {
-  if (a.c[0].i == ~0ull) {
-    a.c[0] = a.c[1] = a.c[2] = a.c[3] = Cand{x, y, i};
-    return;
-  }
-  if (less_xy(x, y, a.c[0].x, a.c[0].y)) a.c[0] = Cand{x, y, i};
-  if (less_yx(x, y, a.c[1].x, a.c[1].y)) a.c[1] = Cand{x, y, i};
-  if (less_xy(a.c[2].x, a.c[2].y, x, y)) a.c[2] = Cand{x, y, i};
-  if (less_yx(a.c[3].x, a.c[3].y, x, y)) a.c[3] = Cand{x, y, i};
+  if (!(x > a.c[0].x) && less_xy(x, y, a.c[0].x, a.c[0].y)) a.c[0] = Cand{x, y, i};
+  if (!(y > a.c[1].y) && less_yx(x, y, a.c[1].x, a.c[1].y)) a.c[1] = Cand{x, y, i};
+  if (!(x < a.c[2].x) && less_xy(a.c[2].x, a.c[2].y, x, y)) a.c[2] = Cand{x, y, i};
+  if (!(y < a.c[3].y) && less_yx(a.c[3].x, a.c[3].y, x, y)) a.c[3] = Cand{x, y, i};
+}
+
+__device__ __forceinline__ void empty_quad(QuadCand& a) {
+  a.c[0] = Cand{INFINITY, INFINITY, ~0ull};
+  a.c[1] = Cand{INFINITY, INFINITY, ~0ull};
+  a.c[2] = Cand{-INFINITY, -INFINITY, ~0ull};
+  a.c[3] = Cand{-INFINITY, -INFINITY, ~0ull};
 }
 
 constexpr int kK1Threads = 256;
@@ -76,12 +83,11 @@ constexpr int kK1Unroll = 4;
 
 // Grid-stride pass: thread t visits t, t+T, t+2T, ... in increasing order,
 // so its running fold is the sequential fold of its subsequence.
-__global__ __launch_bounds__(kK1Threads) void k_extremes_partial(const double2* __restrict__ pts,
+__global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(const double2* __restrict__ pts,
                                                                  u64 n, u64 base_index,
                                                                  QuadCand* __restrict__ partials) {
   QuadCand acc;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) acc.c[c] = Cand{0.0, 0.0, ~0ull};
+  empty_quad(acc);
   const u64 stride = (u64)gridDim.x * blockDim.x;
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
@@ -117,8 +123,7 @@ __global__ __launch_bounds__(kK1Threads) void k_extremes_partial(const double2* 
 __global__ void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
                                  QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
   QuadCand acc;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) acc.c[c] = Cand{0.0, 0.0, ~0ull};
+  empty_quad(acc);
   for (int p = threadIdx.x; p < nparts; p += blockDim.x) merge_quad(acc, partials[p]);
   // Tree combine: warp shuffles, then the 8 warp results (order-free: ties
   // fall back to the global index).
@@ -200,26 +205,33 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Persistent CTAs, double-buffered: while a tile is classified and its
-// survivors scattered, the next tile streams into shared memory with
-// cp.async (no registers held by in-flight loads). Tiles are claimed in
-// increasing order by running CTAs, which keeps the look-back deadlock-free.
+// One tile (2048 points) per CTA, streamed into shared memory with
+// cp.async. The region sort that follows canonically orders each region by
+// its full key, so the order of records inside a stream is free: a tile
+// reserves its output range per stream with one global atomicAdd each,
+// instead of an ordered (look-back) scan. Per point the work is the
+// classification, a register counter increment and one record store.
 template <bool kGivenLabels>
 __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
-    u64* __restrict__ vbuf, u64 ncap, u64* __restrict__ status, u32 tag,
-    u32* __restrict__ tile_ctr, u32 num_tiles, u32* __restrict__ counts_out) {
-  extern __shared__ __align__(16) double2 sbuf[];  // [2][kK2Tile]
-  __shared__ u32 s_tile[2];
-  __shared__ u32 s_warp_cnt[kK2Threads / 32][4];
-  __shared__ u32 s_excl[4];
+    u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out) {
+  extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
+  __shared__ u32 s_wtot[kK2Threads / 32][4];
+  __shared__ u32 s_base[4];
   __shared__ QuadEdges s_edges;
   __shared__ int s_lex;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u64 tile_base = (u64)blockIdx.x * kK2Tile;
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    const bool ok = idx < n;
+    cp_async16(sbuf + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
+  }
+  cp_async_commit();
   if (tid == 0) {
-    s_tile[0] = atomicAdd(tile_ctr, 1u);
     const QuadInfo qi = *qinfo;
     for (int c = 0; c < 4; ++c) {
       const int d = (c + 1) & 3;
@@ -234,118 +246,71 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
   }
   __syncthreads();
   const bool lex = s_lex != 0;
+  const QuadEdges e = s_edges;
+  cp_async_wait<0>();  // each thread reads back only its own copies
 
-  auto issue = [&](int stage, u32 t) {
-    const u64 base = (u64)t * kK2Tile;
-    double2* dst = sbuf + stage * kK2Tile;
+  u32 codes = 0;  // 3 bits of stream id per item
+  u32 cnt[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int j = 0; j < kK2Items; ++j) {
-      const u64 idx = base + (u64)j * kK2Threads + tid;
-      const bool ok = idx < n;
-      cp_async16(dst + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
-    }
-  };
-  if (s_tile[0] < num_tiles) issue(0, s_tile[0]);
-  cp_async_commit();
-
-  int stage = 0;
-  while (true) {
-    const u32 tile = s_tile[stage];
-    if (tile >= num_tiles) break;
-    if (tid == 0) s_tile[stage ^ 1] = atomicAdd(tile_ctr, 1u);
-    __syncthreads();  // next tile id visible; previous use of sbuf[stage^1] finished
-    const u32 nt = s_tile[stage ^ 1];
-    if (nt < num_tiles) issue(stage ^ 1, nt);
-    cp_async_commit();
-    cp_async_wait<1>();  // this thread's copies of the current tile have landed
-
-    const double2* sb = sbuf + stage * kK2Tile;
-    const u64 tile_base = (u64)tile * kK2Tile;
-    int reg[kK2Items];
-    u32 rank[kK2Items];
-    u32 run[4] = {0, 0, 0, 0};  // warp-uniform running counts per stream
-#pragma unroll
-    for (int j = 0; j < kK2Items; ++j) {
-      const u64 idx = tile_base + (u64)j * kK2Threads + tid;
-      int r = 0;
-      if (idx < n) {
-        if (kGivenLabels) {
-          r = (int)given_labels[idx];
-        } else {
-          const double2 p = sb[j * kK2Threads + tid];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (cross_edge(s_edges.ax[c], s_edges.ay[c], s_edges.ex[c], s_edges.ey[c], p.x, p.y) <
-                0.0) {
-              r = c + 1;
-              break;
-            }
-          }
-        }
-        if (lex && r != 0) r = 1;
-      }
-      reg[j] = r;
-      u32 rk = 0;
-#pragma unroll
-      for (int s = 1; s <= 4; ++s) {
-        const unsigned m = __ballot_sync(0xffffffffu, r == s);
-        rk = (r == s) ? run[s - 1] + __popc(m & lanemask_lt()) : rk;
-        run[s - 1] += __popc(m);
-      }
-      rank[j] = rk;
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < 4; ++s) s_warp_cnt[warp][s] = run[s];
-    }
-    __syncthreads();
-
-    // Warp s (s < 4) owns stream s+1: block-exclusive scan over warps, then
-    // the look-back for this tile.
-    if (warp < 4) {
-      const int s = warp;
-      u32 agg = 0;
-      if (lane == 0) {
-        for (int w = 0; w < kK2Threads / 32; ++w) {
-          const u32 c = s_warp_cnt[w][s];
-          s_warp_cnt[w][s] = agg;
-          agg += c;
-        }
-      }
-      agg = __shfl_sync(0xffffffffu, agg, 0);
-      u64* col = status + s;
-      u32 excl = 0;
-      if (tile == 0) {
-        if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, agg));
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    int r = 0;
+    if (idx < n) {
+      if (kGivenLabels) {
+        r = (int)given_labels[idx];
       } else {
-        if (lane == 0) store_status(col + (size_t)tile * 4, make_status(tag, kFlagAgg, agg));
-        excl = warp_lookback(col, 4, (int)tile, 0, tag);
-        if (lane == 0)
-          store_status(col + (size_t)tile * 4, make_status(tag, kFlagPrefix, excl + agg));
+        const double2 p = sbuf[j * kK2Threads + tid];
+        r = classify(e, p.x, p.y);
       }
-      if (lane == 0) {
-        s_excl[s] = excl;
-        if (tile == num_tiles - 1) counts_out[s + 1] = excl + agg;
-      }
+      if (lex && r != 0) r = 1;
     }
-    __syncthreads();
-
+    codes |= (u32)r << (3 * j);
 #pragma unroll
-    for (int j = 0; j < kK2Items; ++j) {
-      const int s = reg[j];
-      if (s != 0) {
-        const double2 p = sb[j * kK2Threads + tid];
-        const u64 pos = (u64)s_excl[s - 1] + s_warp_cnt[warp][s - 1] + rank[j];
-        const u64 slot = stream_slot(s, pos, ncap);
-        u64 k, v;
-        encode_point(lex ? 0 : s, p.x, p.y, k, v);
-        kbuf[slot] = k;
-        vbuf[slot] = v;
-      }
-    }
-    stage ^= 1;
+    for (int s = 0; s < 4; ++s) cnt[s] += (r == s + 1);
   }
-  cp_async_wait<0>();
+  // Warp-exclusive prefix of the per-thread counts, per stream.
+  u32 excl[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    u32 x = cnt[s];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    excl[s] = x - cnt[s];
+    if (lane == 31) s_wtot[warp][s] = x;
+  }
+  __syncthreads();
+  if (tid < 4) {
+    u32 tot = 0;
+    for (int w = 0; w < kK2Threads / 32; ++w) {
+      const u32 c = s_wtot[w][tid];
+      s_wtot[w][tid] = tot;
+      tot += c;
+    }
+    s_base[tid] = tot ? atomicAdd(&counts_out[tid + 1], tot) : 0u;
+  }
+  __syncthreads();
+  u32 pos[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) pos[s] = s_base[s] + s_wtot[warp][s] + excl[s];
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const int r = (codes >> (3 * j)) & 7;
+    if (r != 0) {
+      const double2 p = sbuf[j * kK2Threads + tid];
+      u32 slot_pos = 0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (r == s + 1) slot_pos = pos[s]++;
+      const u64 slot = stream_slot(r, slot_pos, ncap);
+      u64 k, v;
+      encode_point(lex ? 0 : r, p.x, p.y, k, v);
+      kbuf[slot] = k;
+      vbuf[slot] = v;
+    }
+  }
 }
 
 // Labels only (the classify() stage tap, classify.cpp:9-33).
@@ -411,32 +376,16 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
 
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf,
-                             u64* vbuf, u64 ncap, u64* status, u32 tag, u32* tile_ctr,
-                             u32* counts_out, cudaStream_t st) {
+                             u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
-  constexpr size_t smem = 2 * kK2Tile * sizeof(double2);
-  static int occ[2] = {0, 0};
-  static int sms = 0;
-  const int g = given_labels ? 1 : 0;
-  if (!occ[g]) {
-    auto fn = given_labels ? k_classify_compact<true> : k_classify_compact<false>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[g], fn, kK2Threads, smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ[g] < 1) occ[g] = 1;
-  }
-  const u32 grid = std::min<u32>(tiles, (u32)(occ[g] * sms));
+  constexpr size_t smem = kK2Tile * sizeof(double2);
   if (given_labels)
-    k_classify_compact<true><<<grid, kK2Threads, smem, st>>>(pts, n, qinfo, given_labels, force_lex,
-                                                             kbuf, vbuf, ncap, status, tag, tile_ctr,
-                                                             tiles, counts_out);
+    k_classify_compact<true><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, given_labels,
+                                                              force_lex, kbuf, vbuf, ncap, counts_out);
   else
-    k_classify_compact<false><<<grid, kK2Threads, smem, st>>>(pts, n, qinfo, nullptr, force_lex,
-                                                              kbuf, vbuf, ncap, status, tag,
-                                                              tile_ctr, tiles, counts_out);
+    k_classify_compact<false><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, nullptr, force_lex,
+                                                               kbuf, vbuf, ncap, counts_out);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

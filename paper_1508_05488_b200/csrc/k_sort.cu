@@ -170,7 +170,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
     const u32* __restrict__ digit_excl, int pass, u64* __restrict__ status, u32 tag,
-    u32* __restrict__ tile_ctr) {
+    u32* __restrict__ tile_ctr, u32 total_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
@@ -208,23 +208,32 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   asm volatile("cp.async.commit_group;" ::: "memory");
 
   // Warp-local multisplit: items are ranked in (warp, item, lane) order,
-  // which is the input order inside the tile, so the pass is stable.
+  // which is the input order inside the tile, so the pass is stable. The
+  // peer masks are independent of each other and are computed first; only
+  // the per-warp counter updates form a chain.
+  unsigned peers[kSortItems];
+  u32 dig[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u32 li = wbase + j * 32 + lane;
+    const bool valid = li < cnt;
+    dig[j] = digit_of<kMode>(sd, kk[j], kk[j], pass);
+    peers[j] = __match_any_sync(0xffffffffu, valid ? dig[j] : (0x100u | (u32)lane));
+  }
   u32 code[kSortItems];  // digit | rank << 8
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const u32 li = wbase + j * 32 + lane;
     const bool valid = li < cnt;
-    const u32 d = digit_of<kMode>(sd, kk[j], kk[j], pass);
-    const u32 key = valid ? d : (0x100u | (u32)lane);
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
+    const u32 d = dig[j];
+    const int leader = __ffs(peers[j]) - 1;
     u32 old = 0;
     if (valid && lane == leader) {
       old = S.whist[warp][d];
-      S.whist[warp][d] = old + __popc(peers);
+      S.whist[warp][d] = old + __popc(peers[j]);
     }
     old = __shfl_sync(0xffffffffu, old, leader);
-    code[j] = d | ((old + __popc(peers & lanemask_lt())) << 8);
+    code[j] = d | ((old + __popc(peers[j] & lanemask_lt())) << 8);
   }
   __syncthreads();
 
@@ -250,26 +259,70 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   const u32 bexcl = wpre + incl - tile_cnt;
   S.bin_excl[b] = bexcl;
 
-  // Decoupled look-back, one chain per (segment, bin).
-  u64* col = status + b;
+  // Tile-level decoupled look-back. status[0, T) holds one flag word per
+  // tile; agg[T][256] and inc[T][256] (u32, after the flags) hold the
+  // per-digit tile counts and inclusive prefixes. A tile publishes its whole
+  // row at once, so the look-back finds the nearest predecessor with a
+  // prefix using one warp over 32 flags at a time and then reads the rows in
+  // between with independent loads: a few round trips whatever the depth.
+  u32* agg = reinterpret_cast<u32*>(status + total_tiles);
+  u32* inc = agg + (size_t)total_tiles * kDigits;
   u32 before = 0;
+  // Publication is the release pattern "row stores; bar.sync; one thread:
+  // fence.acq_rel.gpu + flag store"; readers acquire the flag in one warp
+  // and bar.sync before touching rows.
   if (tile == sd.tile_begin) {
-    store_status(col + (size_t)tile * kDigits, make_status(tag, kFlagPrefix, tile_cnt));
-  } else {
-    store_status(col + (size_t)tile * kDigits, make_status(tag, kFlagAgg, tile_cnt));
-    int j = (int)tile - 1;
-    while (true) {
-      u64 w;
-      u32 f;
-      do {
-        w = load_status(col + (size_t)j * kDigits);
-        f = status_flag(w, tag);
-      } while (f == kFlagNone);
-      before += (u32)w;
-      if (f == kFlagPrefix || j == (int)sd.tile_begin) break;
-      --j;
+    __stcg(inc + (size_t)tile * kDigits + b, tile_cnt);
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel_gpu();
+      store_status(status + tile, make_status(tag, kFlagPrefix, 0));
     }
-    store_status(col + (size_t)tile * kDigits, make_status(tag, kFlagPrefix, before + tile_cnt));
+  } else {
+    __stcg(agg + (size_t)tile * kDigits + b, tile_cnt);
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {
+        fence_acq_rel_gpu();
+        store_status(status + tile, make_status(tag, kFlagAgg, 0));
+      }
+      int base = (int)tile - 1;
+      int front;
+      while (true) {
+        const int j = base - lane;
+        u32 f = kFlagPrefix;  // the segment's first tile always holds a prefix
+        if (j >= (int)sd.tile_begin) {
+          do {
+            f = status_flag(load_status_acquire(status + j), tag);
+          } while (f == kFlagNone);
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, f == kFlagPrefix);
+        if (pm) {
+          front = base - (__ffs(pm) - 1);
+          break;
+        }
+        base -= 32;
+      }
+      if (lane == 0) S.seg = front;  // reuse: frontier tile
+    }
+    __syncthreads();
+    const int front = S.seg;
+    before = __ldcg(inc + (size_t)front * kDigits + b);
+    int j = front + 1;
+    for (; j + 3 < (int)tile; j += 4) {
+      const u32 a0 = __ldcg(agg + (size_t)j * kDigits + b);
+      const u32 a1 = __ldcg(agg + (size_t)(j + 1) * kDigits + b);
+      const u32 a2 = __ldcg(agg + (size_t)(j + 2) * kDigits + b);
+      const u32 a3 = __ldcg(agg + (size_t)(j + 3) * kDigits + b);
+      before += a0 + a1 + a2 + a3;
+    }
+    for (; j < (int)tile; ++j) before += __ldcg(agg + (size_t)j * kDigits + b);
+    __stcg(inc + (size_t)tile * kDigits + b, before + tile_cnt);
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel_gpu();
+      store_status(status + tile, make_status(tag, kFlagPrefix, 0));
+    }
   }
   S.bin_base[b] =
       sd.dst_off + digit_excl[((size_t)segi * kPasses + pass) * kDigits + b] + before - bexcl;
@@ -293,6 +346,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   // global memory, so warps write contiguous runs.
   u64* rout = kMode == kDigitV ? vout : kout;
   u64* oout = kMode == kDigitV ? kout : vout;
+#pragma unroll 4
   for (u32 i = tid; i < cnt; i += kSortThreads) {
     const u64 dst = S.bin_base[S.sdig[i]] + i;
     rout[dst] = S.kstage[i];
@@ -328,9 +382,12 @@ __device__ __forceinline__ bool group_eq(int eqmode, const SegDesc& s, u64 a, u6
   return eqmode == kEqQ ? quantize(s, a) == quantize(s, b) : prim_eq(s.region, a, b);
 }
 
+// region_less on (canonical k, v); ties (==-equal points) fall back to the
+// raw k so the order is total on bits and the sort output is independent of
+// the order records arrived in.
 __device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u64 kb, u64 vb) {
   const u64 ca = canon_k(region, ka), cb = canon_k(region, kb);
-  return ca < cb || (ca == cb && va < vb);
+  return ca < cb || (ca == cb && (va < vb || (va == vb && ka < kb)));
 }
 
 struct GroupRun {
@@ -348,69 +405,81 @@ __device__ __forceinline__ u64 group_key(int eqmode, const SegDesc& s, u64 k) {
   return eqmode == kEqQ ? (u64)quantize(s, k) : canon_k(s.region, k);
 }
 
-// Detects group starts tile by tile (group keys computed once per record
-// into shared memory) and fixes each group on the spot: the thread owning a
-// group start insertion-sorts it in registers when it holds at most
-// kSmallGroup records, else queues it for k_group_fix_medium.
+// Detects group starts tile by tile and fixes each group on the spot, all
+// in shared memory: the tile's records plus a kSmallGroup halo are loaded
+// once (coalesced), the thread owning a group start insertion-sorts it in
+// shared memory when it holds at most kSmallGroup records and writes only
+// that group back; longer groups are queued for k_group_fix_medium.
+constexpr int kGroupWin = kSortTile + kSmallGroup + 1;
+struct GroupSmem {
+  u64 k[kGroupWin];
+  u64 v[kGroupWin];
+  u64 g[kGroupWin + 1];  // g[0]: group key of the record before the tile
+};
+
 __global__ __launch_bounds__(256) void k_group_scan(u64* __restrict__ k, u64* __restrict__ v,
                                                     const SegDesc* __restrict__ segs, int nseg,
                                                     int eqmode, GroupRun* __restrict__ medium,
                                                     u32* __restrict__ nmedium,
                                                     unsigned long long* __restrict__ ngroups) {
-  __shared__ u64 gk[kSortTile + 2];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GroupSmem& S = *reinterpret_cast<GroupSmem*>(smem_raw);
+  __shared__ u32 s_found;
   const u32 tile = blockIdx.x;
   const int s = find_segment(segs, nseg, tile);
   const SegDesc sd = segs[s];
   const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
   if (e0 >= sd.len) return;
   const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
+  const u32 win = (u32)min((u64)cnt + kSmallGroup + 1, (u64)sd.len - e0);
   const u64 base = sd.dst_off + e0;
-  // gk[0] = record e0-1 (if any), gk[1 + i] = record e0+i, gk[cnt+1] = e0+cnt (if any)
-  for (u32 i = threadIdx.x; i < cnt + 2; i += blockDim.x) {
-    const long long pos = (long long)e0 + (long long)i - 1;
-    u64 g = ~0ull;
-    if (pos >= 0 && (u64)pos < sd.len) g = group_key(eqmode, sd, k[sd.dst_off + pos]);
-    gk[i] = g;
+  if (threadIdx.x == 0) {
+    s_found = 0;
+    S.g[0] = e0 > 0 ? group_key(eqmode, sd, k[base - 1]) : ~0ull;
+  }
+  for (u32 i = threadIdx.x; i < win; i += blockDim.x) {
+    const u64 kx = k[base + i];
+    S.k[i] = kx;
+    S.v[i] = v[base + i];
+    S.g[i + 1] = group_key(eqmode, sd, kx);
   }
   __syncthreads();
   u32 found = 0;
   for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const u64 pos = e0 + i;
-    if (pos + 1 >= sd.len || gk[i + 1] != gk[i + 2]) continue;
-    if (pos > 0 && gk[i] == gk[i + 1]) continue;  // not the first of its group
+    if (i + 1 >= win || S.g[i + 1] != S.g[i + 2]) continue;  // no successor in the group
+    if (S.g[i] == S.g[i + 1]) continue;                        // not the first of its group
     ++found;
-    const u64 a = base + i;
-    const u64 g0 = gk[i + 1];
+    const u64 g0 = S.g[i + 1];
     u32 len = 2;
-    while (pos + len < sd.len && len <= kSmallGroup) {
-      const u64 gn = (i + len + 1 < cnt + 2) ? gk[i + len + 1]
-                                             : group_key(eqmode, sd, k[a + len]);
-      if (gn != g0) break;
-      ++len;
-    }
-    if (len > kSmallGroup) {
-      while (pos + len < sd.len && group_key(eqmode, sd, k[a + len]) == g0) ++len;
+    while (i + len < win && S.g[i + len + 1] == g0) ++len;
+    if (len > kSmallGroup || (i + len == win && e0 + win < sd.len)) {
+      // Longer than the halo: measure it in global memory, queue it.
+      const u64 a = base + i;
+      while (e0 + i + len < sd.len && group_key(eqmode, sd, k[a + len]) == g0) ++len;
+      if (len <= kSmallGroup) goto small;  // ended right at the window edge
       medium[atomicAdd(nmedium, 1u)] = GroupRun{a, len, s};
       continue;
     }
-    u64 rk[kSmallGroup], rv[kSmallGroup];
-    for (u32 j = 0; j < len; ++j) {
-      const u64 kx = k[a + j], vx = v[a + j];
+  small:
+    for (u32 j = 1; j < len; ++j) {
+      const u64 kx = S.k[i + j], vx = S.v[i + j];
       u32 t = j;
-      while (t > 0 && rec_less(sd.region, kx, vx, rk[t - 1], rv[t - 1])) {
-        rk[t] = rk[t - 1];
-        rv[t] = rv[t - 1];
+      while (t > 0 && rec_less(sd.region, kx, vx, S.k[i + t - 1], S.v[i + t - 1])) {
+        S.k[i + t] = S.k[i + t - 1];
+        S.v[i + t] = S.v[i + t - 1];
         --t;
       }
-      rk[t] = kx;
-      rv[t] = vx;
+      S.k[i + t] = kx;
+      S.v[i + t] = vx;
     }
     for (u32 j = 0; j < len; ++j) {
-      k[a + j] = rk[j];
-      v[a + j] = rv[j];
+      k[base + i + j] = S.k[i + j];
+      v[base + i + j] = S.v[i + j];
     }
   }
-  if (found) atomicAdd(ngroups, (unsigned long long)found);
+  if (found) atomicAdd(&s_found, found);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_found) atomicAdd(ngroups, (unsigned long long)s_found);
 }
 
 // One block per medium group: bitonic sort in shared memory; groups longer
@@ -448,7 +517,8 @@ __global__ __launch_bounds__(256) void k_group_fix_medium(u64* __restrict__ k, u
           const u32 jx = i ^ stride;
           if (jx > i) {
             const bool up = (i & size) == 0;
-            const bool gt = sc[i] > sc[jx] || (sc[i] == sc[jx] && sv[i] > sv[jx]);
+            const bool gt = sc[i] > sc[jx] ||
+                            (sc[i] == sc[jx] && (sv[i] > sv[jx] || (sv[i] == sv[jx] && sk[i] > sk[jx])));
             if (gt == up) {
               u64 t = sk[i]; sk[i] = sk[jx]; sk[jx] = t;
               t = sv[i]; sv[i] = sv[jx]; sv[jx] = t;
@@ -506,7 +576,8 @@ static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout
     configured = true;
   }
   k_onesweep<kMode><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
-      kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr);
+      kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr,
+      total_tiles);
 }
 
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
@@ -537,7 +608,14 @@ void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const
 void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
                        void* medium, u32* nmedium, unsigned long long* ngroups, cudaStream_t st) {
   if (total_tiles == 0) return;
-  k_group_scan<<<total_tiles, 256, 0, st>>>(k, v, segs, nseg, eqmode, (GroupRun*)medium, nmedium,
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_group_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(GroupSmem));
+    configured = true;
+  }
+  k_group_scan<<<total_tiles, 256, sizeof(GroupSmem), st>>>(k, v, segs, nseg, eqmode,
+                                                           (GroupRun*)medium, nmedium,
                                             ngroups);
 }
 

@@ -25,8 +25,7 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, 
 // K2
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
-                             u64 ncap, u64* status, u32 tag, u32* tile_ctr, u32* counts_out,
-                             cudaStream_t st);
+                             u64 ncap, u32* counts_out, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

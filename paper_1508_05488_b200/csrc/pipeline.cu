@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -92,10 +93,16 @@ struct chgpu_ctx {
 
 namespace {
 
+// Look-back tags are drawn from one process-wide counter, so no two
+// launches (of any context) share a tag until it wraps after 2^30.
 u32 next_tag(chgpu_ctx* c) {
-  c->tag = (c->tag + 1) & 0x3FFFFFFFu;
-  if (c->tag == 0) c->tag = 1;
-  return c->tag;
+  static std::atomic<u32> counter{0};
+  u32 t;
+  do {
+    t = (counter.fetch_add(1, std::memory_order_relaxed) + 1) & 0x3FFFFFFFu;
+  } while (t == 0);
+  c->tag = t;
+  return t;
 }
 
 #define CK(call)                                                     \
@@ -187,7 +194,9 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
   // 4096-record tile (+1 tile per segment), the SPA one per chunk (<= cap).
   ctx->status_words = std::max(cap + 4096, (cap / kSortTile + 4096) * (size_t)kDigits);
   CK(cudaMalloc(&ctx->d_status, ctx->status_words * sizeof(u64)));
-  CK(cudaMemset(ctx->d_status, 0, ctx->status_words * sizeof(u64)));
+  // Ordered on the context stream: a stale word from recycled memory must
+  // never be mistaken for a current one.
+  CK(cudaMemsetAsync(ctx->d_status, 0, ctx->status_words * sizeof(u64), ctx->st));
   CK(cudaMalloc(&ctx->d_starts, (cap / 2 + 16) * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_medium, (cap / 2 + 16) * group_run_bytes()));
   CK(cudaMalloc(&ctx->d_long, (cap / 2049 + 16) * group_run_bytes()));
@@ -563,11 +572,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   CK(cudaEventRecord(ctx->ev[1], st));
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87).
-  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
   launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
-                          ctx->cap, ctx->d_status, next_tag(ctx), ctx->d_ctr + k2_slot,
-                          ctx->d_ctr + cnt_slot, st);
+                          ctx->cap, ctx->d_ctr + cnt_slot, st);
   ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
@@ -871,11 +879,10 @@ int chgpu_discard_round1(chgpu_ctx* ctx, const double* xy, const uint8_t* labels
   TRY(upload_points(ctx, xy, n));
   CK(cudaMemcpyAsync(ctx->d_flags, labels, n, cudaMemcpyHostToDevice, ctx->st));
   TRY(begin_call(ctx));
-  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
   launch_classify_compact(ctx->d_pts, (u32)n, ctx->d_qinfo, ctx->d_flags, 0, ctx->d_kbuf,
-                          ctx->d_vbuf, ctx->cap, ctx->d_status, next_tag(ctx),
-                          ctx->d_ctr + k2_slot, ctx->d_ctr + cnt_slot, ctx->st);
+                          ctx->d_vbuf, ctx->cap, ctx->d_ctr + cnt_slot, ctx->st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, ctx->st));
@@ -1033,11 +1040,11 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
   TRY(begin_call(ctx));
   TRY(upload_quad(ctx, quad));
   const bool degenerate = ctx->h->qi.degenerate != 0;
-  const int k2_slot = take_ctr(ctx), cnt_slot = ctx->ctr_used;
+  const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
   launch_classify_compact(reinterpret_cast<const double2*>(d_xy), (u32)n, ctx->d_qinfo, nullptr,
-                          degenerate ? 1 : 0, ctx->d_kbuf, ctx->d_vbuf, ctx->cap, ctx->d_status,
-                          next_tag(ctx), ctx->d_ctr + k2_slot, ctx->d_ctr + cnt_slot, st);
+                          degenerate ? 1 : 0, ctx->d_kbuf, ctx->d_vbuf, ctx->cap,
+                          ctx->d_ctr + cnt_slot, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
