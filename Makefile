@@ -25,7 +25,8 @@ CXXFLAGS := -O3 -std=gnu++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$
             -I/usr/local/cuda/include
 REF      ?= /root/reference/proj
 
-CU_SRCS  := $(CSRC)/k_discard.cu $(CSRC)/k_sort.cu $(CSRC)/k_spa.cu $(CSRC)/pipeline.cu
+CU_SRCS  := $(CSRC)/k_discard.cu $(CSRC)/k_sort.cu $(CSRC)/k_bucket.cu $(CSRC)/k_spa.cu \
+            $(CSRC)/pipeline.cu
 CXX_SRCS := $(CSRC)/finisher.cpp $(CSRC)/datasets.cpp
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CXX_SRCS))

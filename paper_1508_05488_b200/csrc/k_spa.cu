@@ -273,3 +273,137 @@ void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status,
 }
 
 }  // namespace chgpu
+
+namespace chgpu {
+
+// ------------------------------------------------------------------ SPA, warp per chunk
+//
+// One warp scans one chunk, 256 records per step (8 coalesced rows of 32),
+// with a shuffle scan per row and the carry in a register: no block
+// barriers and no inter-chunk dependency. Kept records are written,
+// decoded, compactly at the start of the chunk's own range of a scratch
+// array (ranges never overlap); k_spa_offsets scans the per-chunk counts and
+// k_spa_gather moves each chunk's run to its final, region-ordered place.
+
+constexpr int kSpaRows = 8;
+
+__global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
+                                                  const u64* __restrict__ v, SpaPlan plan,
+                                                  double2* __restrict__ scratch,
+                                                  u32* __restrict__ chunk_kept) {
+  const int lane = threadIdx.x & 31;
+  const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= plan.total_chunks) return;
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const u64 cl = c - plan.chunk_begin[r];
+  const u64 begin = plan.off[r] + cl * plan.chunk_size[r];
+  const u64 len = min((u64)plan.chunk_size[r], (u64)plan.m[r] - cl * plan.chunk_size[r]);
+  const bool is_min = (region == 1 || region == 4);
+  const double ident = is_min ? INFINITY : -INFINITY;
+  double carry = (cl == 0) ? plan.seed[r] : ident;
+  u32 kept = 0;
+  for (u64 t0 = 0; t0 < len; t0 += 32 * kSpaRows) {
+    double g[kSpaRows];
+#pragma unroll
+    for (int j = 0; j < kSpaRows; ++j) {
+      const u64 idx = t0 + j * 32 + lane;
+      g[j] = idx < len ? guarded_of(region, v[begin + idx]) : ident;
+    }
+#pragma unroll
+    for (int j = 0; j < kSpaRows; ++j) {
+      double x = g[j];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = op_ext(is_min, y, x);
+      }
+      double ex = __shfl_up_sync(0xffffffffu, x, 1);
+      if (lane == 0) ex = ident;
+      const u64 idx = t0 + j * 32 + lane;
+      const bool keep = idx < len && !steps_back(is_min, g[j], op_ext(is_min, carry, ex));
+      carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, x, 31));
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const u64 a = begin + idx;
+        double px, py;
+        decode_point(region, k[a], v[a], px, py);
+        scratch[begin + kept + __popc(mask & lanemask_lt())] = make_double2(px, py);
+      }
+      kept += __popc(mask);
+    }
+  }
+  if (lane == 0) chunk_kept[c] = kept;
+}
+
+// Exclusive scan of the per-chunk kept counts (one block) and the
+// per-region totals.
+__global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ chunk_kept, SpaPlan plan,
+                                                      u32* __restrict__ offs,
+                                                      unsigned long long* __restrict__ kept_counts) {
+  __shared__ u32 wsum[32];
+  __shared__ u32 carry;
+  __shared__ unsigned long long reg[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x < 4) reg[threadIdx.x] = 0;
+  __syncthreads();
+  for (u32 c0 = 0; c0 < plan.total_chunks; c0 += blockDim.x) {
+    const u32 c = c0 + threadIdx.x;
+    const u32 x0 = c < plan.total_chunks ? chunk_kept[c] : 0u;
+    u32 x = x0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    u32 pre = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) pre += wsum[w];
+      tot += wsum[w];
+    }
+    if (c < plan.total_chunks) {
+      offs[c] = carry + pre + x - x0;
+      if (x0) {
+        int r = 0;
+        while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+        atomicAdd(&reg[r], (unsigned long long)x0);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) kept_counts[threadIdx.x] = reg[threadIdx.x];
+}
+
+__global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ scratch,
+                                                    SpaPlan plan, const u32* __restrict__ chunk_kept,
+                                                    const u32* __restrict__ offs,
+                                                    double2* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= plan.total_chunks) return;
+  const u32 kc = chunk_kept[c];
+  if (!kc) return;
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const u64 begin = plan.off[r] + (u64)(c - plan.chunk_begin[r]) * plan.chunk_size[r];
+  const u32 o = offs[c];
+  for (u32 i = lane; i < kc; i += 32) out[o + i] = scratch[begin + i];
+}
+
+void launch_spa_warp(const u64* k, const u64* v, const SpaPlan& plan, double2* scratch,
+                     u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
+                     cudaStream_t st) {
+  if (plan.total_chunks == 0) return;
+  const u32 blocks = (plan.total_chunks + 7) / 8;
+  k_spa_warp<<<blocks, 256, 0, st>>>(k, v, plan, scratch, chunk_kept);
+  k_spa_offsets<<<1, 1024, 0, st>>>(chunk_kept, plan, offs, kept_counts);
+  k_spa_gather<<<blocks, 256, 0, st>>>(scratch, plan, chunk_kept, offs, out);
+}
+
+}  // namespace chgpu

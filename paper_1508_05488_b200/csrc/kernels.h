@@ -8,6 +8,23 @@
 
 namespace chgpu {
 
+// Bucket sort (k_bucket.cu).
+constexpr int kLocalBits = 10;     // low bits of q sorted inside a bucket
+constexpr u32 kBucketCap = 3072;   // largest bucket sorted in shared memory
+constexpr int kMaxBucketBits = 13;
+
+struct BucketPlan {
+  int nseg;
+  int bbits;            // buckets per segment = 2^bbits
+  u64 src_off[4];       // segment start in the source layout (K2 streams)
+  u64 dst_off[4];       // segment start in the sorted layout
+  u64 cum[5];           // prefix of segment lengths
+  int region[4];
+  double qlo[4], qscale[4];
+  double qmax;          // 2^(bbits + kLocalBits) - 1
+  u32 tile_begin[5];    // scatter tiles per segment
+};
+
 struct SpaPlan {
   u64 off[4];         // region offset in the sorted array
   u64 m[4];           // region size
@@ -44,10 +61,21 @@ void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_
 void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium,
                              const u32* nmedium, void* longr, u32* nlong, cudaStream_t st);
 size_t group_run_bytes();
+void launch_bucket_hist(const u64* kbuf, const BucketPlan& P, u32* hist, cudaStream_t st);
+void launch_bucket_scan(const u32* hist, const BucketPlan& P, u64* base, u32* cursor, u32* big,
+                        u32* nbig, cudaStream_t st);
+u32 bucket_scatter_tiles(BucketPlan& P);
+void launch_bucket_scatter(const u64* kin, const u64* vin, u64* kout, u64* vout, const BucketPlan& P,
+                           u32 tiles, u32* cursor, cudaStream_t st);
+void launch_bucket_sort(u64* k, u64* v, const BucketPlan& P, const u64* base, const u32* hist,
+                        unsigned long long* ngroups, cudaStream_t st);
 // K4/K5
 void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
                 double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,
                 u32* chunk_ctr, cudaStream_t st);
+void launch_spa_warp(const u64* k, const u64* v, const SpaPlan& plan, double2* scratch,
+                     u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
+                     cudaStream_t st);
 void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
                    u32* tile_ctr, unsigned long long* total, cudaStream_t st);
 

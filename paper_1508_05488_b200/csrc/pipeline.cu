@@ -77,6 +77,10 @@ struct chgpu_ctx {
   unsigned long long* d_u64 = nullptr;  // [0..3] kept counts, [4] unique total, [5..9] label counts
   u32* d_hist = nullptr;
   u32* d_digit_excl = nullptr;
+  u32* d_bhist = nullptr;   // bucket counts   [4 << kMaxBucketBits]
+  u64* d_bbase = nullptr;   // bucket bases    [4 << kMaxBucketBits]
+  u32* d_bcur = nullptr;    // scatter cursors [4 << kMaxBucketBits]
+  u32* d_big = nullptr;     // oversized buckets
   SegDesc* d_segs = nullptr;
   size_t seg_cap = 0;
 
@@ -323,14 +327,17 @@ struct Run {
 
 // Groups left for the host to resolve after the in-place fix-up.
 struct PendingLong {
-  int slot = -1;
+  int slot = -1;      // device counter of pending items (groups or buckets)
   int eqmode = 0;
   int depth = 0;
+  bool buckets = false;  // items are oversized buckets of a bucket sort
+  int bbits = 0;
   std::vector<int> regions;
   u64 *kF = nullptr, *vF = nullptr, *kS = nullptr, *vS = nullptr;
 };
 
 int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long);
+int resolve_big_buckets(chgpu_ctx* ctx, const PendingLong& p, bool* had);
 
 // Orders every group of the sorted layout (segments in ctx->h_segs, at
 // dst_off of (kF, vF)) by (canon k, v), in place. eqmode kEqQ: groups of
@@ -372,6 +379,7 @@ int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int
 int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long) {
   *had_long = false;
   if (p.slot < 0) return CHGPU_OK;
+  if (p.buckets) return resolve_big_buckets(ctx, p, had_long);
   u32 nlong = 0;
   TRY(read_ctr(ctx, p.slot, &nlong));
   if (nlong == 0) return CHGPU_OK;
@@ -444,6 +452,120 @@ int sort_segments(chgpu_ctx* ctx, int nseg, int qbits, bool timed, bool defer_lo
   return CHGPU_OK;
 }
 
+// Bucket sort of nseg (<= 4) segments of the K2 two-ended layout (src_off
+// into kbuf/vbuf) into contiguous region order in (ka, va): see k_bucket.cu.
+// lo/hi bound each segment's primary coordinate (the quantizer range).
+// Buckets too large for shared memory are left in *pend (resolved now
+// unless `defer`).
+int bucket_sort(chgpu_ctx* ctx, int nseg, const u64* src_off, const u64* m, const int* region,
+                const double* lo, const double* hi, bool timed, bool defer, Sorted* out) {
+  BucketPlan P{};
+  P.nseg = nseg;
+  u64 mmax = 0, total = 0;
+  for (int s = 0; s < nseg; ++s) mmax = std::max(mmax, m[s]);
+  int bb = 1;
+  while (bb < kMaxBucketBits && (mmax >> bb) > 1024) ++bb;
+  P.bbits = bb;
+  P.qmax = std::ldexp(1.0, bb + kLocalBits) - 1.0;
+  for (int s = 0; s < nseg; ++s) {
+    P.src_off[s] = src_off[s];
+    P.dst_off[s] = total;
+    P.cum[s] = total;
+    P.region[s] = region[s];
+    P.qlo[s] = lo[s];
+    const double span = hi[s] - lo[s];
+    double scale = span > 0.0 ? P.qmax / span : 0.0;
+    if (!std::isfinite(scale)) scale = 0.0;
+    P.qscale[s] = scale;
+    total += m[s];
+  }
+  P.cum[nseg] = total;
+  out->kF = ctx->d_ka;
+  out->vF = ctx->d_va;
+  out->kS = ctx->d_kbuf;
+  out->vS = ctx->d_vbuf;
+  out->passes = 0;
+  out->pend = PendingLong{};
+  if (total == 0) return CHGPU_OK;
+  const int nbig_slot = take_ctr(ctx);
+  cudaStream_t st = ctx->st;
+  CK(cudaMemsetAsync(ctx->d_bhist, 0, (sizeof(u32) * nseg) << bb, st));
+  launch_bucket_hist(ctx->d_kbuf, P, ctx->d_bhist, st);
+  launch_bucket_scan(ctx->d_bhist, P, ctx->d_bbase, ctx->d_bcur, ctx->d_big, ctx->d_ctr + nbig_slot,
+                     st);
+  if (timed) CK(cudaEventRecord(ctx->ev[3], st));
+  const u32 tiles = bucket_scatter_tiles(P);
+  if (timed) CK(cudaEventRecord(ctx->ev[4], st));
+  launch_bucket_scatter(ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, P, tiles, ctx->d_bcur, st);
+  if (timed) CK(cudaEventRecord(ctx->ev[5], st));
+  launch_bucket_sort(ctx->d_ka, ctx->d_va, P, ctx->d_bbase, ctx->d_bhist, ctx->d_u64 + 10, st);
+  ctx->launches += 4;
+  CK(cudaGetLastError());
+  out->passes = 1;
+  PendingLong& p = out->pend;
+  p.slot = nbig_slot;
+  p.buckets = true;
+  p.bbits = bb;
+  p.regions.assign(region, region + nseg);
+  p.kF = out->kF;
+  p.vF = out->vF;
+  p.kS = out->kS;
+  p.vS = out->vS;
+  if (defer) return CHGPU_OK;
+  bool had = false;
+  return resolve_long(ctx, p, &had);
+}
+
+// Oversized buckets: each is sorted completely with the onesweep engine on
+// k, then its ==-primary runs are ordered by v (fix_groups).
+int resolve_big_buckets(chgpu_ctx* ctx, const PendingLong& p, bool* had) {
+  *had = false;
+  u32 nbig = 0;
+  TRY(read_ctr(ctx, p.slot, &nbig));
+  if (nbig == 0) return CHGPU_OK;
+  *had = true;
+  const size_t nb = size_t(1) << p.bbits;
+  const size_t nall = nb * p.regions.size();
+  std::vector<u32> ids(nbig), cnt(nall);
+  std::vector<u64> base(nall);
+  CK(cudaMemcpyAsync(ids.data(), ctx->d_big, nbig * sizeof(u32), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaMemcpyAsync(cnt.data(), ctx->d_bhist, nall * sizeof(u32), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaMemcpyAsync(base.data(), ctx->d_bbase, nall * sizeof(u64), cudaMemcpyDeviceToHost, ctx->st));
+  TRY(sync(ctx));
+  std::sort(ids.begin(), ids.end());
+  TRY(ensure_segs(ctx, nbig));
+  auto load = [&]() {
+    for (u32 i = 0; i < nbig; ++i)
+      ctx->h_segs[i] = make_seg(base[ids[i]], base[ids[i]], cnt[ids[i]], p.regions[ids[i] / nb]);
+  };
+  load();
+  bool in_a = true;
+  int passes = 0;
+  TRY(radix_sort(ctx, (int)nbig, p.kF, p.vF, p.kS, p.vS, p.kF, p.vF, kDigitK, kPasses, &in_a,
+                 &passes));
+  if (passes % 2 == 1) {
+    const u32 t2 = plan_tiles(ctx->h_segs, (int)nbig);
+    launch_seg_copy(p.kS, p.vS, p.kF, p.vF, ctx->d_segs, (int)nbig, t2, 0, ctx->st);
+    ++ctx->launches;
+  }
+  CK(cudaGetLastError());
+  load();
+  PendingLong inner;
+  return fix_groups(ctx, (int)nbig, p.kF, p.vF, p.kS, p.vS, kEqPrim, &inner, false, 1);
+}
+
+// The four region streams of K2 (two-ended layout), bucket-sorted into
+// region order LL | LR | UR | UL.
+int sort_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, bool timed, bool defer,
+                 Sorted* out) {
+  const u64 cap = ctx->cap;
+  const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
+  const int region[4] = {1, 2, 3, 4};
+  double lo[4], hi[4];
+  for (int s = 0; s < 4; ++s) region_range(quad, s + 1, &lo[s], &hi[s]);
+  return bucket_sort(ctx, 4, src_off, m, region, lo, hi, timed, defer, out);
+}
+
 // Region segments of the K2 two-ended layout, with quantizers.
 int plan_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, int* qbits) {
   TRY(ensure_segs(ctx, 4));
@@ -485,14 +607,12 @@ SpaPlan make_spa_plan(const u64 m[4], size_t chunk_count, const double* quad) {
 // into d_kept; returns the unique count.
 int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* nuniq, int* passes,
                             size_t* groups) {
-  TRY(ensure_segs(ctx, 1));
-  ctx->h_segs[0] = make_seg(0, 0, s1, 0);
   double lo, hi;
   region_range(quad, 0, &lo, &hi);
-  const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
-  set_quantizer(ctx->h_segs[0], lo, hi, qbits);
+  const u64 src_off[1] = {0}, m[1] = {s1};
+  const int region[1] = {0};
   Sorted so{};
-  TRY(sort_segments(ctx, 1, qbits, false, false, &so));
+  TRY(bucket_sort(ctx, 1, src_off, m, region, &lo, &hi, false, false, &so));
   *passes = so.passes;
   *groups = 0;
   const int slot = take_ctr(ctx);
@@ -504,6 +624,18 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
                      cudaMemcpyDeviceToHost, ctx->st));
   TRY(sync(ctx));
   *nuniq = (size_t)ctx->h->uniq;
+  return CHGPU_OK;
+}
+
+// K4/K5 over the sorted regions in (kF, vF): kept chains, decoded, in
+// d_kept (region order) and per-region counts in d_u64[0..3]. The input
+// copy d_pts is dead by now and serves as the per-chunk scratch.
+int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
+  u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
+  u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
+  launch_spa_warp(kF, vF, plan, ctx->d_pts, chunk_kept, offs, ctx->d_u64, ctx->d_kept, ctx->st);
+  if (plan.total_chunks) ctx->launches += 3;
+  CK(cudaGetLastError());
   return CHGPU_OK;
 }
 
@@ -621,10 +753,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     for (int s = 0; s < 4; ++s) D.region_counts[s + 1] = m[s];
     D.region_counts[0] = n - s1;
     // ---- K3: region sort (spa.cpp:59-81).
-    int qbits = 0;
-    TRY(plan_regions(ctx, m, qi.q, &qbits));
     Sorted so{};
-    TRY(sort_segments(ctx, 4, qbits, true, true, &so));
+    TRY(sort_regions(ctx, m, qi.q, true, true, &so));
     D.sort_passes = so.passes;
     const bool sort_timed = s1 > 0;
     CK(cudaEventRecord(ctx->ev[6], st));
@@ -635,10 +765,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     const SpaPlan plan = make_spa_plan(m, chunk_count, qi.q);
     auto spa_and_read = [&]() -> int {
       CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), st));
-      launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
-                 next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
-      if (plan.total_chunks) ++ctx->launches;
-      CK(cudaGetLastError());
+      TRY(run_spa(ctx, so.kF, so.vF, plan));
       CK(cudaEventRecord(ctx->ev[8], st));
       // kept counts, the group count and the long-group count in one trip
       CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
@@ -761,6 +888,10 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_rawquad, sizeof(QuadCand))) ||
       bad(cudaMalloc(&ctx->d_ctr, kCtrSlots * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_u64, 16 * sizeof(unsigned long long))) ||
+      bad(cudaMalloc(&ctx->d_bhist, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
+      bad(cudaMalloc(&ctx->d_bbase, (size_t(4) << kMaxBucketBits) * sizeof(u64))) ||
+      bad(cudaMalloc(&ctx->d_bcur, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
+      bad(cudaMalloc(&ctx->d_big, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
       bad(cudaMallocHost(&ctx->h, sizeof(Pinned)))) {
     chgpu_ctx_destroy(ctx);
     return CHGPU_CUDA_ERR;
@@ -786,6 +917,10 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_u64);
   cudaFree(ctx->d_segs);
   cudaFree(ctx->d_hist);
+  cudaFree(ctx->d_bhist);
+  cudaFree(ctx->d_bbase);
+  cudaFree(ctx->d_bcur);
+  cudaFree(ctx->d_big);
   cudaFree(ctx->d_digit_excl);
   cudaFreeHost(ctx->h);
   cudaFreeHost(ctx->h_segs);
@@ -961,9 +1096,7 @@ int chgpu_spa_filter(chgpu_ctx* ctx, int region, const double* xy, size_t m, con
   }
   plan.total_chunks = (u32)((m + cs - 1) / cs);
   plan.seed[r] = (region == 1 || region == 3) ? anchors[1] : anchors[0];
-  launch_spa(ctx->d_ka, ctx->d_va, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
-             next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->st);
-  CK(cudaGetLastError());
+  TRY(run_spa(ctx, ctx->d_ka, ctx->d_va, plan));
   CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost, ctx->st));
   TRY(sync(ctx));
@@ -1063,14 +1196,10 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     kept_counts[0] = nu;
   } else {
     if (chunk_count == 0) return fail(ctx, CHGPU_INVALID_ARG, "spa_filter: chunk_count must be >= 1");
-    int qbits = 0;
-    TRY(plan_regions(ctx, m, quad, &qbits));
     Sorted so{};
-    TRY(sort_segments(ctx, 4, qbits, false, false, &so));
+    TRY(sort_regions(ctx, m, quad, false, false, &so));
     const SpaPlan plan = make_spa_plan(m, chunk_count, quad);
-    launch_spa(so.kF, so.vF, plan, ctx->d_flags, ctx->d_kept, ctx->d_u64, ctx->d_status,
-               next_tag(ctx), ctx->d_ctr + take_ctr(ctx), st);
-    CK(cudaGetLastError());
+    TRY(run_spa(ctx, so.kF, so.vF, plan));
     CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
     TRY(sync(ctx));
