@@ -8,7 +8,7 @@
 // Three kernels, all without look-back chains:
 //   k_bucket_hist    per-bucket counts (shared-memory histograms per CTA)
 //   k_bucket_scan    exclusive scan -> bucket bases and scatter cursors
-//   k_bucket_scatter a CTA bins a 8192-record tile in shared memory,
+//   k_bucket_scatter a CTA bins a 16384-record tile in shared memory,
 //                    reserves each bucket's slice with one atomicAdd, and
 //                    scatters the records there (order inside a bucket is
 //                    free: the next kernel sorts it completely)
@@ -132,9 +132,9 @@ __global__ __launch_bounds__(1024) void k_bucket_scan(const u32* __restrict__ hi
 // ------------------------------------------------------------------ scatter
 
 constexpr int kScatterThreads = 512;
-constexpr int kScatterTile = 8192;
+constexpr int kScatterTile = 16384;
 
-__global__ __launch_bounds__(kScatterThreads) void k_bucket_scatter(
+__global__ __launch_bounds__(kScatterThreads, 3) void k_bucket_scatter(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, BucketPlan P, u32* __restrict__ cursor) {
   extern __shared__ __align__(16) u32 sm[];
@@ -175,19 +175,23 @@ __global__ __launch_bounds__(kScatterThreads) void k_bucket_scatter(
 
 // ------------------------------------------------------------------ local sort
 
-constexpr int kSortThreadsB = 256;
+constexpr int kSortThreadsB = 512;
 constexpr u32 kLocalBins = 1u << kLocalBits;
 
 struct BucketSmem {
   u64 k[kBucketCap];
   u64 v[kBucketCap];
-  u64 k2[kBucketCap];
-  u64 v2[kBucketCap];
+  unsigned short lk[kBucketCap];    // local key of record i
+  unsigned short perm[kBucketCap];  // sorted position -> record
   u32 bin[kLocalBins];
   u32 wsum[kSortThreadsB / 32];
 };
 
-__global__ __launch_bounds__(kSortThreadsB, 2) void k_bucket_sort(
+// One CTA per bucket: the records are loaded once (coalesced), their local
+// keys computed once, and the sort moves 16-bit indices only: a counting
+// sort on the local key, then equal-q groups insertion-sorted by the total
+// order. The bucket is written back in sorted order.
+__global__ __launch_bounds__(kSortThreadsB, 3) void k_bucket_sort(
     u64* __restrict__ k, u64* __restrict__ v, BucketPlan P, const u64* __restrict__ base,
     const u32* __restrict__ hist, unsigned long long* __restrict__ ngroups) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -202,15 +206,17 @@ __global__ __launch_bounds__(kSortThreadsB, 2) void k_bucket_sort(
   const int tid = threadIdx.x;
 
   for (u32 i = tid; i < kLocalBins; i += blockDim.x) S.bin[i] = 0;
+  __syncthreads();
   for (u32 i = tid; i < n; i += blockDim.x) {
-    S.k[i] = k[b0 + i];
+    const u64 kx = k[b0 + i];
+    S.k[i] = kx;
     S.v[i] = v[b0 + i];
+    const u32 l = bq_quantize(P, s, kx) & (kLocalBins - 1);
+    S.lk[i] = (unsigned short)l;
+    atomicAdd(&S.bin[l], 1u);
   }
   __syncthreads();
-  for (u32 i = tid; i < n; i += blockDim.x)
-    atomicAdd(&S.bin[bq_quantize(P, s, S.k[i]) & (kLocalBins - 1)], 1u);
-  __syncthreads();
-  // Exclusive scan of the local bins (kLocalBins / 256 per thread).
+  // Exclusive scan of the local bins (two per thread).
   constexpr int per = kLocalBins / kSortThreadsB;
   u32 loc[per];
   u32 sum = 0;
@@ -237,38 +243,32 @@ __global__ __launch_bounds__(kSortThreadsB, 2) void k_bucket_sort(
     run += loc[j];
   }
   __syncthreads();
-  for (u32 i = tid; i < n; i += blockDim.x) {
-    const u32 pos = atomicAdd(&S.bin[bq_quantize(P, s, S.k[i]) & (kLocalBins - 1)], 1u);
-    S.k2[pos] = S.k[i];
-    S.v2[pos] = S.v[i];
-  }
+  for (u32 i = tid; i < n; i += blockDim.x) S.perm[atomicAdd(&S.bin[S.lk[i]], 1u)] = (unsigned short)i;
   __syncthreads();
-  // Groups of equal q (equal local key inside the bucket): the thread that
-  // owns a group's first record insertion-sorts it by the total order.
+  // After the counting sort, bin[l] is the end of local key l's run; a run
+  // of length >= 2 is a group of equal q, ordered here by the total order.
   u32 found = 0;
-  for (u32 i = tid; i < n; i += blockDim.x) {
-    const u32 qi = bq_quantize(P, s, S.k2[i]) & (kLocalBins - 1);
-    if (i > 0 && (bq_quantize(P, s, S.k2[i - 1]) & (kLocalBins - 1)) == qi) continue;
-    u32 len = 1;
-    while (i + len < n && (bq_quantize(P, s, S.k2[i + len]) & (kLocalBins - 1)) == qi) ++len;
-    if (len < 2) continue;
+  for (u32 l = tid; l < kLocalBins; l += blockDim.x) {
+    const u32 end = S.bin[l];
+    const u32 beg = l ? S.bin[l - 1] : 0u;
+    if (end - beg < 2) continue;
     ++found;
-    for (u32 j = 1; j < len; ++j) {
-      const u64 kx = S.k2[i + j], vx = S.v2[i + j];
+    for (u32 j = beg + 1; j < end; ++j) {
+      const unsigned short rx = S.perm[j];
+      const u64 kx = S.k[rx], vx = S.v[rx];
       u32 t = j;
-      while (t > 0 && total_less(region, kx, vx, S.k2[i + t - 1], S.v2[i + t - 1])) {
-        S.k2[i + t] = S.k2[i + t - 1];
-        S.v2[i + t] = S.v2[i + t - 1];
+      while (t > beg && total_less(region, kx, vx, S.k[S.perm[t - 1]], S.v[S.perm[t - 1]])) {
+        S.perm[t] = S.perm[t - 1];
         --t;
       }
-      S.k2[i + t] = kx;
-      S.v2[i + t] = vx;
+      S.perm[t] = rx;
     }
   }
   __syncthreads();
   for (u32 i = tid; i < n; i += blockDim.x) {
-    k[b0 + i] = S.k2[i];
-    v[b0 + i] = S.v2[i];
+    const unsigned short rx = S.perm[i];
+    k[b0 + i] = S.k[rx];
+    v[b0 + i] = S.v[rx];
   }
   if (found) atomicAdd(ngroups, (unsigned long long)found);
 }

@@ -174,12 +174,15 @@ struct QuadEdges {
   double ax[4], ay[4], ex[4], ey[4];
 };
 
+// All four predicates are evaluated and the first Right one selected, so the
+// warp never diverges on the data; evaluating a predicate the reference would
+// have skipped has no effect on the result.
 __device__ __forceinline__ int classify(const QuadEdges& e, double px, double py) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    if (cross_edge(e.ax[c], e.ay[c], e.ex[c], e.ey[c], px, py) < 0.0) return c + 1;
-  }
-  return 0;
+  const bool r0 = cross_edge(e.ax[0], e.ay[0], e.ex[0], e.ey[0], px, py) < 0.0;
+  const bool r1 = cross_edge(e.ax[1], e.ay[1], e.ex[1], e.ey[1], px, py) < 0.0;
+  const bool r2 = cross_edge(e.ax[2], e.ay[2], e.ex[2], e.ey[2], px, py) < 0.0;
+  const bool r3 = cross_edge(e.ax[3], e.ay[3], e.ex[3], e.ey[3], px, py) < 0.0;
+  return r0 ? 1 : (r1 ? 2 : (r2 ? 3 : (r3 ? 4 : 0)));
 }
 
 // Two-ended stream layout: streams 1 and 2 share kbuf[0, ncap) growing

@@ -285,8 +285,13 @@ namespace chgpu {
 // array (ranges never overlap); k_spa_offsets scans the per-chunk counts and
 // k_spa_gather moves each chunk's run to its final, region-ordered place.
 
-constexpr int kSpaRows = 8;
+constexpr int kSpaPer = 8;                  // consecutive records per lane and step
+constexpr int kSpaStep = 32 * kSpaPer;      // records per warp step
 
+// Lane L of a step owns records [t0 + 8L, t0 + 8L + 8): it folds them
+// sequentially, one warp scan combines the 32 lane aggregates, and the lane
+// replays its 8 records against the exclusive prefix. The next step's loads
+// are issued before the current step is scanned.
 __global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
                                                   const u64* __restrict__ v, SpaPlan plan,
                                                   double2* __restrict__ scratch,
@@ -304,54 +309,78 @@ __global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
   const double ident = is_min ? INFINITY : -INFINITY;
   double carry = (cl == 0) ? plan.seed[r] : ident;
   u32 kept = 0;
-  for (u64 t0 = 0; t0 < len; t0 += 32 * kSpaRows) {
-    double g[kSpaRows];
+
+  u64 nv[kSpaPer];
+  auto fetch = [&](u64 t0) {
 #pragma unroll
-    for (int j = 0; j < kSpaRows; ++j) {
-      const u64 idx = t0 + j * 32 + lane;
-      g[j] = idx < len ? guarded_of(region, v[begin + idx]) : ident;
+    for (int j = 0; j < kSpaPer; ++j) {
+      const u64 idx = t0 + (u64)lane * kSpaPer + j;
+      nv[j] = idx < len ? v[begin + idx] : 0ull;
     }
+  };
+  fetch(0);
+  for (u64 t0 = 0; t0 < len; t0 += kSpaStep) {
+    double g[kSpaPer];
+    double agg = ident;
 #pragma unroll
-    for (int j = 0; j < kSpaRows; ++j) {
-      double x = g[j];
+    for (int j = 0; j < kSpaPer; ++j) {
+      const u64 idx = t0 + (u64)lane * kSpaPer + j;
+      g[j] = idx < len ? guarded_of(region, nv[j]) : ident;
+      agg = op_ext(is_min, agg, g[j]);
+    }
+    if (t0 + kSpaStep < len) fetch(t0 + kSpaStep);
+    double x = agg;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x = op_ext(is_min, y, x);
-      }
-      double ex = __shfl_up_sync(0xffffffffu, x, 1);
-      if (lane == 0) ex = ident;
-      const u64 idx = t0 + j * 32 + lane;
-      const bool keep = idx < len && !steps_back(is_min, g[j], op_ext(is_min, carry, ex));
-      carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, x, 31));
-      const unsigned mask = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const u64 a = begin + idx;
-        double px, py;
-        decode_point(region, k[a], v[a], px, py);
-        scratch[begin + kept + __popc(mask & lanemask_lt())] = make_double2(px, py);
-      }
-      kept += __popc(mask);
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = op_ext(is_min, y, x);
+    }
+    double ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = ident;
+    double t = op_ext(is_min, carry, ex);
+    carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, x, 31));
+    u32 kmask = 0;
+#pragma unroll
+    for (int j = 0; j < kSpaPer; ++j) {
+      const u64 idx = t0 + (u64)lane * kSpaPer + j;
+      if (idx < len && !steps_back(is_min, g[j], t)) kmask |= 1u << j;
+      t = op_ext(is_min, t, g[j]);
+    }
+    const u32 nk = __popc(kmask);
+    u32 pre = nk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    u32 pos = kept + pre - nk;
+    kept += __shfl_sync(0xffffffffu, pre, 31);
+    while (kmask) {
+      const int j = __ffs(kmask) - 1;
+      kmask &= kmask - 1;
+      const u64 a = begin + t0 + (u64)lane * kSpaPer + j;
+      double px, py;
+      decode_point(region, k[a], v[a], px, py);
+      scratch[begin + pos++] = make_double2(px, py);
     }
   }
   if (lane == 0) chunk_kept[c] = kept;
 }
 
-// Exclusive scan of the per-chunk kept counts (one block) and the
-// per-region totals.
+// Exclusive scan of the per-chunk kept counts (one block); per-region
+// totals follow from the offsets at the region boundaries.
 __global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ chunk_kept, SpaPlan plan,
                                                       u32* __restrict__ offs,
                                                       unsigned long long* __restrict__ kept_counts) {
   __shared__ u32 wsum[32];
   __shared__ u32 carry;
-  __shared__ unsigned long long reg[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
-  if (threadIdx.x < 4) reg[threadIdx.x] = 0;
   __syncthreads();
-  for (u32 c0 = 0; c0 < plan.total_chunks; c0 += blockDim.x) {
+  const u32 total = plan.total_chunks;
+  for (u32 c0 = 0; c0 < total; c0 += blockDim.x) {
     const u32 c = c0 + threadIdx.x;
-    const u32 x0 = c < plan.total_chunks ? chunk_kept[c] : 0u;
+    const u32 x0 = c < total ? chunk_kept[c] : 0u;
     u32 x = x0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -362,22 +391,25 @@ __global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ ch
     __syncthreads();
     u32 pre = 0, tot = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      if (w < warp) pre += wsum[w];
-      tot += wsum[w];
+      const u32 ws = wsum[w];
+      pre += (w < warp) ? ws : 0u;
+      tot += ws;
     }
-    if (c < plan.total_chunks) {
-      offs[c] = carry + pre + x - x0;
-      if (x0) {
-        int r = 0;
-        while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
-        atomicAdd(&reg[r], (unsigned long long)x0);
-      }
-    }
+    if (c < total) offs[c] = carry + pre + x - x0;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x < 4) kept_counts[threadIdx.x] = reg[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const u32 grand = carry;
+    for (int r = 0; r < 4; ++r) {
+      const u32 a = plan.chunk_begin[r];
+      const u32 b = r < 3 ? plan.chunk_begin[r + 1] : total;
+      const u32 oa = a < total ? offs[a] : grand;
+      const u32 ob = b < total ? offs[b] : grand;
+      kept_counts[r] = (unsigned long long)(ob - oa);
+    }
+  }
 }
 
 __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ scratch,
