@@ -73,8 +73,21 @@ __global__ __launch_bounds__(512) void k_bucket_hist(const u64* __restrict__ kbu
   while (i < i1) {
     const u64 seg_end = min(i1, P.cum[s + 1]);
     const u64 src = P.src_off[s] - P.cum[s];
-    for (u64 j = i + threadIdx.x; j < seg_end; j += blockDim.x)
-      atomicAdd(&sh[bq_quantize(P, s, kbuf[src + j]) >> kLocalBits], 1u);
+    // Loads are batched ahead of the shared atomics so each thread keeps
+    // kBatch requests in flight.
+    constexpr int kBatch = 8;
+    for (u64 j0 = i + threadIdx.x; j0 < seg_end; j0 += (u64)kBatch * blockDim.x) {
+      u64 kk[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const u64 j = j0 + (u64)u * blockDim.x;
+        kk[u] = j < seg_end ? kbuf[src + j] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (j0 + (u64)u * blockDim.x < seg_end)
+          atomicAdd(&sh[bq_quantize(P, s, kk[u]) >> kLocalBits], 1u);
+    }
     __syncthreads();
     for (u32 b = threadIdx.x; b < nb; b += blockDim.x) {
       const u32 c = sh[b];
@@ -153,10 +166,23 @@ __global__ __launch_bounds__(kScatterThreads, 3) void k_bucket_scatter(
   const u64 src = P.src_off[s] + e0;
   for (u32 b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
-  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-    const u32 b = bq_quantize(P, s, kin[src + i]) >> kLocalBits;
-    bid[i] = (unsigned short)b;
-    atomicAdd(&cnt[b], 1u);
+  constexpr int kBatch = 8;
+  for (u32 i0 = threadIdx.x; i0 < n; i0 += kBatch * blockDim.x) {
+    u64 kk[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      kk[u] = i < n ? kin[src + i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      if (i < n) {
+        const u32 b = bq_quantize(P, s, kk[u]) >> kLocalBits;
+        bid[i] = (unsigned short)b;
+        atomicAdd(&cnt[b], 1u);
+      }
+    }
   }
   __syncthreads();
   u32* cur = cursor + (size_t)s * nb;
@@ -166,17 +192,33 @@ __global__ __launch_bounds__(kScatterThreads, 3) void k_bucket_scatter(
   }
   __syncthreads();
   const u64 dst = P.dst_off[s];
-  for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-    const u32 pos = atomicAdd(&cnt[bid[i]], 1u);
-    kout[dst + pos] = kin[src + i];
-    vout[dst + pos] = vin[src + i];
+  for (u32 i0 = threadIdx.x; i0 < n; i0 += kBatch * blockDim.x) {
+    u64 kk[kBatch], vv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      if (i < n) {
+        kk[u] = kin[src + i];
+        vv[u] = vin[src + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      if (i < n) {
+        const u32 pos = atomicAdd(&cnt[bid[i]], 1u);
+        kout[dst + pos] = kk[u];
+        vout[dst + pos] = vv[u];
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------ local sort
 
-constexpr int kSortThreadsB = 512;
-constexpr u32 kLocalBins = 1u << kLocalBits;
+constexpr int kSortThreadsB = 128;
+constexpr int kSortBinBits = 8;  // counting-sort bins: the top bits of the local key
+constexpr u32 kLocalBins = 1u << kSortBinBits;
 
 struct BucketSmem {
   u64 k[kBucketCap];
@@ -191,7 +233,7 @@ struct BucketSmem {
 // keys computed once, and the sort moves 16-bit indices only: a counting
 // sort on the local key, then equal-q groups insertion-sorted by the total
 // order. The bucket is written back in sorted order.
-__global__ __launch_bounds__(kSortThreadsB, 3) void k_bucket_sort(
+__global__ __launch_bounds__(kSortThreadsB, 4) void k_bucket_sort(
     u64* __restrict__ k, u64* __restrict__ v, BucketPlan P, const u64* __restrict__ base,
     const u32* __restrict__ hist, unsigned long long* __restrict__ ngroups) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -207,13 +249,28 @@ __global__ __launch_bounds__(kSortThreadsB, 3) void k_bucket_sort(
 
   for (u32 i = tid; i < kLocalBins; i += blockDim.x) S.bin[i] = 0;
   __syncthreads();
-  for (u32 i = tid; i < n; i += blockDim.x) {
-    const u64 kx = k[b0 + i];
-    S.k[i] = kx;
-    S.v[i] = v[b0 + i];
-    const u32 l = bq_quantize(P, s, kx) & (kLocalBins - 1);
-    S.lk[i] = (unsigned short)l;
-    atomicAdd(&S.bin[l], 1u);
+  constexpr int kBatch = 8;
+  for (u32 i0 = tid; i0 < n; i0 += kBatch * blockDim.x) {
+    u64 kk[kBatch], vv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      if (i < n) {
+        kk[u] = k[b0 + i];
+        vv[u] = v[b0 + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const u32 i = i0 + u * blockDim.x;
+      if (i < n) {
+        S.k[i] = kk[u];
+        S.v[i] = vv[u];
+        const u32 l = (bq_quantize(P, s, kk[u]) & ((1u << kLocalBits) - 1)) >> (kLocalBits - kSortBinBits);
+        S.lk[i] = (unsigned short)l;
+        atomicAdd(&S.bin[l], 1u);
+      }
+    }
   }
   __syncthreads();
   // Exclusive scan of the local bins (two per thread).

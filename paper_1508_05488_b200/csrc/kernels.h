@@ -10,7 +10,7 @@ namespace chgpu {
 
 // Bucket sort (k_bucket.cu).
 constexpr int kLocalBits = 10;     // low bits of q sorted inside a bucket
-constexpr u32 kBucketCap = 3072;   // largest bucket sorted in shared memory (< 65536)
+constexpr u32 kBucketCap = 2048;   // largest bucket sorted in shared memory (< 65536)
 constexpr int kMaxBucketBits = 13;
 
 struct BucketPlan {
