@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -554,10 +555,28 @@ int resolve_big_buckets(chgpu_ctx* ctx, const PendingLong& p, bool* had) {
   return fix_groups(ctx, (int)nbig, p.kF, p.vF, p.kS, p.vS, kEqPrim, &inner, false, 1);
 }
 
-// The four region streams of K2 (two-ended layout), bucket-sorted into
-// region order LL | LR | UR | UL.
+int plan_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, int* qbits);
+
+// Which engine sorts the regions: the segmented onesweep passes on the
+// quantized primary (default) or the experimental bucket sort
+// (CHGPU_SORT=bucket).
+bool use_bucket_sort() {
+  static const bool b = [] {
+    const char* e = std::getenv("CHGPU_SORT");
+    return e && std::strcmp(e, "bucket") == 0;
+  }();
+  return b;
+}
+
+// The four region streams of K2 (two-ended layout), sorted into region
+// order LL | LR | UR | UL.
 int sort_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, bool timed, bool defer,
                  Sorted* out) {
+  if (!use_bucket_sort()) {
+    int qbits = 0;
+    TRY(plan_regions(ctx, m, quad, &qbits));
+    return sort_segments(ctx, 4, qbits, timed, defer, out);
+  }
   const u64 cap = ctx->cap;
   const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
   const int region[4] = {1, 2, 3, 4};
@@ -609,10 +628,18 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
                             size_t* groups) {
   double lo, hi;
   region_range(quad, 0, &lo, &hi);
-  const u64 src_off[1] = {0}, m[1] = {s1};
-  const int region[1] = {0};
   Sorted so{};
-  TRY(bucket_sort(ctx, 1, src_off, m, region, &lo, &hi, false, false, &so));
+  if (use_bucket_sort()) {
+    const u64 src_off[1] = {0}, m[1] = {s1};
+    const int region[1] = {0};
+    TRY(bucket_sort(ctx, 1, src_off, m, region, &lo, &hi, false, false, &so));
+  } else {
+    TRY(ensure_segs(ctx, 1));
+    ctx->h_segs[0] = make_seg(0, 0, s1, 0);
+    const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
+    set_quantizer(ctx->h_segs[0], lo, hi, qbits);
+    TRY(sort_segments(ctx, 1, qbits, false, false, &so));
+  }
   *passes = so.passes;
   *groups = 0;
   const int slot = take_ctr(ctx);
