@@ -120,7 +120,7 @@ __global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(const double
   }
 }
 
-__global__ void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
+__global__ __launch_bounds__(1024) void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
                                  QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
   QuadCand acc;
   empty_quad(acc);
@@ -134,7 +134,7 @@ __global__ void k_extremes_final(const QuadCand* __restrict__ partials, int npar
     for (int c = 0; c < 4; ++c) other.c[c] = shfl_cand(acc.c[c], o);
     merge_quad(acc, other);
   }
-  __shared__ QuadCand sacc[8];
+  __shared__ QuadCand sacc[32];
   if ((threadIdx.x & 31) == 0) sacc[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -295,21 +295,31 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     s_base[tid] = tot ? atomicAdd(&counts_out[tid + 1], tot) : 0u;
   }
   __syncthreads();
-  u32 pos[4];
-#pragma unroll
-  for (int s = 0; s < 4; ++s) pos[s] = s_base[s] + s_wtot[warp][s] + excl[s];
+  u32 pos0 = s_base[0] + s_wtot[warp][0] + excl[0];
+  u32 pos1 = s_base[1] + s_wtot[warp][1] + excl[1];
+  u32 pos2 = s_base[2] + s_wtot[warp][2] + excl[2];
+  u32 pos3 = s_base[3] + s_wtot[warp][3] + excl[3];
+  // Straight-line per item (selects, one predicated store pair): the key
+  // codec of chgpu_internal.cuh written as swap + complement masks, and the
+  // two-ended stream slot as base +/- position.
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
-    const int r = (codes >> (3 * j)) & 7;
-    if (r != 0) {
-      const double2 p = sbuf[j * kK2Threads + tid];
-      u32 slot_pos = 0;
-#pragma unroll
-      for (int s = 0; s < 4; ++s)
-        if (r == s + 1) slot_pos = pos[s]++;
-      const u64 slot = stream_slot(r, slot_pos, ncap);
-      u64 k, v;
-      encode_point(lex ? 0 : r, p.x, p.y, k, v);
+    const u32 r = (codes >> (3 * j)) & 7;
+    const double2 p = sbuf[j * kK2Threads + tid];
+    const u64 ox = ord_enc(p.x), oy = ord_enc(p.y);
+    const bool sw = !lex && !(r & 1u);
+    const u64 kmask = (!lex && r >= 3) ? ~0ull : 0ull;
+    const u64 vmask = (!lex && (r == 1 || r == 4)) ? ~0ull : 0ull;
+    const u64 k = (sw ? oy : ox) ^ kmask;
+    const u64 v = (sw ? ox : oy) ^ vmask;
+    const u32 pp = r == 1 ? pos0 : (r == 2 ? pos1 : (r == 3 ? pos2 : pos3));
+    pos0 += (r == 1);
+    pos1 += (r == 2);
+    pos2 += (r == 3);
+    pos3 += (r == 4);
+    const u64 base = r == 1 ? 0ull : (r == 2 ? ncap - 1 : (r == 3 ? ncap : 2 * ncap - 1));
+    const u64 slot = (r & 1u) ? base + pp : base - pp;
+    if (r) {
       kbuf[slot] = k;
       vbuf[slot] = v;
     }
@@ -374,7 +384,7 @@ int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand*
 
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
                            QuadCand* raw_out, cudaStream_t st) {
-  k_extremes_final<<<1, 256, 0, st>>>(partials, nparts, out, raw_out);
+  k_extremes_final<<<1, 1024, 0, st>>>(partials, nparts, out, raw_out);
 }
 
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,

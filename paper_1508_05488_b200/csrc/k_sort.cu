@@ -293,7 +293,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
         u32 f = kFlagPrefix;  // the segment's first tile always holds a prefix
         if (j >= (int)sd.tile_begin) {
           do {
-            f = status_flag(load_status_acquire(status + j), tag);
+            f = status_flag(load_status(status + j), tag);
           } while (f == kFlagNone);
         }
         const unsigned pm = __ballot_sync(0xffffffffu, f == kFlagPrefix);
@@ -304,6 +304,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
         base -= 32;
       }
       if (lane == 0) S.seg = front;  // reuse: frontier tile
+      fence_acq_rel_gpu();            // acquire for the flags observed above
     }
     __syncthreads();
     const int front = S.seg;
