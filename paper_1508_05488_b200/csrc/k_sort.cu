@@ -165,18 +165,23 @@ struct OnesweepSmem {
 // One LSD pass. Keys stay in registers for the ranking; values travel
 // global -> shared with cp.async and are only touched again by the scatter,
 // so a thread holds kSortItems keys and nothing else across the pass.
-template <int kMode>
+//
+// kScan = false: one-pass ("onesweep") with a decoupled look-back for the
+// per-(tile, digit) global offsets. kScan = true: the downsweep of a
+// reduce-then-scan pass, reading those offsets from tile_prefix (written by
+// k_upsweep + k_colscan), so tiles never wait on each other.
+template <int kMode, bool kScan>
 __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
     const u32* __restrict__ digit_excl, int pass, u64* __restrict__ status, u32 tag,
-    u32* __restrict__ tile_ctr, u32 total_tiles) {
+    u32* __restrict__ tile_ctr, u32 total_tiles, const u32* __restrict__ tile_prefix) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    const u32 t = atomicAdd(tile_ctr, 1u);
+    const u32 t = kScan ? blockIdx.x : atomicAdd(tile_ctr, 1u);
     S.tile = t;
     S.seg = find_segment(segs, nseg, t);
   }
@@ -271,7 +276,9 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   // Publication is the release pattern "row stores; bar.sync; one thread:
   // fence.acq_rel.gpu + flag store"; readers acquire the flag in one warp
   // and bar.sync before touching rows.
-  if (tile == sd.tile_begin) {
+  if (kScan) {
+    before = tile_prefix[(size_t)tile * kDigits + b];
+  } else if (tile == sd.tile_begin) {
     __stcg(inc + (size_t)tile * kDigits + b, tile_cnt);
     __syncthreads();
     if (tid == 0) {
@@ -565,20 +572,20 @@ void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, int npasse
   k_hist_scan<<<nseg * kPasses, kDigits, 0, st>>>(hist, segs, npasses, digit_excl, needed_mask);
 }
 
-template <int kMode>
+template <int kMode, bool kScan>
 static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout,
                             const SegDesc* segs, int nseg, u32 total_tiles, int use_src,
                             const u32* digit_excl, int pass, u64* status, u32 tag, u32* tile_ctr,
-                            cudaStream_t st) {
+                            const u32* tile_prefix, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<kMode, kScan>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(OnesweepSmem));
     configured = true;
   }
-  k_onesweep<kMode><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
+  k_onesweep<kMode, kScan><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
       kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr,
-      total_tiles);
+      total_tiles, tile_prefix);
 }
 
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
@@ -587,16 +594,116 @@ void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const
   if (total_tiles == 0) return;
   switch (mode) {
     case kDigitQ:
-      onesweep_launch<kDigitQ>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
-                               pass, status, tag, tile_ctr, st);
+      onesweep_launch<kDigitQ, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
+                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
       break;
     case kDigitV:
-      onesweep_launch<kDigitV>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
-                               pass, status, tag, tile_ctr, st);
+      onesweep_launch<kDigitV, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
+                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
       break;
     default:
-      onesweep_launch<kDigitK>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
-                               pass, status, tag, tile_ctr, st);
+      onesweep_launch<kDigitK, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
+                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
+  }
+}
+
+// ------------------------------------------------------------------ reduce-then-scan pass
+
+// Upsweep: the digit histogram of every tile (same tiling as the downsweep).
+template <int kMode>
+__global__ __launch_bounds__(kSortThreads) void k_upsweep(const u64* __restrict__ kin,
+                                                          const u64* __restrict__ vin,
+                                                          const SegDesc* __restrict__ segs,
+                                                          int nseg, int use_src, int pass,
+                                                          u32* __restrict__ counts) {
+  __shared__ u32 h[kDigits];
+  const u32 tile = blockIdx.x;
+  const int s = find_segment(segs, nseg, tile);
+  const SegDesc sd = segs[s];
+  const u64 e0 = (u64)(tile - sd.tile_begin) * kSortTile;
+  const u32 cnt = (u32)min((u64)kSortTile, (u64)sd.len - e0);
+  const u64 src = (use_src ? sd.src_off : sd.dst_off) + e0;
+  const u64* rin = kMode == kDigitV ? vin : kin;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  u64 kk[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u32 i = j * kSortThreads + threadIdx.x;
+    kk[j] = i < cnt ? rin[src + i] : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u32 i = j * kSortThreads + threadIdx.x;
+    if (i < cnt) atomicAdd(&h[digit_of<kMode>(sd, kk[j], kk[j], pass)], 1u);
+  }
+  __syncthreads();
+  counts[(size_t)tile * kDigits + threadIdx.x] = h[threadIdx.x];
+}
+
+// Column scan: for digit d (one block each), the exclusive prefix of
+// counts[t][d] over the tiles of each segment, in place.
+__global__ __launch_bounds__(1024) void k_colscan(u32* __restrict__ counts,
+                                                  const SegDesc* __restrict__ segs, int nseg,
+                                                  u32 total_tiles) {
+  const u32 d = blockIdx.x;
+  __shared__ u32 wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int s = 0; s < nseg; ++s) {
+    const u32 tb = segs[s].tile_begin;
+    const u32 te = (s + 1 < nseg) ? segs[s + 1].tile_begin : total_tiles;
+    u32 carry = 0;
+    for (u32 t0 = tb; t0 < te; t0 += blockDim.x) {
+      const u32 t = t0 + threadIdx.x;
+      const u32 x0 = t < te ? counts[(size_t)t * kDigits + d] : 0u;
+      u32 x = x0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      u32 pre = 0, tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const u32 ws = wsum[w];
+        pre += (w < warp) ? ws : 0u;
+        tot += ws;
+      }
+      if (t < te) counts[(size_t)t * kDigits + d] = carry + pre + x - x0;
+      carry += tot;
+      __syncthreads();
+    }
+  }
+}
+
+template <int kMode>
+static void lsd_pass_launch(const u64* kin, const u64* vin, u64* kout, u64* vout,
+                            const SegDesc* segs, int nseg, u32 total_tiles, int use_src,
+                            const u32* digit_excl, int pass, u32* counts, cudaStream_t st) {
+  k_upsweep<kMode><<<total_tiles, kSortThreads, 0, st>>>(kin, vin, segs, nseg, use_src, pass,
+                                                         counts);
+  k_colscan<<<kDigits, 1024, 0, st>>>(counts, segs, nseg, total_tiles);
+  onesweep_launch<kMode, true>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, nullptr, 0, nullptr, counts, st);
+}
+
+void launch_lsd_pass(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
+                     int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
+                     int pass, u32* counts, cudaStream_t st) {
+  if (total_tiles == 0) return;
+  switch (mode) {
+    case kDigitQ:
+      lsd_pass_launch<kDigitQ>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, counts, st);
+      break;
+    case kDigitV:
+      lsd_pass_launch<kDigitV>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, counts, st);
+      break;
+    default:
+      lsd_pass_launch<kDigitK>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
+                               pass, counts, st);
   }
 }
 

@@ -51,6 +51,11 @@ void launch_hist(const u64* kin, const u64* vin, const SegDesc* segs, int nseg, 
                  int mode, int npasses, int use_src, u32* hist, cudaStream_t st);
 void launch_hist_scan(const u32* hist, const SegDesc* segs, int nseg, int npasses, u32* digit_excl,
                       u32* needed_mask, cudaStream_t st);
+// Reduce-then-scan LSD pass (upsweep, column scan, downsweep); counts needs
+// total_tiles * 256 u32.
+void launch_lsd_pass(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
+                     int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
+                     int pass, u32* counts, cudaStream_t st);
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
                      int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st);

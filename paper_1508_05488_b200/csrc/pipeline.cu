@@ -265,6 +265,16 @@ void region_range(const double* q, int region, double* lo, double* hi) {
   }
 }
 
+// LSD passes as reduce-then-scan (default) or onesweep look-back
+// (CHGPU_LSD=onesweep).
+bool lsd_scan_passes() {
+  static const bool b = [] {
+    const char* e = std::getenv("CHGPU_LSD");
+    return !(e && std::strcmp(e, "onesweep") == 0);
+  }();
+  return b;
+}
+
 // Segmented LSD radix sort of (k, v) records over the segments in
 // ctx->h_segs. The first executed pass reads (ksrc, vsrc) at src_off;
 // passes alternate between (kA, vA) and (kB, vB) at dst_off. *in_a tells
@@ -297,8 +307,16 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
     if (!(mask & (1u << p))) continue;
     u64* ko = (done % 2 == 0) ? kA : kB;
     u64* vo = (done % 2 == 0) ? vA : vB;
-    launch_onesweep(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode, ctx->d_digit_excl,
-                    p, ctx->d_status, next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->st);
+    if (lsd_scan_passes() && nseg <= 64) {
+      // reduce-then-scan: no inter-tile waiting (3 launches per pass)
+      launch_lsd_pass(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode,
+                      ctx->d_digit_excl, p, reinterpret_cast<u32*>(ctx->d_status), ctx->st);
+      ctx->launches += 2;
+    } else {
+      launch_onesweep(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode,
+                      ctx->d_digit_excl, p, ctx->d_status, next_tag(ctx),
+                      ctx->d_ctr + take_ctr(ctx), ctx->st);
+    }
     kin = ko;
     vin = vo;
     use_src = 0;
