@@ -276,33 +276,57 @@ def main():
         hbm, src = peaks()
         t = d.times_ms
         n = args.n
-        pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)
-        pass_bytes = 32 * s1
         disc_bytes = 32 * n + 16 * s1
         disc_ms = t["t_k1_ms"] + t["t_k2_ms"]
         kernels = {
-            "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n},
-            "k2_classify_compact": {"ms": t["t_k2_ms"], "bytes": 16 * n + 16 * s1},
-            "k3_hist": {"ms": t["t_hist_ms"], "bytes": 8 * s1},
-            "k3_onesweep_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": pass_bytes},
-            "k3_ties": {"ms": t["t_ties_ms"]},
-            "k4_spa": {"ms": t["t_spa_kernel_ms"], "bytes": 8 * s1 + 2 * s1
-                       + 16 * sum(d.kept_counts)},
-            "d2h_chains_ms": t["t_d2h_ms"], "host_melkman_ms": t["t_host_ms"],
+            "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n,
+                            "basis": "16 B/pt read"},
+            "k2_classify_compact": {"ms": t["t_k2_ms"], "bytes": 16 * n + 16 * s1,
+                                    "basis": "16 B/pt read + 16 B/survivor write"},
         }
-        for kname, kv in kernels.items():
-            if isinstance(kv, dict) and kv.get("bytes") and kv.get("ms"):
+        if d.spa_path == 1:
+            lb = d.filter_log2nb
+            nb = 4 * (1 << lb)
+            nc = d.n_candidates
+            kernels.update({
+                "k3_bin_scan": {"ms": t["t_binscan_ms"], "bytes": 24 * nb,
+                                "basis": "12 B/bin read + 12 B/bin write"},
+                "k3_filter": {"ms": t["t_filter_ms"], "bytes": 16 * s1 + 16 * nc,
+                              "basis": "16 B/survivor read + 16 B/candidate write",
+                              "candidates": nc},
+                "k3_bin_sort_big": {"ms": t["t_binsort_ms"]},
+                "k4_spa_bins": {"ms": t["t_spa_kernel_ms"],
+                                "bytes": 16 * nc + 16 * sum(d.kept_counts),
+                                "basis": "16 B/candidate read + 16 B/kept write"},
+            })
+        else:
+            pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)
+            kernels.update({
+                "k3_hist": {"ms": t["t_hist_ms"], "bytes": 8 * s1},
+                "k3_radix_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": 32 * s1,
+                                  "basis": "16 B/record read + 16 B/record write"},
+                "k3_ties": {"ms": t["t_ties_ms"]},
+                "k4_spa": {"ms": t["t_spa_kernel_ms"], "bytes": 8 * s1 + 2 * s1
+                           + 16 * sum(d.kept_counts)},
+            })
+        for kv in kernels.values():
+            if kv.get("bytes") and kv.get("ms"):
                 kv["gbs"] = kv["bytes"] / (kv["ms"] * 1e-3) / 1e9
+        kernels["d2h_chains_ms"] = t["t_d2h_ms"]
+        kernels["host_melkman_ms"] = t["t_host_ms"]
+        dom_name, dom = max(((k, v) for k, v in kernels.items()
+                             if isinstance(v, dict) and v.get("gbs")), key=lambda kv: kv[1]["ms"])
         line["roofline"] = {
-            "bound": "hbm", "kernel": "k_onesweep (region radix pass)",
-            "achieved": pass_bytes / (pass_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "peak_source": src, "frac": pass_bytes / (pass_ms * 1e-3) / 1e9 / hbm,
+            "bound": "hbm", "kernel": dom_name,
+            "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
+            "peak_source": src, "frac": dom["gbs"] / hbm,
             "traffic": None,
-            "algorithmic_bytes": f"32 B/record x {s1} records (16 B read + 16 B write)",
+            "algorithmic_bytes": f"{dom['basis']}: {dom['bytes']} B per launch",
             "discard_kernels": {"kernels": "k_extremes_partial+final, k_classify_compact",
                                 "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
                                 "frac": disc_bytes / (disc_ms * 1e-3) / 1e9 / hbm,
                                 "bytes": disc_bytes, "ms": disc_ms},
+            "spa_path": ["sort", "prefilter", "prefilter->sort"][d.spa_path],
             "per_kernel": kernels,
         }
         line["stats"] = {"n_after_round1": r.stats.n_after_round1,

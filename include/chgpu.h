@@ -79,7 +79,25 @@ typedef struct {
   double t_spa_kernel_ms;   /* SPA scan + chain compaction */
   double t_d2h_ms;          /* chains device->host */
   double t_host_ms;         /* host assemble + Melkman */
+  /* SPA path: 0 = full region sort, 1 = pre-filtered (k_filter.cu),
+   * 2 = pre-filter overflowed (a bin too large) and the full sort ran. */
+  int spa_path;
+  int filter_log2nb;        /* pre-filter bins per region = 2^filter_log2nb */
+  size_t n_candidates;      /* survivors left for the sort by the pre-filter */
+  double t_binscan_ms;      /* pre-filter: bin ranks + thresholds */
+  double t_filter_ms;       /* pre-filter: candidate selection */
+  double t_binsort_ms;      /* pre-filter: sort of bins above 32 candidates */
 } chgpu_diag;
+
+/* Options (chgpu_ctx_set_option). */
+enum {
+  CHGPU_OPT_SPA_PATH = 1  /* value: one of the CHGPU_SPA_* below */
+};
+enum {
+  CHGPU_SPA_AUTO = 0,     /* pre-filter when chunks average >= 16 records (default) */
+  CHGPU_SPA_SORT = 1,     /* always sort every survivor (the reference's sort_region) */
+  CHGPU_SPA_FILTER = 2    /* always pre-filter (falls back to the sort on overflow) */
+};
 
 typedef struct chgpu_ctx chgpu_ctx;
 
@@ -89,6 +107,11 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx);
 const char* chgpu_last_error(const chgpu_ctx* ctx);
 /* The CUDA stream the context launches on (a cudaStream_t). */
 void* chgpu_ctx_stream(chgpu_ctx* ctx);
+/* Per-context option (CHGPU_OPT_*); CHGPU_INVALID_ARG for an unknown
+ * option or value. The environment variable CHGPU_SPA=sort|filter sets
+ * CHGPU_OPT_SPA_PATH for contexts created afterwards. Results never depend
+ * on options: every path returns the reference's hull and counters. */
+int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value);
 /* Pre-size the workspace for n points (optional; grows on demand). */
 int chgpu_reserve(chgpu_ctx* ctx, size_t n);
 

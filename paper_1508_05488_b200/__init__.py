@@ -74,7 +74,14 @@ class _Diag(C.Structure):
                 ("t_h2d_ms", C.c_double), ("t_k1_ms", C.c_double), ("t_k2_ms", C.c_double),
                 ("t_hist_ms", C.c_double), ("t_passes_ms", C.c_double),
                 ("t_ties_ms", C.c_double), ("t_spa_kernel_ms", C.c_double),
-                ("t_d2h_ms", C.c_double), ("t_host_ms", C.c_double)]
+                ("t_d2h_ms", C.c_double), ("t_host_ms", C.c_double),
+                ("spa_path", C.c_int), ("filter_log2nb", C.c_int), ("n_candidates", C.c_size_t),
+                ("t_binscan_ms", C.c_double), ("t_filter_ms", C.c_double),
+                ("t_binsort_ms", C.c_double)]
+
+# chgpu_ctx_set_option (include/chgpu.h)
+OPT_SPA_PATH = 1
+SPA_AUTO, SPA_SORT, SPA_FILTER = 0, 1, 2
 
 
 @dataclass
@@ -108,6 +115,9 @@ class Diag:
     tie_runs: int
     launches: int
     times_ms: dict
+    spa_path: int = 0        # 0 full sort, 1 pre-filtered, 2 pre-filter overflowed -> sort
+    n_candidates: int = 0
+    filter_log2nb: int = 0
 
     @classmethod
     def _from(cls, d: _Diag) -> "Diag":
@@ -115,7 +125,8 @@ class Diag:
         return cls(np.array(d.quad[:], np.float64).reshape(4, 2), int(d.frame_size),
                    [int(c) for c in d.region_counts], [int(c) for c in d.kept_counts],
                    bool(d.degenerate_branch), int(d.sort_passes), int(d.tie_runs),
-                   int(d.launches), times)
+                   int(d.launches), times, int(d.spa_path), int(d.n_candidates),
+                   int(d.filter_log2nb))
 
 
 @dataclass
@@ -156,6 +167,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_ctx_stream.argtypes = [vp]
         L.chgpu_ctx_stream.restype = vp
         L.chgpu_reserve.argtypes = [vp, C.c_size_t]
+        L.chgpu_ctx_set_option.argtypes = [vp, C.c_int, C.c_longlong]
         hull_args = [vp, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
                      C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_hull.argtypes = hull_args
@@ -236,6 +248,10 @@ class Context:
 
     def reserve(self, n: int):
         self._check(self.lib.chgpu_reserve(self.h, n))
+
+    def set_spa_path(self, mode: int):
+        """SPA_AUTO (default), SPA_SORT (sort every survivor) or SPA_FILTER."""
+        self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_SPA_PATH, mode))
 
     def _hull(self, fn, ptr, n, config):
         config = config or PipelineConfig()

@@ -110,6 +110,81 @@ __host__ __device__ __forceinline__ bool prim_eq(int region, u64 a, u64 b) {
   return a == b || primary_of(region, a) == primary_of(region, b);
 }
 
+// -0.0 as primary compares like +0.0: map its code onto +0.0's.
+__host__ __device__ __forceinline__ u64 canon_k(int region, u64 k) {
+  const bool desc = (region == 3 || region == 4);
+  const u64 neg0 = desc ? ~0x7FFFFFFFFFFFFFFFull : 0x7FFFFFFFFFFFFFFFull;
+  const u64 pos0 = desc ? ~0x8000000000000000ull : 0x8000000000000000ull;
+  return k == neg0 ? pos0 : k;
+}
+
+// region_less (spa.cpp:38-52) on (canonical k, v); ties (==-equal points)
+// fall back to the raw k so the order is total on bits and every sort in
+// this library produces the same sequence whatever order records arrive in.
+__host__ __device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u64 kb, u64 vb) {
+  const u64 ca = canon_k(region, ka), cb = canon_k(region, kb);
+  return ca < cb || (ca == cb && (va < vb || (va == vb && ka < kb)));
+}
+
+// ---------------------------------------------------------------- SPA bins
+//
+// The SPA pre-filter (k_filter.cu) groups each region's records into bins
+// of its primary coordinate. bin() is a monotone map onto [0, nb) in the
+// region's sort direction (subtract, multiply by a positive constant,
+// clamp, truncate: all monotone in round-to-nearest), so a region's sorted
+// sequence visits its bins in increasing order and every bin is one
+// contiguous run of it. The geometry depends only on the quad, so the
+// classify kernel (which counts records per bin) and the filter kernel
+// (which re-derives each record's bin from its primary) agree bit for bit.
+struct BinGeom {
+  double lo[4], scale[4], top;  // top = nb - 1
+  int log2nb;
+};
+
+// Primary range of region r (1..4) between its anchors: LL x in
+// [left.x, bottom.x], LR y in [bottom.y, right.y], UR x in [top.x, right.x],
+// UL y in [left.y, top.y] (quad = left, bottom, right, top).
+__host__ __device__ __forceinline__ void bin_range(const double* q, int r, double* lo, double* hi) {
+  switch (r) {
+    case 1: *lo = q[0]; *hi = q[2]; break;
+    case 2: *lo = q[3]; *hi = q[5]; break;
+    case 3: *lo = q[6]; *hi = q[4]; break;
+    default: *lo = q[1]; *hi = q[7]; break;
+  }
+}
+
+__device__ __forceinline__ void make_bin_geom(const double* q, int log2nb, BinGeom* g) {
+  g->log2nb = log2nb;
+  const double nb = (double)(1u << log2nb);
+  g->top = nb - 1.0;
+  for (int r = 1; r <= 4; ++r) {
+    double lo, hi;
+    bin_range(q, r, &lo, &hi);
+    const double span = __dsub_rn(hi, lo);
+    double s = span > 0.0 ? __ddiv_rn(nb, span) : 0.0;
+    if (!(s < 1e300)) s = 0.0;  // inf / nan (denormal spans)
+    g->lo[r - 1] = lo;
+    g->scale[r - 1] = s;
+  }
+}
+
+// Bin of a record of region r (1..4) with primary coordinate p.
+__device__ __forceinline__ u32 bin_of(const BinGeom& g, int r, double p) {
+  double t = __dmul_rn(__dsub_rn(p, g.lo[r - 1]), g.scale[r - 1]);
+  t = fmin(fmax(t, 0.0), g.top);
+  const u32 b = (u32)__double2uint_rz(t);
+  return (r >= 3) ? (u32)g.top - b : b;  // UR / UL sort descending
+}
+
+// The guarded coordinate as a key w on which every region's SPA is a
+// running MAX: steps_back(g, t) <=> w(g) < w(t) (spa.cpp:92-105). w is the
+// record's v word (chgpu_internal codec: LL ~ord(y), LR ord(x), UR ord(y),
+// UL ~ord(x)) with -0.0 mapped onto +0.0, since == does not tell them apart.
+__host__ __device__ __forceinline__ u64 wkey(int r, u64 v) {
+  if (r == 1 || r == 4) return v == 0x8000000000000000ull ? 0x7FFFFFFFFFFFFFFFull : v;
+  return v == 0x7FFFFFFFFFFFFFFFull ? 0x8000000000000000ull : v;
+}
+
 // ---------------------------------------------------------------- look-back
 //
 // Decoupled look-back status words: [tag:30 | flag:2 | value:32]. The tag

@@ -214,15 +214,21 @@ __device__ __forceinline__ void cp_async_wait() {
 // reserves its output range per stream with one global atomicAdd each,
 // instead of an ordered (look-back) scan. Per point the work is the
 // classification, a register counter increment and one record store.
-template <bool kGivenLabels>
+//
+// kStats: every survivor also adds itself to its SPA bin (k_filter.cu):
+// one fire-and-forget count increment and one running max of its guarded
+// key w per record, both resolved in L2 while the tile streams.
+template <bool kGivenLabels, bool kStats>
 __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
-    u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out) {
+    u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out, int log2nb,
+    u32* __restrict__ bcnt, u64* __restrict__ bw) {
   extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
   __shared__ u32 s_wtot[kK2Threads / 32][4];
   __shared__ u32 s_base[4];
   __shared__ QuadEdges s_edges;
+  __shared__ BinGeom s_geom;
   __shared__ int s_lex;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -246,6 +252,7 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     // Degenerate frame: survivors all go to stream 1 in lexicographic
     // encoding for the hull_oracle-style finish (pipeline.cpp:53-71).
     s_lex = force_lex || (!kGivenLabels && qi.degenerate);
+    if (kStats) make_bin_geom(qi.q, log2nb, &s_geom);
   }
   __syncthreads();
   const bool lex = s_lex != 0;
@@ -322,6 +329,12 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     if (r) {
       kbuf[slot] = k;
       vbuf[slot] = v;
+      if (kStats && !lex) {
+        const double prim = (r & 1u) ? p.x : p.y;
+        const u32 b = ((r - 1) << log2nb) | bin_of(s_geom, (int)r, prim);
+        atomicAdd(bcnt + b, 1u);
+        atomicMax(bw + b, wkey((int)r, v));
+      }
     }
   }
 }
@@ -389,16 +402,20 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
 
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf,
-                             u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st) {
+                             u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st, int log2nb,
+                             u32* bcnt, u64* bw) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
   constexpr size_t smem = kK2Tile * sizeof(double2);
   if (given_labels)
-    k_classify_compact<true><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, given_labels,
-                                                              force_lex, kbuf, vbuf, ncap, counts_out);
+    k_classify_compact<true, false><<<tiles, kK2Threads, smem, st>>>(
+        pts, n, qinfo, given_labels, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr);
+  else if (bcnt)
+    k_classify_compact<false, true><<<tiles, kK2Threads, smem, st>>>(
+        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, log2nb, bcnt, bw);
   else
-    k_classify_compact<false><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, nullptr, force_lex,
-                                                               kbuf, vbuf, ncap, counts_out);
+    k_classify_compact<false, false><<<tiles, kK2Threads, smem, st>>>(
+        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

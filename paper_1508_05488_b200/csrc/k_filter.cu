@@ -1,0 +1,723 @@
+// SPA pre-filter: the region sort restricted to the records the SPA can
+// keep. Replaces, on the hull path, sort_region over every survivor
+// (reference spa.cpp:59-81) followed by spa_filter (spa.cpp:109-163), with
+// the same kept chains.
+//
+// Why it is exact. spa_filter keeps record i of chunk c iff its guarded key
+// w_i (chgpu_internal.cuh wkey) is >= the running max of the chunk's seed
+// and every earlier w of the chunk (k_spa.cu header). Cut each region's
+// sorted sequence into bins of its primary coordinate (bin_of, monotone, so
+// bins are contiguous runs in sorted order), and let T_b be the max of the
+// chunk's seed and of w over every bin lying entirely inside the chunk
+// before bin b. T_b never exceeds the true running max at any record of b,
+// so a record with w < T_b steps back: it is not kept and, being below the
+// running max, does not move it. Dropping it therefore changes nothing for
+// any other record. What survives ("candidates") is sorted and scanned
+// exactly like the full sequence, provided every candidate knows its chunk:
+//   * a bin inside one chunk: the bin's chunk (from exact per-bin counts);
+//   * a bin straddling a chunk boundary: T = 0, every record is a candidate,
+//     so after sorting a record's rank inside the bin is its position.
+// The first bin of every chunk c > 0 has T = 0 (seed = identity) as well,
+// so each chunk's first candidate sits at a known dense position.
+//
+// Kernels (all grid-parallel over bins or records; none walks a chunk's
+// bins, since a sparse stretch of a region can put thousands of bins in
+// one chunk):
+//   K2 (kStats)        per survivor: bin count += 1, bin max(w) (k_discard.cu)
+//   k_bin_tile_sums    records per tile of 2048 bins
+//   k_bin_starts       bin start ranks, the bin holding each chunk's first
+//                      rank, and the tile's segmented-max aggregate
+//   k_bin_thresholds   T_b: segmented exclusive max (segments = chunks)
+//   k_filter           survivors with w >= T_b -> their bin's slots of a
+//                      sparse region-ordered layout (unordered in the bin)
+//   k_bin_sort_warp/_big  bins above 32 candidates sorted in place
+//   k_bin_tile_sums    candidates per tile (same kernel, on the cursors)
+//   k_cand_compact     dense candidate order: small bins batched and sorted
+//                      in registers, big bins copied; each chunk's first
+//                      dense index
+//   k_spa_dense (k_spa.cu)  the SPA scan over each chunk's dense candidates
+//
+// Algorithmic traffic: the filter reads 16 B per survivor and writes 16 B
+// per candidate (a few percent of survivors for spread-out inputs); the
+// bin tables are ~40 B per bin and stay in L2.
+
+#include <algorithm>
+
+#include "chgpu_internal.cuh"
+#include "kernels.h"
+
+namespace chgpu {
+
+// ------------------------------------------------------------------ bin scan
+
+// Segmented running max over bins: (seg, val) pairs, seg = chunk id,
+// kNone = empty prefix.
+constexpr u32 kNone = 0xFFFFFFFFu;
+struct SegMax {
+  u32 seg;
+  u64 val;
+};
+__device__ __forceinline__ SegMax seg_combine(SegMax a, SegMax b) {
+  if (b.seg == kNone) return a;
+  if (a.seg == kNone || b.seg != a.seg) return b;
+  return SegMax{b.seg, a.val > b.val ? a.val : b.val};
+}
+__device__ __forceinline__ SegMax shfl_up_seg(SegMax x, int o) {
+  return SegMax{__shfl_up_sync(0xffffffffu, x.seg, o), __shfl_up_sync(0xffffffffu, x.val, o)};
+}
+
+constexpr int kBinThreads = 256;
+constexpr int kBinPer = 8;
+constexpr int kBinTile = kBinThreads * kBinPer;  // 2048 bins
+
+__device__ __forceinline__ u32 bin_tiles(int log2nb) { return max(1u, (1u << log2nb) / kBinTile); }
+
+__device__ __forceinline__ void load8(const u32* p, u32* c) {
+  const uint4 a = reinterpret_cast<const uint4*>(p)[0], d = reinterpret_cast<const uint4*>(p)[1];
+  c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+  c[4] = d.x; c[5] = d.y; c[6] = d.z; c[7] = d.w;
+}
+
+// Block-wide exclusive sum (kBinThreads threads); *total gets the sum.
+__device__ __forceinline__ u32 block_excl_sum(u32 x, u32* sh, u32* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  u32 pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kBinThreads / 32; ++w) {
+    pre += (w < warp) ? sh[w] : 0u;
+    tot += sh[w];
+  }
+  *total = tot;
+  return pre + incl - x;
+}
+
+// Block-wide exclusive segmented max; *total gets the block aggregate.
+__device__ __forceinline__ SegMax block_excl_segmax(SegMax x, u32* sseg, u64* sval, SegMax* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SegMax inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const SegMax y = shfl_up_seg(inc, o);
+    if (lane >= o) inc = seg_combine(y, inc);
+  }
+  if (lane == 31) {
+    sseg[warp] = inc.seg;
+    sval[warp] = inc.val;
+  }
+  __syncthreads();
+  SegMax pre{kNone, 0}, tot{kNone, 0};
+#pragma unroll
+  for (int w = 0; w < kBinThreads / 32; ++w) {
+    const SegMax a{sseg[w], sval[w]};
+    if (w < warp) pre = seg_combine(pre, a);
+    tot = seg_combine(tot, a);
+  }
+  *total = tot;
+  SegMax ex = shfl_up_seg(inc, 1);
+  if (lane == 0) ex = SegMax{kNone, 0};
+  return seg_combine(pre, ex);
+}
+
+// Segmented-max elements of 8 consecutive bins starting at rank s: a bin
+// inside one chunk contributes (chunk, w); a straddling bin restarts its
+// last chunk with nothing known; an empty bin contributes nothing.
+__device__ __forceinline__ void seg_elems(const u32* c, const u64* w, u32 s, u32 cs, SegMax* e) {
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) {
+    if (c[j] == 0) {
+      e[j] = SegMax{kNone, 0};
+    } else {
+      const u32 clo = s / cs, chi = (s + c[j] - 1) / cs;
+      e[j] = clo != chi ? SegMax{chi, 0} : SegMax{clo, w[j]};
+    }
+    s += c[j];
+  }
+}
+
+// Sum of a u32 array per tile of kBinTile bins (record counts, or
+// candidate counts).
+__global__ __launch_bounds__(kBinThreads) void k_bin_tile_sums(const u32* __restrict__ cnt,
+                                                              int log2nb, u32* __restrict__ tsum) {
+  __shared__ u32 sh[kBinThreads / 32];
+  const u32 tiles = bin_tiles(log2nb);
+  const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
+  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
+  u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (b0 < (1u << log2nb)) load8(cnt + ((size_t)r << log2nb) + b0, c);
+  u32 x = 0;
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) x += c[j];
+  u32 tot;
+  block_excl_sum(x, sh, &tot);
+  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+// Bin starts (ranks inside the region), each chunk's first bin, and the
+// tile's segmented-max aggregate.
+__global__ __launch_bounds__(kBinThreads) void k_bin_starts(
+    const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ tsum,
+    FilterPlan P, u32* __restrict__ bstart, u32* __restrict__ first_bin,
+    u32* __restrict__ agg_seg, u64* __restrict__ agg_val) {
+  __shared__ u32 sh[kBinThreads / 32];
+  __shared__ u32 sseg[kBinThreads / 32];
+  __shared__ u64 sval[kBinThreads / 32];
+  __shared__ u32 s_base;
+  const u32 nb = 1u << P.log2nb;
+  const u32 tiles = bin_tiles(P.log2nb);
+  const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
+  if (P.spa.m[r] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    u32 x = 0;
+    for (u32 i = lane; i < t; i += 32) x += tsum[r * tiles + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_base = x;
+  }
+  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
+  const bool in = b0 < nb;
+  const size_t boff = (size_t)r << P.log2nb;
+  u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (in) {
+    load8(bcnt + boff + b0, c);
+#pragma unroll
+    for (int j = 0; j < kBinPer; j += 2) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(bw + boff + b0 + j);
+      w[j] = a.x;
+      w[j + 1] = a.y;
+    }
+  }
+  u32 x = 0;
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) x += c[j];
+  u32 tot;
+  const u32 ex = block_excl_sum(x, sh, &tot);
+  __syncthreads();  // s_base
+  const u32 s0 = s_base + ex;
+  const u32 cs = (u32)P.spa.chunk_size[r];  // ranks and sizes fit 32 bits (n < 2^32)
+  SegMax e[kBinPer];
+  seg_elems(c, w, s0, cs, e);
+  SegMax agg{kNone, 0};
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) agg = seg_combine(agg, e[j]);
+  SegMax tagg;
+  block_excl_segmax(agg, sseg, sval, &tagg);
+  if (threadIdx.x == 0) {
+    agg_seg[blockIdx.x] = tagg.seg;
+    agg_val[blockIdx.x] = tagg.val;
+  }
+  if (!in) return;
+  const u32 cbase = P.spa.chunk_begin[r];
+  u32 s = s0;
+  u32 so[kBinPer];
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) {
+    so[j] = s;
+    if (c[j]) {
+      const u32 chi = (s + c[j] - 1) / cs;
+      for (u32 q = (s + cs - 1) / cs; q <= chi; ++q) first_bin[cbase + q] = b0 + j;
+    }
+    s += c[j];
+  }
+  uint4* o = reinterpret_cast<uint4*>(bstart + boff + b0);
+  o[0] = make_uint4(so[0], so[1], so[2], so[3]);
+  o[1] = make_uint4(so[4], so[5], so[6], so[7]);
+}
+
+// T_b for every bin: max(seed of its chunk, exclusive segmented max of w
+// over the chunk's inner bins); 0 for straddling and empty bins. The carry
+// into a tile folds the aggregates of the region's earlier tiles.
+__global__ __launch_bounds__(kBinThreads) void k_bin_thresholds(
+    const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ bstart,
+    FilterPlan P, const u32* __restrict__ agg_seg, const u64* __restrict__ agg_val,
+    u64* __restrict__ bthr) {
+  __shared__ u32 sseg[kBinThreads / 32];
+  __shared__ u64 sval[kBinThreads / 32];
+  __shared__ u32 c_seg;
+  __shared__ u64 c_val;
+  const u32 nb = 1u << P.log2nb;
+  const u32 tiles = bin_tiles(P.log2nb);
+  const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
+  if (P.spa.m[r] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    // ordered fold of tiles [0, t): lane L folds its contiguous share, then
+    // an ordered warp scan
+    const u32 per = (t + 31) / 32;
+    SegMax a{kNone, 0};
+    for (u32 i = lane * per; i < min(t, (lane + 1) * per); ++i)
+      a = seg_combine(a, SegMax{agg_seg[r * tiles + i], agg_val[r * tiles + i]});
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const SegMax y = shfl_up_seg(a, o);
+      if (lane >= o) a = seg_combine(y, a);
+    }
+    if (lane == 31) {
+      c_seg = a.seg;
+      c_val = a.val;
+    }
+  }
+  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
+  const bool in = b0 < nb;
+  const size_t boff = (size_t)r << P.log2nb;
+  u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  u32 s0 = 0;
+  if (in) {
+    load8(bcnt + boff + b0, c);
+    s0 = bstart[boff + b0];
+#pragma unroll
+    for (int j = 0; j < kBinPer; j += 2) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(bw + boff + b0 + j);
+      w[j] = a.x;
+      w[j + 1] = a.y;
+    }
+  }
+  const u32 cs = (u32)P.spa.chunk_size[r];
+  SegMax e[kBinPer];
+  seg_elems(c, w, s0, cs, e);
+  SegMax agg{kNone, 0};
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) agg = seg_combine(agg, e[j]);
+  SegMax tagg;
+  SegMax run = block_excl_segmax(agg, sseg, sval, &tagg);
+  run = seg_combine(SegMax{c_seg, c_val}, run);  // c_* ready: block_excl_segmax synced
+  if (!in) return;
+  const u64 seedw = P.seed_w[r];
+  u64 th[kBinPer];
+  u32 s = s0;
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) {
+    th[j] = 0;
+    if (c[j]) {
+      const u32 clo = s / cs, chi = (s + c[j] - 1) / cs;
+      if (clo == chi) {
+        u64 tv = clo == 0 ? seedw : 0ull;
+        if (run.seg == clo && run.val > tv) tv = run.val;
+        th[j] = tv;
+      }
+    }
+    run = seg_combine(run, e[j]);
+    s += c[j];
+  }
+#pragma unroll
+  for (int j = 0; j < kBinPer; j += 2)
+    *reinterpret_cast<ulonglong2*>(bthr + boff + b0 + j) = make_ulonglong2(th[j], th[j + 1]);
+}
+
+// ------------------------------------------------------------------ filter
+
+constexpr int kFilterThreads = 256;
+constexpr int kFilterItems = 4;
+
+// Grid-stride over the survivors of the four K2 streams. A candidate takes
+// the next slot of its bin; the bin's 33rd candidate queues the bin for
+// k_bin_sort_big.
+__global__ __launch_bounds__(kFilterThreads) void k_filter(
+    const u64* __restrict__ kbuf, const u64* __restrict__ vbuf, FilterPlan P,
+    const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
+    const u64* __restrict__ bthr, u32* __restrict__ bcur, u64* __restrict__ kout,
+    u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
+    unsigned long long* __restrict__ ncand) {
+  __shared__ BinGeom s_geom;
+  __shared__ u32 s_cand;
+  if (threadIdx.x == 0) {
+    make_bin_geom(qinfo->q, P.log2nb, &s_geom);
+    s_cand = 0;
+  }
+  __syncthreads();
+  const u64 total = P.cum[4];
+  const u64 stride = (u64)gridDim.x * kFilterThreads * kFilterItems;
+  u32 mine = 0;
+  for (u64 i0 = (u64)blockIdx.x * kFilterThreads * kFilterItems + threadIdx.x; i0 < total;
+       i0 += stride) {
+    u64 k[kFilterItems], v[kFilterItems];
+    int rr[kFilterItems];
+#pragma unroll
+    for (int j = 0; j < kFilterItems; ++j) {
+      const u64 i = i0 + (u64)j * kFilterThreads;
+      int r = 0;
+      r += (i >= P.cum[1]);
+      r += (i >= P.cum[2]);
+      r += (i >= P.cum[3]);
+      rr[j] = r;
+      k[j] = v[j] = 0;
+      if (i < total) {
+        const u64 slot = P.src_off[r] + (i - P.cum[r]);
+        k[j] = __ldcs(kbuf + slot);
+        v[j] = __ldcs(vbuf + slot);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kFilterItems; ++j) {
+      const u64 i = i0 + (u64)j * kFilterThreads;
+      if (i >= total) continue;
+      const int reg = rr[j] + 1;
+      const u32 bi = ((u32)rr[j] << P.log2nb) | bin_of(s_geom, reg, primary_of(reg, k[j]));
+      if (wkey(reg, v[j]) < __ldg(bthr + bi)) continue;
+      const u32 pos = atomicAdd(bcur + bi, 1u);
+      const u64 dst = P.spa.off[rr[j]] + bstart[bi] + pos;
+      kout[dst] = k[j];
+      vout[dst] = v[j];
+      if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: sorted by a warp
+      if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: by a CTA
+      ++mine;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_cand, mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cand) atomicAdd(ncand, (unsigned long long)s_cand);
+}
+
+// ------------------------------------------------------------------ big bins
+//
+// Bins above 32 candidates are sorted in place, by (canon k, v, k) =
+// rec_less: up to kWarpSortMax by one warp in its own shared memory, above
+// that by a CTA, above kBinSortMax not at all (*overflow: the caller re-runs
+// the SPA over the full region sort).
+
+__device__ __forceinline__ bool key_gt(u64 ci, u64 vi, u64 ki, u64 cj, u64 vj, u64 kj) {
+  return ci > cj || (ci == cj && (vi > vj || (vi == vj && ki > kj)));
+}
+
+// Bitonic network over sc/sv/sk[0, Pn) executed by `nthreads` threads
+// (index `me`); `sync` separates the stages.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_smem(u64* sc, u64* sv, u64* sk, u32 Pn, u32 me, u32 nthreads,
+                                             Sync sync) {
+  for (u32 size = 2; size <= Pn; size <<= 1) {
+    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+      for (u32 t = me; t < Pn / 2; t += nthreads) {
+        const u32 i = 2 * t - (t & (stride - 1));  // lower index of the pair
+        const u32 jx = i + stride;
+        const bool up = (i & size) == 0;
+        const u64 ci = sc[i], cj = sc[jx], vi = sv[i], vj = sv[jx], ki = sk[i], kj = sk[jx];
+        if (key_gt(ci, vi, ki, cj, vj, kj) == up) {
+          sc[i] = cj; sc[jx] = ci;
+          sv[i] = vj; sv[jx] = vi;
+          sk[i] = kj; sk[jx] = ki;
+        }
+      }
+      sync();
+    }
+  }
+}
+
+constexpr int kWarpSortWarps = 8;
+
+__global__ __launch_bounds__(32 * kWarpSortWarps) void k_bin_sort_warp(
+    u64* __restrict__ k, u64* __restrict__ v, FilterPlan P, const u32* __restrict__ bstart,
+    const u32* __restrict__ bcur, const u32* __restrict__ big, const u32* __restrict__ nbig_p) {
+  __shared__ u64 sh[kWarpSortWarps][3][kWarpSortMax];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u64* sc = sh[wid][0];
+  u64* sv = sh[wid][1];
+  u64* sk = sh[wid][2];
+  const u32 nbig = *nbig_p;
+  for (u32 item = blockIdx.x * kWarpSortWarps + wid; item < nbig;
+       item += gridDim.x * kWarpSortWarps) {
+    const u32 bi = big[item];
+    const u32 len = bcur[bi];
+    if (len > (u32)kWarpSortMax) continue;  // the CTA kernel's
+    const int r = (int)(bi >> P.log2nb);
+    const u64 base = P.spa.off[r] + bstart[bi];
+    u32 Pn = 64;
+    while (Pn < len) Pn <<= 1;
+    for (u32 i = lane; i < Pn; i += 32) {
+      if (i < len) {
+        const u64 kk = k[base + i];
+        sk[i] = kk;
+        sv[i] = v[base + i];
+        sc[i] = canon_k(r + 1, kk);
+      } else {
+        sk[i] = sv[i] = sc[i] = ~0ull;
+      }
+    }
+    __syncwarp();
+    bitonic_smem(sc, sv, sk, Pn, lane, 32, [] { __syncwarp(); });
+    for (u32 i = lane; i < len; i += 32) {
+      k[base + i] = sk[i];
+      v[base + i] = sv[i];
+    }
+    __syncwarp();
+  }
+}
+
+constexpr int kBigThreads = 256;
+
+struct BigSmem {
+  u64 c[kBinSortMax], v[kBinSortMax], k[kBinSortMax];
+};
+
+__global__ __launch_bounds__(kBigThreads) void k_bin_sort_big(u64* __restrict__ k,
+                                                              u64* __restrict__ v, FilterPlan P,
+                                                              const u32* __restrict__ bstart,
+                                                              const u32* __restrict__ bcur,
+                                                              const u32* __restrict__ big,
+                                                              const u32* __restrict__ nbig_p,
+                                                              u32* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BigSmem& S = *reinterpret_cast<BigSmem*>(smem_raw);
+  const u32 nbig = *nbig_p;
+  for (u32 item = blockIdx.x; item < nbig; item += gridDim.x) {
+    const u32 bi = big[item];
+    const int r = (int)(bi >> P.log2nb);
+    const u32 len = bcur[bi];
+    if (len > (u32)kBinSortMax) {
+      if (threadIdx.x == 0) atomicOr(overflow, 1u);
+      continue;
+    }
+    const u64 base = P.spa.off[r] + bstart[bi];
+    u32 Pn = 64;
+    while (Pn < len) Pn <<= 1;
+    for (u32 i = threadIdx.x; i < Pn; i += kBigThreads) {
+      if (i < len) {
+        const u64 kk = k[base + i];
+        S.k[i] = kk;
+        S.v[i] = v[base + i];
+        S.c[i] = canon_k(r + 1, kk);
+      } else {
+        S.k[i] = S.v[i] = S.c[i] = ~0ull;
+      }
+    }
+    __syncthreads();
+    bitonic_smem(S.c, S.v, S.k, Pn, threadIdx.x, kBigThreads, [] { __syncthreads(); });
+    for (u32 i = threadIdx.x; i < len; i += kBigThreads) {
+      k[base + i] = S.k[i];
+      v[base + i] = S.v[i];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ dense candidates
+
+// Ascending bitonic sort of one record per lane by (g, canon k, v, k), g a
+// small group id (the bin's lane); lanes without a record carry g = ~0 and
+// sort last.
+__device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u64& v) {
+  const int lane = threadIdx.x & 31;
+  u64 c = g == ~0u ? ~0ull : canon_k(region, k);
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const u32 og = __shfl_xor_sync(0xffffffffu, g, stride);
+      const u64 oc = __shfl_xor_sync(0xffffffffu, c, stride);
+      const u64 ov = __shfl_xor_sync(0xffffffffu, v, stride);
+      const u64 ok = __shfl_xor_sync(0xffffffffu, k, stride);
+      const bool other_less =
+          og < g || (og == g && (oc < c || (oc == c && (ov < v || (ov == v && ok < k)))));
+      const bool mine_less =
+          g < og || (g == og && (c < oc || (c == oc && (v < ov || (v == ov && k < ok)))));
+      const bool want_min = ((lane & stride) == 0) == ((lane & size) == 0);
+      if (want_min ? other_less : mine_less) {
+        g = og;
+        c = oc;
+        v = ov;
+        k = ok;
+      }
+    }
+  }
+}
+
+// One CTA per tile of 2048 bins: dense position of every bin's candidates
+// (global order: region, bin, record) and each chunk's first dense index.
+__global__ __launch_bounds__(kBinThreads) void k_cand_positions(
+    const u32* __restrict__ bcnt, const u32* __restrict__ bcur, const u32* __restrict__ bstart,
+    const u32* __restrict__ csum, FilterPlan P, u32* __restrict__ cpos, u32* __restrict__ first_cand,
+    u32* __restrict__ region_end) {
+  __shared__ u32 sh[kBinThreads / 32];
+  __shared__ u32 s_base;
+  const u32 nb = 1u << P.log2nb;
+  const u32 tiles = bin_tiles(P.log2nb);
+  const u32 gt = blockIdx.x, r = gt / tiles, t = gt % tiles;
+  if (P.spa.m[r] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    u32 x = 0;
+    for (u32 i = lane; i < gt; i += 32) x += csum[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_base = x;
+  }
+  const size_t boff = (size_t)r << P.log2nb;
+  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
+  const bool in = b0 < nb;
+  u32 nc[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (in) load8(bcur + boff + b0, nc);
+  u32 x = 0;
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) x += nc[j];
+  u32 tot;
+  const u32 ex = block_excl_sum(x, sh, &tot);
+  __syncthreads();  // s_base
+  if (!in) return;
+  u32 cp = s_base + ex;
+  u32 n[kBinPer], st[kBinPer], cps[kBinPer];
+  load8(bcnt + boff + b0, n);
+  load8(bstart + boff + b0, st);
+  const u32 cs = (u32)P.spa.chunk_size[r];
+  const u32 cbase = P.spa.chunk_begin[r];
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) {
+    cps[j] = cp;
+    if (n[j]) {
+      // chunk starts in this bin: chunk 0 starts the region's candidates;
+      // a later chunk's first bin holds every one of its records
+      const u32 s = st[j], chi = (s + n[j] - 1) / cs;
+      for (u32 q = (s + cs - 1) / cs; q <= chi; ++q)
+        first_cand[cbase + q] = q == 0 ? cp : cp + (q * cs - s);
+    }
+    cp += nc[j];
+  }
+  uint4* o = reinterpret_cast<uint4*>(cpos + boff + b0);
+  o[0] = make_uint4(cps[0], cps[1], cps[2], cps[3]);
+  o[1] = make_uint4(cps[4], cps[5], cps[6], cps[7]);
+  if (b0 + kBinPer == nb) region_end[r] = cp;
+}
+
+// One warp per 32 consecutive bins: consecutive bins whose candidates fit
+// in 32 lanes form one batch, loaded one record per lane, sorted once by
+// (bin, record) and stored densely; bins above 32 candidates were sorted in
+// place and are copied.
+__global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
+                                                   const u64* __restrict__ v,
+                                                   const u32* __restrict__ bcur,
+                                                   const u32* __restrict__ bstart,
+                                                   const u32* __restrict__ cpos, FilterPlan P,
+                                                   u64* __restrict__ ck, u64* __restrict__ cv) {
+  __shared__ int s_mark[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 gb = (blockIdx.x * 8 + warp) * 32;  // first bin (all regions)
+  if (gb >= (4u << P.log2nb)) return;
+  const u32 r = gb >> P.log2nb;
+  if (P.spa.m[r] == 0) return;
+  const u32 b = gb + lane;
+  const u32 n = bcur[b];
+  unsigned todo = __ballot_sync(0xffffffffu, n > 0);
+  if (!todo) return;
+  const u32 s = bstart[b];
+  const u32 cp = cpos[b];
+  const bool act = n > 0;
+  const bool small = n <= 32;
+  const int region = (int)r + 1;
+  const u64 rbase = P.spa.off[r];
+  while (todo) {
+    const int p = __ffs(todo) - 1;
+    if (!__shfl_sync(0xffffffffu, small, p)) {
+      const u64 src = rbase + __shfl_sync(0xffffffffu, s, p);
+      const u32 dst = __shfl_sync(0xffffffffu, cp, p), len = __shfl_sync(0xffffffffu, n, p);
+      for (u32 i = lane; i < len; i += 32) {
+        ck[dst + i] = k[src + i];
+        cv[dst + i] = v[src + i];
+      }
+      todo &= todo - 1;
+      continue;
+    }
+    const u32 xx = (lane >= p && act) ? (small ? n : 64u) : 0u;
+    u32 incl = xx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned over = __ballot_sync(0xffffffffu, incl > 32);
+    const int e = over ? __ffs(over) - 1 : 32;  // batch = active bins in [p, e)
+    const bool inb = lane >= p && lane < e && act;
+    const u32 excl = incl - xx;
+    const u32 total = __shfl_sync(0xffffffffu, incl, e - 1);
+    s_mark[warp][lane] = -1;
+    __syncwarp();
+    if (inb) s_mark[warp][excl] = lane;
+    __syncwarp();
+    int jj = s_mark[warp][lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, jj, o);
+      if (lane >= o && y > jj) jj = y;
+    }
+    __syncwarp();
+    const bool has = (u32)lane < total;
+    const int src = has ? jj : 0;
+    const u32 bs = __shfl_sync(0xffffffffu, s, src);
+    const u32 bex = __shfl_sync(0xffffffffu, excl, src);
+    u64 kk = 0, vv = 0;
+    u32 g = ~0u;
+    if (has) {
+      const u64 a = rbase + bs + (lane - bex);
+      kk = k[a];
+      vv = v[a];
+      g = (u32)jj;
+    }
+    if (total > 1) warp_sort_records(region, g, kk, vv);
+    // bin g's records now occupy lanes [excl_g, excl_g + n_g) in order
+    const int gs = has ? (int)g : 0;
+    const u32 gex = __shfl_sync(0xffffffffu, excl, gs);
+    const u32 gcp = __shfl_sync(0xffffffffu, cp, gs);
+    if (has) {
+      ck[gcp + (lane - gex)] = kk;
+      cv[gcp + (lane - gex)] = vv;
+    }
+    todo &= ~__ballot_sync(0xffffffffu, inb);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan& P, u32* bstart, u64* bthr,
+                     u32* first_bin, FilterAux aux, cudaStream_t st) {
+  const u32 tiles = std::max(1u, (1u << P.log2nb) / kBinTile);
+  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, P.log2nb, aux.tsum);
+  k_bin_starts<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, aux.tsum, P, bstart, first_bin,
+                                                  aux.agg_seg, aux.agg_val);
+  k_bin_thresholds<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, bstart, P, aux.agg_seg,
+                                                      aux.agg_val, bthr);
+}
+
+void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan& P, const QuadInfo* qinfo,
+                   const u32* bstart, const u64* bthr, u32* bcur, u64* kout, u64* vout, u32* big,
+                   u32* nbig, unsigned long long* ncand, cudaStream_t st) {
+  const u64 total = P.cum[4];
+  if (total == 0) return;
+  const u64 per = (u64)kFilterThreads * kFilterItems;
+  const u64 blocks = std::min<u64>((total + per - 1) / per, 148ull * 8);
+  k_filter<<<(unsigned)blocks, kFilterThreads, 0, st>>>(kbuf, vbuf, P, qinfo, bstart, bthr, bcur,
+                                                          kout, vout, big, nbig, ncand);
+}
+
+void launch_bin_sort_big(u64* k, u64* v, const FilterPlan& P, const u32* bstart, const u32* bcur,
+                         const u32* big, const u32* nbig, u32* overflow, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_bin_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(BigSmem));
+    configured = true;
+  }
+  k_bin_sort_warp<<<148 * 4, 32 * kWarpSortWarps, 0, st>>>(k, v, P, bstart, bcur, big, nbig);
+  k_bin_sort_big<<<148 * 2, kBigThreads, sizeof(BigSmem), st>>>(k, v, P, bstart, bcur,
+                                                                big + kBigListB, nbig + 1, overflow);
+}
+
+void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
+                         const u32* bstart, const FilterPlan& P, u64* ck, u64* cv,
+                         u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st) {
+  const u32 tiles = std::max(1u, (1u << P.log2nb) / kBinTile);
+  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcur, P.log2nb, aux.csum);
+  k_cand_positions<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bcur, bstart, aux.csum, P, cpos,
+                                                      first_cand, aux.region_end);
+  k_cand_copy<<<(4u << P.log2nb) / 256, 256, 0, st>>>(k, v, bcur, bstart, cpos, P, ck, cv);
+}
+
+}  // namespace chgpu

@@ -46,13 +46,6 @@ __device__ __forceinline__ u32 quantize(const SegDesc& s, u64 k) {
   return (s.region == 3 || s.region == 4) ? (u32)((u64)qmax - q) : q;
 }
 
-// -0.0 as primary compares like +0.0: map its code onto +0.0's.
-__device__ __forceinline__ u64 canon_k(int region, u64 k) {
-  const bool desc = (region == 3 || region == 4);
-  const u64 neg0 = desc ? ~0x7FFFFFFFFFFFFFFFull : 0x7FFFFFFFFFFFFFFFull;
-  const u64 pos0 = desc ? ~0x8000000000000000ull : 0x8000000000000000ull;
-  return k == neg0 ? pos0 : k;
-}
 
 template <int kMode>
 __device__ __forceinline__ u32 digit_of(const SegDesc& s, u64 k, u64 v, int pass) {
@@ -390,13 +383,6 @@ __device__ __forceinline__ bool group_eq(int eqmode, const SegDesc& s, u64 a, u6
   return eqmode == kEqQ ? quantize(s, a) == quantize(s, b) : prim_eq(s.region, a, b);
 }
 
-// region_less on (canonical k, v); ties (==-equal points) fall back to the
-// raw k so the order is total on bits and the sort output is independent of
-// the order records arrived in.
-__device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u64 kb, u64 vb) {
-  const u64 ca = canon_k(region, ka), cb = canon_k(region, kb);
-  return ca < cb || (ca == cb && (va < vb || (va == vb && ka < kb)));
-}
 
 struct GroupRun {
   u64 start;  // absolute record index

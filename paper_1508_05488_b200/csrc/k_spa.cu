@@ -428,6 +428,82 @@ __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ 
   for (u32 i = lane; i < kc; i += 32) out[o + i] = scratch[begin + i];
 }
 
+// ------------------------------------------------------------------ SPA over dense candidates
+//
+// Same scan as k_spa_warp, over the pre-filter's candidates (k_filter.cu):
+// they are in region_less order in (ck, cv) and chunk c owns the dense
+// range [first_cand[c], first_cand[c + 1]) (the region's end for its last
+// chunk). One warp per chunk, 32 records per step, the running extremum in
+// a register.
+__global__ __launch_bounds__(256) void k_spa_dense(const u64* __restrict__ ck,
+                                                   const u64* __restrict__ cv, FilterPlan P,
+                                                   const u32* __restrict__ first_cand,
+                                                   const u32* __restrict__ region_end,
+                                                   double2* __restrict__ scratch,
+                                                   u32* __restrict__ chunk_kept) {
+  const SpaPlan& plan = P.spa;
+  const int lane = threadIdx.x & 31;
+  const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= plan.total_chunks) return;
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const u32 cl = c - plan.chunk_begin[r];
+  const u32 nchunks = (r < 3 ? plan.chunk_begin[r + 1] : plan.total_chunks) - plan.chunk_begin[r];
+  const u32 beg = first_cand[c];
+  const u32 end = cl + 1 < nchunks ? first_cand[c + 1] : region_end[r];
+  const bool is_min = (region == 1 || region == 4);
+  const double ident = is_min ? INFINITY : -INFINITY;
+  double carry = (cl == 0) ? plan.seed[r] : ident;
+  u32 kept = 0;
+  const u64 out0 = plan.off[r] + (u64)cl * plan.chunk_size[r];  // the chunk's scratch range
+
+  u64 nk = 0, nv = 0;
+  if (beg + lane < end) {
+    nk = ck[beg + lane];
+    nv = cv[beg + lane];
+  }
+  for (u32 t = beg; t < end; t += 32) {
+    const bool active = t + lane < end;
+    const u64 kk = nk, vv = nv;
+    if (t + 32 + lane < end) {  // next step's records in flight during this scan
+      nk = ck[t + 32 + lane];
+      nv = cv[t + 32 + lane];
+    }
+    const double g = active ? guarded_of(region, vv) : ident;
+    double incl = g;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = op_ext(is_min, y, incl);
+    }
+    double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) ex = ident;
+    const double th = op_ext(is_min, carry, ex);
+    const bool keep = active && !steps_back(is_min, g, th);
+    carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, incl, 31));
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      double px, py;
+      decode_point(region, kk, vv, px, py);
+      scratch[out0 + kept + __popc(km & lanemask_lt())] = make_double2(px, py);
+    }
+    kept += __popc(km);
+  }
+  if (lane == 0) chunk_kept[c] = kept;
+}
+
+void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan& P, const u32* first_cand,
+                      const u32* region_end, double2* scratch, u32* chunk_kept, u32* offs,
+                      unsigned long long* kept_counts, double2* out, cudaStream_t st) {
+  const SpaPlan& plan = P.spa;
+  if (plan.total_chunks == 0) return;
+  const u32 blocks = (plan.total_chunks + 7) / 8;
+  k_spa_dense<<<blocks, 256, 0, st>>>(ck, cv, P, first_cand, region_end, scratch, chunk_kept);
+  k_spa_offsets<<<1, 1024, 0, st>>>(chunk_kept, plan, offs, kept_counts);
+  k_spa_gather<<<blocks, 256, 0, st>>>(scratch, plan, chunk_kept, offs, out);
+}
+
 void launch_spa_warp(const u64* k, const u64* v, const SpaPlan& plan, double2* scratch,
                      u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
                      cudaStream_t st) {

@@ -34,6 +34,39 @@ struct SpaPlan {
   double seed[4];     // guarded(anchors.first)           (spa.cpp:130-132)
 };
 
+// SPA pre-filter (k_filter.cu + k_spa.cu k_spa_bins).
+constexpr int kBinSortMax = 4096;   // candidates of one bin sorted in shared memory (a CTA)
+constexpr int kWarpSortMax = 256;   // ... by one warp
+constexpr u32 kBigListB = 4u << 18; // offset of the CTA-sort list in the big-bin lists
+struct FilterPlan {
+  SpaPlan spa;          // chunk geometry, region offsets of the sorted layout
+  u64 src_off[4];       // region streams in the K2 two-ended layout
+  u64 cum[5];           // prefix of region sizes
+  u64 seed_w[4];        // wkey of guarded(anchors.first)
+  int log2nb;           // bins per region = 2^log2nb
+};
+// Small per-call scratch of the pre-filter (<= 512 bin tiles).
+struct FilterAux {
+  u32* tsum;        // records per bin tile
+  u32* csum;        // candidates per bin tile
+  u32* agg_seg;     // tile aggregates of the segmented max
+  u64* agg_val;
+  u32* region_end;  // [4] dense end of each region's candidates
+};
+void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan& P, u32* bstart, u64* bthr,
+                     u32* first_bin, FilterAux aux, cudaStream_t st);
+void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan& P, const QuadInfo* qinfo,
+                   const u32* bstart, const u64* bthr, u32* bcur, u64* kout, u64* vout, u32* big,
+                   u32* nbig, unsigned long long* ncand, cudaStream_t st);
+void launch_bin_sort_big(u64* k, u64* v, const FilterPlan& P, const u32* bstart, const u32* bcur,
+                         const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
+void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
+                         const u32* bstart, const FilterPlan& P, u64* ck, u64* cv,
+                         u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st);
+void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan& P, const u32* first_cand,
+                      const u32* region_end, double2* scratch, u32* chunk_kept, u32* offs,
+                      unsigned long long* kept_counts, double2* out, cudaStream_t st);
+
 // K1
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
                             int blocks, cudaStream_t st);
@@ -42,7 +75,8 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, 
 // K2
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
-                             u64 ncap, u32* counts_out, cudaStream_t st);
+                             u64 ncap, u32* counts_out, cudaStream_t st, int log2nb = 0,
+                             u32* bcnt = nullptr, u64* bw = nullptr);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

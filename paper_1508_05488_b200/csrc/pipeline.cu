@@ -40,7 +40,10 @@ struct Pinned {
   unsigned long long kept[4];
   unsigned long long uniq;
   unsigned long long counts5[5];
+  unsigned long long ncand;
 };
+
+constexpr int kMaxFilterBits = 18;  // SPA pre-filter: at most 2^18 bins per region
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -84,6 +87,19 @@ struct chgpu_ctx {
   u32* d_big = nullptr;     // oversized buckets
   SegDesc* d_segs = nullptr;
   size_t seg_cap = 0;
+  // SPA pre-filter tables (k_filter.cu), nbt = 4 << log2nb bins per call:
+  // d_ftab holds [max w: u64 x nbt][count: u32 x nbt][candidates: u32 x nbt],
+  // cleared by one memset per call.
+  unsigned char* d_ftab = nullptr;
+  u32* d_fstart = nullptr;   // per-bin first rank          [4 << kMaxFilterBits]
+  u64* d_fthr = nullptr;     // per-bin threshold            [4 << kMaxFilterBits]
+  u32* d_fbig = nullptr;     // bins queued for the big sorts [2 * kBigListB]
+  unsigned char* d_faux = nullptr;  // FilterAux scratch (bin-tile sums and aggregates)
+  u64* d_ck = nullptr;       // dense candidates (k words)    [cap]
+  u64* d_cv = nullptr;       // dense candidates (v words)    [cap]
+  u32* d_ffirst = nullptr;   // per-chunk first bin
+  size_t ffirst_cap = 0;
+  int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
 
   Pinned* h = nullptr;
   SegDesc* h_segs = nullptr;
@@ -143,6 +159,8 @@ void free_ws(chgpu_ctx* c) {
   cudaFree(c->d_va);
   cudaFree(c->d_flags);
   cudaFree(c->d_kept);
+  cudaFree(c->d_ck);
+  cudaFree(c->d_cv);
   cudaFree(c->d_status);
   cudaFree(c->d_starts);
   cudaFree(c->d_medium);
@@ -151,6 +169,7 @@ void free_ws(chgpu_ctx* c) {
   c->d_kbuf = c->d_vbuf = c->d_ka = c->d_va = nullptr;
   c->d_flags = nullptr;
   c->d_kept = nullptr;
+  c->d_ck = c->d_cv = nullptr;
   c->d_status = nullptr;
   c->d_starts = nullptr;
   c->d_medium = c->d_long = nullptr;
@@ -195,6 +214,8 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
   CK(cudaMalloc(&ctx->d_va, cap * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_flags, cap));
   CK(cudaMalloc(&ctx->d_kept, cap * sizeof(double2)));
+  CK(cudaMalloc(&ctx->d_ck, cap * sizeof(u64)));
+  CK(cudaMalloc(&ctx->d_cv, cap * sizeof(u64)));
   // Status words: K2 needs 4 per 2048-point tile, a sort pass 256 per
   // 4096-record tile (+1 tile per segment), the SPA one per chunk (<= cap).
   ctx->status_words = std::max(cap + 4096, (cap / kSortTile + 4096) * (size_t)kDigits);
@@ -684,6 +705,105 @@ int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
   return CHGPU_OK;
 }
 
+// Bins per region for the SPA pre-filter: about 64 per chunk (so a
+// chunk's first bin, whose records are all candidates, is ~1/64 of it),
+// at most 2^kMaxFilterBits, and not many more than there are points.
+int filter_bits(size_t n, size_t chunk_count) {
+  static const int per_chunk_log2 = [] {
+    const char* e = std::getenv("CHGPU_FILTER_BINS_PER_CHUNK_LOG2");  // tuning knob
+    return e ? std::max(0, std::min(12, std::atoi(e))) : 6;
+  }();
+  int b = 11;
+  while (b < kMaxFilterBits && ((size_t(1) << b) >> per_chunk_log2) < chunk_count) ++b;
+  while (b > 11 && (size_t(1) << b) > 2 * n) --b;
+  return b;
+}
+
+struct FilterTabs {
+  u64* w;
+  u32* cnt;
+  u32* cur;
+};
+FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
+  const size_t nbt = size_t(4) << log2nb;
+  FilterTabs t;
+  t.w = reinterpret_cast<u64*>(ctx->d_ftab);
+  t.cnt = reinterpret_cast<u32*>(t.w + nbt);
+  t.cur = t.cnt + nbt;
+  return t;
+}
+
+// The pre-filtered SPA (k_filter.cu): bin scan, filter, big-bin sort and
+// the SPA over bins; kept chains land in d_kept exactly as run_spa leaves
+// them. Reads back the kept counts, the candidate count and the overflow
+// flag (a bin too large for the shared-memory sort: *overflow = true and
+// the caller redoes the SPA over the full region sort).
+int run_filter_spa(chgpu_ctx* ctx, const u64 m[4], const SpaPlan& plan, int log2nb, bool* overflow,
+                   size_t* ncand) {
+  cudaStream_t st = ctx->st;
+  FilterPlan fp{};
+  fp.spa = plan;
+  fp.log2nb = log2nb;
+  const u64 cap = ctx->cap;
+  const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
+  fp.cum[0] = 0;
+  for (int r = 0; r < 4; ++r) {
+    fp.src_off[r] = src_off[r];
+    fp.cum[r + 1] = fp.cum[r] + m[r];
+    const int reg = r + 1;
+    const u64 enc = (reg == 1 || reg == 4) ? ~ord_enc(plan.seed[r]) : ord_enc(plan.seed[r]);
+    fp.seed_w[r] = wkey(reg, enc);
+  }
+  if (2 * (size_t)plan.total_chunks > ctx->ffirst_cap) {
+    cudaFree(ctx->d_ffirst);
+    ctx->d_ffirst = nullptr;
+    const size_t want = std::max<size_t>(2 * (size_t)plan.total_chunks, 8192);
+    CK(cudaMalloc(&ctx->d_ffirst, want * sizeof(u32)));
+    ctx->ffirst_cap = want;
+  }
+  u32* first_bin = ctx->d_ffirst;
+  u32* first_cand = ctx->d_ffirst + plan.total_chunks;
+  FilterAux aux;
+  aux.tsum = reinterpret_cast<u32*>(ctx->d_faux);
+  aux.csum = aux.tsum + 512;
+  aux.agg_seg = aux.csum + 512;
+  aux.region_end = aux.agg_seg + 512;
+  aux.agg_val = reinterpret_cast<u64*>(ctx->d_faux + 8192);
+  const FilterTabs t = filter_tabs(ctx, log2nb);
+  const int nbig_slot = take_ctr(ctx), nbig2_slot = take_ctr(ctx), ovf_slot = take_ctr(ctx);
+  (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
+  launch_bin_scan(t.cnt, t.w, fp, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
+  CK(cudaEventRecord(ctx->ev[3], st));
+  launch_filter(ctx->d_kbuf, ctx->d_vbuf, fp, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr, t.cur,
+                ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
+  CK(cudaEventRecord(ctx->ev[4], st));
+  launch_bin_sort_big(ctx->d_ka, ctx->d_va, fp, ctx->d_fstart, t.cur, ctx->d_fbig,
+                      ctx->d_ctr + nbig_slot, ctx->d_ctr + ovf_slot, st);
+  // the bin thresholds are dead once the filter ran: their table holds the
+  // dense positions now
+  launch_cand_compact(ctx->d_ka, ctx->d_va, t.cnt, t.cur, ctx->d_fstart, fp, ctx->d_ck, ctx->d_cv,
+                      first_cand, reinterpret_cast<u32*>(ctx->d_fthr), aux, st);
+  CK(cudaEventRecord(ctx->ev[5], st));
+  CK(cudaEventRecord(ctx->ev[6], st));
+  u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
+  u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
+  launch_spa_dense(ctx->d_ck, ctx->d_cv, fp, first_cand, aux.region_end, ctx->d_pts, chunk_kept,
+                   offs, ctx->d_u64, ctx->d_kept, st);
+  ctx->launches += 10 + (plan.total_chunks ? 3 : 0);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[8], st));
+  CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ctx->h->ncand, ctx->d_u64 + 11, sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
+                     cudaMemcpyDeviceToHost, st));
+  TRY(sync(ctx));
+  *overflow = ctx->h->ctr[ovf_slot] != 0;
+  *ncand = (size_t)ctx->h->ncand;
+  return CHGPU_OK;
+}
+
 void frame_of(const double* quad, Pt* fr, int* nf) {
   *nf = 0;
   for (int c = 0; c < 4; ++c) {
@@ -748,11 +868,20 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   launch_extremes_final(ctx->d_partials, nparts, ctx->d_qinfo, nullptr, st);
   CK(cudaEventRecord(ctx->ev[1], st));
 
-  // ---- K2: classify + round-1 discard (classify.cpp:9-87).
+  // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
+  // pre-filter's per-bin statistics when that path is taken.
+  const bool want_filter =
+      ctx->spa_mode == CHGPU_SPA_FILTER ||
+      (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count >= 1 && chunk_count <= n / 64);
+  const int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
+  if (want_filter)
+    CK(cudaMemsetAsync(ctx->d_ftab, 0, (size_t(4) << log2nb) * 16, st));
+  const FilterTabs ftabs = filter_tabs(ctx, log2nb);
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
   launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
-                          ctx->cap, ctx->d_ctr + cnt_slot, st);
+                          ctx->cap, ctx->d_ctr + cnt_slot, st, log2nb,
+                          want_filter ? ftabs.cnt : nullptr, ftabs.w);
   ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
@@ -797,39 +926,71 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   } else {
     for (int s = 0; s < 4; ++s) D.region_counts[s + 1] = m[s];
     D.region_counts[0] = n - s1;
-    // ---- K3: region sort (spa.cpp:59-81).
-    Sorted so{};
-    TRY(sort_regions(ctx, m, qi.q, true, true, &so));
-    D.sort_passes = so.passes;
-    const bool sort_timed = s1 > 0;
-    CK(cudaEventRecord(ctx->ev[6], st));
-
-    // ---- K4/K5: SPA (spa.cpp:109-163). chunk_count == 0 raises here, on
-    // the non-degenerate branch only, exactly like the reference.
+    // chunk_count == 0 raises on the non-degenerate branch only, exactly
+    // like the reference (spa.cpp:112-113).
     if (chunk_count == 0) return fail(ctx, CHGPU_INVALID_ARG, "spa_filter: chunk_count must be >= 1");
     const SpaPlan plan = make_spa_plan(m, chunk_count, qi.q);
-    auto spa_and_read = [&]() -> int {
-      CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), st));
-      TRY(run_spa(ctx, so.kF, so.vF, plan));
-      CK(cudaEventRecord(ctx->ev[8], st));
-      // kept counts, the group count and the long-group count in one trip
-      CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 10, sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, st));
-      if (so.pend.slot >= 0)
-        CK(cudaMemcpyAsync(&ctx->h->ctr[so.pend.slot], ctx->d_ctr + so.pend.slot, sizeof(u32),
+    bool filtered = false;
+    if (want_filter) {
+      // ---- K3 + K4/K5 on the SPA candidates only (k_filter.cu).
+      bool overflow = false;
+      size_t ncand = 0;
+      TRY(run_filter_spa(ctx, m, plan, log2nb, &overflow, &ncand));
+      D.n_candidates = ncand;
+      D.filter_log2nb = log2nb;
+      D.spa_path = overflow ? 2 : 1;
+      filtered = !overflow;
+      if (!filtered) t_sort_ms = ms_between(ctx->ev[2], ctx->ev[8]);  // the attempt
+      if (filtered) {
+        t_sort_ms = ms_between(ctx->ev[2], ctx->ev[6]);
+        t_spa_ms = ms_between(ctx->ev[6], ctx->ev[8]);
+        D.t_spa_kernel_ms = t_spa_ms;
+        D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
+        D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
+        D.t_binsort_ms = ms_between(ctx->ev[4], ctx->ev[5]);
+      }
+    }
+    if (!filtered) {
+      // ---- K3: region sort (spa.cpp:59-81) of every survivor.
+      CK(cudaEventRecord(ctx->ev[7], st));
+      Sorted so{};
+      TRY(sort_regions(ctx, m, qi.q, true, true, &so));
+      D.sort_passes = so.passes;
+      const bool sort_timed = s1 > 0;
+      CK(cudaEventRecord(ctx->ev[6], st));
+
+      // ---- K4/K5: SPA (spa.cpp:109-163).
+      auto spa_and_read = [&]() -> int {
+        CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), st));
+        TRY(run_spa(ctx, so.kF, so.vF, plan));
+        CK(cudaEventRecord(ctx->ev[8], st));
+        // kept counts, the group count and the long-group count in one trip
+        CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
-      return sync(ctx);
-    };
-    TRY(spa_and_read());
-    D.tie_runs = (size_t)ctx->h->uniq;
-    if (so.pend.slot >= 0 && ctx->h->ctr[so.pend.slot] > 0) {
-      // Rare: groups too long for shared memory. Sort them, then redo the
-      // SPA over the now fully ordered regions.
-      bool had = false;
-      TRY(resolve_long(ctx, so.pend, &had));
+        CK(cudaMemcpyAsync(&ctx->h->uniq, ctx->d_u64 + 10, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+        if (so.pend.slot >= 0)
+          CK(cudaMemcpyAsync(&ctx->h->ctr[so.pend.slot], ctx->d_ctr + so.pend.slot, sizeof(u32),
+                             cudaMemcpyDeviceToHost, st));
+        return sync(ctx);
+      };
       TRY(spa_and_read());
+      D.tie_runs = (size_t)ctx->h->uniq;
+      if (so.pend.slot >= 0 && ctx->h->ctr[so.pend.slot] > 0) {
+        // Rare: groups too long for shared memory. Sort them, then redo the
+        // SPA over the now fully ordered regions.
+        bool had = false;
+        TRY(resolve_long(ctx, so.pend, &had));
+        TRY(spa_and_read());
+      }
+      t_sort_ms += ms_between(ctx->ev[7], ctx->ev[6]);
+      t_spa_ms = ms_between(ctx->ev[6], ctx->ev[8]);
+      D.t_spa_kernel_ms = t_spa_ms;
+      if (sort_timed) {
+        D.t_hist_ms = ms_between(ctx->ev[7], ctx->ev[3]);
+        D.t_passes_ms = ms_between(ctx->ev[4], ctx->ev[5]);
+        D.t_ties_ms = ms_between(ctx->ev[5], ctx->ev[6]);
+      }
     }
     size_t kept_counts[4], kept = 0;
     for (int r = 0; r < 4; ++r) {
@@ -838,14 +999,6 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       kept += kept_counts[r];
     }
     S.n_after_spa = kept + qi.frame_size;  // pipeline.cpp:96
-    t_sort_ms = ms_between(ctx->ev[2], ctx->ev[6]);
-    t_spa_ms = ms_between(ctx->ev[6], ctx->ev[8]);
-    D.t_spa_kernel_ms = t_spa_ms;
-    if (sort_timed) {
-      D.t_hist_ms = ms_between(ctx->ev[2], ctx->ev[3]);
-      D.t_passes_ms = ms_between(ctx->ev[4], ctx->ev[5]);
-      D.t_ties_ms = ms_between(ctx->ev[5], ctx->ev[6]);
-    }
 
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
@@ -937,11 +1090,20 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_bbase, (size_t(4) << kMaxBucketBits) * sizeof(u64))) ||
       bad(cudaMalloc(&ctx->d_bcur, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_big, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
+      bad(cudaMalloc(&ctx->d_ftab, (size_t(4) << kMaxFilterBits) * 16)) ||
+      bad(cudaMalloc(&ctx->d_fstart, (size_t(4) << kMaxFilterBits) * sizeof(u32))) ||
+      bad(cudaMalloc(&ctx->d_fthr, (size_t(4) << kMaxFilterBits) * sizeof(u64))) ||
+      bad(cudaMalloc(&ctx->d_fbig, 2 * (size_t)kBigListB * sizeof(u32))) ||
+      bad(cudaMalloc(&ctx->d_faux, 16384)) ||
       bad(cudaMallocHost(&ctx->h, sizeof(Pinned)))) {
     chgpu_ctx_destroy(ctx);
     return CHGPU_CUDA_ERR;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  if (const char* e = std::getenv("CHGPU_SPA")) {
+    if (std::strcmp(e, "sort") == 0) ctx->spa_mode = CHGPU_SPA_SORT;
+    if (std::strcmp(e, "filter") == 0) ctx->spa_mode = CHGPU_SPA_FILTER;
+  }
   if (ensure_segs(ctx, 64) != CHGPU_OK) {
     chgpu_ctx_destroy(ctx);
     return CHGPU_CUDA_ERR;
@@ -966,6 +1128,12 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_bbase);
   cudaFree(ctx->d_bcur);
   cudaFree(ctx->d_big);
+  cudaFree(ctx->d_ftab);
+  cudaFree(ctx->d_fstart);
+  cudaFree(ctx->d_fthr);
+  cudaFree(ctx->d_fbig);
+  cudaFree(ctx->d_faux);
+  cudaFree(ctx->d_ffirst);
   cudaFree(ctx->d_digit_excl);
   cudaFreeHost(ctx->h);
   cudaFreeHost(ctx->h_segs);
@@ -979,6 +1147,19 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
 }
 
 const char* chgpu_last_error(const chgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
+  if (!ctx) return CHGPU_INVALID_ARG;
+  switch (option) {
+    case CHGPU_OPT_SPA_PATH:
+      if (value < CHGPU_SPA_AUTO || value > CHGPU_SPA_FILTER) break;
+      ctx->spa_mode = (int)value;
+      return CHGPU_OK;
+    default:
+      break;
+  }
+  return fail(ctx, CHGPU_INVALID_ARG, "chgpu_ctx_set_option: unknown option or value");
+}
 
 void* chgpu_ctx_stream(chgpu_ctx* ctx) { return ctx ? (void*)ctx->st : nullptr; }
 

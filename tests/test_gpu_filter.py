@@ -1,0 +1,112 @@
+"""GPU parity of the SPA pre-filter path (k_filter.cu + k_spa_bins) and of
+the full-sort path it replaces, forced per context, against the reference's
+golden outputs and the C oracle. Both paths must give the reference's hull
+and every stage counter (n_after_spa counts the kept chains, so the kept set
+itself is pinned)."""
+import numpy as np
+import pytest
+
+from conftest import load_golden, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=["sort", "filter"])
+def path_ctx(request):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1508_05488_b200 as P
+    ctx = P.Context(0)
+    ctx.set_spa_path(P.SPA_SORT if request.param == "sort" else P.SPA_FILTER)
+    ctx.path = request.param
+    yield ctx
+    ctx.close()
+
+
+def _counts(r):
+    s = r.stats
+    return [s.n_input, s.n_after_round1, s.n_after_spa, s.n_hull]
+
+
+def test_sweep_both_paths(path_ctx, product):
+    """acceptance.cpp:57-94 sweep (n = 1 .. 100000, chunk counts 1, 4, 1024)."""
+    n = 0
+    for case in load_golden("pipeline_sweep.json"):
+        pts = product.generate(case["dist"], case["n"], case["seed"])
+        for run in case["runs"]:
+            r = path_ctx.convex_hull(pts, product.PipelineConfig(chunk_count=run["chunk_count"]))
+            assert _counts(r) == run["counts"], (path_ctx.path, case["dist"], case["n"], run)
+            assert sha(r.hull.vertices) == run["hull_sha"]
+            if not r.diag.degenerate_branch:
+                assert r.diag.spa_path == (0 if path_ctx.path == "sort" else 1)
+            n += 1
+    assert n >= 700
+
+
+@pytest.mark.parametrize("idx", range(10))
+def test_big_configs_both_paths(path_ctx, product, idx):
+    case = load_golden("big.json")[idx]
+    pts = product.generate(case["dist"], case["n"], case["seed"])
+    r = path_ctx.convex_hull(pts)
+    assert _counts(r) == case["counts"]
+    assert sha(r.hull.vertices) == case["hull_sha"]
+    if path_ctx.path == "filter" and case["dist"] in ("uniform_square", "uniform_disk"):
+        assert r.diag.spa_path == 1
+        s1 = r.stats.n_after_round1
+        assert r.diag.n_candidates < 0.1 * s1, (r.diag.n_candidates, s1)
+
+
+def _clustered(n, seed):
+    """Dense clusters (bins far above 32 candidates), exact duplicates and
+    a ring of coincident extremes."""
+    rng = np.random.default_rng(seed)
+    c = rng.random((40, 2))
+    pts = c[rng.integers(0, 40, n)] + 1e-4 * rng.standard_normal((n, 2))
+    dup = pts[rng.integers(0, n, n // 10)]
+    return np.vstack([pts, dup, [[-1, 0.5], [0.5, -1], [2, 0.5], [0.5, 2]] * 3])
+
+
+@pytest.mark.parametrize("n,seed", [(1000, 1), (100_000, 2), (3_000_000, 3)])
+def test_clustered_and_duplicates(path_ctx, product, oracle, n, seed):
+    pts = _clustered(n, seed)
+    for cc in (1, 5, 1024, 20_000):
+        want = oracle.convex_hull(pts, cc)
+        r = path_ctx.convex_hull(pts, product.PipelineConfig(chunk_count=cc))
+        assert _counts(r) == want.counts.tolist(), (path_ctx.path, n, cc)
+        assert np.array_equal(r.hull.vertices, want.hull)
+        assert r.diag.kept_counts == want.kept_counts.tolist()
+
+
+def test_grid_ties_and_signed_zeros(path_ctx, product, oracle):
+    rng = np.random.default_rng(17)
+    for trial in range(6):
+        n = 50_000 * (trial + 1)
+        x = rng.integers(0, 33, n) / 32.0 - 0.5
+        y = rng.integers(0, 17, n) / 16.0 - 0.5
+        pts = np.stack([x, y], 1)
+        flip = rng.random(n) < 0.2
+        pts[flip] = -pts[flip]
+        pts = np.vstack([pts, [[-0.7, 0.0], [0.0, -0.7], [0.7, 0.0], [0.0, 0.7]]])
+        for cc in (1, 16, 1024):
+            want = oracle.convex_hull(pts, cc)
+            r = path_ctx.convex_hull(pts, product.PipelineConfig(chunk_count=cc))
+            assert _counts(r) == want.counts.tolist(), (trial, cc)
+            assert (r.hull.vertices == want.hull).all()
+
+
+def test_overflow_falls_back(product, oracle):
+    """A bin with more than kBinSortMax candidates (all points on a circle
+    arc, every one kept) makes the filter hand over to the full sort."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = product.Context(0)
+    ctx.set_spa_path(product.SPA_FILTER)
+    pts = product.generate("circle", 2_000_000, 3)
+    want = oracle.convex_hull(pts, 1024)
+    r = ctx.convex_hull(pts)
+    assert _counts(r) == want.counts.tolist()
+    assert np.array_equal(r.hull.vertices, want.hull)
+    assert r.diag.spa_path in (1, 2)
+    ctx.close()
