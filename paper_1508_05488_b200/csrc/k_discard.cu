@@ -81,52 +81,14 @@ __device__ __forceinline__ void empty_quad(QuadCand& a) {
 constexpr int kK1Threads = 256;
 constexpr int kK1Unroll = 4;
 
-// Grid-stride pass: thread t visits t, t+T, t+2T, ... in increasing order,
-// so its running fold is the sequential fold of its subsequence.
-__global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(const double2* __restrict__ pts,
-                                                                 u64 n, u64 base_index,
-                                                                 QuadCand* __restrict__ partials) {
-  QuadCand acc;
-  empty_quad(acc);
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
-    double2 p[kK1Unroll];
-#pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i + u * stride);
-#pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
-  }
-  for (; i < n; i += stride) {
-    const double2 p = ldg_stream(pts + i);
-    fold_point(acc, p.x, p.y, base_index + i);
-  }
-  // Warp then block combine; ties fall back to the index so the result is
-  // independent of the combine order.
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    QuadCand other;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) other.c[c] = shfl_cand(acc.c[c], o);
-    merge_quad(acc, other);
-  }
-  __shared__ QuadCand warp_acc[kK1Threads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) warp_acc[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < kK1Threads / 32; ++w) merge_quad(acc, warp_acc[w]);
-    partials[blockIdx.x] = acc;
-  }
-}
-
-__global__ __launch_bounds__(1024) void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
-                                 QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
+// Block-wide merge of nparts partials and the QuadInfo (with
+// frame_vertices, extremes.cpp:49-57). Ties fall back to the global index,
+// so the result is independent of the merge order.
+__device__ void merge_partials_block(const QuadCand* __restrict__ partials, int nparts,
+                                     QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
   QuadCand acc;
   empty_quad(acc);
   for (int p = threadIdx.x; p < nparts; p += blockDim.x) merge_quad(acc, partials[p]);
-  // Tree combine: warp shuffles, then the 8 warp results (order-free: ties
-  // fall back to the global index).
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     QuadCand other;
@@ -142,28 +104,87 @@ __global__ __launch_bounds__(1024) void k_extremes_final(const QuadCand* __restr
     if (raw_out) *raw_out = acc;
     if (out) {
       QuadInfo qi;
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
         qi.q[2 * c] = acc.c[c].x;
         qi.q[2 * c + 1] = acc.c[c].y;
         qi.idx[c] = acc.c[c].i;
       }
-      // frame_vertices (extremes.cpp:49-57)
-      double fx[4], fy[4];
-      int k = 0;
-      for (int c = 0; c < 4; ++c) {
+      // frame_vertices (extremes.cpp:49-57): consecutive and wrap duplicates
+      // collapse; compared by == like Point2::operator==.
+      u32 k = 1;
+      double lx = qi.q[0], ly = qi.q[1];
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
         const double x = qi.q[2 * c], y = qi.q[2 * c + 1];
-        if (k == 0 || !(fx[k - 1] == x && fy[k - 1] == y)) {
-          fx[k] = x;
-          fy[k] = y;
+        if (!(lx == x && ly == y)) {
           ++k;
+          lx = x;
+          ly = y;
         }
       }
-      if (k > 1 && fx[0] == fx[k - 1] && fy[0] == fy[k - 1]) --k;
-      qi.frame_size = (u32)k;
+      if (k > 1 && qi.q[0] == lx && qi.q[1] == ly) --k;
+      qi.frame_size = k;
       qi.degenerate = k <= 2 ? 1u : 0u;
       *out = qi;
     }
   }
+}
+
+// Grid-stride pass: thread t visits t, t+T, t+2T, ... in increasing order,
+// so its running fold is the sequential fold of its subsequence. With a
+// ticket counter, the last block to finish (over every launch of the call:
+// total_parts blocks) merges all partials itself, so no final launch is
+// needed.
+__global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(
+    const double2* __restrict__ pts, u64 n, u64 base_index, QuadCand* __restrict__ partials,
+    u32 part_base, u32* __restrict__ ticket, u32 total_parts, QuadInfo* __restrict__ out) {
+  QuadCand acc;
+  empty_quad(acc);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
+    double2 p[kK1Unroll];
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kK1Unroll; ++u) fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
+  }
+  for (; i < n; i += stride) {
+    const double2 p = ldg_stream(pts + i);
+    fold_point(acc, p.x, p.y, base_index + i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    QuadCand other;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) other.c[c] = shfl_cand(acc.c[c], o);
+    merge_quad(acc, other);
+  }
+  __shared__ QuadCand warp_acc[kK1Threads / 32];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) warp_acc[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kK1Threads / 32; ++w) merge_quad(acc, warp_acc[w]);
+    partials[part_base + blockIdx.x] = acc;
+    s_last = 0;
+    if (ticket) {
+      __threadfence();
+      s_last = atomicAdd(ticket, 1u) == total_parts - 1;
+    }
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    merge_partials_block(partials, (int)total_parts, out, nullptr);
+  }
+}
+
+__global__ __launch_bounds__(1024) void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
+                                 QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
+  merge_partials_block(partials, nparts, out, raw_out);
 }
 
 // ------------------------------------------------------------------ K2
@@ -223,7 +244,7 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out, int log2nb,
-    u32* __restrict__ bcnt, u64* __restrict__ bw) {
+    u32* __restrict__ bcnt, u64* __restrict__ bw, u32 wmask) {
   extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
   __shared__ u32 s_wtot[kK2Threads / 32][4];
   __shared__ u32 s_base[4];
@@ -333,7 +354,8 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
         const double prim = (r & 1u) ? p.x : p.y;
         const u32 b = ((r - 1) << log2nb) | bin_of(s_geom, (int)r, prim);
         atomicAdd(bcnt + b, 1u);
-        atomicMax(bw + b, wkey((int)r, v));
+        // any subset of a bin's records gives a valid (lower) max: sample
+        if ((pp & wmask) == 0) atomicMax(bw + b, wkey((int)r, v));
       }
     }
   }
@@ -378,8 +400,7 @@ __global__ void k_classify_labels(const double2* __restrict__ pts, u64 n,
 
 // ------------------------------------------------------------------ launchers
 
-int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
-                            int blocks, cudaStream_t st) {
+int extremes_blocks(int requested) {
   // One resident wave at most: a grid-stride kernel gains nothing from a
   // second partial wave, it only adds a tail.
   static int wave = 0;
@@ -390,8 +411,15 @@ int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     wave = std::max(1, occ) * std::max(1, sms);
   }
-  blocks = std::max(1, std::min(blocks, wave));
-  k_extremes_partial<<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials);
+  return std::max(1, std::min(requested, wave));
+}
+
+int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
+                            int blocks, cudaStream_t st, u32 part_base, u32* ticket,
+                            u32 total_parts, QuadInfo* out) {
+  blocks = extremes_blocks(blocks);
+  k_extremes_partial<<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base, ticket,
+                                                    total_parts, out);
   return blocks;
 }
 
@@ -403,19 +431,19 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf,
                              u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st, int log2nb,
-                             u32* bcnt, u64* bw) {
+                             u32* bcnt, u64* bw, u32 wmask) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
   constexpr size_t smem = kK2Tile * sizeof(double2);
   if (given_labels)
     k_classify_compact<true, false><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, given_labels, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr);
+        pts, n, qinfo, given_labels, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr, 0);
   else if (bcnt)
     k_classify_compact<false, true><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, log2nb, bcnt, bw);
+        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, log2nb, bcnt, bw, wmask);
   else
     k_classify_compact<false, false><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr);
+        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr, 0);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

@@ -68,15 +68,20 @@ void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan& P, const u
                       unsigned long long* kept_counts, double2* out, cudaStream_t st);
 
 // K1
+// Blocks launch_extremes_partial will use for a request of `requested`.
+int extremes_blocks(int requested);
+// With a ticket counter (zeroed) and the call's total partial count, the
+// last block merges every partial into *out: no launch_extremes_final.
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
-                            int blocks, cudaStream_t st);
+                            int blocks, cudaStream_t st, u32 part_base = 0,
+                            u32* ticket = nullptr, u32 total_parts = 0, QuadInfo* out = nullptr);
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, QuadCand* raw_out,
                            cudaStream_t st);
 // K2
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
                              u64 ncap, u32* counts_out, cudaStream_t st, int log2nb = 0,
-                             u32* bcnt = nullptr, u64* bw = nullptr);
+                             u32* bcnt = nullptr, u64* bw = nullptr, u32 wmask = 0);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

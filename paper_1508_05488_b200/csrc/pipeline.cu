@@ -705,18 +705,29 @@ int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
   return CHGPU_OK;
 }
 
-// Bins per region for the SPA pre-filter: about 64 per chunk (so a
-// chunk's first bin, whose records are all candidates, is ~1/64 of it),
+// Bins per region for the SPA pre-filter: about 256 per chunk (so a
+// chunk's first bin, whose records are all candidates, is ~1/256 of it),
 // at most 2^kMaxFilterBits, and not many more than there are points.
 int filter_bits(size_t n, size_t chunk_count) {
   static const int per_chunk_log2 = [] {
     const char* e = std::getenv("CHGPU_FILTER_BINS_PER_CHUNK_LOG2");  // tuning knob
-    return e ? std::max(0, std::min(12, std::atoi(e))) : 6;
+    return e ? std::max(0, std::min(12, std::atoi(e))) : 8;
   }();
   int b = 11;
   while (b < kMaxFilterBits && ((size_t(1) << b) >> per_chunk_log2) < chunk_count) ++b;
   while (b > 11 && (size_t(1) << b) > 2 * n) --b;
   return b;
+}
+
+// Records per bin whose w feeds the bin's max (1 in 2^k; tuning knob).
+// Any subset gives a valid threshold (the max of a subset is a lower bound).
+u32 filter_wmask() {
+  static const u32 m = [] {
+    const char* e = std::getenv("CHGPU_FILTER_WSAMPLE_LOG2");
+    const int k = e ? std::max(0, std::min(8, std::atoi(e))) : 0;
+    return (1u << k) - 1u;
+  }();
+  return m;
 }
 
 struct FilterTabs {
@@ -847,6 +858,13 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     }
     CK(cudaEventRecord(ctx->ev[11], st));
     CK(cudaStreamWaitEvent(ctx->st_copy, ctx->ev[11], 0));
+    // the last partial block of the call merges the quad (no final launch)
+    u32 total_parts = 0;
+    for (size_t c = 0; c < nchunks; ++c) {
+      const size_t cnt = std::min(kH2DChunk, n - c * kH2DChunk);
+      total_parts += (u32)extremes_blocks((int)std::min<size_t>(per, (cnt + 255) / 256));
+    }
+    const int ticket = take_ctr(ctx);
     for (size_t c = 0; c < nchunks; ++c) {
       const size_t off = c * kH2DChunk, cnt = std::min(kH2DChunk, n - off);
       CK(cudaMemcpyAsync(ctx->d_pts + off, h_src + 2 * off, cnt * sizeof(double2),
@@ -854,18 +872,21 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       CK(cudaEventRecord(ctx->ev_copy[c], ctx->st_copy));
       CK(cudaStreamWaitEvent(st, ctx->ev_copy[c], 0));
       const int blocks = (int)std::min<size_t>(per, (cnt + 255) / 256);
-      nparts += launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials + nparts,
-                                        blocks, st);
+      nparts += launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials, blocks, st,
+                                        (u32)nparts, ctx->d_ctr + ticket, total_parts,
+                                        ctx->d_qinfo);
       ++ctx->launches;
     }
     CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
   } else {
     const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
-    nparts = launch_extremes_partial(pts_dev, n, 0, ctx->d_partials, blocks, st);
+    const int ticket = take_ctr(ctx);
+    nparts = launch_extremes_partial(pts_dev, n, 0, ctx->d_partials, blocks, st, 0,
+                                     ctx->d_ctr + ticket, (u32)extremes_blocks(blocks),
+                                     ctx->d_qinfo);
     ++ctx->launches;
   }
   const double2* pts = h_src ? ctx->d_pts : pts_dev;
-  launch_extremes_final(ctx->d_partials, nparts, ctx->d_qinfo, nullptr, st);
   CK(cudaEventRecord(ctx->ev[1], st));
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
@@ -881,7 +902,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   ctx->ctr_used += 5;
   launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
                           ctx->cap, ctx->d_ctr + cnt_slot, st, log2nb,
-                          want_filter ? ftabs.cnt : nullptr, ftabs.w);
+                          want_filter ? ftabs.cnt : nullptr, ftabs.w, filter_wmask());
   ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));

@@ -1,8 +1,9 @@
 #!/bin/bash
-# Filter-path tuning sweep: bins per chunk (log2) -> per-kernel times.
-for b in 6 7 8; do
-  echo "== bins/chunk 2^$b"
-  CHGPU_FILTER_BINS_PER_CHUNK_LOG2=$b timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+# Filter-path tuning sweep: env knob settings -> per-kernel times.
+# usage: bench_sweep.sh "VAR=a VAR2=b" "VAR=c" ...
+for cfg in "$@"; do
+  echo "== $cfg"
+  env $cfg timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
 pk=d['roofline']['per_kernel']
