@@ -164,8 +164,9 @@ __global__ __launch_bounds__(kBinThreads) void k_bin_tile_sums(const u32* __rest
 // tile's segmented-max aggregate.
 __global__ __launch_bounds__(kBinThreads) void k_bin_starts(
     const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ tsum,
-    FilterPlan P, u32* __restrict__ bstart, u32* __restrict__ first_bin,
+    const FilterPlan* __restrict__ P_p, u32* __restrict__ bstart, u32* __restrict__ first_bin,
     u32* __restrict__ agg_seg, u64* __restrict__ agg_val) {
+  const FilterPlan& P = *P_p;
   __shared__ u32 sh[kBinThreads / 32];
   __shared__ u32 sseg[kBinThreads / 32];
   __shared__ u64 sval[kBinThreads / 32];
@@ -238,8 +239,9 @@ __global__ __launch_bounds__(kBinThreads) void k_bin_starts(
 // into a tile folds the aggregates of the region's earlier tiles.
 __global__ __launch_bounds__(kBinThreads) void k_bin_thresholds(
     const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ bstart,
-    FilterPlan P, const u32* __restrict__ agg_seg, const u64* __restrict__ agg_val,
+    const FilterPlan* __restrict__ P_p, const u32* __restrict__ agg_seg, const u64* __restrict__ agg_val,
     u64* __restrict__ bthr) {
+  const FilterPlan& P = *P_p;
   __shared__ u32 sseg[kBinThreads / 32];
   __shared__ u64 sval[kBinThreads / 32];
   __shared__ u32 c_seg;
@@ -323,11 +325,12 @@ constexpr int kFilterItems = 4;
 // the next slot of its bin; the bin's 33rd candidate queues the bin for
 // k_bin_sort_big.
 __global__ __launch_bounds__(kFilterThreads) void k_filter(
-    const u64* __restrict__ kbuf, const u64* __restrict__ vbuf, FilterPlan P,
+    const u64* __restrict__ kbuf, const u64* __restrict__ vbuf, const FilterPlan* __restrict__ P_p,
     const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
     const u64* __restrict__ bthr, u32* __restrict__ bcur, u64* __restrict__ kout,
     u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
     unsigned long long* __restrict__ ncand) {
+  const FilterPlan& P = *P_p;
   __shared__ BinGeom s_geom;
   __shared__ u32 s_cand;
   if (threadIdx.x == 0) {
@@ -417,8 +420,9 @@ __device__ __forceinline__ void bitonic_smem(u64* sc, u64* sv, u64* sk, u32 Pn, 
 constexpr int kWarpSortWarps = 8;
 
 __global__ __launch_bounds__(32 * kWarpSortWarps) void k_bin_sort_warp(
-    u64* __restrict__ k, u64* __restrict__ v, FilterPlan P, const u32* __restrict__ bstart,
+    u64* __restrict__ k, u64* __restrict__ v, const FilterPlan* __restrict__ P_p, const u32* __restrict__ bstart,
     const u32* __restrict__ bcur, const u32* __restrict__ big, const u32* __restrict__ nbig_p) {
+  const FilterPlan& P = *P_p;
   __shared__ u64 sh[kWarpSortWarps][3][kWarpSortMax];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sc = sh[wid][0];
@@ -461,12 +465,13 @@ struct BigSmem {
 };
 
 __global__ __launch_bounds__(kBigThreads) void k_bin_sort_big(u64* __restrict__ k,
-                                                              u64* __restrict__ v, FilterPlan P,
+                                                              u64* __restrict__ v, const FilterPlan* __restrict__ P_p,
                                                               const u32* __restrict__ bstart,
                                                               const u32* __restrict__ bcur,
                                                               const u32* __restrict__ big,
                                                               const u32* __restrict__ nbig_p,
                                                               u32* __restrict__ overflow) {
+  const FilterPlan& P = *P_p;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BigSmem& S = *reinterpret_cast<BigSmem*>(smem_raw);
   const u32 nbig = *nbig_p;
@@ -536,8 +541,9 @@ __device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u6
 // (global order: region, bin, record) and each chunk's first dense index.
 __global__ __launch_bounds__(kBinThreads) void k_cand_positions(
     const u32* __restrict__ bcnt, const u32* __restrict__ bcur, const u32* __restrict__ bstart,
-    const u32* __restrict__ csum, FilterPlan P, u32* __restrict__ cpos, u32* __restrict__ first_cand,
+    const u32* __restrict__ csum, const FilterPlan* __restrict__ P_p, u32* __restrict__ cpos, u32* __restrict__ first_cand,
     u32* __restrict__ region_end) {
+  const FilterPlan& P = *P_p;
   __shared__ u32 sh[kBinThreads / 32];
   __shared__ u32 s_base;
   const u32 nb = 1u << P.log2nb;
@@ -596,8 +602,9 @@ __global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
                                                    const u64* __restrict__ v,
                                                    const u32* __restrict__ bcur,
                                                    const u32* __restrict__ bstart,
-                                                   const u32* __restrict__ cpos, FilterPlan P,
+                                                   const u32* __restrict__ cpos, const FilterPlan* __restrict__ P_p,
                                                    u64* __restrict__ ck, u64* __restrict__ cv) {
+  const FilterPlan& P = *P_p;
   __shared__ int s_mark[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u32 gb = (blockIdx.x * 8 + warp) * 32;  // first bin (all regions)
@@ -674,30 +681,72 @@ __global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
   }
 }
 
+// ------------------------------------------------------------------ device-side plan
+//
+// The plan of the filter path, computed on the device from K2's region
+// counts and the quad, so the host enqueues the whole path without waiting
+// for K2. A degenerate frame (no SPA, pipeline.cpp:53-71) leaves every
+// region empty and the path idle.
+__global__ void k_filter_plan(const QuadInfo* __restrict__ qinfo, const u32* __restrict__ counts,
+                              u64 ncap, u64 chunk_count, int log2nb, FilterPlan* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const QuadInfo qi = *qinfo;
+  FilterPlan P;
+  P.log2nb = log2nb;
+  u64 m[4];
+  for (int r = 0; r < 4; ++r) m[r] = qi.degenerate ? 0ull : (u64)counts[r];
+  P.src_off[0] = 0;
+  P.src_off[1] = ncap - m[1];
+  P.src_off[2] = ncap;
+  P.src_off[3] = 2 * ncap - m[3];
+  P.cum[0] = 0;
+  u32 chunks = 0;
+  for (int r = 0; r < 4; ++r) {
+    P.cum[r + 1] = P.cum[r] + m[r];
+    P.spa.off[r] = P.cum[r];
+    P.spa.m[r] = m[r];
+    P.spa.chunk_begin[r] = chunks;
+    const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;  // spa.cpp:121
+    P.spa.chunk_size[r] = cs;
+    if (m[r]) chunks += (u32)((m[r] + cs - 1) / cs);                   // spa.cpp:122
+    // guarded(region, anchors.first): LL left.y, LR bottom.x, UR right.y, UL top.x
+    const double seed = (r == 0 || r == 2) ? qi.q[2 * r + 1] : qi.q[2 * r];
+    P.spa.seed[r] = seed;
+    const int reg = r + 1;
+    P.seed_w[r] = wkey(reg, (reg == 1 || reg == 4) ? ~ord_enc(seed) : ord_enc(seed));
+  }
+  P.spa.total_chunks = chunks;
+  *out = P;
+}
+
 // ------------------------------------------------------------------ launchers
 
-void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan& P, u32* bstart, u64* bthr,
-                     u32* first_bin, FilterAux aux, cudaStream_t st) {
-  const u32 tiles = std::max(1u, (1u << P.log2nb) / kBinTile);
-  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, P.log2nb, aux.tsum);
+void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 ncap, u64 chunk_count,
+                        int log2nb, FilterPlan* out, cudaStream_t st) {
+  k_filter_plan<<<1, 32, 0, st>>>(qinfo, counts, ncap, chunk_count, log2nb, out);
+}
+
+void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
+                     u64* bthr, u32* first_bin, FilterAux aux, cudaStream_t st) {
+  const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
+  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, log2nb, aux.tsum);
   k_bin_starts<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, aux.tsum, P, bstart, first_bin,
                                                   aux.agg_seg, aux.agg_val);
   k_bin_thresholds<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, bstart, P, aux.agg_seg,
                                                       aux.agg_val, bthr);
 }
 
-void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan& P, const QuadInfo* qinfo,
-                   const u32* bstart, const u64* bthr, u32* bcur, u64* kout, u64* vout, u32* big,
-                   u32* nbig, unsigned long long* ncand, cudaStream_t st) {
-  const u64 total = P.cum[4];
-  if (total == 0) return;
+void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan* P, u64 max_records,
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
+                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st) {
+  if (max_records == 0) return;
   const u64 per = (u64)kFilterThreads * kFilterItems;
-  const u64 blocks = std::min<u64>((total + per - 1) / per, 148ull * 8);
+  const u64 blocks = std::min<u64>((max_records + per - 1) / per, 148ull * 8);
   k_filter<<<(unsigned)blocks, kFilterThreads, 0, st>>>(kbuf, vbuf, P, qinfo, bstart, bthr, bcur,
                                                           kout, vout, big, nbig, ncand);
 }
 
-void launch_bin_sort_big(u64* k, u64* v, const FilterPlan& P, const u32* bstart, const u32* bcur,
+void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
@@ -711,13 +760,13 @@ void launch_bin_sort_big(u64* k, u64* v, const FilterPlan& P, const u32* bstart,
 }
 
 void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
-                         const u32* bstart, const FilterPlan& P, u64* ck, u64* cv,
+                         const u32* bstart, const FilterPlan* P, int log2nb, u64* ck, u64* cv,
                          u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st) {
-  const u32 tiles = std::max(1u, (1u << P.log2nb) / kBinTile);
-  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcur, P.log2nb, aux.csum);
+  const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
+  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcur, log2nb, aux.csum);
   k_cand_positions<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bcur, bstart, aux.csum, P, cpos,
                                                       first_cand, aux.region_end);
-  k_cand_copy<<<(4u << P.log2nb) / 256, 256, 0, st>>>(k, v, bcur, bstart, cpos, P, ck, cv);
+  k_cand_copy<<<(4u << log2nb) / 256, 256, 0, st>>>(k, v, bcur, bstart, cpos, P, ck, cv);
 }
 
 }  // namespace chgpu

@@ -76,125 +76,6 @@ __device__ __forceinline__ u32 block_excl_sum(u32 x, u32* sw, u32* total) {
   return pre + incl - x;
 }
 
-__global__ __launch_bounds__(kSpaThreads) void k_spa(const u64* __restrict__ k,
-                                                     const u64* __restrict__ v, SpaPlan plan,
-                                                     unsigned char* __restrict__ flags,
-                                                     double2* __restrict__ kept_out,
-                                                     unsigned long long* __restrict__ kept_counts,
-                                                     u64* __restrict__ status, u32 tag,
-                                                     u32* __restrict__ chunk_ctr) {
-  __shared__ double sg[kSpaTile + kSpaTile / 16];
-  __shared__ double swd[kSpaThreads / 32];
-  __shared__ u32 swu[kSpaThreads / 32];
-  __shared__ u32 s_chunk, s_excl;
-
-  const int tid = threadIdx.x;
-  if (tid == 0) s_chunk = atomicAdd(chunk_ctr, 1u);
-  __syncthreads();
-  const u32 chunk = s_chunk;
-  int r = 0;
-  while (r < 3 && chunk >= plan.chunk_begin[r + 1]) ++r;
-  const int region = r + 1;
-  const u64 c = chunk - plan.chunk_begin[r];
-  const u64 begin = plan.off[r] + c * plan.chunk_size[r];
-  const u64 len = min((u64)plan.chunk_size[r], (u64)plan.m[r] - c * plan.chunk_size[r]);
-  const bool is_min = (region == 1 || region == 4);
-  const double ident = is_min ? INFINITY : -INFINITY;
-  double carry = (c == 0) ? plan.seed[r] : ident;
-
-  // Pass A: keep flags (kept in registers when the chunk is one tile, the
-  // common case; spilled to global memory as bytes otherwise).
-  const bool single = len <= kSpaTile;
-  unsigned char fr[kSpaItems];
-  u32 kept = 0;
-  for (u64 t0 = 0; t0 < len; t0 += kSpaTile) {
-    const u32 cnt = (u32)min((u64)kSpaTile, len - t0);
-    for (u32 i = tid; i < cnt; i += kSpaThreads) sg[i + (i >> 4)] = guarded_of(region, v[begin + t0 + i]);
-    __syncthreads();
-    double g[kSpaItems];
-    double agg = ident;
-#pragma unroll
-    for (int j = 0; j < kSpaItems; ++j) {
-      const u32 i = tid * kSpaItems + j;
-      g[j] = i < cnt ? sg[i + (i >> 4)] : ident;
-      agg = op_ext(is_min, agg, g[j]);
-    }
-    double tile_agg;
-    const double excl = block_excl_ext(is_min, agg, ident, swd, &tile_agg);
-    double t = op_ext(is_min, carry, excl);
-    unsigned char f[kSpaItems];
-#pragma unroll
-    for (int j = 0; j < kSpaItems; ++j) {
-      const u32 i = tid * kSpaItems + j;
-      f[j] = 0;
-      if (i < cnt) {
-        f[j] = steps_back(is_min, g[j], t) ? 0 : 1;
-        kept += f[j];
-        t = op_ext(is_min, t, g[j]);
-      }
-    }
-    if (single) {
-#pragma unroll
-      for (int j = 0; j < kSpaItems; ++j) fr[j] = f[j];
-    } else {
-      // Flags go out through shared memory as coalesced bytes.
-      __syncthreads();
-      unsigned char* sf = reinterpret_cast<unsigned char*>(sg);
-#pragma unroll
-      for (int j = 0; j < kSpaItems; ++j) sf[tid * kSpaItems + j] = f[j];
-      __syncthreads();
-      for (u32 i = tid; i < cnt; i += kSpaThreads) flags[begin + t0 + i] = sf[i];
-    }
-    carry = op_ext(is_min, carry, tile_agg);
-    __syncthreads();
-  }
-  u32 chunk_kept;
-  block_excl_sum(kept, swu, &chunk_kept);
-
-  // Look-back over chunks in (region, chunk) order.
-  if (tid < 32) {
-    u32 excl = 0;
-    if (chunk == 0) {
-      if (tid == 0) store_status(status, make_status(tag, kFlagPrefix, chunk_kept));
-    } else {
-      if (tid == 0) store_status(status + chunk, make_status(tag, kFlagAgg, chunk_kept));
-      excl = warp_lookback(status, 1, (int)chunk, 0, tag);
-      if (tid == 0) store_status(status + chunk, make_status(tag, kFlagPrefix, excl + chunk_kept));
-    }
-    if (tid == 0) {
-      s_excl = excl;
-      if (chunk_kept) atomicAdd(&kept_counts[r], (unsigned long long)chunk_kept);
-    }
-  }
-  __syncthreads();
-
-  // Pass B: stable scatter of the kept records as decoded points.
-  u32 out = s_excl;
-  for (u64 t0 = 0; t0 < len; t0 += kSpaTile) {
-    const u32 cnt = (u32)min((u64)kSpaTile, len - t0);
-    unsigned char f[kSpaItems];
-    u32 mine = 0;
-#pragma unroll
-    for (int j = 0; j < kSpaItems; ++j) {
-      const u32 i = tid * kSpaItems + j;
-      f[j] = single ? fr[j] : (i < cnt ? flags[begin + t0 + i] : 0);
-      mine += f[j];
-    }
-    u32 tile_kept;
-    u32 pos = out + block_excl_sum(mine, swu, &tile_kept);
-#pragma unroll
-    for (int j = 0; j < kSpaItems; ++j) {
-      if (f[j]) {
-        const u64 a = begin + t0 + tid * kSpaItems + j;
-        double x, y;
-        decode_point(region, k[a], v[a], x, y);
-        kept_out[pos++] = make_double2(x, y);
-      }
-    }
-    out += tile_kept;
-  }
-}
-
 // Degenerate branch: unique over the lexicographically sorted survivors
 // (oracle.cpp:16-17 std::sort + std::unique), compacted in order.
 __global__ __launch_bounds__(kSpaThreads) void k_unique(const u64* __restrict__ k,
@@ -257,14 +138,6 @@ __global__ __launch_bounds__(kSpaThreads) void k_unique(const u64* __restrict__ 
   }
 }
 
-void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
-                double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,
-                u32* chunk_ctr, cudaStream_t st) {
-  if (plan.total_chunks == 0) return;
-  k_spa<<<plan.total_chunks, kSpaThreads, 0, st>>>(k, v, plan, flags, kept_out, kept_counts,
-                                                    status, tag, chunk_ctr);
-}
-
 void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
                    u32* tile_ctr, unsigned long long* total, cudaStream_t st) {
   const u64 tiles = (n + kSpaTile - 1) / kSpaTile;
@@ -293,9 +166,11 @@ constexpr int kSpaStep = 32 * kSpaPer;      // records per warp step
 // replays its 8 records against the exclusive prefix. The next step's loads
 // are issued before the current step is scanned.
 __global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
-                                                  const u64* __restrict__ v, SpaPlan plan,
+                                                  const u64* __restrict__ v,
+                                                  const SpaPlan* __restrict__ plan_p,
                                                   double2* __restrict__ scratch,
                                                   u32* __restrict__ chunk_kept) {
+  const SpaPlan& plan = *plan_p;
   const int lane = threadIdx.x & 31;
   const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= plan.total_chunks) return;
@@ -369,9 +244,11 @@ __global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
 
 // Exclusive scan of the per-chunk kept counts (one block); per-region
 // totals follow from the offsets at the region boundaries.
-__global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ chunk_kept, SpaPlan plan,
+__global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ chunk_kept,
+                                                      const SpaPlan* __restrict__ plan_p,
                                                       u32* __restrict__ offs,
                                                       unsigned long long* __restrict__ kept_counts) {
+  const SpaPlan& plan = *plan_p;
   __shared__ u32 wsum[32];
   __shared__ u32 carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -413,9 +290,11 @@ __global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ ch
 }
 
 __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ scratch,
-                                                    SpaPlan plan, const u32* __restrict__ chunk_kept,
+                                                    const SpaPlan* __restrict__ plan_p,
+                                                    const u32* __restrict__ chunk_kept,
                                                     const u32* __restrict__ offs,
                                                     double2* __restrict__ out) {
+  const SpaPlan& plan = *plan_p;
   const int lane = threadIdx.x & 31;
   const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= plan.total_chunks) return;
@@ -436,12 +315,13 @@ __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ 
 // chunk). One warp per chunk, 32 records per step, the running extremum in
 // a register.
 __global__ __launch_bounds__(256) void k_spa_dense(const u64* __restrict__ ck,
-                                                   const u64* __restrict__ cv, FilterPlan P,
+                                                   const u64* __restrict__ cv,
+                                                   const FilterPlan* __restrict__ P_p,
                                                    const u32* __restrict__ first_cand,
                                                    const u32* __restrict__ region_end,
                                                    double2* __restrict__ scratch,
                                                    u32* __restrict__ chunk_kept) {
-  const SpaPlan& plan = P.spa;
+  const SpaPlan& plan = P_p->spa;
   const int lane = threadIdx.x & 31;
   const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= plan.total_chunks) return;
@@ -493,22 +373,23 @@ __global__ __launch_bounds__(256) void k_spa_dense(const u64* __restrict__ ck,
   if (lane == 0) chunk_kept[c] = kept;
 }
 
-void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan& P, const u32* first_cand,
-                      const u32* region_end, double2* scratch, u32* chunk_kept, u32* offs,
-                      unsigned long long* kept_counts, double2* out, cudaStream_t st) {
-  const SpaPlan& plan = P.spa;
-  if (plan.total_chunks == 0) return;
-  const u32 blocks = (plan.total_chunks + 7) / 8;
+void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max_chunks,
+                      const u32* first_cand, const u32* region_end, double2* scratch,
+                      u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
+                      cudaStream_t st) {
+  if (max_chunks == 0) return;
+  const u32 blocks = (max_chunks + 7) / 8;
+  const SpaPlan* plan = &P->spa;
   k_spa_dense<<<blocks, 256, 0, st>>>(ck, cv, P, first_cand, region_end, scratch, chunk_kept);
   k_spa_offsets<<<1, 1024, 0, st>>>(chunk_kept, plan, offs, kept_counts);
   k_spa_gather<<<blocks, 256, 0, st>>>(scratch, plan, chunk_kept, offs, out);
 }
 
-void launch_spa_warp(const u64* k, const u64* v, const SpaPlan& plan, double2* scratch,
-                     u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
-                     cudaStream_t st) {
-  if (plan.total_chunks == 0) return;
-  const u32 blocks = (plan.total_chunks + 7) / 8;
+void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
+                     double2* scratch, u32* chunk_kept, u32* offs,
+                     unsigned long long* kept_counts, double2* out, cudaStream_t st) {
+  if (max_chunks == 0) return;
+  const u32 blocks = (max_chunks + 7) / 8;
   k_spa_warp<<<blocks, 256, 0, st>>>(k, v, plan, scratch, chunk_kept);
   k_spa_offsets<<<1, 1024, 0, st>>>(chunk_kept, plan, offs, kept_counts);
   k_spa_gather<<<blocks, 256, 0, st>>>(scratch, plan, chunk_kept, offs, out);

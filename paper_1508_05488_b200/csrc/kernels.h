@@ -53,19 +53,23 @@ struct FilterAux {
   u64* agg_val;
   u32* region_end;  // [4] dense end of each region's candidates
 };
-void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan& P, u32* bstart, u64* bthr,
-                     u32* first_bin, FilterAux aux, cudaStream_t st);
-void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan& P, const QuadInfo* qinfo,
-                   const u32* bstart, const u64* bthr, u32* bcur, u64* kout, u64* vout, u32* big,
-                   u32* nbig, unsigned long long* ncand, cudaStream_t st);
-void launch_bin_sort_big(u64* k, u64* v, const FilterPlan& P, const u32* bstart, const u32* bcur,
+// The plan of the filter path on the device (from K2's counts).
+void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 ncap, u64 chunk_count,
+                        int log2nb, FilterPlan* out, cudaStream_t st);
+void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
+                     u64* bthr, u32* first_bin, FilterAux aux, cudaStream_t st);
+void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan* P, u64 max_records,
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
+                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st);
+void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
 void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
-                         const u32* bstart, const FilterPlan& P, u64* ck, u64* cv,
+                         const u32* bstart, const FilterPlan* P, int log2nb, u64* ck, u64* cv,
                          u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st);
-void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan& P, const u32* first_cand,
-                      const u32* region_end, double2* scratch, u32* chunk_kept, u32* offs,
-                      unsigned long long* kept_counts, double2* out, cudaStream_t st);
+void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max_chunks,
+                      const u32* first_cand, const u32* region_end, double2* scratch,
+                      u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
+                      cudaStream_t st);
 
 // K1
 // Blocks launch_extremes_partial will use for a request of `requested`.
@@ -114,12 +118,9 @@ void launch_bucket_scatter(const u64* kin, const u64* vin, u64* kout, u64* vout,
 void launch_bucket_sort(u64* k, u64* v, const BucketPlan& P, const u64* base, const u32* hist,
                         unsigned long long* ngroups, cudaStream_t st);
 // K4/K5
-void launch_spa(const u64* k, const u64* v, const SpaPlan& plan, unsigned char* flags,
-                double2* kept_out, unsigned long long* kept_counts, u64* status, u32 tag,
-                u32* chunk_ctr, cudaStream_t st);
-void launch_spa_warp(const u64* k, const u64* v, const SpaPlan& plan, double2* scratch,
-                     u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
-                     cudaStream_t st);
+void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
+                     double2* scratch, u32* chunk_kept, u32* offs,
+                     unsigned long long* kept_counts, double2* out, cudaStream_t st);
 void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
                    u32* tile_ctr, unsigned long long* total, cudaStream_t st);
 

@@ -100,6 +100,13 @@ struct chgpu_ctx {
   u32* d_ffirst = nullptr;   // per-chunk first bin
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
+  FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
+  size_t kept_hint = 0;          // chain points of the previous call (speculative D2H size)
+  // Pinned staging arena for host->device uploads of small host-built
+  // tables (segments, plans, quads): every upload gets its own slice, so a
+  // host buffer can be rewritten while earlier copies are still queued.
+  unsigned char* h_stage = nullptr;
+  size_t stage_cap = 0, stage_used = 0;
 
   Pinned* h = nullptr;
   SegDesc* h_segs = nullptr;
@@ -235,6 +242,30 @@ int sync(chgpu_ctx* ctx) {
   return CHGPU_OK;
 }
 
+// Enqueues the upload of `bytes` of host memory `src` to device `dst` on the
+// context stream through a fresh slice of the pinned staging arena. The
+// source may be modified as soon as this returns (an async copy from pinned
+// memory reads it only when the stream reaches the copy).
+int upload(chgpu_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  size_t off = (ctx->stage_used + 255) & ~size_t(255);
+  if (off + bytes > ctx->stage_cap) {
+    TRY(sync(ctx));  // queued copies out of the arena are done: reuse it
+    off = 0;
+    if (bytes > ctx->stage_cap) {
+      cudaFreeHost(ctx->h_stage);
+      ctx->h_stage = nullptr;
+      ctx->stage_cap = 0;
+      const size_t want = std::max<size_t>(bytes * 2, size_t(1) << 20);
+      CK(cudaMallocHost(&ctx->h_stage, want));
+      ctx->stage_cap = want;
+    }
+  }
+  std::memcpy(ctx->h_stage + off, src, bytes);
+  ctx->stage_used = off + bytes;
+  CK(cudaMemcpyAsync(dst, ctx->h_stage + off, bytes, cudaMemcpyHostToDevice, ctx->st));
+  return CHGPU_OK;
+}
+
 // Reads one device counter (synchronising the stream).
 int read_ctr(chgpu_ctx* ctx, int slot, u32* out) {
   CK(cudaMemcpyAsync(&ctx->h->ctr[slot], ctx->d_ctr + slot, sizeof(u32), cudaMemcpyDeviceToHost,
@@ -308,8 +339,7 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
   *in_a = true;
   if (tiles == 0) return CHGPU_OK;
   const int mask_slot = take_ctr(ctx);
-  CK(cudaMemcpyAsync(ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc), cudaMemcpyHostToDevice,
-                     ctx->st));
+  TRY(upload(ctx, ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc)));
   CK(cudaMemsetAsync(ctx->d_hist, 0, (size_t)nseg * kPasses * kDigits * sizeof(u32), ctx->st));
   launch_hist(ksrc, vsrc, ctx->d_segs, nseg, tiles, mode, npasses, 1, ctx->d_hist, ctx->st);
   launch_hist_scan(ctx->d_hist, ctx->d_segs, nseg, npasses, ctx->d_digit_excl,
@@ -391,8 +421,7 @@ int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int
   pend->slot = -1;
   if (tiles == 0) return CHGPU_OK;
   const int s_medium = take_ctr(ctx), s_long = take_ctr(ctx);
-  CK(cudaMemcpyAsync(ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc), cudaMemcpyHostToDevice,
-                     ctx->st));
+  TRY(upload(ctx, ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc)));
   launch_group_scan(kF, vF, ctx->d_segs, nseg, tiles, eqmode, ctx->d_medium,
                     ctx->d_ctr + s_medium, ctx->d_u64 + 10, ctx->st);
   launch_group_fix_medium(kF, vF, ctx->d_segs, ctx->d_medium, ctx->d_ctr + s_medium, ctx->d_long,
@@ -699,7 +728,10 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
 int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
   u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
   u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
-  launch_spa_warp(kF, vF, plan, ctx->d_pts, chunk_kept, offs, ctx->d_u64, ctx->d_kept, ctx->st);
+  SpaPlan* d_splan = &ctx->d_plan->spa;
+  TRY(upload(ctx, d_splan, &plan, sizeof(SpaPlan)));
+  launch_spa_warp(kF, vF, d_splan, plan.total_chunks, ctx->d_pts, chunk_kept, offs, ctx->d_u64,
+                  ctx->d_kept, ctx->st);
   if (plan.total_chunks) ctx->launches += 3;
   CK(cudaGetLastError());
   return CHGPU_OK;
@@ -744,36 +776,27 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
   return t;
 }
 
-// The pre-filtered SPA (k_filter.cu): bin scan, filter, big-bin sort and
-// the SPA over bins; kept chains land in d_kept exactly as run_spa leaves
-// them. Reads back the kept counts, the candidate count and the overflow
-// flag (a bin too large for the shared-memory sort: *overflow = true and
-// the caller redoes the SPA over the full region sort).
-int run_filter_spa(chgpu_ctx* ctx, const u64 m[4], const SpaPlan& plan, int log2nb, bool* overflow,
-                   size_t* ncand) {
+// Enqueues the pre-filtered SPA (k_filter.cu) right behind K2, with no
+// host round trip: the plan is built on the device from K2's counts
+// (cnt_slot + 1 .. 4), then bin scan, filter, big-bin sorts, dense
+// compaction and the SPA over the candidates; kept chains land in d_kept
+// exactly as run_spa leaves them and the kept counts in d_u64[0..3].
+// Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
+// *ovf_slot / *ncand land in the counters for the caller's read-back.
+int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb, int cnt_slot,
+                       int* ovf_slot) {
   cudaStream_t st = ctx->st;
-  FilterPlan fp{};
-  fp.spa = plan;
-  fp.log2nb = log2nb;
-  const u64 cap = ctx->cap;
-  const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
-  fp.cum[0] = 0;
-  for (int r = 0; r < 4; ++r) {
-    fp.src_off[r] = src_off[r];
-    fp.cum[r + 1] = fp.cum[r] + m[r];
-    const int reg = r + 1;
-    const u64 enc = (reg == 1 || reg == 4) ? ~ord_enc(plan.seed[r]) : ord_enc(plan.seed[r]);
-    fp.seed_w[r] = wkey(reg, enc);
-  }
-  if (2 * (size_t)plan.total_chunks > ctx->ffirst_cap) {
+  const FilterPlan* P = ctx->d_plan;
+  const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
+  if (2 * (size_t)max_chunks > ctx->ffirst_cap) {
     cudaFree(ctx->d_ffirst);
     ctx->d_ffirst = nullptr;
-    const size_t want = std::max<size_t>(2 * (size_t)plan.total_chunks, 8192);
+    const size_t want = std::max<size_t>(2 * (size_t)max_chunks, 8192);
     CK(cudaMalloc(&ctx->d_ffirst, want * sizeof(u32)));
     ctx->ffirst_cap = want;
   }
   u32* first_bin = ctx->d_ffirst;
-  u32* first_cand = ctx->d_ffirst + plan.total_chunks;
+  u32* first_cand = ctx->d_ffirst + max_chunks;
   FilterAux aux;
   aux.tsum = reinterpret_cast<u32*>(ctx->d_faux);
   aux.csum = aux.tsum + 512;
@@ -781,37 +804,31 @@ int run_filter_spa(chgpu_ctx* ctx, const u64 m[4], const SpaPlan& plan, int log2
   aux.region_end = aux.agg_seg + 512;
   aux.agg_val = reinterpret_cast<u64*>(ctx->d_faux + 8192);
   const FilterTabs t = filter_tabs(ctx, log2nb);
-  const int nbig_slot = take_ctr(ctx), nbig2_slot = take_ctr(ctx), ovf_slot = take_ctr(ctx);
+  const int nbig_slot = take_ctr(ctx), nbig2_slot = take_ctr(ctx);
   (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
-  launch_bin_scan(t.cnt, t.w, fp, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
+  *ovf_slot = take_ctr(ctx);
+  launch_filter_plan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, ctx->cap, chunk_count, log2nb,
+                     ctx->d_plan, st);
+  launch_bin_scan(t.cnt, t.w, P, log2nb, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
   CK(cudaEventRecord(ctx->ev[3], st));
-  launch_filter(ctx->d_kbuf, ctx->d_vbuf, fp, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr, t.cur,
+  launch_filter(ctx->d_kbuf, ctx->d_vbuf, P, n, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr, t.cur,
                 ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
   CK(cudaEventRecord(ctx->ev[4], st));
-  launch_bin_sort_big(ctx->d_ka, ctx->d_va, fp, ctx->d_fstart, t.cur, ctx->d_fbig,
-                      ctx->d_ctr + nbig_slot, ctx->d_ctr + ovf_slot, st);
+  launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
+                      ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, st);
   // the bin thresholds are dead once the filter ran: their table holds the
   // dense positions now
-  launch_cand_compact(ctx->d_ka, ctx->d_va, t.cnt, t.cur, ctx->d_fstart, fp, ctx->d_ck, ctx->d_cv,
-                      first_cand, reinterpret_cast<u32*>(ctx->d_fthr), aux, st);
+  launch_cand_compact(ctx->d_ka, ctx->d_va, t.cnt, t.cur, ctx->d_fstart, P, log2nb, ctx->d_ck,
+                      ctx->d_cv, first_cand, reinterpret_cast<u32*>(ctx->d_fthr), aux, st);
   CK(cudaEventRecord(ctx->ev[5], st));
   CK(cudaEventRecord(ctx->ev[6], st));
   u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
-  u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
-  launch_spa_dense(ctx->d_ck, ctx->d_cv, fp, first_cand, aux.region_end, ctx->d_pts, chunk_kept,
-                   offs, ctx->d_u64, ctx->d_kept, st);
-  ctx->launches += 10 + (plan.total_chunks ? 3 : 0);
+  u32* offs = chunk_kept + ((max_chunks + 31) & ~31u);
+  launch_spa_dense(ctx->d_ck, ctx->d_cv, P, max_chunks, first_cand, aux.region_end, ctx->d_pts,
+                   chunk_kept, offs, ctx->d_u64, ctx->d_kept, st);
+  ctx->launches += 14;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[8], st));
-  CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ctx->h->ncand, ctx->d_u64 + 11, sizeof(unsigned long long),
-                     cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
-                     cudaMemcpyDeviceToHost, st));
-  TRY(sync(ctx));
-  *overflow = ctx->h->ctr[ovf_slot] != 0;
-  *ncand = (size_t)ctx->h->ncand;
   return CHGPU_OK;
 }
 
@@ -825,6 +842,8 @@ void frame_of(const double* quad, Pt* fr, int* nf) {
 }
 
 int begin_call(chgpu_ctx* ctx) {
+  TRY(sync(ctx));  // nothing of an earlier call may still read the staging arena
+  ctx->stage_used = 0;
   ctx->launches = 0;
   ctx->ctr_used = 0;
   CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
@@ -892,8 +911,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
   // pre-filter's per-bin statistics when that path is taken.
   const bool want_filter =
-      ctx->spa_mode == CHGPU_SPA_FILTER ||
-      (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count >= 1 && chunk_count <= n / 64);
+      chunk_count >= 1 &&
+      (ctx->spa_mode == CHGPU_SPA_FILTER ||
+       (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
   const int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
   if (want_filter)
     CK(cudaMemsetAsync(ctx->d_ftab, 0, (size_t(4) << log2nb) * 16, st));
@@ -906,6 +926,25 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
+  // The filter path is enqueued before the host sees K2's results (it idles
+  // itself on a degenerate frame), with a speculative read-back of the
+  // chains sized by the previous call.
+  int ovf_slot = -1;
+  size_t spec = 0;
+  if (want_filter) {
+    TRY(enqueue_filter_spa(ctx, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
+    spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 4));
+    TRY(ensure_host_out(ctx, spec + 4));
+    CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ctx->h->ncand, ctx->d_u64 + 11, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaEventRecord(ctx->ev[9], st));
+  }
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
@@ -953,11 +992,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     const SpaPlan plan = make_spa_plan(m, chunk_count, qi.q);
     bool filtered = false;
     if (want_filter) {
-      // ---- K3 + K4/K5 on the SPA candidates only (k_filter.cu).
-      bool overflow = false;
-      size_t ncand = 0;
-      TRY(run_filter_spa(ctx, m, plan, log2nb, &overflow, &ncand));
-      D.n_candidates = ncand;
+      // ---- K3 + K4/K5 ran on the SPA candidates only (k_filter.cu).
+      const bool overflow = ctx->h->ctr[ovf_slot] != 0;
+      D.n_candidates = (size_t)ctx->h->ncand;
       D.filter_log2nb = log2nb;
       D.spa_path = overflow ? 2 : 1;
       filtered = !overflow;
@@ -1023,11 +1060,14 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
 
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
-    TRY(ensure_host_out(ctx, kept + 4));
-    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, kept * sizeof(double2), cudaMemcpyDeviceToHost,
-                       st));
-    CK(cudaEventRecord(ctx->ev[9], st));
-    TRY(sync(ctx));
+    ctx->kept_hint = kept;
+    if (!(filtered && kept <= spec)) {  // else the speculative read-back holds them
+      TRY(ensure_host_out(ctx, kept + 4));
+      CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, kept * sizeof(double2), cudaMemcpyDeviceToHost,
+                         st));
+      CK(cudaEventRecord(ctx->ev[9], st));
+      TRY(sync(ctx));
+    }
     D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
     const auto t_host0 = std::chrono::steady_clock::now();
     const int a = chgpu::host::assemble_ring(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
@@ -1075,7 +1115,7 @@ int upload_quad(chgpu_ctx* ctx, const double* quad) {
   qi.frame_size = (u32)nf;
   qi.degenerate = nf <= 2;
   ctx->h->qi = qi;
-  CK(cudaMemcpyAsync(ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo), cudaMemcpyHostToDevice, ctx->st));
+  TRY(upload(ctx, ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo)));
   return CHGPU_OK;
 }
 
@@ -1116,6 +1156,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_fthr, (size_t(4) << kMaxFilterBits) * sizeof(u64))) ||
       bad(cudaMalloc(&ctx->d_fbig, 2 * (size_t)kBigListB * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_faux, 16384)) ||
+      bad(cudaMalloc(&ctx->d_plan, sizeof(FilterPlan))) ||
       bad(cudaMallocHost(&ctx->h, sizeof(Pinned)))) {
     chgpu_ctx_destroy(ctx);
     return CHGPU_CUDA_ERR;
@@ -1154,11 +1195,13 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_fthr);
   cudaFree(ctx->d_fbig);
   cudaFree(ctx->d_faux);
+  cudaFree(ctx->d_plan);
   cudaFree(ctx->d_ffirst);
   cudaFree(ctx->d_digit_excl);
   cudaFreeHost(ctx->h);
   cudaFreeHost(ctx->h_segs);
   cudaFreeHost(ctx->h_out);
+  cudaFreeHost(ctx->h_stage);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->ev_copy) cudaEventDestroy(e);
