@@ -168,12 +168,14 @@ __device__ __forceinline__ void make_bin_geom(const double* q, int log2nb, BinGe
   }
 }
 
-// Bin of a record of region r (1..4) with primary coordinate p.
+// Bin of a record of region r (1..4) with primary coordinate p. The
+// float->int conversion saturates (negative and NaN -> 0), then the top
+// clamps: trunc(clamp(t, 0, top)) in two integer instructions.
 __device__ __forceinline__ u32 bin_of(const BinGeom& g, int r, double p) {
-  double t = __dmul_rn(__dsub_rn(p, g.lo[r - 1]), g.scale[r - 1]);
-  t = fmin(fmax(t, 0.0), g.top);
-  const u32 b = (u32)__double2uint_rz(t);
-  return (r >= 3) ? (u32)g.top - b : b;  // UR / UL sort descending
+  const double t = __dmul_rn(__dsub_rn(p, g.lo[r - 1]), g.scale[r - 1]);
+  const u32 top = (u32)g.top;
+  const u32 b = min((u32)__double2uint_rz(t), top);
+  return (r >= 3) ? top - b : b;  // UR / UL sort descending
 }
 
 // The guarded coordinate as a key w on which every region's SPA is a

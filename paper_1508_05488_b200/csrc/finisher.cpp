@@ -80,15 +80,8 @@ struct Scratch {
 
 }  // namespace
 
-int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
-  // melkman.cpp:20-25: consecutive duplicates (and a closing repeat) go.
-  thread_local Scratch ring_s, deque_s;
-  Pt* ring = ring_s.get(n_in + 1);
-  size_t n = 0;
-  for (size_t i = 0; i < n_in; ++i)
-    if (n == 0 || !same(ring[n - 1], poly[i])) ring[n++] = poly[i];
-  if (n > 1 && same(ring[0], ring[n - 1])) --n;
-
+int melkman_ring(const Pt* ring, size_t n, std::vector<Pt>& hull) {
+  thread_local Scratch deque_s;
   // melkman.cpp:30-47: absorb the leading collinear run; remember its two
   // extreme endpoints (lo, hi) and the last vertex visited.
   Pt lo = n ? ring[0] : Pt{0.0, 0.0};
@@ -106,31 +99,71 @@ int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
   }
   if (i >= n) return kDegenerate;
 
-  // melkman.cpp:52-60: seed triangle; the deque lives in buf[head, tail).
+  // melkman.cpp:52-60: seed triangle; the deque lives in [head, tail).
   Pt* buf = deque_s.get(2 * n + 8);
-  size_t head = n + 4, tail = head;
+  Pt* head = buf + n + 4;
+  Pt* tail = head;
   const Pt w = ring[i];
   const Pt second = last;
   const Pt first = same(last, lo) ? hi : lo;
   const bool ccw = turn(first, second, w) == kLeft;
-  buf[tail++] = w;
-  buf[tail++] = ccw ? first : second;
-  buf[tail++] = ccw ? second : first;
-  buf[tail++] = w;
+  *tail++ = w;
+  *tail++ = ccw ? first : second;
+  *tail++ = ccw ? second : first;
+  *tail++ = w;
 
-  // melkman.cpp:62-80
-  for (++i; i < n; ++i) {
-    const Pt v = ring[i];
-    if (turn(buf[head], buf[head + 1], v) == kLeft && turn(buf[tail - 2], buf[tail - 1], v) == kLeft)
-      continue;
-    while (tail - head >= 2 && turn(buf[tail - 2], buf[tail - 1], v) != kLeft) --tail;
-    buf[tail++] = v;
-    while (tail - head >= 2 && turn(v, buf[head], buf[head + 1]) != kLeft) ++head;
-    buf[--head] = v;
+  // melkman.cpp:62-80. The two end edges of the deque are cached as
+  // (origin, edge vector): the edge vector is the same rounded difference
+  // turn() computes, so every predicate is bit-identical; they change only
+  // when a vertex is pushed.
+  double hax = head[0].x, hay = head[0].y, hex = head[1].x - hax, hey = head[1].y - hay;
+  double tax = tail[-2].x, tay = tail[-2].y, tex = tail[-1].x - tax, tey = tail[-1].y - tay;
+  for (const Pt* rp = ring + i + 1; rp < ring + n; ++rp) {
+    const double vx = rp->x, vy = rp->y;
+    const bool left_head = hex * (vy - hay) - hey * (vx - hax) > 0.0;
+    const bool left_tail = tex * (vy - tay) - tey * (vx - tax) > 0.0;
+    if (left_head & left_tail) continue;  // inside the current hull
+    // pop the back while v is not strictly left of its last edge (the first
+    // test is left_tail)
+    if (!left_tail && tail - head >= 2) {
+      --tail;
+      while (tail - head >= 2) {
+        const Pt a = tail[-2], b = tail[-1];
+        if ((b.x - a.x) * (vy - a.y) - (b.y - a.y) * (vx - a.x) > 0.0) break;
+        --tail;
+      }
+    }
+    *tail++ = *rp;
+    // pop the front while turn(v, front, next) is not left
+    while (tail - head >= 2) {
+      const Pt a = head[0], b = head[1];
+      if ((a.x - vx) * (b.y - vy) - (a.y - vy) * (b.x - vx) > 0.0) break;
+      ++head;
+    }
+    *--head = *rp;
+    hax = vx;
+    hay = vy;
+    hex = head[1].x - vx;
+    hey = head[1].y - vy;
+    tax = tail[-2].x;
+    tay = tail[-2].y;
+    tex = tail[-1].x - tax;
+    tey = tail[-1].y - tay;
   }
-  hull.assign(buf + head, buf + (tail - 1));  // ends coincide (:83)
+  hull.assign(head, tail - 1);  // ends coincide (:83)
   canonicalize(hull.data(), hull.size());
   return kOk;
+}
+
+int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
+  // melkman.cpp:20-25: consecutive duplicates (and a closing repeat) go.
+  thread_local Scratch ring_s;
+  Pt* ring = ring_s.get(n_in + 1);
+  size_t n = 0;
+  for (size_t i = 0; i < n_in; ++i)
+    if (n == 0 || !same(ring[n - 1], poly[i])) ring[n++] = poly[i];
+  if (n > 1 && same(ring[0], ring[n - 1])) --n;
+  return melkman_ring(ring, n, hull);
 }
 
 int monotone_chain(const Pt* pts, size_t n, std::vector<Pt>& hull) {

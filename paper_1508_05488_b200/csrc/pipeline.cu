@@ -1073,7 +1073,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     const int a = chgpu::host::assemble_ring(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
                                              corners, ctx->ring);
     if (a) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon: fewer than 3 distinct vertices");
-    const int mk = chgpu::host::melkman(ctx->ring.data(), ctx->ring.size(), ctx->hull);
+    // assemble_ring already collapsed duplicates exactly as melkman.cpp:20-25
+    const int mk = chgpu::host::melkman_ring(ctx->ring.data(), ctx->ring.size(), ctx->hull);
     if (mk) return fail(ctx, CHGPU_DEGENERATE, "melkman: degenerate polygon");
     D.t_host_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();

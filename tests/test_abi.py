@@ -91,3 +91,35 @@ def test_host_finisher_matches_oracle_random_polygons(product, oracle):
 
 def test_stats_struct_layout(product):
     assert C.sizeof(product._Stats) == 4 * 8 + 7 * 8
+
+
+def test_host_melkman_on_pipeline_polygons(product, oracle):
+    """The finisher on the polygons the pipeline actually builds (SPA chains
+    + corners, reference stage dumps) and on collinear-heavy grid rings:
+    bit-identical hulls and the same degenerate verdicts as the reference's
+    melkman (melkman.cpp:17-86)."""
+    from pyoracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefLib()
+    for dist, n, seed in (("uniform_square", 200_000, 42), ("uniform_disk", 200_000, 3),
+                          ("gaussian", 100_000, 5), ("circle", 5_000, 9)):
+        pts = ref.generate(dist, n, seed)
+        for cc in (1, 7, 1024):
+            quad, rc, srt, kept, kc = ref.stage_dump(pts, cc)
+            poly = product.assemble_polygon(kept, kc, quad)
+            st, want = ref.melkman(poly)
+            assert st == 0
+            assert np.array_equal(product.melkman(poly), want), (dist, cc)
+    rng = np.random.default_rng(4242)
+    for trial in range(300):
+        k = int(rng.integers(3, 60))
+        g = rng.integers(0, 5, (k, 2)).astype(np.float64)
+        c = g.mean(axis=0) + 1e-3
+        ring = g[np.argsort(np.arctan2(g[:, 1] - c[1], g[:, 0] - c[0]), kind="stable")]
+        st, want = ref.melkman(ring)
+        if st != 0:
+            with pytest.raises(product.DegenerateInput):
+                product.melkman(ring)
+        else:
+            assert np.array_equal(product.melkman(ring), want), trial
