@@ -26,7 +26,7 @@ CXXFLAGS := -O3 -std=gnu++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$
 REF      ?= /root/reference/proj
 
 CU_SRCS  := $(CSRC)/k_discard.cu $(CSRC)/k_sort.cu $(CSRC)/k_bucket.cu $(CSRC)/k_spa.cu \
-            $(CSRC)/k_filter.cu \
+            $(CSRC)/k_filter.cu $(CSRC)/k_convex.cu \
             $(CSRC)/pipeline.cu
 CXX_SRCS := $(CSRC)/finisher.cpp $(CSRC)/datasets.cpp
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))

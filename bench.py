@@ -210,13 +210,13 @@ def main():
 
     def step_device():
         if world == 1:
-            return ctx.convex_hull_device(d_pts.data_ptr(), args.n, cfg)
+            return ctx.convex_hull_device(d_pts.data_ptr(), args.n, cfg, copy=False)
         ops = GpuShardOps(ctx, d_pts, rank * args.n)
         return sharded_convex_hull(ops, args.chunk_count)
 
     def step_host():
         if world == 1:
-            return ctx.convex_hull(h_pin.numpy(), cfg)
+            return ctx.convex_hull(h_pin.numpy(), cfg, copy=False)
         # host-resident shard: copy in, then the sharded step
         d_pts.copy_(h_pin, non_blocking=True)
         torch.cuda.synchronize()

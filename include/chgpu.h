@@ -87,6 +87,8 @@ typedef struct {
   double t_binscan_ms;      /* pre-filter: bin ranks + thresholds */
   double t_filter_ms;       /* pre-filter: candidate selection */
   double t_binsort_ms;      /* pre-filter: sort of bins above 32 candidates */
+  int convex_fast_path;     /* 1: Melkman's all-kept trajectory verified on the GPU (k_convex.cu) */
+  int pad3_;
 } chgpu_diag;
 
 /* Options (chgpu_ctx_set_option). */
@@ -158,6 +160,12 @@ int chgpu_assemble_polygon(const double* chains, const size_t* kept_counts, cons
                            double* out, size_t* n_out);
 /* melkman (melkman.hpp:29); out capacity n. */
 int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out);
+/* assemble_polygon (polygon.hpp:25) followed by melkman (melkman.hpp:29)
+ * in one streaming pass: the hull of the chains' polygon without
+ * materialising it. out capacity sum + 4; CHGPU_DEGENERATE where either
+ * reference stage throws DegenerateInput. */
+int chgpu_finish_chains(const double* chains, const size_t* kept_counts, const double* quad,
+                        double* out, size_t* n_out);
 /* canonicalize_ring (melkman.hpp:20), in place. */
 void chgpu_canonicalize_ring(double* ring, size_t n);
 /* hull_oracle (pipeline.hpp:62): host reference hull; out capacity n. */

@@ -77,7 +77,7 @@ class _Diag(C.Structure):
                 ("t_d2h_ms", C.c_double), ("t_host_ms", C.c_double),
                 ("spa_path", C.c_int), ("filter_log2nb", C.c_int), ("n_candidates", C.c_size_t),
                 ("t_binscan_ms", C.c_double), ("t_filter_ms", C.c_double),
-                ("t_binsort_ms", C.c_double)]
+                ("t_binsort_ms", C.c_double), ("convex_fast_path", C.c_int), ("pad3_", C.c_int)]
 
 # chgpu_ctx_set_option (include/chgpu.h)
 OPT_SPA_PATH = 1
@@ -118,6 +118,7 @@ class Diag:
     spa_path: int = 0        # 0 full sort, 1 pre-filtered, 2 pre-filter overflowed -> sort
     n_candidates: int = 0
     filter_log2nb: int = 0
+    convex_fast_path: bool = False
 
     @classmethod
     def _from(cls, d: _Diag) -> "Diag":
@@ -126,7 +127,7 @@ class Diag:
                    [int(c) for c in d.region_counts], [int(c) for c in d.kept_counts],
                    bool(d.degenerate_branch), int(d.sort_passes), int(d.tie_runs),
                    int(d.launches), times, int(d.spa_path), int(d.n_candidates),
-                   int(d.filter_log2nb))
+                   int(d.filter_log2nb), bool(d.convex_fast_path))
 
 
 @dataclass
@@ -179,6 +180,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_sort_region.argtypes = [vp, C.c_int, _dp, C.c_size_t]
         L.chgpu_spa_filter.argtypes = [vp, C.c_int, _dp, C.c_size_t, _dp, C.c_size_t, _dp, _sz]
         L.chgpu_assemble_polygon.argtypes = [_dp, _sz, _dp, _dp, _sz]
+        L.chgpu_finish_chains.argtypes = [_dp, _sz, _dp, _dp, _sz]
         L.chgpu_melkman.argtypes = [_dp, C.c_size_t, _dp, _sz]
         L.chgpu_canonicalize_ring.argtypes = [_dp, C.c_size_t]
         L.chgpu_canonicalize_ring.restype = None
@@ -253,7 +255,7 @@ class Context:
         """SPA_AUTO (default), SPA_SORT (sort every survivor) or SPA_FILTER."""
         self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_SPA_PATH, mode))
 
-    def _hull(self, fn, ptr, n, config):
+    def _hull(self, fn, ptr, n, config, copy=True):
         config = config or PipelineConfig()
         out = _dp()
         k = C.c_size_t()
@@ -262,25 +264,31 @@ class Context:
         st = fn(self.h, ptr, n, config.chunk_count, int(bool(config.degenerate_fallback)),
                 C.byref(out), C.byref(k), C.byref(s), C.byref(d))
         self._check(st)
-        verts = np.ctypeslib.as_array(out, shape=(k.value * 2,)).reshape(-1, 2).copy() \
+        verts = np.ctypeslib.as_array(out, shape=(k.value * 2,)).reshape(-1, 2) \
             if k.value else np.empty((0, 2))
+        if copy:
+            verts = verts.copy()
         return HullResult(Hull(verts), StageStats._from(s), Diag._from(d))
 
-    def convex_hull(self, points, config: PipelineConfig | None = None) -> HullResult:
-        """pipeline.hpp:55 over host points (any (n, 2) float64 array)."""
+    def convex_hull(self, points, config: PipelineConfig | None = None,
+                    copy: bool = True) -> HullResult:
+        """pipeline.hpp:55 over host points (any (n, 2) float64 array);
+        copy as in convex_hull_device."""
         a = _pts(points)
         if len(a) == 0:
             raise EmptyInput("convex_hull: no points")
-        return self._hull(self.lib.chgpu_hull, a.ctypes.data, len(a), config)
+        return self._hull(self.lib.chgpu_hull, a.ctypes.data, len(a), config, copy)
 
-    def convex_hull_device(self, ptr: int, n: int,
-                           config: PipelineConfig | None = None) -> HullResult:
+    def convex_hull_device(self, ptr: int, n: int, config: PipelineConfig | None = None,
+                           copy: bool = True) -> HullResult:
         """Same, over n points already in device memory at `ptr` (e.g. a
         torch.float64 CUDA tensor's data_ptr(); synchronise its producer
-        stream first)."""
+        stream first). copy=False returns the hull as a view of the
+        context's host buffer (the C ABI's result), valid until the next
+        call on this context."""
         if n == 0:
             raise EmptyInput("convex_hull: no points")
-        return self._hull(self.lib.chgpu_hull_device, C.c_void_p(ptr), n, config)
+        return self._hull(self.lib.chgpu_hull_device, C.c_void_p(ptr), n, config, copy)
 
     # ---- stage taps -----------------------------------------------------
     def find_extremes(self, points) -> np.ndarray:
@@ -410,6 +418,21 @@ def assemble_polygon(chains, kept_counts, quad) -> np.ndarray:
     st = L.chgpu_assemble_polygon(_p(a), kc, _p(q), _p(out), C.byref(k))
     if st:
         _raise(st, "assemble_polygon: fewer than 3 distinct vertices")
+    return out[:k.value]
+
+
+def finish_chains(chains, kept_counts, quad) -> np.ndarray:
+    """assemble_polygon (polygon.hpp:25) + melkman (melkman.hpp:29) in one
+    streaming pass (the hull path's finisher)."""
+    L = load_library()
+    a = _pts(chains)
+    kc = (C.c_size_t * 4)(*[int(c) for c in kept_counts])
+    q = np.ascontiguousarray(np.asarray(quad, np.float64).reshape(8))
+    out = np.empty((len(a) + 4, 2), np.float64)
+    k = C.c_size_t()
+    st = L.chgpu_finish_chains(_p(a), kc, _p(q), _p(out), C.byref(k))
+    if st:
+        _raise(st, "finish_chains: degenerate polygon")
     return out[:k.value]
 
 

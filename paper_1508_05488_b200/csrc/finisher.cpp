@@ -166,6 +166,157 @@ int melkman(const Pt* poly, size_t n_in, std::vector<Pt>& hull) {
   return melkman_ring(ring, n, hull);
 }
 
+// assemble_polygon + melkman in one streaming pass over the chains: the
+// ring (corner r, then chain r, consecutive duplicates collapsed, the
+// closing duplicate dropped: polygon.cpp:7-29) is fed to Melkman point by
+// point instead of being materialised, and the canonical rotation
+// (melkman.cpp:10-15) is written straight into `hull`. Same predicates,
+// same pop order, same output as assemble_ring + melkman_ring; a ring of
+// fewer than three distinct vertices (polygon.cpp:26) cannot seed the
+// triangle either, so both report kDegenerate. For survivor-heavy inputs
+// (20 M on-circle points) this removes three full passes over the polygon.
+int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
+                  std::vector<Pt>& hull) {
+  size_t total = 4;
+  for (int r = 0; r < 4; ++r) total += kept_counts[r];
+  thread_local Scratch deque_s;
+  Pt* buf = deque_s.get(2 * total + 8);
+  Pt* head = buf + total + 4;
+  Pt* tail = head;
+
+  // Phase A (melkman.cpp:30-60): absorb the leading collinear run, then
+  // seed the triangle. Phase B (:62-80): the deque loop with cached edges.
+  int phase = 0;  // 0: no point yet, 1: collinear run, 2: deque
+  Pt lo{0.0, 0.0}, hi{0.0, 0.0}, last{0.0, 0.0};
+  double hax = 0, hay = 0, hex = 0, hey = 0, tax = 0, tay = 0, tex = 0, tey = 0;
+  auto feed = [&](const Pt& v) {
+    if (phase == 2) {
+      const double vx = v.x, vy = v.y;
+      const bool left_head = hex * (vy - hay) - hey * (vx - hax) > 0.0;
+      const bool left_tail = tex * (vy - tay) - tey * (vx - tax) > 0.0;
+      if (left_head & left_tail) return;
+      if (!left_tail && tail - head >= 2) {
+        --tail;
+        while (tail - head >= 2) {
+          const Pt a = tail[-2], b = tail[-1];
+          if ((b.x - a.x) * (vy - a.y) - (b.y - a.y) * (vx - a.x) > 0.0) break;
+          --tail;
+        }
+      }
+      *tail++ = v;
+      while (tail - head >= 2) {
+        const Pt a = head[0], b = head[1];
+        if ((a.x - vx) * (b.y - vy) - (a.y - vy) * (b.x - vx) > 0.0) break;
+        ++head;
+      }
+      *--head = v;
+      hax = vx;
+      hay = vy;
+      hex = head[1].x - vx;
+      hey = head[1].y - vy;
+      tax = tail[-2].x;
+      tay = tail[-2].y;
+      tex = tail[-1].x - tax;
+      tey = tail[-1].y - tay;
+      return;
+    }
+    if (phase == 0) {
+      lo = hi = last = v;
+      phase = 1;
+      return;
+    }
+    if (turn(lo, hi, v) == 0) {  // still collinear
+      if (lex_less(v, lo))
+        lo = v;
+      else if (lex_less(hi, v))
+        hi = v;
+      last = v;
+      return;
+    }
+    const Pt second = last;
+    const Pt first = same(last, lo) ? hi : lo;
+    const bool ccw = turn(first, second, v) == kLeft;
+    *tail++ = v;
+    *tail++ = ccw ? first : second;
+    *tail++ = ccw ? second : first;
+    *tail++ = v;
+    hax = head[0].x, hay = head[0].y, hex = head[1].x - hax, hey = head[1].y - hay;
+    tax = tail[-2].x, tay = tail[-2].y, tex = tail[-1].x - tax, tey = tail[-1].y - tay;
+    phase = 2;
+  };
+
+  // The virtual ring: 8 segments (corner r, chain r). The run of trailing
+  // elements equal to the very last one emits at most one vertex, which
+  // polygon.cpp:22-24 drops when it repeats the first vertex (corner 0).
+  const Pt* seg_ptr[8];
+  size_t seg_len[8];
+  {
+    const Pt* c = chains;
+    for (int r = 0; r < 4; ++r) {
+      seg_ptr[2 * r] = &corners[r];
+      seg_len[2 * r] = 1;
+      seg_ptr[2 * r + 1] = c;
+      seg_len[2 * r + 1] = kept_counts[r];
+      c += kept_counts[r];
+    }
+  }
+  int last_seg = 7;
+  while (seg_len[last_seg] == 0) --last_seg;  // segment 6 (corner 3) is never empty
+  const Pt last_pt = seg_ptr[last_seg][seg_len[last_seg] - 1];
+  const bool drop_last = same(last_pt, corners[0]);
+  // cut the trailing run of last_pt off the segments
+  int cut_seg = last_seg;
+  size_t cut_idx = seg_len[last_seg] - 1;
+  for (;;) {
+    if (cut_idx > 0 && same(seg_ptr[cut_seg][cut_idx - 1], last_pt)) {
+      --cut_idx;
+      continue;
+    }
+    if (cut_idx == 0) {
+      int s2 = cut_seg - 1;
+      while (s2 >= 0 && seg_len[s2] == 0) --s2;
+      if (s2 >= 0 && same(seg_ptr[s2][seg_len[s2] - 1], last_pt)) {
+        cut_seg = s2;
+        cut_idx = seg_len[s2] - 1;
+        continue;
+      }
+    }
+    break;
+  }
+  Pt prev{0.0, 0.0};
+  bool have_prev = false;
+  size_t ring_n = 0;
+  for (int sgi = 0; sgi <= cut_seg; ++sgi) {
+    const size_t end = sgi == cut_seg ? cut_idx : seg_len[sgi];
+    const Pt* p = seg_ptr[sgi];
+    for (size_t j = 0; j < end; ++j) {
+      if (have_prev && same(prev, p[j])) continue;
+      prev = p[j];
+      have_prev = true;
+      ++ring_n;
+      feed(p[j]);
+    }
+  }
+  // the trailing run: one vertex unless it repeats the previous one or
+  // closes the ring onto corner 0 (when the ring has more than one vertex)
+  if (!(have_prev && same(prev, last_pt)) && !(drop_last && ring_n >= 1)) {
+    ++ring_n;
+    feed(last_pt);
+  }
+  if (phase != 2) return kDegenerate;
+
+  // hull = deque [head, tail - 1) rotated to its first lexicographic
+  // minimum (canonicalize_ring), written once.
+  const size_t m = (size_t)(tail - 1 - head);
+  size_t lo_i = 0;
+  for (size_t i = 1; i < m; ++i)
+    if (lex_less(head[i], head[lo_i])) lo_i = i;
+  hull.resize(m);
+  std::memcpy(hull.data(), head + lo_i, (m - lo_i) * sizeof(Pt));
+  std::memcpy(hull.data() + (m - lo_i), head, lo_i * sizeof(Pt));
+  return kOk;
+}
+
 int monotone_chain(const Pt* pts, size_t n, std::vector<Pt>& hull) {
   // oracle.cpp:19-37 over lexicographically sorted, duplicate-free points.
   hull.clear();
@@ -220,6 +371,20 @@ extern "C" int chgpu_assemble_polygon(const double* chains, const size_t* kept_c
   std::memcpy(out, ring.data(), ring.size() * sizeof(Pt));
   *n_out = ring.size();
   return st;
+}
+
+extern "C" int chgpu_finish_chains(const double* chains, const size_t* kept_counts,
+                                   const double* quad, double* out, size_t* n_out) {
+  std::vector<Pt> hull;
+  const int st = chgpu::host::finish_chains(reinterpret_cast<const Pt*>(chains), kept_counts,
+                                            reinterpret_cast<const Pt*>(quad), hull);
+  if (st) {
+    *n_out = 0;
+    return st;
+  }
+  std::memcpy(out, hull.data(), hull.size() * sizeof(Pt));
+  *n_out = hull.size();
+  return 0;
 }
 
 extern "C" int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out) {

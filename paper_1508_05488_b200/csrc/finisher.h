@@ -21,6 +21,9 @@ int melkman(const Pt* poly, size_t n, std::vector<Pt>& hull);
 // melkman() over a ring that is already free of consecutive and wrap
 // duplicates (what assemble_ring returns).
 int melkman_ring(const Pt* ring, size_t n, std::vector<Pt>& hull);
+// assemble_ring + melkman_ring in one streaming pass (no ring copy).
+int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
+                  std::vector<Pt>& hull);
 int monotone_chain(const Pt* sorted_unique, size_t n, std::vector<Pt>& hull);
 int sorted_hull(const Pt* pts, size_t n, std::vector<Pt>& hull);
 void insert_sorted_unique(std::vector<Pt>& sorted, const Pt& p);

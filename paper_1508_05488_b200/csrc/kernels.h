@@ -71,6 +71,13 @@ void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max
                       u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
                       cudaStream_t st);
 
+// Melkman's convex-position trajectory on the device (k_convex.cu).
+int convex_blocks();
+void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInfo* qinfo, u32* ok,
+                         u64* block_best, cudaStream_t st);
+void launch_convex_emit(const double2* chains, const u64 kept[4], const QuadInfo* qinfo,
+                        const u64* block_best, double2* out, cudaStream_t st);
+
 // K1
 // Blocks launch_extremes_partial will use for a request of `requested`.
 int extremes_blocks(int requested);

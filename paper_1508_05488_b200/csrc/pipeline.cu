@@ -43,7 +43,8 @@ struct Pinned {
   unsigned long long ncand;
 };
 
-constexpr int kMaxFilterBits = 18;  // SPA pre-filter: at most 2^18 bins per region
+constexpr int kMaxFilterBits = 18;
+constexpr size_t kConvexMin = size_t(1) << 16;  // ring size from which k_convex.cu is tried  // SPA pre-filter: at most 2^18 bins per region
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -114,6 +115,8 @@ struct chgpu_ctx {
   size_t h_out_cap = 0;
 
   std::vector<Pt> hull, ring, chains;
+  const Pt* hull_ptr = nullptr;  // the last call's hull (hull.data() or h_out)
+  size_t hull_n = 0;
   int launches = 0;
   cudaEvent_t ev[12] = {};
   std::vector<cudaEvent_t> ev_copy;
@@ -214,7 +217,7 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
   free_ws(ctx);
   size_t cap = std::max<size_t>(n, 4096);
   cap = (cap + 4095) & ~size_t(4095);
-  CK(cudaMalloc(&ctx->d_pts, cap * sizeof(double2)));
+  CK(cudaMalloc(&ctx->d_pts, (cap + 64) * sizeof(double2)));  // + the convex path's hull
   CK(cudaMalloc(&ctx->d_kbuf, 2 * cap * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_vbuf, 2 * cap * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_ka, cap * sizeof(u64)));
@@ -832,6 +835,38 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
   return CHGPU_OK;
 }
 
+// Melkman's all-vertices-kept trajectory checked on the device
+// (k_convex.cu). On success the canonical hull is in h_out (hull_ptr /
+// hull_n set, event 9 after its copy) and *convex = true.
+int convex_finish(chgpu_ctx* ctx, const size_t kept_counts[4], size_t kept, bool* convex) {
+  cudaStream_t st = ctx->st;
+  *convex = false;
+  const int ok_slot = take_ctr(ctx);
+  const u32 one = 1;
+  TRY(upload(ctx, ctx->d_ctr + ok_slot, &one, sizeof one));
+  const u64 k4[4] = {kept_counts[0], kept_counts[1], kept_counts[2], kept_counts[3]};
+  u64* block_best = reinterpret_cast<u64*>(ctx->d_faux + 16384);
+  launch_convex_check(ctx->d_kept, k4, ctx->d_qinfo, ctx->d_ctr + ok_slot, block_best, st);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&ctx->h->ctr[ok_slot], ctx->d_ctr + ok_slot, sizeof(u32),
+                     cudaMemcpyDeviceToHost, st));
+  TRY(sync(ctx));
+  if (!ctx->h->ctr[ok_slot]) return CHGPU_OK;
+  const size_t N = kept + 4;
+  launch_convex_emit(ctx->d_kept, k4, ctx->d_qinfo, block_best, ctx->d_pts, st);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  TRY(ensure_host_out(ctx, N + 4));
+  CK(cudaMemcpyAsync(ctx->h_out, ctx->d_pts, N * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ctx->ev[9], st));
+  TRY(sync(ctx));
+  ctx->hull_ptr = reinterpret_cast<const Pt*>(ctx->h_out);
+  ctx->hull_n = N;
+  *convex = true;
+  return CHGPU_OK;
+}
+
 void frame_of(const double* quad, Pt* fr, int* nf) {
   *nf = 0;
   for (int c = 0; c < 4; ++c) {
@@ -983,6 +1018,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     frame_of(qi.q, fr, &nf);
     for (int f = 0; f < nf; ++f) chgpu::host::insert_sorted_unique(ctx->chains, fr[f]);
     chgpu::host::monotone_chain(ctx->chains.data(), ctx->chains.size(), ctx->hull);
+    ctx->hull_ptr = ctx->hull.data();
+    ctx->hull_n = ctx->hull.size();
   } else {
     for (int s = 0; s < 4; ++s) D.region_counts[s + 1] = m[s];
     D.region_counts[0] = n - s1;
@@ -1061,6 +1098,17 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
     ctx->kept_hint = kept;
+    if (kept + 4 >= kConvexMin) {
+      // Survivor-heavy: try Melkman's convex-position trajectory on the
+      // device (k_convex.cu); on success the hull comes back canonical.
+      bool convex = false;
+      TRY(convex_finish(ctx, kept_counts, kept, &convex));
+      if (convex) {
+        D.convex_fast_path = 1;
+        D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
+        goto finished;
+      }
+    }
     if (!(filtered && kept <= spec)) {  // else the speculative read-back holds them
       TRY(ensure_host_out(ctx, kept + 4));
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, kept * sizeof(double2), cudaMemcpyDeviceToHost,
@@ -1070,18 +1118,19 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     }
     D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
     const auto t_host0 = std::chrono::steady_clock::now();
-    const int a = chgpu::host::assemble_ring(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
-                                             corners, ctx->ring);
-    if (a) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon: fewer than 3 distinct vertices");
-    // assemble_ring already collapsed duplicates exactly as melkman.cpp:20-25
-    const int mk = chgpu::host::melkman_ring(ctx->ring.data(), ctx->ring.size(), ctx->hull);
-    if (mk) return fail(ctx, CHGPU_DEGENERATE, "melkman: degenerate polygon");
+    // polygon.cpp:7-29 + melkman.cpp:17-86 in one streaming pass
+    const int mk = chgpu::host::finish_chains(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
+                                              corners, ctx->hull);
+    if (mk) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon/melkman: degenerate polygon");
     D.t_host_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    ctx->hull_ptr = ctx->hull.data();
+    ctx->hull_n = ctx->hull.size();
   }
+finished:
   const auto t_end = std::chrono::steady_clock::now();
 
-  S.n_hull = ctx->hull.size();
+  S.n_hull = ctx->hull_n;
   S.t_extremes_ms = ms_between(ctx->ev[0], ctx->ev[1]);
   S.t_classify_ms = ms_between(ctx->ev[1], ctx->ev[2]);
   S.t_partition_ms = 0.0;
@@ -1094,8 +1143,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   if (h_src) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
   D.launches = ctx->launches;
 
-  *hull_xy = reinterpret_cast<const double*>(ctx->hull.data());
-  *n_hull = ctx->hull.size();
+  *hull_xy = reinterpret_cast<const double*>(ctx->hull_ptr);
+  *n_hull = ctx->hull_n;
   if (stats) *stats = S;
   if (diag) *diag = D;
   return CHGPU_OK;
@@ -1156,7 +1205,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_fstart, (size_t(4) << kMaxFilterBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_fthr, (size_t(4) << kMaxFilterBits) * sizeof(u64))) ||
       bad(cudaMalloc(&ctx->d_fbig, 2 * (size_t)kBigListB * sizeof(u32))) ||
-      bad(cudaMalloc(&ctx->d_faux, 16384)) ||
+      bad(cudaMalloc(&ctx->d_faux, 32768)) ||
       bad(cudaMalloc(&ctx->d_plan, sizeof(FilterPlan))) ||
       bad(cudaMallocHost(&ctx->h, sizeof(Pinned)))) {
     chgpu_ctx_destroy(ctx);

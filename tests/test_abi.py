@@ -123,3 +123,56 @@ def test_host_melkman_on_pipeline_polygons(product, oracle):
                 product.melkman(ring)
         else:
             assert np.array_equal(product.melkman(ring), want), trial
+
+
+def _finish_reference(ref, chains, kc, quad):
+    """assemble_polygon + melkman of the reference (None when degenerate)."""
+    try:
+        poly = np.asarray(quad).reshape(4, 2)
+        ring = []
+        off = 0
+        for r in range(4):
+            for p in [poly[r]] + list(chains[off:off + kc[r]]):
+                if not ring or not (ring[-1][0] == p[0] and ring[-1][1] == p[1]):
+                    ring.append(p)
+            off += kc[r]
+        if len(ring) > 1 and ring[0][0] == ring[-1][0] and ring[0][1] == ring[-1][1]:
+            ring.pop()
+        if len(ring) < 3:
+            return None
+        st, hull = ref.melkman(np.array(ring))
+        return None if st else hull
+    except Exception:
+        return None
+
+
+def test_finish_chains_equals_assemble_then_melkman(product, oracle):
+    """The fused streaming finisher == assemble_polygon + melkman (reference
+    polygon.cpp:7-29, melkman.cpp:17-86) on pipeline chains and on
+    adversarial rings: duplicates across segment joints, empty chains, a
+    closing vertex equal to corner 0, collinear and tiny inputs."""
+    from pyoracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefLib()
+    for dist, n, seed in (("uniform_square", 100_000, 42), ("circle", 3_000, 9),
+                          ("gaussian", 50_000, 5), ("uniform_disk", 30_000, 1)):
+        pts = ref.generate(dist, n, seed)
+        for cc in (1, 3, 1024):
+            quad, rc, srt, kept, kc = ref.stage_dump(pts, cc)
+            want = _finish_reference(ref, kept, kc, quad)
+            got = product.finish_chains(kept, kc, quad)
+            assert np.array_equal(got, want), (dist, cc)
+    rng = np.random.default_rng(99)
+    for trial in range(2000):
+        quad = rng.integers(0, 4, (4, 2)).astype(np.float64)
+        kc = [int(x) for x in rng.integers(0, 4, 4)]
+        chains = rng.integers(0, 4, (sum(kc), 2)).astype(np.float64)
+        if rng.random() < 0.3 and sum(kc):  # close onto corner 0
+            chains[-1] = quad[0]
+        want = _finish_reference(ref, chains, kc, quad)
+        if want is None:
+            with pytest.raises(product.DegenerateInput):
+                product.finish_chains(chains, kc, quad)
+        else:
+            assert np.array_equal(product.finish_chains(chains, kc, quad), want), trial

@@ -110,3 +110,48 @@ def test_overflow_falls_back(product, oracle):
     assert np.array_equal(r.hull.vertices, want.hull)
     assert r.diag.spa_path in (1, 2)
     ctx.close()
+
+
+def _ring_points(n, seed, r=1.0):
+    rng = np.random.default_rng(seed)
+    t = np.sort(rng.random(n)) * 2 * np.pi
+    return np.stack([r * np.cos(t), r * np.sin(t)], 1)
+
+
+@pytest.mark.parametrize("case", ["circle", "circle_noisy", "square_edges", "duplicates",
+                                  "near_flat_arc"])
+def test_convex_fast_path(gpu_ctx, product, oracle, case):
+    """Melkman's all-vertices-kept trajectory verified on the GPU
+    (k_convex.cu) must give the reference hull, and must hand over to the
+    host loop whenever any predicate deviates (inner survivors, collinear
+    edge runs, duplicates, near-collinear arcs)."""
+    rng = np.random.default_rng(7)
+    if case == "circle":
+        pts = product.generate("circle", 300_000, 11)
+    elif case == "circle_noisy":
+        pts = _ring_points(300_000, 1)
+        pts[::97] *= 1.0 - 1e-9 * rng.random((len(pts[::97]), 1))  # a few just inside
+    elif case == "square_edges":
+        s = rng.random(200_000)
+        side = rng.integers(0, 4, len(s))
+        pts = np.stack([np.where(side == 0, s, np.where(side == 1, 1.0, np.where(side == 2, 1 - s, 0.0))),
+                        np.where(side == 0, 0.0, np.where(side == 1, s, np.where(side == 2, 1.0, 1 - s)))], 1)
+        pts = np.vstack([pts, [[0.5, -0.5], [1.5, 0.5], [0.5, 1.5], [-0.5, 0.5]]])
+    elif case == "duplicates":
+        pts = _ring_points(200_000, 2)
+        pts = np.vstack([pts, pts[::1000]])
+    else:  # points on a very flat arc: consecutive triples round to collinear
+        x = np.sort(rng.random(300_000)) * 1e-3
+        pts = np.stack([x, 1e-12 * x * x], 1)
+        pts = np.vstack([pts, [[0.0005, -1.0], [0.0005, 1.0]]])
+    for cc in (1024, 100_000):
+        want = oracle.convex_hull(pts, cc)
+        r = gpu_ctx.convex_hull(pts, product.PipelineConfig(chunk_count=cc))
+        s = r.stats
+        assert [s.n_input, s.n_after_round1, s.n_after_spa, s.n_hull] == want.counts.tolist(), \
+            (case, cc)
+        assert np.array_equal(r.hull.vertices, want.hull), (case, cc)
+        if case == "circle":
+            assert r.diag.convex_fast_path
+        if case in ("duplicates", "square_edges"):
+            assert not r.diag.convex_fast_path
