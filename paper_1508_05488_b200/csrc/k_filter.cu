@@ -668,7 +668,8 @@ __global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
       vv = v[a];
       g = (u32)jj;
     }
-    if (total > 1) warp_sort_records(region, g, kk, vv);
+    // one record per bin: lane order is already (bin, record) order
+    if (__any_sync(0xffffffffu, inb && n > 1)) warp_sort_records(region, g, kk, vv);
     // bin g's records now occupy lanes [excl_g, excl_g + n_g) in order
     const int gs = has ? (int)g : 0;
     const u32 gex = __shfl_sync(0xffffffffu, excl, gs);

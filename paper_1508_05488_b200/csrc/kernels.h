@@ -67,8 +67,8 @@ void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32*
                          const u32* bstart, const FilterPlan* P, int log2nb, u64* ck, u64* cv,
                          u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st);
 void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max_chunks,
-                      const u32* first_cand, const u32* region_end, double2* scratch,
-                      u32* chunk_kept, u32* offs, unsigned long long* kept_counts, double2* out,
+                      const u32* first_cand, const u32* region_end, u64* status, u32 tag,
+                      u32* chunk_ctr, unsigned long long* kept_counts, double2* out,
                       cudaStream_t st);
 
 // Melkman's convex-position trajectory on the device (k_convex.cu).

@@ -825,11 +825,9 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
                       ctx->d_cv, first_cand, reinterpret_cast<u32*>(ctx->d_fthr), aux, st);
   CK(cudaEventRecord(ctx->ev[5], st));
   CK(cudaEventRecord(ctx->ev[6], st));
-  u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
-  u32* offs = chunk_kept + ((max_chunks + 31) & ~31u);
-  launch_spa_dense(ctx->d_ck, ctx->d_cv, P, max_chunks, first_cand, aux.region_end, ctx->d_pts,
-                   chunk_kept, offs, ctx->d_u64, ctx->d_kept, st);
-  ctx->launches += 14;
+  launch_spa_dense(ctx->d_ck, ctx->d_cv, P, max_chunks, first_cand, aux.region_end, ctx->d_status,
+                   next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->d_u64, ctx->d_kept, st);
+  ctx->launches += 12;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[8], st));
   return CHGPU_OK;
