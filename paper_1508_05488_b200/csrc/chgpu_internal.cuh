@@ -178,6 +178,25 @@ __device__ __forceinline__ u32 bin_of(const BinGeom& g, int r, double p) {
   return (r >= 3) ? top - b : b;  // UR / UL sort descending
 }
 
+// The record word v of region r (1..4) for point (x, y) (key codec above).
+__device__ __forceinline__ u64 v_of(int r, double x, double y) {
+  switch (r) {
+    case 1: return ~ord_enc(y);
+    case 2: return ord_enc(x);
+    case 3: return ord_enc(y);
+    default: return ~ord_enc(x);
+  }
+}
+// ... and its word k.
+__device__ __forceinline__ u64 k_of(int r, double x, double y) {
+  switch (r) {
+    case 1: return ord_enc(x);
+    case 2: return ord_enc(y);
+    case 3: return ~ord_enc(x);
+    default: return ~ord_enc(y);
+  }
+}
+
 // The guarded coordinate as a key w on which every region's SPA is a
 // running MAX: steps_back(g, t) <=> w(g) < w(t) (spa.cpp:92-105). w is the
 // record's v word (chgpu_internal codec: LL ~ord(y), LR ord(x), UR ord(y),

@@ -361,6 +361,136 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
   }
 }
 
+// K2 of the pre-filtered path (k_filter.cu): classify, count, and for
+// every survivor one fire-and-forget increment of its SPA bin's count and
+// (for one record in 2^k, wmask) a running max of its guarded key w. The
+// survivors are written as raw points (one 16-byte store) into two
+// two-ended stream pairs: LL | LR growing from both ends of pair12 and
+// UR | UL of pair34 (each cap points); the filter derives the sort record
+// only for the few it keeps. The four region counts travel packed in one
+// u64 (16-bit fields) through a single warp scan. A degenerate frame
+// (pipeline.cpp:53-71) writes LEX records into stream 1 of (kbuf, vbuf)
+// exactly like k_classify_compact.
+__global__ __launch_bounds__(kK2Threads, 4) void k_classify_survivors(
+    const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo, u64 ncap,
+    double2* __restrict__ pair12, double2* __restrict__ pair34, u64* __restrict__ kbuf,
+    u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
+    u64* __restrict__ bw, u32 wmask) {
+  extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
+  // Per-region tables (index r - 1), so the per-item code has no region
+  // branches: stream origin and direction, bin map, guarded-key mask.
+  __shared__ unsigned long long s_wtot[kK2Threads / 32];
+  __shared__ u32 s_base[4];
+  __shared__ double2* s_org[4];
+  __shared__ long long s_dir[4];
+  __shared__ double s_lo[4], s_scale[4];
+  __shared__ u32 s_rev[4];
+  __shared__ unsigned long long s_vmask[4];
+  __shared__ QuadEdges s_edges;
+  __shared__ double s_top;
+  __shared__ int s_lex;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const u64 tile_base = (u64)blockIdx.x * kK2Tile;
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    const bool ok = idx < n;
+    cp_async16(sbuf + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
+  }
+  cp_async_commit();
+  if (tid == 0) {
+    const QuadInfo qi = *qinfo;
+    for (int c = 0; c < 4; ++c) {
+      const int d = (c + 1) & 3;
+      s_edges.ax[c] = qi.q[2 * c];
+      s_edges.ay[c] = qi.q[2 * c + 1];
+      s_edges.ex[c] = __dsub_rn(qi.q[2 * d], qi.q[2 * c]);
+      s_edges.ey[c] = __dsub_rn(qi.q[2 * d + 1], qi.q[2 * c + 1]);
+    }
+    s_lex = qi.degenerate;
+    BinGeom g;
+    make_bin_geom(qi.q, log2nb, &g);
+    s_top = g.top;
+    for (int r = 0; r < 4; ++r) {
+      s_lo[r] = g.lo[r];
+      s_scale[r] = g.scale[r];
+      s_rev[r] = r >= 2 ? 1u : 0u;                                  // UR / UL descending
+      s_vmask[r] = (r == 0 || r == 3) ? ~0ull : 0ull;               // LL / UL: min-regions
+      s_org[r] = (r & 1) ? ((r < 2 ? pair12 : pair34) + ncap - 1) : (r < 2 ? pair12 : pair34);
+      s_dir[r] = (r & 1) ? -1 : 1;
+    }
+  }
+  __syncthreads();
+  const bool lex = s_lex != 0;
+  const QuadEdges e = s_edges;
+  cp_async_wait<0>();  // each thread reads back only its own copies
+
+  u32 codes = 0;        // 3 bits of stream id per item
+  u64 cnt = 0;          // 16-bit count per stream
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    const double2 p = sbuf[j * kK2Threads + tid];
+    int r = idx < n ? classify(e, p.x, p.y) : 0;
+    if (lex && r != 0) r = 1;
+    codes |= (u32)r << (3 * j);
+    cnt += r ? 1ull << (16 * (r - 1)) : 0ull;
+  }
+  u64 incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wtot[warp] = incl;
+  __syncthreads();
+  if (tid < 4) {
+    u32 tot = 0;
+    for (int w = 0; w < kK2Threads / 32; ++w) tot += (u32)(s_wtot[w] >> (16 * tid)) & 0xFFFFu;
+    s_base[tid] = tot ? atomicAdd(&counts_out[tid + 1], tot) : 0u;
+  }
+  __syncthreads();
+  u64 run = 0;  // this thread's exclusive position in each stream (16-bit fields)
+  for (int w = 0; w < warp; ++w) run += s_wtot[w];
+  run += incl - cnt;
+  if (lex) {
+#pragma unroll
+    for (int j = 0; j < kK2Items; ++j) {
+      if (!((codes >> (3 * j)) & 7)) continue;
+      const double2 p = sbuf[j * kK2Threads + tid];
+      const u32 pp = s_base[0] + (u32)(run & 0xFFFFu);
+      run += 1;
+      kbuf[pp] = ord_enc(p.x);
+      vbuf[pp] = ord_enc(p.y);
+    }
+    return;
+  }
+  const u32 top = (u32)s_top;
+#pragma unroll
+  for (int j = 0; j < kK2Items; ++j) {
+    const u32 r = (codes >> (3 * j)) & 7;
+    if (!r) continue;
+    const u32 ri = r - 1;
+    const u32 sh = 16 * ri;
+    const u32 pp = s_base[ri] + (u32)((run >> sh) & 0xFFFFu);
+    run += 1ull << sh;
+    const double2 p = sbuf[j * kK2Threads + tid];
+    s_org[ri][(long long)pp * s_dir[ri]] = p;
+    const bool odd = (r & 1u) != 0;
+    const double prim = odd ? p.x : p.y;   // bin_of (chgpu_internal.cuh), tables
+    const u32 bq = min((u32)__double2uint_rz(__dmul_rn(__dsub_rn(prim, s_lo[ri]), s_scale[ri])), top);
+    const u32 b = (ri << log2nb) | (s_rev[ri] ? top - bq : bq);
+    atomicAdd(bcnt + b, 1u);
+    // any subset of a bin's records gives a valid (lower) max: sample; w =
+    // wkey(v): the guarded coordinate with -0.0 folded onto +0.0 (+ 0.0)
+    if ((pp & wmask) == 0) {
+      const double g = odd ? p.y : p.x;
+      atomicMax(bw + b, ord_enc(__dadd_rn(g, 0.0)) ^ s_vmask[ri]);
+    }
+  }
+}
+
 // Labels only (the classify() stage tap, classify.cpp:9-33).
 __global__ void k_classify_labels(const double2* __restrict__ pts, u64 n,
                                   const QuadInfo* __restrict__ qinfo,
@@ -444,6 +574,17 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
   else
     k_classify_compact<false, false><<<tiles, kK2Threads, smem, st>>>(
         pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr, 0);
+}
+
+void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64 ncap,
+                               double2* pair12, double2* pair34, u64* kbuf, u64* vbuf,
+                               u32* counts_out, int log2nb, u32* bcnt, u64* bw, u32 wmask,
+                               cudaStream_t st) {
+  const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
+  if (tiles == 0) return;
+  constexpr size_t smem = kK2Tile * sizeof(double2);
+  k_classify_survivors<<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, ncap, pair12, pair34, kbuf,
+                                                        vbuf, counts_out, log2nb, bcnt, bw, wmask);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

@@ -325,10 +325,10 @@ constexpr int kFilterItems = 4;
 // the next slot of its bin; the bin's 33rd candidate queues the bin for
 // k_bin_sort_big.
 __global__ __launch_bounds__(kFilterThreads) void k_filter(
-    const u64* __restrict__ kbuf, const u64* __restrict__ vbuf, const FilterPlan* __restrict__ P_p,
-    const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
-    const u64* __restrict__ bthr, u32* __restrict__ bcur, u64* __restrict__ kout,
-    u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
+    const double2* __restrict__ pair12, const double2* __restrict__ pair34,
+    const FilterPlan* __restrict__ P_p, const QuadInfo* __restrict__ qinfo,
+    const u32* __restrict__ bstart, const u64* __restrict__ bthr, u32* __restrict__ bcur,
+    u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
     unsigned long long* __restrict__ ncand) {
   const FilterPlan& P = *P_p;
   __shared__ BinGeom s_geom;
@@ -343,7 +343,7 @@ __global__ __launch_bounds__(kFilterThreads) void k_filter(
   u32 mine = 0;
   for (u64 i0 = (u64)blockIdx.x * kFilterThreads * kFilterItems + threadIdx.x; i0 < total;
        i0 += stride) {
-    u64 k[kFilterItems], v[kFilterItems];
+    double2 p[kFilterItems];
     int rr[kFilterItems];
 #pragma unroll
     for (int j = 0; j < kFilterItems; ++j) {
@@ -353,26 +353,34 @@ __global__ __launch_bounds__(kFilterThreads) void k_filter(
       r += (i >= P.cum[2]);
       r += (i >= P.cum[3]);
       rr[j] = r;
-      k[j] = v[j] = 0;
+      p[j] = make_double2(0.0, 0.0);
       if (i < total) {
-        const u64 slot = P.src_off[r] + (i - P.cum[r]);
-        k[j] = __ldcs(kbuf + slot);
-        v[j] = __ldcs(vbuf + slot);
+        const double2* pair = r < 2 ? pair12 : pair34;
+        p[j] = __ldcs(pair + P.src_off[r] + (i - P.cum[r]));
       }
     }
+    // all threshold loads in flight before any test
+    u32 bi[kFilterItems];
+    u64 th[kFilterItems];
 #pragma unroll
     for (int j = 0; j < kFilterItems; ++j) {
       const u64 i = i0 + (u64)j * kFilterThreads;
-      if (i >= total) continue;
       const int reg = rr[j] + 1;
-      const u32 bi = ((u32)rr[j] << P.log2nb) | bin_of(s_geom, reg, primary_of(reg, k[j]));
-      if (wkey(reg, v[j]) < __ldg(bthr + bi)) continue;
-      const u32 pos = atomicAdd(bcur + bi, 1u);
-      const u64 dst = P.spa.off[rr[j]] + bstart[bi] + pos;
-      kout[dst] = k[j];
-      vout[dst] = v[j];
-      if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: sorted by a warp
-      if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: by a CTA
+      const double prim = (reg & 1) ? p[j].x : p[j].y;
+      bi[j] = ((u32)rr[j] << P.log2nb) | bin_of(s_geom, reg, prim);
+      th[j] = i < total ? __ldg(bthr + bi[j]) : ~0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < kFilterItems; ++j) {
+      const int reg = rr[j] + 1;
+      const u64 v = v_of(reg, p[j].x, p[j].y);
+      if (wkey(reg, v) < th[j]) continue;  // (also every i >= total: th = ~0)
+      const u32 pos = atomicAdd(bcur + bi[j], 1u);
+      const u64 dst = P.spa.off[rr[j]] + bstart[bi[j]] + pos;
+      kout[dst] = k_of(reg, p[j].x, p[j].y);
+      vout[dst] = v;
+      if (pos == 32) big[atomicAdd(nbig, 1u)] = bi[j];                       // > 32: sorted by a warp
+      if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi[j];  // > 256: by a CTA
       ++mine;
     }
   }
@@ -696,10 +704,11 @@ __global__ void k_filter_plan(const QuadInfo* __restrict__ qinfo, const u32* __r
   P.log2nb = log2nb;
   u64 m[4];
   for (int r = 0; r < 4; ++r) m[r] = qi.degenerate ? 0ull : (u64)counts[r];
+  // survivor points: LL | LR at both ends of pair12, UR | UL of pair34
   P.src_off[0] = 0;
   P.src_off[1] = ncap - m[1];
-  P.src_off[2] = ncap;
-  P.src_off[3] = 2 * ncap - m[3];
+  P.src_off[2] = 0;
+  P.src_off[3] = ncap - m[3];
   P.cum[0] = 0;
   u32 chunks = 0;
   for (int r = 0; r < 4; ++r) {
@@ -737,14 +746,15 @@ void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int lo
                                                       aux.agg_val, bthr);
 }
 
-void launch_filter(const u64* kbuf, const u64* vbuf, const FilterPlan* P, u64 max_records,
-                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
-                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st) {
+void launch_filter(const double2* pair12, const double2* pair34, const FilterPlan* P,
+                   u64 max_records, const QuadInfo* qinfo, const u32* bstart, const u64* bthr,
+                   u32* bcur, u64* kout, u64* vout, u32* big, u32* nbig,
+                   unsigned long long* ncand, cudaStream_t st) {
   if (max_records == 0) return;
   const u64 per = (u64)kFilterThreads * kFilterItems;
   const u64 blocks = std::min<u64>((max_records + per - 1) / per, 148ull * 8);
-  k_filter<<<(unsigned)blocks, kFilterThreads, 0, st>>>(kbuf, vbuf, P, qinfo, bstart, bthr, bcur,
-                                                          kout, vout, big, nbig, ncand);
+  k_filter<<<(unsigned)blocks, kFilterThreads, 0, st>>>(pair12, pair34, P, qinfo, bstart, bthr,
+                                                          bcur, kout, vout, big, nbig, ncand);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,

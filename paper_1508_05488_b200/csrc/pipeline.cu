@@ -814,7 +814,9 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
                      ctx->d_plan, st);
   launch_bin_scan(t.cnt, t.w, P, log2nb, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
   CK(cudaEventRecord(ctx->ev[3], st));
-  launch_filter(ctx->d_kbuf, ctx->d_vbuf, P, n, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr, t.cur,
+  launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf),
+                reinterpret_cast<const double2*>(ctx->d_vbuf), P, n, ctx->d_qinfo, ctx->d_fstart,
+                ctx->d_fthr, t.cur,
                 ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
   CK(cudaEventRecord(ctx->ev[4], st));
   launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
@@ -953,9 +955,17 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   const FilterTabs ftabs = filter_tabs(ctx, log2nb);
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
-  launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
-                          ctx->cap, ctx->d_ctr + cnt_slot, st, log2nb,
-                          want_filter ? ftabs.cnt : nullptr, ftabs.w, filter_wmask());
+  if (want_filter) {
+    // raw survivor points + bin statistics (a degenerate frame writes the
+    // LEX records of stream 1 instead)
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->cap,
+                              reinterpret_cast<double2*>(ctx->d_kbuf),
+                              reinterpret_cast<double2*>(ctx->d_vbuf), ctx->d_kbuf, ctx->d_vbuf,
+                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
+  } else {
+    launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
+                            ctx->cap, ctx->d_ctr + cnt_slot, st);
+  }
   ctx->launches += 2;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
@@ -984,6 +994,18 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   TRY(sync(ctx));
 
   const QuadInfo qi = ctx->h->qi;
+  const bool overflow = want_filter && !qi.degenerate && ctx->h->ctr[ovf_slot] != 0;
+  if (overflow) {
+    // The full region sort needs K2's (k, v) streams, which the filter
+    // path's K2 does not write: run the record-writing K2 (the input is
+    // intact; the counts are the same classification).
+    const int rec_slot = take_ctr(ctx);
+    (void)take_ctr(ctx), (void)take_ctr(ctx), (void)take_ctr(ctx), (void)take_ctr(ctx);
+    launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
+                            ctx->cap, ctx->d_ctr + rec_slot, st);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+  }
   u64 m[4];
   for (int s = 0; s < 4; ++s) m[s] = ctx->h->ctr[cnt_slot + 1 + s];
   const u64 s1 = m[0] + m[1] + m[2] + m[3];
@@ -1028,7 +1050,6 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     bool filtered = false;
     if (want_filter) {
       // ---- K3 + K4/K5 ran on the SPA candidates only (k_filter.cu).
-      const bool overflow = ctx->h->ctr[ovf_slot] != 0;
       D.n_candidates = (size_t)ctx->h->ncand;
       D.filter_log2nb = log2nb;
       D.spa_path = overflow ? 2 : 1;
