@@ -99,6 +99,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
+# the pipeline's kernels from the committed ncu --set full captures of this
+# workload (profiles/, tools/round_measure.sh); None when absent.
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "round1", "traffic.json")
+
+
+def measured_traffic(kernel_key: str):
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+        return t.get(kernel_key)
+    except Exception:
+        return None
+
+
 def cpu_baseline(pts: np.ndarray, steps: int = 3):
     """The reference CPU path (oracle/_ref) on this host; port if absent."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -281,7 +296,8 @@ def main():
         kernels = {
             "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n,
                             "basis": "16 B/pt read"},
-            "k2_classify_compact": {"ms": t["t_k2_ms"], "bytes": 16 * n + 16 * s1,
+            ("k2_classify_survivors" if d.spa_path == 1 else "k2_classify_compact"):
+                {"ms": t["t_k2_ms"], "bytes": 16 * n + 16 * s1,
                                     "basis": "16 B/pt read + 16 B/survivor write"},
         }
         if d.spa_path == 1:
@@ -294,20 +310,21 @@ def main():
                 "k3_filter": {"ms": t["t_filter_ms"], "bytes": 16 * s1 + 16 * nc,
                               "basis": "16 B/survivor read + 16 B/candidate write",
                               "candidates": nc},
-                "k3_bin_sort_big": {"ms": t["t_binsort_ms"]},
-                "k4_spa_bins": {"ms": t["t_spa_kernel_ms"],
+                "k3_bin_sort_compact": {"ms": t["t_binsort_ms"]},
+                "k4_spa_dense": {"ms": t["t_spa_kernel_ms"],
                                 "bytes": 16 * nc + 16 * sum(d.kept_counts),
                                 "basis": "16 B/candidate read + 16 B/kept write"},
             })
         else:
             pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)
             kernels.update({
-                "k3_hist": {"ms": t["t_hist_ms"], "bytes": 8 * s1},
+                "k3_hist": {"ms": t["t_hist_ms"], "bytes": 8 * s1, "basis": "8 B/record read"},
                 "k3_radix_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": 32 * s1,
                                   "basis": "16 B/record read + 16 B/record write"},
                 "k3_ties": {"ms": t["t_ties_ms"]},
                 "k4_spa": {"ms": t["t_spa_kernel_ms"], "bytes": 8 * s1 + 2 * s1
-                           + 16 * sum(d.kept_counts)},
+                           + 16 * sum(d.kept_counts),
+                           "basis": "8 B/record read + 16 B/kept write (+ flags)"},
             })
         for kv in kernels.values():
             if kv.get("bytes") and kv.get("ms"):
@@ -320,8 +337,8 @@ def main():
             "bound": "hbm", "kernel": dom_name,
             "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
             "peak_source": src, "frac": dom["gbs"] / hbm,
-            "traffic": None,
-            "algorithmic_bytes": f"{dom['basis']}: {dom['bytes']} B per launch",
+            "traffic": measured_traffic(dom_name),
+            "algorithmic_bytes": f"{dom.get('basis', 'bytes moved')}: {dom['bytes']} B per launch",
             "discard_kernels": {"kernels": "k_extremes_partial+final, k_classify_compact",
                                 "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
                                 "frac": disc_bytes / (disc_ms * 1e-3) / 1e9 / hbm,
