@@ -199,11 +199,13 @@ struct QuadEdges {
 // warp never diverges on the data; evaluating a predicate the reference would
 // have skipped has no effect on the result.
 __device__ __forceinline__ int classify(const QuadEdges& e, double px, double py) {
-  const bool r0 = cross_edge(e.ax[0], e.ay[0], e.ex[0], e.ey[0], px, py) < 0.0;
-  const bool r1 = cross_edge(e.ax[1], e.ay[1], e.ex[1], e.ey[1], px, py) < 0.0;
-  const bool r2 = cross_edge(e.ax[2], e.ay[2], e.ex[2], e.ey[2], px, py) < 0.0;
-  const bool r3 = cross_edge(e.ax[3], e.ay[3], e.ex[3], e.ey[3], px, py) < 0.0;
-  return r0 ? 1 : (r1 ? 2 : (r2 ? 3 : (r3 ? 4 : 0)));
+  // The four Right flags as a bit mask, the region as its lowest set bit:
+  // no select chain the compiler could turn into divergent early exits.
+  const u32 m = (u32)(cross_edge(e.ax[0], e.ay[0], e.ex[0], e.ey[0], px, py) < 0.0) |
+                (u32)(cross_edge(e.ax[1], e.ay[1], e.ex[1], e.ey[1], px, py) < 0.0) << 1 |
+                (u32)(cross_edge(e.ax[2], e.ay[2], e.ex[2], e.ey[2], px, py) < 0.0) << 2 |
+                (u32)(cross_edge(e.ax[3], e.ay[3], e.ex[3], e.ey[3], px, py) < 0.0) << 3;
+  return __ffs(m);  // 0 when no edge has the point on its right (Interior)
 }
 
 // Two-ended stream layout: streams 1 and 2 share kbuf[0, ncap) growing
@@ -391,10 +393,10 @@ __global__ __launch_bounds__(kK2Threads, 4) void k_classify_survivors(
   __shared__ int s_lex;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u64 tile_base = (u64)blockIdx.x * kK2Tile;
+  const u32 tile_base = blockIdx.x * kK2Tile;  // n < 2^32
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
-    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    const u32 idx = tile_base + j * kK2Threads + tid;
     const bool ok = idx < n;
     cp_async16(sbuf + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
   }
@@ -430,7 +432,7 @@ __global__ __launch_bounds__(kK2Threads, 4) void k_classify_survivors(
   u64 cnt = 0;          // 16-bit count per stream
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
-    const u64 idx = tile_base + (u64)j * kK2Threads + tid;
+    const u32 idx = tile_base + j * kK2Threads + tid;
     const double2 p = sbuf[j * kK2Threads + tid];
     int r = idx < n ? classify(e, p.x, p.y) : 0;
     if (lex && r != 0) r = 1;

@@ -168,7 +168,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
     const u32* __restrict__ digit_excl, int pass, u64* __restrict__ status, u32 tag,
-    u32* __restrict__ tile_ctr, u32 total_tiles, const u32* __restrict__ tile_prefix) {
+    u32* __restrict__ tile_ctr, u32 total_tiles, u32* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
@@ -263,14 +263,17 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   // row at once, so the look-back finds the nearest predecessor with a
   // prefix using one warp over 32 flags at a time and then reads the rows in
   // between with independent loads: a few round trips whatever the depth.
-  u32* agg = reinterpret_cast<u32*>(status + total_tiles);
+  // rows: kScan = the per-(tile, digit) offsets from k_colscan; onesweep =
+  // the published per-tile counts (agg) and inclusive prefixes (inc), raw
+  // words kept apart from the tagged status words
+  u32* agg = rows;
   u32* inc = agg + (size_t)total_tiles * kDigits;
   u32 before = 0;
   // Publication is the release pattern "row stores; bar.sync; one thread:
   // fence.acq_rel.gpu + flag store"; readers acquire the flag in one warp
   // and bar.sync before touching rows.
   if (kScan) {
-    before = tile_prefix[(size_t)tile * kDigits + b];
+    before = rows[(size_t)tile * kDigits + b];
   } else if (tile == sd.tile_begin) {
     __stcg(inc + (size_t)tile * kDigits + b, tile_cnt);
     __syncthreads();
@@ -562,7 +565,7 @@ template <int kMode, bool kScan>
 static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout,
                             const SegDesc* segs, int nseg, u32 total_tiles, int use_src,
                             const u32* digit_excl, int pass, u64* status, u32 tag, u32* tile_ctr,
-                            const u32* tile_prefix, cudaStream_t st) {
+                            u32* rows, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_onesweep<kMode, kScan>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -571,25 +574,25 @@ static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout
   }
   k_onesweep<kMode, kScan><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
       kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr,
-      total_tiles, tile_prefix);
+      total_tiles, rows);
 }
 
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
-                     int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st) {
+                     int pass, u64* status, u32 tag, u32* tile_ctr, u32* rows, cudaStream_t st) {
   if (total_tiles == 0) return;
   switch (mode) {
     case kDigitQ:
       onesweep_launch<kDigitQ, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
-                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
+                                      digit_excl, pass, status, tag, tile_ctr, rows, st);
       break;
     case kDigitV:
       onesweep_launch<kDigitV, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
-                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
+                                      digit_excl, pass, status, tag, tile_ctr, rows, st);
       break;
     default:
       onesweep_launch<kDigitK, false>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src,
-                                      digit_excl, pass, status, tag, tile_ctr, nullptr, st);
+                                      digit_excl, pass, status, tag, tile_ctr, rows, st);
   }
 }
 

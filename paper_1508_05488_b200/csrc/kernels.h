@@ -114,7 +114,7 @@ void launch_lsd_pass(const u64* kin, const u64* vin, u64* kout, u64* vout, const
                      int pass, u32* counts, cudaStream_t st);
 void launch_onesweep(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, int mode, const u32* digit_excl,
-                     int pass, u64* status, u32 tag, u32* tile_ctr, cudaStream_t st);
+                     int pass, u64* status, u32 tag, u32* tile_ctr, u32* rows, cudaStream_t st);
 void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const SegDesc* segs,
                      int nseg, u32 total_tiles, int use_src, cudaStream_t st);
 void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,

@@ -68,7 +68,9 @@ struct chgpu_ctx {
   u64* d_va = nullptr;          // cap
   unsigned char* d_flags = nullptr;  // cap
   double2* d_kept = nullptr;    // cap
-  u64* d_status = nullptr;      // look-back status words
+  u64* d_status = nullptr;      // tagged look-back status words, nothing else
+  u32* d_raw = nullptr;         // raw per-tile / per-chunk scratch (never tagged)
+  size_t raw_words = 0;
   size_t status_words = 0;
   u64* d_starts = nullptr;      // group starts (cap/2+16)
   void* d_medium = nullptr;     // medium groups (cap/2+16)
@@ -172,6 +174,7 @@ void free_ws(chgpu_ctx* c) {
   cudaFree(c->d_ck);
   cudaFree(c->d_cv);
   cudaFree(c->d_status);
+  cudaFree(c->d_raw);
   cudaFree(c->d_starts);
   cudaFree(c->d_medium);
   cudaFree(c->d_long);
@@ -181,6 +184,7 @@ void free_ws(chgpu_ctx* c) {
   c->d_kept = nullptr;
   c->d_ck = c->d_cv = nullptr;
   c->d_status = nullptr;
+  c->d_raw = nullptr;
   c->d_starts = nullptr;
   c->d_medium = c->d_long = nullptr;
   c->cap = 0;
@@ -226,13 +230,17 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
   CK(cudaMalloc(&ctx->d_kept, cap * sizeof(double2)));
   CK(cudaMalloc(&ctx->d_ck, cap * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_cv, cap * sizeof(u64)));
-  // Status words: K2 needs 4 per 2048-point tile, a sort pass 256 per
-  // 4096-record tile (+1 tile per segment), the SPA one per chunk (<= cap).
-  ctx->status_words = std::max(cap + 4096, (cap / kSortTile + 4096) * (size_t)kDigits);
+  // Tagged status words only (a raw value there could decode as a live word
+  // of a later look-back): one per sort tile, unique tile or SPA chunk.
+  ctx->status_words = cap + 4096;
   CK(cudaMalloc(&ctx->d_status, ctx->status_words * sizeof(u64)));
   // Ordered on the context stream: a stale word from recycled memory must
   // never be mistaken for a current one.
   CK(cudaMemsetAsync(ctx->d_status, 0, ctx->status_words * sizeof(u64), ctx->st));
+  // Raw scratch: onesweep agg + inc rows (2 x 256 per tile), LSD tile
+  // counts, SPA per-chunk counts and offsets (2 per chunk, chunks <= cap).
+  ctx->raw_words = std::max((cap / kSortTile + 4096) * 2 * (size_t)kDigits, 2 * cap + 64);
+  CK(cudaMalloc(&ctx->d_raw, ctx->raw_words * sizeof(u32)));
   CK(cudaMalloc(&ctx->d_starts, (cap / 2 + 16) * sizeof(u64)));
   CK(cudaMalloc(&ctx->d_medium, (cap / 2 + 16) * group_run_bytes()));
   CK(cudaMalloc(&ctx->d_long, (cap / 2049 + 16) * group_run_bytes()));
@@ -364,12 +372,12 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
     if (lsd_scan_passes() && nseg <= 64) {
       // reduce-then-scan: no inter-tile waiting (3 launches per pass)
       launch_lsd_pass(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode,
-                      ctx->d_digit_excl, p, reinterpret_cast<u32*>(ctx->d_status), ctx->st);
+                      ctx->d_digit_excl, p, ctx->d_raw, ctx->st);
       ctx->launches += 2;
     } else {
       launch_onesweep(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode,
                       ctx->d_digit_excl, p, ctx->d_status, next_tag(ctx),
-                      ctx->d_ctr + take_ctr(ctx), ctx->st);
+                      ctx->d_ctr + take_ctr(ctx), ctx->d_raw, ctx->st);
     }
     kin = ko;
     vin = vo;
@@ -729,7 +737,7 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
 // d_kept (region order) and per-region counts in d_u64[0..3]. The input
 // copy d_pts is dead by now and serves as the per-chunk scratch.
 int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
-  u32* chunk_kept = reinterpret_cast<u32*>(ctx->d_status);
+  u32* chunk_kept = ctx->d_raw;
   u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
   SpaPlan* d_splan = &ctx->d_plan->spa;
   TRY(upload(ctx, d_splan, &plan, sizeof(SpaPlan)));

@@ -155,3 +155,24 @@ def test_convex_fast_path(gpu_ctx, product, oracle, case):
             assert r.diag.convex_fast_path
         if case in ("duplicates", "square_edges"):
             assert not r.diag.convex_fast_path
+
+
+def test_paths_interleaved_on_one_context(product):
+    """One context alternating the full-sort and the pre-filtered paths (and
+    the degenerate branch) over the acceptance sweep: every look-back of one
+    path must ignore whatever the other left in the context's scratch."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = product.Context(0)
+    modes = [product.SPA_SORT, product.SPA_FILTER]
+    i = 0
+    for case in load_golden("pipeline_sweep.json"):
+        pts = product.generate(case["dist"], case["n"], case["seed"])
+        for run in case["runs"]:
+            ctx.set_spa_path(modes[i % 2])
+            i += 1
+            r = ctx.convex_hull(pts, product.PipelineConfig(chunk_count=run["chunk_count"]))
+            assert _counts(r) == run["counts"], (case["dist"], case["n"], run)
+            assert sha(r.hull.vertices) == run["hull_sha"]
+    ctx.close()
