@@ -40,7 +40,10 @@ typedef enum {
   CHGPU_INVALID_ARG = 3, /* std::invalid_argument (spa.cpp:112, region_less/sort_region) */
   CHGPU_CUDA_ERR = 4,    /* CUDA runtime failure; see chgpu_last_error */
   CHGPU_NO_DEVICE = 5,   /* no CUDA device: the product never falls back to the CPU */
-  CHGPU_TOO_LARGE = 6    /* n >= 2^32 points in one call (shard the input) */
+  CHGPU_TOO_LARGE = 6,   /* n >= 2^32 points in one call (shard the input) */
+  CHGPU_IO_ERROR = 7,    /* IoError (io.cpp open_input): unreadable file */
+  CHGPU_PARSE_ERROR = 8, /* ParseError (io.cpp:105-106): not whole float64 pairs */
+  CHGPU_NONFINITE = 9    /* NonFiniteCoordinate (io.cpp:38-42) */
 } chgpu_status;
 
 /* Layout-identical to chainhull::StageStats (pipeline.hpp:30-42). */
@@ -124,6 +127,17 @@ int chgpu_reserve(chgpu_ctx* ctx, size_t n);
 int chgpu_hull(chgpu_ctx* ctx, const double* xy, size_t n, size_t chunk_count,
                int degenerate_fallback, const double** hull_xy, size_t* n_hull,
                chgpu_stats* stats, chgpu_diag* diag);
+
+/* read_points(path, PointFormat::XyBinary) (io.hpp:29-36) followed by
+ * convex_hull, fused: the file's bytes (little-endian float64 pairs, the
+ * layout of Point2[]) are read in 32 MB chunks by parallel preads into a
+ * pinned ring, each chunk's host->device copy and extremes pass overlapping
+ * the next read. Errors in the reference's order: CHGPU_IO_ERROR,
+ * CHGPU_PARSE_ERROR (size not a multiple of 16), CHGPU_NONFINITE, then the
+ * convex_hull statuses (CHGPU_EMPTY for an empty file). */
+int chgpu_hull_xy_binary(chgpu_ctx* ctx, const char* path, size_t chunk_count,
+                         int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+                         chgpu_stats* stats, chgpu_diag* diag);
 
 /* Same, with xy already resident in device memory (16-byte aligned). */
 int chgpu_hull_device(chgpu_ctx* ctx, const double* d_xy, size_t n, size_t chunk_count,

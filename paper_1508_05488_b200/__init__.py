@@ -34,6 +34,7 @@ DISTRIBUTIONS = ["uniform_square", "uniform_disk", "circle", "gaussian", "collin
 
 CHGPU_OK, CHGPU_EMPTY, CHGPU_DEGENERATE, CHGPU_INVALID_ARG = 0, 1, 2, 3
 CHGPU_CUDA_ERR, CHGPU_NO_DEVICE, CHGPU_TOO_LARGE = 4, 5, 6
+CHGPU_IO_ERROR, CHGPU_PARSE_ERROR, CHGPU_NONFINITE = 7, 8, 9
 
 
 class Error(RuntimeError):
@@ -42,6 +43,19 @@ class Error(RuntimeError):
 
 class EmptyInput(Error):
     """chainhull::EmptyInput (errors.hpp:15)."""
+
+
+class IoError(Error):
+    """errors.hpp:42-44."""
+
+
+class ParseError(Error):
+    """errors.hpp:27-35 (binary payload errors carry line 0)."""
+    line = 0
+
+
+class NonFiniteCoordinate(Error):
+    """errors.hpp:37-40."""
 
 
 class DegenerateInput(Error):
@@ -173,6 +187,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                      C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_hull.argtypes = hull_args
         L.chgpu_hull_device.argtypes = hull_args
+        L.chgpu_hull_xy_binary.argtypes = [vp, C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
+                                           C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_find_extremes.argtypes = [vp, _dp, C.c_size_t, _dp]
         L.chgpu_classify.argtypes = [vp, _dp, C.c_size_t, _dp, C.POINTER(C.c_uint8), _sz]
         L.chgpu_discard_round1.argtypes = [vp, _dp, C.POINTER(C.c_uint8), C.c_size_t, _dp,
@@ -214,6 +230,12 @@ def _raise(status: int, msg: str):
         raise DegenerateInput(msg)
     if status == CHGPU_INVALID_ARG:
         raise ValueError(msg)
+    if status == CHGPU_IO_ERROR:
+        raise IoError(msg)
+    if status == CHGPU_PARSE_ERROR:
+        raise ParseError(msg)
+    if status == CHGPU_NONFINITE:
+        raise NonFiniteCoordinate(msg)
     raise Error(f"chgpu status {status}: {msg}")
 
 
@@ -289,6 +311,26 @@ class Context:
         if n == 0:
             raise EmptyInput("convex_hull: no points")
         return self._hull(self.lib.chgpu_hull_device, C.c_void_p(ptr), n, config, copy)
+
+    def hull_xy_binary(self, path, config: PipelineConfig | None = None,
+                       copy: bool = True) -> HullResult:
+        """read_points(path, xy_binary) + convex_hull (io.hpp:29-36,
+        pipeline.hpp:55) fused: the file streams through pinned staging
+        into the device pipeline."""
+        config = config or PipelineConfig()
+        out = _dp()
+        k = C.c_size_t()
+        s = _Stats()
+        d = _Diag()
+        st = self.lib.chgpu_hull_xy_binary(self.h, os.fsencode(path), config.chunk_count,
+                                           int(bool(config.degenerate_fallback)), C.byref(out),
+                                           C.byref(k), C.byref(s), C.byref(d))
+        self._check(st)
+        verts = np.ctypeslib.as_array(out, shape=(k.value * 2,)).reshape(-1, 2) \
+            if k.value else np.empty((0, 2))
+        if copy:
+            verts = verts.copy()
+        return HullResult(Hull(verts), StageStats._from(s), Diag._from(d))
 
     # ---- stage taps -----------------------------------------------------
     def find_extremes(self, points) -> np.ndarray:

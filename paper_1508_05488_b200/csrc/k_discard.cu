@@ -136,11 +136,17 @@ __device__ void merge_partials_block(const QuadCand* __restrict__ partials, int 
 // ticket counter, the last block to finish (over every launch of the call:
 // total_parts blocks) merges all partials itself, so no final launch is
 // needed.
+//
+// kCheck (file ingestion): also flags any non-finite coordinate
+// (io.cpp:38-42 require_finite; the reference rejects them before hulling).
+template <bool kCheck>
 __global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(
     const double2* __restrict__ pts, u64 n, u64 base_index, QuadCand* __restrict__ partials,
-    u32 part_base, u32* __restrict__ ticket, u32 total_parts, QuadInfo* __restrict__ out) {
+    u32 part_base, u32* __restrict__ ticket, u32 total_parts, QuadInfo* __restrict__ out,
+    u32* __restrict__ nonfinite) {
   QuadCand acc;
   empty_quad(acc);
+  bool finite = true;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
@@ -148,12 +154,17 @@ __global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(
 #pragma unroll
     for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
+    for (int u = 0; u < kK1Unroll; ++u) {
+      if (kCheck) finite &= isfinite(p[u].x) && isfinite(p[u].y);
+      fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
+    }
   }
   for (; i < n; i += stride) {
     const double2 p = ldg_stream(pts + i);
+    if (kCheck) finite &= isfinite(p.x) && isfinite(p.y);
     fold_point(acc, p.x, p.y, base_index + i);
   }
+  if (kCheck && !__all_sync(0xffffffffu, finite) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     QuadCand other;
@@ -538,7 +549,7 @@ int extremes_blocks(int requested) {
   static int wave = 0;
   if (!wave) {
     int occ = 0, sms = 0, dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_extremes_partial, kK1Threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_extremes_partial<true>, kK1Threads, 0);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     wave = std::max(1, occ) * std::max(1, sms);
@@ -548,10 +559,14 @@ int extremes_blocks(int requested) {
 
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
                             int blocks, cudaStream_t st, u32 part_base, u32* ticket,
-                            u32 total_parts, QuadInfo* out) {
+                            u32 total_parts, QuadInfo* out, u32* nonfinite) {
   blocks = extremes_blocks(blocks);
-  k_extremes_partial<<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base, ticket,
-                                                    total_parts, out);
+  if (nonfinite)
+    k_extremes_partial<true><<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base,
+                                                            ticket, total_parts, out, nonfinite);
+  else
+    k_extremes_partial<false><<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base,
+                                                             ticket, total_parts, out, nullptr);
   return blocks;
 }
 

@@ -86,7 +86,8 @@ int extremes_blocks(int requested);
 // last block merges every partial into *out: no launch_extremes_final.
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
                             int blocks, cudaStream_t st, u32 part_base = 0,
-                            u32* ticket = nullptr, u32 total_parts = 0, QuadInfo* out = nullptr);
+                            u32* ticket = nullptr, u32 total_parts = 0, QuadInfo* out = nullptr,
+                            u32* nonfinite = nullptr);
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, QuadCand* raw_out,
                            cudaStream_t st);
 // K2

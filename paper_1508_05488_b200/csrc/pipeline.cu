@@ -10,8 +10,13 @@
 
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -32,6 +37,7 @@ namespace {
 constexpr int kMaxPartials = 148 * 8 * 16;
 constexpr int kPartialBlocks = 148 * 8;
 constexpr size_t kH2DChunk = size_t(1) << 21;  // points per staged copy (32 MB)
+constexpr size_t kFileSlots = 4;               // pinned file-ingestion chunks in flight
 constexpr int kCtrSlots = 256;                 // u32 counters, cleared once per call
 
 struct Pinned {
@@ -110,6 +116,8 @@ struct chgpu_ctx {
   // host buffer can be rewritten while earlier copies are still queued.
   unsigned char* h_stage = nullptr;
   size_t stage_cap = 0, stage_used = 0;
+  // File ingestion (chgpu_hull_xy_binary): pinned ring of kFileSlots chunks.
+  double2* h_fslots = nullptr;
 
   Pinned* h = nullptr;
   SegDesc* h_segs = nullptr;
@@ -896,9 +904,66 @@ int begin_call(chgpu_ctx* ctx) {
 
 // Core of chgpu_hull / chgpu_hull_device. h_src != nullptr: the input is on
 // the host and is staged in chunks on a copy stream, overlapped with K1.
+// Copies bytes [off, off + len) of the source into dst with up to
+// `threads` parallel workers: pread from fd (>= 0), else memcpy from the
+// pageable host array src (page-cache reads and pageable copies are
+// memcpy-bound on one core). false on a read error.
+bool stage_bytes(int fd, const unsigned char* src, unsigned char* dst, size_t off, size_t len,
+                 int threads) {
+  auto part = [&](size_t a, size_t b, bool* ok) {
+    if (fd < 0) {
+      std::memcpy(dst + (a - off), src + a, b - a);
+      *ok = true;
+      return;
+    }
+    while (a < b) {
+      const ssize_t r = pread(fd, dst + (a - off), b - a, (off_t)a);
+      if (r <= 0) {
+        *ok = false;
+        return;
+      }
+      a += (size_t)r;
+    }
+    *ok = true;
+  };
+  if (threads <= 1 || len < (size_t(4) << 20)) {
+    bool ok = false;
+    part(off, off + len, &ok);
+    return ok;
+  }
+  std::vector<std::thread> th;
+  std::vector<char> oks(threads, 0);
+  const size_t step = ((len + threads - 1) / threads + 4095) & ~size_t(4095);
+  for (int t = 1; t < threads; ++t) {
+    const size_t a = off + t * step, b = std::min(off + len, a + step);
+    if (a >= b) {
+      oks[t] = 1;
+      continue;
+    }
+    th.emplace_back([&, a, b, t] {
+      bool ok = false;
+      part(a, b, &ok);
+      oks[t] = ok;
+    });
+  }
+  bool ok0 = false;
+  part(off, std::min(off + len, off + step), &ok0);
+  for (auto& x : th) x.join();
+  oks[0] = ok0;
+  for (char o : oks)
+    if (!o) return false;
+  return true;
+}
+
+// Core of chgpu_hull / chgpu_hull_device / chgpu_hull_xy_binary. h_src !=
+// nullptr: the input is on the host and is staged in chunks on a copy
+// stream, overlapped with K1; fd >= 0: the input is read from a file
+// (xy_binary: the bytes of Point2[]) chunk by chunk into a pinned ring,
+// each chunk's copy and K1 overlapping the next chunk's read, and K1 also
+// checks finiteness (io.cpp:38-42).
 int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, size_t n,
                  size_t chunk_count, int fallback, const double** hull_xy, size_t* n_hull,
-                 chgpu_stats* stats, chgpu_diag* diag) {
+                 chgpu_stats* stats, chgpu_diag* diag, int fd = -1) {
   const auto t_wall0 = std::chrono::steady_clock::now();
   chgpu_stats S{};
   chgpu_diag D{};
@@ -909,7 +974,19 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
 
   // ---- K1: extremes (extremes.cpp:28-47).
   int nparts = 0;
+  const bool from_file = fd >= 0;
+  int nonfinite_slot = -1;
+  // Pageable host input goes through the pinned ring too (a copy engine
+  // reads pageable memory at a fraction of PCIe speed).
+  bool pageable = false;
   if (h_src) {
+    cudaPointerAttributes attr{};
+    pageable = cudaPointerGetAttributes(&attr, h_src) != cudaSuccess ||
+               attr.type == cudaMemoryTypeUnregistered;
+    cudaGetLastError();  // clear a non-sticky "invalid value" for unknown pointers
+  }
+  const bool staged = from_file || pageable;
+  if (h_src || from_file) {
     const size_t nchunks = (n + kH2DChunk - 1) / kH2DChunk;
     const int per = std::max(1, std::min(kPartialBlocks, kMaxPartials / (int)nchunks));
     if (ctx->ev_copy.size() < nchunks) {
@@ -927,16 +1004,34 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       total_parts += (u32)extremes_blocks((int)std::min<size_t>(per, (cnt + 255) / 256));
     }
     const int ticket = take_ctr(ctx);
+    if (from_file) nonfinite_slot = take_ctr(ctx);
+    if (staged && !ctx->h_fslots)
+      CK(cudaMallocHost(&ctx->h_fslots, kFileSlots * kH2DChunk * sizeof(double2)));
+    static const int readers = std::max(1, std::min(8, (int)std::thread::hardware_concurrency()));
     for (size_t c = 0; c < nchunks; ++c) {
       const size_t off = c * kH2DChunk, cnt = std::min(kH2DChunk, n - off);
-      CK(cudaMemcpyAsync(ctx->d_pts + off, h_src + 2 * off, cnt * sizeof(double2),
+      const double* src = h_src ? h_src + 2 * off : nullptr;
+      if (staged) {
+        // the slot's previous chunk must have reached the device
+        if (c >= kFileSlots) CK(cudaEventSynchronize(ctx->ev_copy[c - kFileSlots]));
+        double2* slot = ctx->h_fslots + (c % kFileSlots) * kH2DChunk;
+        if (!stage_bytes(fd, reinterpret_cast<const unsigned char*>(h_src),
+                         reinterpret_cast<unsigned char*>(slot), off * sizeof(double2),
+                         cnt * sizeof(double2), readers)) {
+          sync(ctx);
+          return fail(ctx, CHGPU_IO_ERROR, "cannot read the xy_binary input");
+        }
+        src = reinterpret_cast<const double*>(slot);
+      }
+      CK(cudaMemcpyAsync(ctx->d_pts + off, src, cnt * sizeof(double2),
                          cudaMemcpyHostToDevice, ctx->st_copy));
       CK(cudaEventRecord(ctx->ev_copy[c], ctx->st_copy));
       CK(cudaStreamWaitEvent(st, ctx->ev_copy[c], 0));
       const int blocks = (int)std::min<size_t>(per, (cnt + 255) / 256);
       nparts += launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials, blocks, st,
                                         (u32)nparts, ctx->d_ctr + ticket, total_parts,
-                                        ctx->d_qinfo);
+                                        ctx->d_qinfo,
+                                        from_file ? ctx->d_ctr + nonfinite_slot : nullptr);
       ++ctx->launches;
     }
     CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
@@ -948,7 +1043,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
                                      ctx->d_qinfo);
     ++ctx->launches;
   }
-  const double2* pts = h_src ? ctx->d_pts : pts_dev;
+  const double2* pts = (h_src || from_file) ? ctx->d_pts : pts_dev;
   CK(cudaEventRecord(ctx->ev[1], st));
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
@@ -999,7 +1094,13 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));
+  if (from_file)
+    CK(cudaMemcpyAsync(&ctx->h->ctr[nonfinite_slot], ctx->d_ctr + nonfinite_slot, sizeof(u32),
+                       cudaMemcpyDeviceToHost, st));
   TRY(sync(ctx));
+  // read_points rejects the file before convex_hull runs (io.cpp:38-42)
+  if (from_file && ctx->h->ctr[nonfinite_slot])
+    return fail(ctx, CHGPU_NONFINITE, "non-finite coordinate");
 
   const QuadInfo qi = ctx->h->qi;
   const bool overflow = want_filter && !qi.degenerate && ctx->h->ctr[ovf_slot] != 0;
@@ -1167,7 +1268,7 @@ finished:
   S.t_total_ms = std::chrono::duration<double, std::milli>(t_end - t_wall0).count();
   D.t_k1_ms = S.t_extremes_ms;
   D.t_k2_ms = S.t_classify_ms;
-  if (h_src) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
+  if (h_src || from_file) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
   D.launches = ctx->launches;
 
   *hull_xy = reinterpret_cast<const double*>(ctx->hull_ptr);
@@ -1279,6 +1380,7 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFreeHost(ctx->h_segs);
   cudaFreeHost(ctx->h_out);
   cudaFreeHost(ctx->h_stage);
+  cudaFreeHost(ctx->h_fslots);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->ev_copy) cudaEventDestroy(e);
@@ -1319,6 +1421,39 @@ int chgpu_hull(chgpu_ctx* ctx, const double* xy, size_t n, size_t chunk_count,
   TRY(ensure_cap(ctx, n));
   return run_pipeline(ctx, xy, nullptr, n, chunk_count, degenerate_fallback, hull_xy, n_hull, stats,
                       diag);
+}
+
+int chgpu_hull_xy_binary(chgpu_ctx* ctx, const char* path, size_t chunk_count,
+                         int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+                         chgpu_stats* stats, chgpu_diag* diag) {
+  *n_hull = 0;
+  const int fd = open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0)
+    return fail(ctx, CHGPU_IO_ERROR, (std::string("cannot open '") + path + "' for reading").c_str());
+  struct stat sb;
+  if (fstat(fd, &sb) != 0) {
+    close(fd);
+    return fail(ctx, CHGPU_IO_ERROR, "cannot stat the xy_binary input");
+  }
+  const size_t bytes = (size_t)sb.st_size;
+  int st = CHGPU_OK;
+  if (bytes % 16 != 0) {  // io.cpp:105-106
+    st = fail(ctx, CHGPU_PARSE_ERROR,
+              "parse error: binary payload is not a whole number of float64 pairs");
+  } else if (bytes == 0) {
+    st = fail(ctx, CHGPU_EMPTY, "convex_hull: no points");
+  } else if (bytes / 16 >= (size_t(1) << 32)) {
+    st = fail(ctx, CHGPU_TOO_LARGE, "more than 2^32-1 points per call");
+  } else {
+    cudaSetDevice(ctx->device);
+    const size_t n = bytes / 16;
+    st = ensure_cap(ctx, n);
+    if (st == CHGPU_OK)
+      st = run_pipeline(ctx, nullptr, nullptr, n, chunk_count, degenerate_fallback, hull_xy, n_hull,
+                        stats, diag, fd);
+  }
+  close(fd);
+  return st;
 }
 
 int chgpu_hull_device(chgpu_ctx* ctx, const double* d_xy, size_t n, size_t chunk_count,
