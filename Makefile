@@ -37,7 +37,7 @@ API_SRCS := $(wildcard $(PKG)/cpp/*.cpp)
 API_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(BUILD)/api_%.o,$(API_SRCS))
 API_HDRS := $(wildcard include/chainhull/*.hpp)
 
-all: $(PKG)/libchgpu.so $(PKG)/libchainhull.so acceptance
+all: $(PKG)/libchgpu.so $(PKG)/libchainhull.so acceptance $(BUILD)/io_probe_b200
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -66,6 +66,11 @@ else
 acceptance:
 	@echo "acceptance: /root/reference absent; using prebuilt build/acceptance_b200 if any"
 endif
+
+# I/O parity probe against the drop-in (tests/test_io_parity.py).
+$(BUILD)/io_probe_b200: tests/io_probe.cpp $(PKG)/libchainhull.so $(API_HDRS)
+	$(CXX) -O2 -std=gnu++20 -ffp-contract=off -Iinclude -o $@ $< \
+	  -L$(PKG) -lchainhull -lchgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)' -lpthread
 
 sass: $(PKG)/libchgpu.so
 	/usr/local/cuda/bin/cuobjdump -sass $< > $(BUILD)/libchgpu.sass

@@ -1007,7 +1007,11 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     if (from_file) nonfinite_slot = take_ctr(ctx);
     if (staged && !ctx->h_fslots)
       CK(cudaMallocHost(&ctx->h_fslots, kFileSlots * kH2DChunk * sizeof(double2)));
-    static const int readers = std::max(1, std::min(8, (int)std::thread::hardware_concurrency()));
+    static const int readers = [] {
+      const char* e = std::getenv("CHGPU_STAGE_THREADS");  // tuning knob
+      const int hw = (int)std::thread::hardware_concurrency();
+      return std::max(1, e ? std::atoi(e) : std::min(16, hw));
+    }();
     for (size_t c = 0; c < nchunks; ++c) {
       const size_t off = c * kH2DChunk, cnt = std::min(kH2DChunk, n - off);
       const double* src = h_src ? h_src + 2 * off : nullptr;
