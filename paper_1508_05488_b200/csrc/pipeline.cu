@@ -1679,11 +1679,43 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
   TRY(begin_call(ctx));
   TRY(upload_quad(ctx, quad));
   const bool degenerate = ctx->h->qi.degenerate != 0;
+  const double2* pts = reinterpret_cast<const double2*>(d_xy);
+  if (!degenerate && chunk_count >= 1 && ctx->spa_mode != CHGPU_SPA_SORT &&
+      (ctx->spa_mode == CHGPU_SPA_FILTER || chunk_count <= n / 64)) {
+    // The pre-filtered SPA against the global quad (the same kernels as
+    // chgpu_hull), falling back to the full region sort on overflow.
+    const int log2nb = filter_bits(n, chunk_count);
+    CK(cudaMemsetAsync(ctx->d_ftab, 0, (size_t(4) << log2nb) * 16, st));
+    const FilterTabs ftabs = filter_tabs(ctx, log2nb);
+    const int cnt_slot = ctx->ctr_used;
+    ctx->ctr_used += 5;
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->cap,
+                              reinterpret_cast<double2*>(ctx->d_kbuf),
+                              reinterpret_cast<double2*>(ctx->d_vbuf), ctx->d_kbuf, ctx->d_vbuf,
+                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
+    CK(cudaGetLastError());
+    int ovf_slot = -1;
+    TRY(enqueue_filter_spa(ctx, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
+    CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
+                       cudaMemcpyDeviceToHost, st));
+    TRY(sync(ctx));
+    if (!ctx->h->ctr[ovf_slot]) {
+      for (int r = 0; r < 4; ++r) kept_counts[r] = (size_t)ctx->h->kept[r];
+      const size_t total = kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3];
+      TRY(ensure_host_out(ctx, total + 4));
+      CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, total * sizeof(double2),
+                         cudaMemcpyDeviceToHost, st));
+      TRY(sync(ctx));
+      *chains_xy = reinterpret_cast<const double*>(ctx->h_out);
+      return CHGPU_OK;
+    }
+  }
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
-  launch_classify_compact(reinterpret_cast<const double2*>(d_xy), (u32)n, ctx->d_qinfo, nullptr,
-                          degenerate ? 1 : 0, ctx->d_kbuf, ctx->d_vbuf, ctx->cap,
-                          ctx->d_ctr + cnt_slot, st);
+  launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, degenerate ? 1 : 0, ctx->d_kbuf,
+                          ctx->d_vbuf, ctx->cap, ctx->d_ctr + cnt_slot, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
                      cudaMemcpyDeviceToHost, st));

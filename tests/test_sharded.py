@@ -124,7 +124,7 @@ def test_fold_extremes_python_and_c_agree(product):
         assert np.array_equal(out.reshape(4, 2), want)
 
 
-def _gpu_worker(rank, world, port, results):
+def _gpu_worker(rank, world, port, results, mode=0):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -134,6 +134,7 @@ def _gpu_worker(rank, world, port, results):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     ctx = P.Context(0)
+    ctx.set_spa_path(mode)
     for i, (dist_name, n, seed) in enumerate(DATASETS):
         pts = P.generate(dist_name, n, seed)
         bounds = np.linspace(0, n, world + 1).astype(int)
@@ -149,7 +150,8 @@ def _gpu_worker(rank, world, port, results):
 
 
 @pytest.mark.gpu
-def test_sharded_hull_gpu_ranks(oracle):
+@pytest.mark.parametrize("mode", [0, 1, 2])  # SPA_AUTO, SPA_SORT, SPA_FILTER
+def test_sharded_hull_gpu_ranks(oracle, mode):
     """Two ranks sharing cuda:0 (gloo carries the exchange): the GPU shard
     entry points (chgpu_shard_extremes / chgpu_shard_chains) + merge."""
     import torch
@@ -158,7 +160,7 @@ def test_sharded_hull_gpu_ranks(oracle):
     mgr = mp.Manager()
     results = mgr.dict()
     port = _free_port()
-    mp.spawn(_gpu_worker, args=(2, port, results), nprocs=2, join=True)
+    mp.spawn(_gpu_worker, args=(2, port, results, mode), nprocs=2, join=True)
     for i, (dist_name, n, seed) in enumerate(DATASETS):
         pts = oracle.generate(dist_name, n, seed)
         want = oracle.convex_hull(pts, 1024)
