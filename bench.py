@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--chunk-count", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="exchange backend for N > 1 (gloo: testing several ranks on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,9 +208,13 @@ def main():
     import paper_1508_05488_b200 as P
     from paper_1508_05488_b200.sharded import GpuShardOps, sharded_convex_hull
 
+    local = local % max(1, torch.cuda.device_count())  # gloo testing: ranks may share a GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     ctx = P.Context(local)
     cfg = P.PipelineConfig(chunk_count=args.chunk_count)
 
@@ -253,7 +259,8 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([ms], dtype=torch.float64,
+                             device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, out
