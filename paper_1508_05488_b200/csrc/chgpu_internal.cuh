@@ -72,6 +72,12 @@ __host__ __device__ __forceinline__ u64 ord_enc(double d) {
   const u64 b = dbits(d);
   return b ^ ((u64)((long long)b >> 63) | 0x8000000000000000ull);
 }
+// ord_enc with -0.0 folded onto +0.0 (== does not tell them apart), in
+// integer ops only (the same bits as ord_enc(d + 0.0)).
+__host__ __device__ __forceinline__ u64 ord_enc_z(double d) {
+  const u64 e = ord_enc(d);
+  return e == 0x7FFFFFFFFFFFFFFFull ? 0x8000000000000000ull : e;
+}
 __host__ __device__ __forceinline__ double ord_dec(u64 u) {
   return bitsd(u ^ ((u >> 63) ? 0x8000000000000000ull : 0xFFFFFFFFFFFFFFFFull));
 }
@@ -129,17 +135,14 @@ __host__ __device__ __forceinline__ bool rec_less(int region, u64 ka, u64 va, u6
 // ---------------------------------------------------------------- SPA bins
 //
 // The SPA pre-filter (k_filter.cu) groups each region's records into bins
-// of its primary coordinate. bin() is a monotone map onto [0, nb) in the
-// region's sort direction (subtract, multiply by a positive constant,
-// clamp, truncate: all monotone in round-to-nearest), so a region's sorted
-// sequence visits its bins in increasing order and every bin is one
-// contiguous run of it. The geometry depends only on the quad, so the
-// classify kernel (which counts records per bin) and the filter kernel
-// (which re-derives each record's bin from its primary) agree bit for bit.
-struct BinGeom {
-  double lo[4], scale[4], top;  // top = nb - 1
-  int log2nb;
-};
+// of its primary coordinate. The bin is a monotone map onto [0, nb) in the
+// region's sort direction (subtract, multiply by positive constants, one of
+// them a power of two, clamp, truncate: all monotone in round-to-nearest),
+// so a region's sorted sequence visits its bins in increasing order and
+// every bin is one contiguous run of it. The map's constants live in
+// QuadInfo (quad_derive, computed once per call), so the classify kernel
+// (which counts records per bin) and the filter kernel (which re-derives
+// each record's bin from its primary) agree bit for bit.
 
 // Primary range of region r (1..4) between its anchors: LL x in
 // [left.x, bottom.x], LR y in [bottom.y, right.y], UR x in [top.x, right.x],
@@ -151,31 +154,6 @@ __host__ __device__ __forceinline__ void bin_range(const double* q, int r, doubl
     case 3: *lo = q[6]; *hi = q[4]; break;
     default: *lo = q[1]; *hi = q[7]; break;
   }
-}
-
-__device__ __forceinline__ void make_bin_geom(const double* q, int log2nb, BinGeom* g) {
-  g->log2nb = log2nb;
-  const double nb = (double)(1u << log2nb);
-  g->top = nb - 1.0;
-  for (int r = 1; r <= 4; ++r) {
-    double lo, hi;
-    bin_range(q, r, &lo, &hi);
-    const double span = __dsub_rn(hi, lo);
-    double s = span > 0.0 ? __ddiv_rn(nb, span) : 0.0;
-    if (!(s < 1e300)) s = 0.0;  // inf / nan (denormal spans)
-    g->lo[r - 1] = lo;
-    g->scale[r - 1] = s;
-  }
-}
-
-// Bin of a record of region r (1..4) with primary coordinate p. The
-// float->int conversion saturates (negative and NaN -> 0), then the top
-// clamps: trunc(clamp(t, 0, top)) in two integer instructions.
-__device__ __forceinline__ u32 bin_of(const BinGeom& g, int r, double p) {
-  const double t = __dmul_rn(__dsub_rn(p, g.lo[r - 1]), g.scale[r - 1]);
-  const u32 top = (u32)g.top;
-  const u32 b = min((u32)__double2uint_rz(t), top);
-  return (r >= 3) ? top - b : b;  // UR / UL sort descending
 }
 
 // The record word v of region r (1..4) for point (x, y) (key codec above).
@@ -294,7 +272,42 @@ struct QuadInfo {
   u64 idx[4];        // index of each corner (earliest among == ties)
   u32 frame_size;    // frame_vertices(quad).size()
   u32 degenerate;    // frame_size <= 2
+  // derived once per call (quad_derive)
+  double ex[4], ey[4];     // edge c = corner (c + 1) & 3 - corner c (classify's cross products)
+  double blo[4], bspan[4]; // SPA bin map of region r + 1: origin and span of its primary
 };
+
+// Fills QuadInfo's derived fields from q (host and device: IEEE subtracts,
+// so both sides derive the same bits).
+__host__ __device__ inline void quad_derive(QuadInfo& qi) {
+  for (int c = 0; c < 4; ++c) {
+    const int d = (c + 1) & 3;
+    qi.ex[c] = qi.q[2 * d] - qi.q[2 * c];
+    qi.ey[c] = qi.q[2 * d + 1] - qi.q[2 * c + 1];
+    double lo, hi;
+    bin_range(qi.q, c + 1, &lo, &hi);
+    qi.blo[c] = lo;
+    qi.bspan[c] = hi - lo;
+  }
+}
+
+// The bin scale nb / span of a region (0 for a null, negative or denormal
+// span: every record then falls in one bin). Computed once per CTA by each
+// kernel that bins, from the same inputs, so all of them agree.
+__device__ __forceinline__ double bin_scale(double span, int log2nb) {
+  double s = span > 0.0 ? __ddiv_rn((double)(1u << log2nb), span) : 0.0;
+  if (!(s < 1e300)) s = 0.0;  // inf / nan
+  return s;
+}
+
+// Bin of a record of region ri + 1 with primary coordinate p:
+// trunc(clamp((p - lo) * scale, 0, top)) in the region's sort direction.
+// The float->int conversion saturates (negative and NaN -> 0), then the top
+// clamps. One dependent multiply: this sits on K2's per-survivor path.
+__device__ __forceinline__ u32 bin_of(double lo, double scale, u32 top, u32 ri, double p) {
+  const u32 b = min((u32)__double2uint_rz(__dmul_rn(__dsub_rn(p, lo), scale)), top);
+  return ri >= 2 ? top - b : b;  // UR / UL sort descending
+}
 
 // One extremes candidate per corner: the point and its index.
 struct Cand {
@@ -332,5 +345,6 @@ constexpr int kPasses = 8;
 constexpr int kK2Threads = 256;
 constexpr int kK2Items = 8;
 constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
+constexpr int kSegPts = 32 * kK2Items;            // one K2 warp's survivor segment (256)
 
 }  // namespace chgpu

@@ -126,6 +126,7 @@ __device__ void merge_partials_block(const QuadCand* __restrict__ partials, int 
       if (k > 1 && qi.q[0] == lx && qi.q[1] == ly) --k;
       qi.frame_size = k;
       qi.degenerate = k <= 2 ? 1u : 0u;
+      quad_derive(qi);
       *out = qi;
     }
   }
@@ -248,21 +249,15 @@ __device__ __forceinline__ void cp_async_wait() {
 // reserves its output range per stream with one global atomicAdd each,
 // instead of an ordered (look-back) scan. Per point the work is the
 // classification, a register counter increment and one record store.
-//
-// kStats: every survivor also adds itself to its SPA bin (k_filter.cu):
-// one fire-and-forget count increment and one running max of its guarded
-// key w per record, both resolved in L2 while the tile streams.
-template <bool kGivenLabels, bool kStats>
+template <bool kGivenLabels>
 __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     const unsigned char* __restrict__ given_labels, int force_lex, u64* __restrict__ kbuf,
-    u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out, int log2nb,
-    u32* __restrict__ bcnt, u64* __restrict__ bw, u32 wmask) {
+    u64* __restrict__ vbuf, u64 ncap, u32* __restrict__ counts_out) {
   extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
   __shared__ u32 s_wtot[kK2Threads / 32][4];
   __shared__ u32 s_base[4];
   __shared__ QuadEdges s_edges;
-  __shared__ BinGeom s_geom;
   __shared__ int s_lex;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -286,7 +281,6 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     // Degenerate frame: survivors all go to stream 1 in lexicographic
     // encoding for the hull_oracle-style finish (pipeline.cpp:53-71).
     s_lex = force_lex || (!kGivenLabels && qi.degenerate);
-    if (kStats) make_bin_geom(qi.q, log2nb, &s_geom);
   }
   __syncthreads();
   const bool lex = s_lex != 0;
@@ -363,89 +357,66 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
     if (r) {
       kbuf[slot] = k;
       vbuf[slot] = v;
-      if (kStats && !lex) {
-        const double prim = (r & 1u) ? p.x : p.y;
-        const u32 b = ((r - 1) << log2nb) | bin_of(s_geom, (int)r, prim);
-        atomicAdd(bcnt + b, 1u);
-        // any subset of a bin's records gives a valid (lower) max: sample
-        if ((pp & wmask) == 0) atomicMax(bw + b, wkey((int)r, v));
-      }
     }
   }
 }
 
+#ifndef CHGPU_K2_MINB
+#define CHGPU_K2_MINB 3
+#endif
 // K2 of the pre-filtered path (k_filter.cu): classify, count, and for
 // every survivor one fire-and-forget increment of its SPA bin's count and
-// (for one record in 2^k, wmask) a running max of its guarded key w. The
-// survivors are written as raw points (one 16-byte store) into two
-// two-ended stream pairs: LL | LR growing from both ends of pair12 and
-// UR | UL of pair34 (each cap points); the filter derives the sort record
-// only for the few it keeps. The four region counts travel packed in one
-// u64 (16-bit fields) through a single warp scan. A degenerate frame
-// (pipeline.cpp:53-71) writes LEX records into stream 1 of (kbuf, vbuf)
-// exactly like k_classify_compact.
-__global__ __launch_bounds__(kK2Threads, 4) void k_classify_survivors(
-    const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo, u64 ncap,
-    double2* __restrict__ pair12, double2* __restrict__ pair34, u64* __restrict__ kbuf,
+// (for one record in 2^k, wmask) a running max of its guarded key w.
+//
+// Survivor layout: each warp owns the 256-slot segment of its 256 input
+// points (seg + 256 * warp index) and writes its survivors there as raw
+// points, grouped LL | LR | UR | UL, with the four group sizes packed in
+// segcnt[warp index] (16-bit fields). Positions come from one warp scan,
+// so no CTA barrier or global reservation sits between the loads and the
+// stores; the filter reads the segments back (its order within a bin is
+// re-established by the bin sort). A degenerate frame (pipeline.cpp:53-71)
+// writes LEX records into dense stream 1 of (kbuf, vbuf) instead, exactly
+// like k_classify_compact.
+__global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivors(
+    const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
+    double2* __restrict__ seg, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
     u64* __restrict__ bw, u32 wmask) {
-  extern __shared__ __align__(16) double2 sbuf[];  // [kK2Tile]
-  // Per-region tables (index r - 1), so the per-item code has no region
-  // branches: stream origin and direction, bin map, guarded-key mask.
-  __shared__ unsigned long long s_wtot[kK2Threads / 32];
-  __shared__ u32 s_base[4];
-  __shared__ double2* s_org[4];
-  __shared__ long long s_dir[4];
-  __shared__ double s_lo[4], s_scale[4];
-  __shared__ u32 s_rev[4];
-  __shared__ unsigned long long s_vmask[4];
   __shared__ QuadEdges s_edges;
-  __shared__ double s_top;
+  __shared__ double s_lo[4], s_scale[4];
+  __shared__ u64 s_segT[kK2Threads / 32];
+  __shared__ u32 s_base;
   __shared__ int s_lex;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const u32 tile_base = blockIdx.x * kK2Tile;  // n < 2^32
+  const u32 sidx = blockIdx.x * (kK2Threads / 32) + warp;
+  const u32 base = sidx * kSegPts;  // n < 2^32
+  double2 p[kK2Items];
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
-    const u32 idx = tile_base + j * kK2Threads + tid;
-    const bool ok = idx < n;
-    cp_async16(sbuf + j * kK2Threads + tid, ok ? (const void*)(pts + idx) : (const void*)pts, ok);
+    const u32 idx = base + j * 32 + lane;
+    p[j] = idx < n ? ldg_stream(pts + idx) : make_double2(0.0, 0.0);
   }
-  cp_async_commit();
-  if (tid == 0) {
-    const QuadInfo qi = *qinfo;
-    for (int c = 0; c < 4; ++c) {
-      const int d = (c + 1) & 3;
-      s_edges.ax[c] = qi.q[2 * c];
-      s_edges.ay[c] = qi.q[2 * c + 1];
-      s_edges.ex[c] = __dsub_rn(qi.q[2 * d], qi.q[2 * c]);
-      s_edges.ey[c] = __dsub_rn(qi.q[2 * d + 1], qi.q[2 * c + 1]);
-    }
-    s_lex = qi.degenerate;
-    BinGeom g;
-    make_bin_geom(qi.q, log2nb, &g);
-    s_top = g.top;
-    for (int r = 0; r < 4; ++r) {
-      s_lo[r] = g.lo[r];
-      s_scale[r] = g.scale[r];
-      s_rev[r] = r >= 2 ? 1u : 0u;                                  // UR / UL descending
-      s_vmask[r] = (r == 0 || r == 3) ? ~0ull : 0ull;               // LL / UL: min-regions
-      s_org[r] = (r & 1) ? ((r < 2 ? pair12 : pair34) + ncap - 1) : (r < 2 ? pair12 : pair34);
-      s_dir[r] = (r & 1) ? -1 : 1;
-    }
+  if (tid < 4) {  // while the loads fly
+    const int c = tid;
+    s_edges.ax[c] = qinfo->q[2 * c];
+    s_edges.ay[c] = qinfo->q[2 * c + 1];
+    s_edges.ex[c] = qinfo->ex[c];
+    s_edges.ey[c] = qinfo->ey[c];
+    s_lo[c] = qinfo->blo[c];
+    s_scale[c] = bin_scale(qinfo->bspan[c], log2nb);
+    if (c == 0) s_lex = qinfo->degenerate;
   }
   __syncthreads();
   const bool lex = s_lex != 0;
   const QuadEdges e = s_edges;
-  cp_async_wait<0>();  // each thread reads back only its own copies
 
-  u32 codes = 0;        // 3 bits of stream id per item
-  u64 cnt = 0;          // 16-bit count per stream
+  u32 codes = 0;  // 3 bits of stream id per item
+  u64 cnt = 0;    // 16-bit count per stream
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
-    const u32 idx = tile_base + j * kK2Threads + tid;
-    const double2 p = sbuf[j * kK2Threads + tid];
-    int r = idx < n ? classify(e, p.x, p.y) : 0;
+    const u32 idx = base + j * 32 + lane;
+    int r = idx < n ? classify(e, p[j].x, p[j].y) : 0;
     if (lex && r != 0) r = 1;
     codes |= (u32)r << (3 * j);
     cnt += r ? 1ull << (16 * (r - 1)) : 0ull;
@@ -456,51 +427,60 @@ __global__ __launch_bounds__(kK2Threads, 4) void k_classify_survivors(
     const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) s_wtot[warp] = incl;
-  __syncthreads();
-  if (tid < 4) {
-    u32 tot = 0;
-    for (int w = 0; w < kK2Threads / 32; ++w) tot += (u32)(s_wtot[w] >> (16 * tid)) & 0xFFFFu;
-    s_base[tid] = tot ? atomicAdd(&counts_out[tid + 1], tot) : 0u;
-  }
-  __syncthreads();
-  u64 run = 0;  // this thread's exclusive position in each stream (16-bit fields)
-  for (int w = 0; w < warp; ++w) run += s_wtot[w];
-  run += incl - cnt;
-  if (lex) {
+  const u64 T = __shfl_sync(0xffffffffu, incl, 31);  // the segment's four group sizes
+  if (lane == 0) s_segT[warp] = T;
+
+  if (lex) {  // uniform: dense stream 1 through a CTA reservation
+    __syncthreads();
+    if (tid == 0) {
+      u32 sum = 0;
+      for (int w = 0; w < kK2Threads / 32; ++w) sum += (u32)s_segT[w] & 0xFFFFu;
+      s_base = sum ? atomicAdd(&counts_out[1], sum) : 0u;
+    }
+    __syncthreads();
+    u32 pp = s_base + (u32)((incl - cnt) & 0xFFFFu);
+    for (int w = 0; w < warp; ++w) pp += (u32)s_segT[w] & 0xFFFFu;
 #pragma unroll
     for (int j = 0; j < kK2Items; ++j) {
       if (!((codes >> (3 * j)) & 7)) continue;
-      const double2 p = sbuf[j * kK2Threads + tid];
-      const u32 pp = s_base[0] + (u32)(run & 0xFFFFu);
-      run += 1;
-      kbuf[pp] = ord_enc(p.x);
-      vbuf[pp] = ord_enc(p.y);
+      kbuf[pp] = ord_enc(p[j].x);
+      vbuf[pp] = ord_enc(p[j].y);
+      ++pp;
     }
     return;
   }
-  const u32 top = (u32)s_top;
+
+  if (lane == 0) segcnt[sidx] = T;
+  // exclusive position of this lane's next record of each group (16-bit
+  // fields): the group's start in the segment plus the lanes before it
+  u64 pos = (T << 16) + (T << 32) + (T << 48) + (incl - cnt);
+  double2* out = seg + (u64)base;
+  const u32 top = (1u << log2nb) - 1u;
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
     const u32 r = (codes >> (3 * j)) & 7;
     if (!r) continue;
-    const u32 ri = r - 1;
-    const u32 sh = 16 * ri;
-    const u32 pp = s_base[ri] + (u32)((run >> sh) & 0xFFFFu);
-    run += 1ull << sh;
-    const double2 p = sbuf[j * kK2Threads + tid];
-    s_org[ri][(long long)pp * s_dir[ri]] = p;
+    const u32 ri = r - 1, sh = 16 * ri;
+    const u32 slot = (u32)(pos >> sh) & 0xFFFFu;
+    pos += 1ull << sh;
+    out[slot] = p[j];
     const bool odd = (r & 1u) != 0;
-    const double prim = odd ? p.x : p.y;   // bin_of (chgpu_internal.cuh), tables
-    const u32 bq = min((u32)__double2uint_rz(__dmul_rn(__dsub_rn(prim, s_lo[ri]), s_scale[ri])), top);
-    const u32 b = (ri << log2nb) | (s_rev[ri] ? top - bq : bq);
+    const double prim = odd ? p[j].x : p[j].y;  // LL, UR: x; LR, UL: y
+    const u32 b = (ri << log2nb) | bin_of(s_lo[ri], s_scale[ri], top, ri, prim);
     atomicAdd(bcnt + b, 1u);
     // any subset of a bin's records gives a valid (lower) max: sample; w =
-    // wkey(v): the guarded coordinate with -0.0 folded onto +0.0 (+ 0.0)
-    if ((pp & wmask) == 0) {
-      const double g = odd ? p.y : p.x;
-      atomicMax(bw + b, ord_enc(__dadd_rn(g, 0.0)) ^ s_vmask[ri]);
+    // wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
+    // complemented for the min-regions LL and UL
+    if ((slot & wmask) == 0) {
+      const double g = odd ? p[j].y : p[j].x;
+      atomicMax(bw + b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     }
+  }
+  __syncthreads();
+  if (tid < 4) {
+    u32 sum = 0;
+    for (int w = 0; w < kK2Threads / 32; ++w) sum += (u32)(s_segT[w] >> (16 * tid)) & 0xFFFFu;
+    if (sum) atomicAdd(&counts_out[tid + 1], sum);
   }
 }
 
@@ -577,31 +557,25 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
 
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf,
-                             u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st, int log2nb,
-                             u32* bcnt, u64* bw, u32 wmask) {
+                             u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
   constexpr size_t smem = kK2Tile * sizeof(double2);
   if (given_labels)
-    k_classify_compact<true, false><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, given_labels, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr, 0);
-  else if (bcnt)
-    k_classify_compact<false, true><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, log2nb, bcnt, bw, wmask);
+    k_classify_compact<true><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, given_labels,
+                                                              force_lex, kbuf, vbuf, ncap, counts_out);
   else
-    k_classify_compact<false, false><<<tiles, kK2Threads, smem, st>>>(
-        pts, n, qinfo, nullptr, force_lex, kbuf, vbuf, ncap, counts_out, 0, nullptr, nullptr, 0);
+    k_classify_compact<false><<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, nullptr, force_lex,
+                                                               kbuf, vbuf, ncap, counts_out);
 }
 
-void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64 ncap,
-                               double2* pair12, double2* pair34, u64* kbuf, u64* vbuf,
-                               u32* counts_out, int log2nb, u32* bcnt, u64* bw, u32 wmask,
-                               cudaStream_t st) {
+void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, double2* seg,
+                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+                               u32* bcnt, u64* bw, u32 wmask, cudaStream_t st) {
   const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
   if (tiles == 0) return;
-  constexpr size_t smem = kK2Tile * sizeof(double2);
-  k_classify_survivors<<<tiles, kK2Threads, smem, st>>>(pts, n, qinfo, ncap, pair12, pair34, kbuf,
-                                                        vbuf, counts_out, log2nb, bcnt, bw, wmask);
+  k_classify_survivors<<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, seg, segcnt, kbuf, vbuf,
+                                                     counts_out, log2nb, bcnt, bw, wmask);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

@@ -318,70 +318,92 @@ __global__ __launch_bounds__(kBinThreads) void k_bin_thresholds(
 
 // ------------------------------------------------------------------ filter
 
+#ifndef CHGPU_FILTER_ITEMS
+#define CHGPU_FILTER_ITEMS 1
+#endif
+#ifndef CHGPU_FILTER_WAVES
+#define CHGPU_FILTER_WAVES 1
+#endif
+#ifndef CHGPU_FILTER_MINB
+#define CHGPU_FILTER_MINB 8
+#endif
 constexpr int kFilterThreads = 256;
-constexpr int kFilterItems = 4;
+constexpr int kFilterItems = CHGPU_FILTER_ITEMS;
 
-// Grid-stride over the survivors of the four K2 streams. A candidate takes
+// Warp-stride over K2's survivor segments (k_classify_survivors: 256
+// slots each, groups LL | LR | UR | UL sized by segcnt). A candidate takes
 // the next slot of its bin; the bin's 33rd candidate queues the bin for
-// k_bin_sort_big.
-__global__ __launch_bounds__(kFilterThreads) void k_filter(
-    const double2* __restrict__ pair12, const double2* __restrict__ pair34,
+// k_bin_sort_warp, its 257th for k_bin_sort_big.
+__global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
+    const double2* __restrict__ seg, const u64* __restrict__ segcnt, u32 nseg,
     const FilterPlan* __restrict__ P_p, const QuadInfo* __restrict__ qinfo,
     const u32* __restrict__ bstart, const u64* __restrict__ bthr, u32* __restrict__ bcur,
     u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
     unsigned long long* __restrict__ ncand) {
-  const FilterPlan& P = *P_p;
-  __shared__ BinGeom s_geom;
+  // The plan's per-region values, read once into shared memory (the loop's
+  // stores would otherwise force re-reads from global memory per item).
+  __shared__ u64 s_off[4];
+  __shared__ double s_lo[4], s_scale[4];
+  __shared__ u32 s_lg, s_nseg;
   __shared__ u32 s_cand;
-  if (threadIdx.x == 0) {
-    make_bin_geom(qinfo->q, P.log2nb, &s_geom);
-    s_cand = 0;
+  if (threadIdx.x < 4) {
+    const int r = threadIdx.x;
+    s_off[r] = P_p->spa.off[r];
+    s_lo[r] = qinfo->blo[r];
+    s_scale[r] = bin_scale(qinfo->bspan[r], P_p->log2nb);
+    if (r == 0) {
+      s_lg = (u32)P_p->log2nb;
+      s_nseg = qinfo->degenerate ? 0u : nseg;  // no segments then (K2 wrote LEX records)
+      s_cand = 0;
+    }
   }
   __syncthreads();
-  const u64 total = P.cum[4];
-  const u64 stride = (u64)gridDim.x * kFilterThreads * kFilterItems;
+  const u32 lg = s_lg, top = (1u << lg) - 1u;
+  nseg = s_nseg;
+  const int lane = threadIdx.x & 31;
+  const u32 wstride = gridDim.x * (kFilterThreads / 32);
   u32 mine = 0;
-  for (u64 i0 = (u64)blockIdx.x * kFilterThreads * kFilterItems + threadIdx.x; i0 < total;
-       i0 += stride) {
-    double2 p[kFilterItems];
-    int rr[kFilterItems];
+  for (u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5); sg < nseg; sg += wstride) {
+    const u64 T = __ldg(segcnt + sg);
+    const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
+              c3 = c2 + ((u32)(T >> 32) & 0xFFFFu), tot = c3 + (u32)(T >> 48);
+    const double2* sp = seg + (u64)sg * kSegPts;
+    for (u32 s0 = 0; s0 < tot; s0 += 32 * kFilterItems) {
+      double2 p[kFilterItems];
+      u32 rr[kFilterItems];
 #pragma unroll
-    for (int j = 0; j < kFilterItems; ++j) {
-      const u64 i = i0 + (u64)j * kFilterThreads;
-      int r = 0;
-      r += (i >= P.cum[1]);
-      r += (i >= P.cum[2]);
-      r += (i >= P.cum[3]);
-      rr[j] = r;
-      p[j] = make_double2(0.0, 0.0);
-      if (i < total) {
-        const double2* pair = r < 2 ? pair12 : pair34;
-        p[j] = __ldcs(pair + P.src_off[r] + (i - P.cum[r]));
+      for (int j = 0; j < kFilterItems; ++j) {
+        const u32 sl = s0 + j * 32 + lane;
+        rr[j] = (u32)(sl >= c1) + (u32)(sl >= c2) + (u32)(sl >= c3);
+        p[j] = sl < tot ? __ldcs(sp + sl) : make_double2(0.0, 0.0);
       }
-    }
-    // all threshold loads in flight before any test
-    u32 bi[kFilterItems];
-    u64 th[kFilterItems];
+      // all threshold loads in flight before any test
+      u32 bi[kFilterItems];
+      u64 th[kFilterItems];
 #pragma unroll
-    for (int j = 0; j < kFilterItems; ++j) {
-      const u64 i = i0 + (u64)j * kFilterThreads;
-      const int reg = rr[j] + 1;
-      const double prim = (reg & 1) ? p[j].x : p[j].y;
-      bi[j] = ((u32)rr[j] << P.log2nb) | bin_of(s_geom, reg, prim);
-      th[j] = i < total ? __ldg(bthr + bi[j]) : ~0ull;
-    }
+      for (int j = 0; j < kFilterItems; ++j) {
+        const u32 sl = s0 + j * 32 + lane;
+        const u32 r = rr[j];
+        const double prim = (r & 1u) ? p[j].y : p[j].x;  // LL, UR: x; LR, UL: y
+        bi[j] = (r << lg) | bin_of(s_lo[r], s_scale[r], top, r, prim);
+        th[j] = sl < tot ? __ldg(bthr + bi[j]) : ~0ull;
+      }
 #pragma unroll
-    for (int j = 0; j < kFilterItems; ++j) {
-      const int reg = rr[j] + 1;
-      const u64 v = v_of(reg, p[j].x, p[j].y);
-      if (wkey(reg, v) < th[j]) continue;  // (also every i >= total: th = ~0)
-      const u32 pos = atomicAdd(bcur + bi[j], 1u);
-      const u64 dst = P.spa.off[rr[j]] + bstart[bi[j]] + pos;
-      kout[dst] = k_of(reg, p[j].x, p[j].y);
-      vout[dst] = v;
-      if (pos == 32) big[atomicAdd(nbig, 1u)] = bi[j];                       // > 32: sorted by a warp
-      if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi[j];  // > 256: by a CTA
-      ++mine;
+      for (int j = 0; j < kFilterItems; ++j) {
+        const u32 r = rr[j];
+        const double gd = (r & 1u) ? p[j].x : p[j].y;  // the guarded coordinate
+        // wkey(v): -0.0 folded onto +0.0, complemented for LL / UL
+        const u64 vm = (r == 0 || r == 3) ? ~0ull : 0ull;
+        if ((ord_enc_z(gd) ^ vm) < th[j]) continue;  // (past tot: th = ~0)
+        const int reg = (int)r + 1;
+        const u32 pos = atomicAdd(bcur + bi[j], 1u);
+        const u64 dst = s_off[r] + bstart[bi[j]] + pos;
+        kout[dst] = k_of(reg, p[j].x, p[j].y);
+        vout[dst] = v_of(reg, p[j].x, p[j].y);
+        if (pos == 32) big[atomicAdd(nbig, 1u)] = bi[j];                       // > 32: by a warp
+        if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi[j];  // > 256: a CTA
+        ++mine;
+      }
     }
   }
 #pragma unroll
@@ -697,23 +719,18 @@ __global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
 // for K2. A degenerate frame (no SPA, pipeline.cpp:53-71) leaves every
 // region empty and the path idle.
 __global__ void k_filter_plan(const QuadInfo* __restrict__ qinfo, const u32* __restrict__ counts,
-                              u64 ncap, u64 chunk_count, int log2nb, FilterPlan* __restrict__ out) {
+                              u64 chunk_count, int log2nb, FilterPlan* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const QuadInfo qi = *qinfo;
   FilterPlan P;
   P.log2nb = log2nb;
   u64 m[4];
   for (int r = 0; r < 4; ++r) m[r] = qi.degenerate ? 0ull : (u64)counts[r];
-  // survivor points: LL | LR at both ends of pair12, UR | UL of pair34
-  P.src_off[0] = 0;
-  P.src_off[1] = ncap - m[1];
-  P.src_off[2] = 0;
-  P.src_off[3] = ncap - m[3];
-  P.cum[0] = 0;
+  u64 off = 0;
   u32 chunks = 0;
   for (int r = 0; r < 4; ++r) {
-    P.cum[r + 1] = P.cum[r] + m[r];
-    P.spa.off[r] = P.cum[r];
+    P.spa.off[r] = off;
+    off += m[r];
     P.spa.m[r] = m[r];
     P.spa.chunk_begin[r] = chunks;
     const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;  // spa.cpp:121
@@ -731,9 +748,9 @@ __global__ void k_filter_plan(const QuadInfo* __restrict__ qinfo, const u32* __r
 
 // ------------------------------------------------------------------ launchers
 
-void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 ncap, u64 chunk_count,
+void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count,
                         int log2nb, FilterPlan* out, cudaStream_t st) {
-  k_filter_plan<<<1, 32, 0, st>>>(qinfo, counts, ncap, chunk_count, log2nb, out);
+  k_filter_plan<<<1, 32, 0, st>>>(qinfo, counts, chunk_count, log2nb, out);
 }
 
 void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
@@ -746,15 +763,20 @@ void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int lo
                                                       aux.agg_val, bthr);
 }
 
-void launch_filter(const double2* pair12, const double2* pair34, const FilterPlan* P,
-                   u64 max_records, const QuadInfo* qinfo, const u32* bstart, const u64* bthr,
-                   u32* bcur, u64* kout, u64* vout, u32* big, u32* nbig,
-                   unsigned long long* ncand, cudaStream_t st) {
-  if (max_records == 0) return;
-  const u64 per = (u64)kFilterThreads * kFilterItems;
-  const u64 blocks = std::min<u64>((max_records + per - 1) / per, 148ull * 8);
-  k_filter<<<(unsigned)blocks, kFilterThreads, 0, st>>>(pair12, pair34, P, qinfo, bstart, bthr,
-                                                          bcur, kout, vout, big, nbig, ncand);
+void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
+                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st) {
+  if (nseg == 0) return;
+  // one resident wave: the warp-stride loop then has no partial last wave
+  static int resident = 0;
+  if (resident == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_filter, kFilterThreads, 0);
+    resident = std::max(resident, 1) * 148 * CHGPU_FILTER_WAVES;
+  }
+  const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
+                                   (u32)resident);
+  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segcnt, nseg, P, qinfo, bstart, bthr, bcur, kout,
+                                              vout, big, nbig, ncand);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,

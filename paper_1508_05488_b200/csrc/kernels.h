@@ -40,8 +40,6 @@ constexpr int kWarpSortMax = 256;   // ... by one warp
 constexpr u32 kBigListB = 4u << 18; // offset of the CTA-sort list in the big-bin lists
 struct FilterPlan {
   SpaPlan spa;          // chunk geometry, region offsets of the sorted layout
-  u64 src_off[4];       // survivor points: offset in pair12 (LL, LR) / pair34 (UR, UL)
-  u64 cum[5];           // prefix of region sizes
   u64 seed_w[4];        // wkey of guarded(anchors.first)
   int log2nb;           // bins per region = 2^log2nb
 };
@@ -54,14 +52,13 @@ struct FilterAux {
   u32* region_end;  // [4] dense end of each region's candidates
 };
 // The plan of the filter path on the device (from K2's counts).
-void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 ncap, u64 chunk_count,
+void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count,
                         int log2nb, FilterPlan* out, cudaStream_t st);
 void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
                      u64* bthr, u32* first_bin, FilterAux aux, cudaStream_t st);
-void launch_filter(const double2* pair12, const double2* pair34, const FilterPlan* P,
-                   u64 max_records, const QuadInfo* qinfo, const u32* bstart, const u64* bthr,
-                   u32* bcur, u64* kout, u64* vout, u32* big, u32* nbig,
-                   unsigned long long* ncand, cudaStream_t st);
+void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
+                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
 void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
@@ -93,13 +90,11 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, 
 // K2
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
-                             u64 ncap, u32* counts_out, cudaStream_t st, int log2nb = 0,
-                             u32* bcnt = nullptr, u64* bw = nullptr, u32 wmask = 0);
+                             u64 ncap, u32* counts_out, cudaStream_t st);
 // K2 of the pre-filtered path: raw survivor points + bin statistics.
-void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64 ncap,
-                               double2* pair12, double2* pair34, u64* kbuf, u64* vbuf,
-                               u32* counts_out, int log2nb, u32* bcnt, u64* bw, u32 wmask,
-                               cudaStream_t st);
+void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, double2* seg,
+                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+                               u32* bcnt, u64* bw, u32 wmask, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

@@ -826,14 +826,14 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
   const int nbig_slot = take_ctr(ctx), nbig2_slot = take_ctr(ctx);
   (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
   *ovf_slot = take_ctr(ctx);
-  launch_filter_plan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, ctx->cap, chunk_count, log2nb,
+  launch_filter_plan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb,
                      ctx->d_plan, st);
   launch_bin_scan(t.cnt, t.w, P, log2nb, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
   CK(cudaEventRecord(ctx->ev[3], st));
-  launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf),
-                reinterpret_cast<const double2*>(ctx->d_vbuf), P, n, ctx->d_qinfo, ctx->d_fstart,
-                ctx->d_fthr, t.cur,
-                ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
+  // K2's survivor segments: points in kbuf, group sizes in vbuf
+  launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf), ctx->d_vbuf,
+                (u32)((n + kSegPts - 1) / kSegPts), P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
+                t.cur, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
   CK(cudaEventRecord(ctx->ev[4], st));
   launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
                       ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, st);
@@ -1065,9 +1065,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   if (want_filter) {
     // raw survivor points + bin statistics (a degenerate frame writes the
     // LEX records of stream 1 instead)
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->cap,
-                              reinterpret_cast<double2*>(ctx->d_kbuf),
-                              reinterpret_cast<double2*>(ctx->d_vbuf), ctx->d_kbuf, ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, reinterpret_cast<double2*>(ctx->d_kbuf),
+                              ctx->d_vbuf, ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
   } else {
     launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
@@ -1296,6 +1295,7 @@ int upload_quad(chgpu_ctx* ctx, const double* quad) {
   frame_of(quad, fr, &nf);
   qi.frame_size = (u32)nf;
   qi.degenerate = nf <= 2;
+  quad_derive(qi);
   ctx->h->qi = qi;
   TRY(upload(ctx, ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo)));
   return CHGPU_OK;
@@ -1689,9 +1689,8 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
     ctx->ctr_used += 5;
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->cap,
-                              reinterpret_cast<double2*>(ctx->d_kbuf),
-                              reinterpret_cast<double2*>(ctx->d_vbuf), ctx->d_kbuf, ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, reinterpret_cast<double2*>(ctx->d_kbuf),
+                              ctx->d_vbuf, ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
     CK(cudaGetLastError());
     int ovf_slot = -1;
