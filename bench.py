@@ -317,10 +317,12 @@ def main():
                 "k3_filter": {"ms": t["t_filter_ms"], "bytes": 16 * s1 + 16 * nc,
                               "basis": "16 B/survivor read + 16 B/candidate write",
                               "candidates": nc},
-                "k3_bin_sort_compact": {"ms": t["t_binsort_ms"]},
-                "k4_spa_dense": {"ms": t["t_spa_kernel_ms"],
-                                "bytes": 16 * nc + 16 * sum(d.kept_counts),
-                                "basis": "16 B/candidate read + 16 B/kept write"},
+                "k3_bin_sort": {"ms": t["t_binsort_ms"],
+                                "basis": "bins above 32 candidates sorted in place"},
+                "k4_spa_chunks_emit": {"ms": t["t_spa_kernel_ms"],
+                                       "bytes": 16 * nc + 32 * sum(d.kept_counts),
+                                       "basis": "16 B/candidate read + 16 B/kept scratch "
+                                                "+ 16 B/kept point write"},
             })
         else:
             pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)

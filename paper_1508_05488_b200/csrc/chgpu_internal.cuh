@@ -257,6 +257,15 @@ __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   return r;
 }
 
+// SPA extremum and step-back test on guarded coordinates (spa.cpp:92-105):
+// LL / UL keep running minima, LR / UR maxima.
+__device__ __forceinline__ double op_ext(bool is_min, double a, double b) {
+  return is_min ? (b < a ? b : a) : (b > a ? b : a);
+}
+__device__ __forceinline__ bool steps_back(bool is_min, double g, double t) {
+  return is_min ? (g > t) : (g < t);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -345,6 +354,10 @@ constexpr int kPasses = 8;
 constexpr int kK2Threads = 256;
 constexpr int kK2Items = 8;
 constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
-constexpr int kSegPts = 32 * kK2Items;            // one K2 warp's survivor segment (256)
+#ifndef CHGPU_SEG_ITEMS
+#define CHGPU_SEG_ITEMS 8
+#endif
+constexpr int kSegItems = CHGPU_SEG_ITEMS;        // points per lane of the filter path's K2
+constexpr int kSegPts = 32 * kSegItems;           // one K2 warp's survivor segment
 
 }  // namespace chgpu

@@ -20,22 +20,20 @@
 // The first bin of every chunk c > 0 has T = 0 (seed = identity) as well,
 // so each chunk's first candidate sits at a known dense position.
 //
-// Kernels (all grid-parallel over bins or records; none walks a chunk's
-// bins, since a sparse stretch of a region can put thousands of bins in
-// one chunk):
-//   K2 (kStats)        per survivor: bin count += 1, bin max(w) (k_discard.cu)
-//   k_bin_tile_sums    records per tile of 2048 bins
-//   k_bin_starts       bin start ranks, the bin holding each chunk's first
-//                      rank, and the tile's segmented-max aggregate
-//   k_bin_thresholds   T_b: segmented exclusive max (segments = chunks)
+// Kernels:
+//   K2 (k_discard.cu)  per survivor: bin count += 1, bin max(w); the
+//                      survivor point into its warp's segment
+//   k_bin_scan         one cooperative launch: the plan, bin starts (ranks),
+//                      each chunk's first bin, T_b: segmented exclusive max
+//                      (segments = chunks)
 //   k_filter           survivors with w >= T_b -> their bin's slots of a
-//                      sparse region-ordered layout (unordered in the bin)
+//                      sparse region-ordered layout (unordered in the bin),
+//                      and a bit per bin holding a candidate
 //   k_bin_sort_warp/_big  bins above 32 candidates sorted in place
-//   k_bin_tile_sums    candidates per tile (same kernel, on the cursors)
-//   k_cand_compact     dense candidate order: small bins batched and sorted
-//                      in registers, big bins copied; each chunk's first
-//                      dense index
-//   k_spa_dense (k_spa.cu)  the SPA scan over each chunk's dense candidates
+//   k_spa_chunks       one warp per chunk: its candidate bins from the
+//                      bitmap, small bins batched and ordered in registers,
+//                      the SPA scan; kept records to scratch
+//   k_spa_emit         kept records at their output offsets, decoded
 //
 // Algorithmic traffic: the filter reads 16 B per survivor and writes 16 B
 // per candidate (a few percent of survivors for spread-out inputs); the
@@ -126,69 +124,131 @@ __device__ __forceinline__ SegMax block_excl_segmax(SegMax x, u32* sseg, u64* sv
   return seg_combine(pre, ex);
 }
 
+// Chunk of a rank, s / cs, for a thread walking increasing ranks: one
+// division on entry and one per chunk boundary crossed, not one per bin.
+struct ChunkCursor {
+  u32 cur;   // chunk of the last rank asked for
+  u64 next;  // first rank of chunk cur + 1
+  u32 cs;
+  __device__ __forceinline__ ChunkCursor(u32 s, u32 chunk_size) : cs(chunk_size) {
+    cur = s / cs;
+    next = (u64)(cur + 1) * cs;
+  }
+  __device__ __forceinline__ u32 at(u32 s) {  // s no smaller than the last rank asked for
+    if (s >= next) {
+      cur = s / cs;
+      next = (u64)(cur + 1) * cs;
+    }
+    return cur;
+  }
+  __device__ __forceinline__ u32 peek(u32 s) const { return s < next ? cur : s / cs; }
+};
+
 // Segmented-max elements of 8 consecutive bins starting at rank s: a bin
 // inside one chunk contributes (chunk, w); a straddling bin restarts its
 // last chunk with nothing known; an empty bin contributes nothing.
-__device__ __forceinline__ void seg_elems(const u32* c, const u64* w, u32 s, u32 cs, SegMax* e) {
+// *straddle bit j: whether bin j crosses a chunk boundary.
+__device__ __forceinline__ void seg_elems(const u32* c, const u64* w, u32 s, u32 cs, SegMax* e,
+                                          u32* straddle) {
+  ChunkCursor cc(s, cs);
+  u32 sm = 0;
 #pragma unroll
   for (int j = 0; j < kBinPer; ++j) {
     if (c[j] == 0) {
       e[j] = SegMax{kNone, 0};
     } else {
-      const u32 clo = s / cs, chi = (s + c[j] - 1) / cs;
+      const u32 clo = cc.at(s), chi = cc.peek(s + c[j] - 1);
+      sm |= (u32)(clo != chi) << j;
       e[j] = clo != chi ? SegMax{chi, 0} : SegMax{clo, w[j]};
     }
     s += c[j];
   }
+  *straddle = sm;
 }
 
-// Sum of a u32 array per tile of kBinTile bins (record counts, or
-// candidate counts).
-__global__ __launch_bounds__(kBinThreads) void k_bin_tile_sums(const u32* __restrict__ cnt,
-                                                              int log2nb, u32* __restrict__ tsum) {
-  __shared__ u32 sh[kBinThreads / 32];
-  const u32 tiles = bin_tiles(log2nb);
-  const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
-  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
-  u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (b0 < (1u << log2nb)) load8(cnt + ((size_t)r << log2nb) + b0, c);
-  u32 x = 0;
-#pragma unroll
-  for (int j = 0; j < kBinPer; ++j) x += c[j];
-  u32 tot;
-  block_excl_sum(x, sh, &tot);
-  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+// The plan of the filter path, computed on the device from K2's region
+// counts and the quad, so the host enqueues the whole path without waiting
+// for K2. A degenerate frame (no SPA, pipeline.cpp:53-71) leaves every
+// region empty and the path idle.
+__device__ void make_filter_plan(const QuadInfo& qi, const u32* __restrict__ counts,
+                                 u64 chunk_count, int log2nb, FilterPlan& P) {
+  P.log2nb = log2nb;
+  u64 m[4];
+  for (int r = 0; r < 4; ++r) m[r] = qi.degenerate ? 0ull : (u64)counts[r];
+  u64 off = 0;
+  u32 chunks = 0;
+  for (int r = 0; r < 4; ++r) {
+    P.spa.off[r] = off;
+    off += m[r];
+    P.spa.m[r] = m[r];
+    P.spa.chunk_begin[r] = chunks;
+    const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;  // spa.cpp:121
+    P.spa.chunk_size[r] = cs;
+    if (m[r]) chunks += (u32)((m[r] + cs - 1) / cs);                   // spa.cpp:122
+    // guarded(region, anchors.first): LL left.y, LR bottom.x, UR right.y, UL top.x
+    const double seed = (r == 0 || r == 2) ? qi.q[2 * r + 1] : qi.q[2 * r];
+    P.spa.seed[r] = seed;
+    const int reg = r + 1;
+    P.seed_w[r] = wkey(reg, (reg == 1 || reg == 4) ? ~ord_enc(seed) : ord_enc(seed));
+  }
+  P.spa.total_chunks = chunks;
 }
 
-// Bin starts (ranks inside the region), each chunk's first bin, and the
-// tile's segmented-max aggregate.
-__global__ __launch_bounds__(kBinThreads) void k_bin_starts(
-    const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ tsum,
-    const FilterPlan* __restrict__ P_p, u32* __restrict__ bstart, u32* __restrict__ first_bin,
-    u32* __restrict__ agg_seg, u64* __restrict__ agg_val) {
-  const FilterPlan& P = *P_p;
+__device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier of a cooperative launch (every CTA resident): arrival
+// count in *ctr (zero at launch); barrier g releases at (g + 1) * gridDim.x.
+__device__ __forceinline__ void grid_barrier(u32* ctr, u32 g) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const u32 target = (g + 1) * gridDim.x;
+    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+// The whole bin scan in one cooperative launch (one CTA per tile of 2048
+// bins, at most 512 CTAs, all resident), bins held in registers across two
+// grid barriers:
+//   plan      every CTA derives the FilterPlan from K2's region counts
+//             (CTA 0 publishes it for the later kernels);
+//   phase 1   records per tile;
+//   phase 2   bin starts (ranks inside the region) from the earlier tiles'
+//             sums, and the tile's segmented-max aggregate;
+//   phase 3   T_b = max(seed of its chunk, exclusive segmented max of w over
+//             the chunk's inner bins), 0 for straddling and empty bins; the
+//             carry into a tile folds the aggregates of the region's earlier
+//             tiles.
+__global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
+    const QuadInfo* __restrict__ qinfo, const u32* __restrict__ counts, u64 chunk_count,
+    int log2nb, const u32* __restrict__ bcnt, const u64* __restrict__ bw,
+    FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u64* __restrict__ bthr,
+    u32* __restrict__ first_bin, u32* __restrict__ tsum, u32* __restrict__ agg_seg,
+    u64* __restrict__ agg_val, u32* __restrict__ bar) {
+  __shared__ FilterPlan sP;
   __shared__ u32 sh[kBinThreads / 32];
   __shared__ u32 sseg[kBinThreads / 32];
   __shared__ u64 sval[kBinThreads / 32];
   __shared__ u32 s_base;
-  const u32 nb = 1u << P.log2nb;
-  const u32 tiles = bin_tiles(P.log2nb);
+  __shared__ u32 c_seg;
+  __shared__ u64 c_val;
+  const u32 nb = 1u << log2nb;
+  const u32 tiles = bin_tiles(log2nb);
   const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
-  if (P.spa.m[r] == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    u32 x = 0;
-    for (u32 i = lane; i < t; i += 32) x += tsum[r * tiles + i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_base = x;
-  }
   const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
-  const bool in = b0 < nb;
-  const size_t boff = (size_t)r << P.log2nb;
+  const size_t boff = (size_t)r << log2nb;
+  // the bins first (an empty region's bins are all zero), the plan while
+  // they load
   u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
   u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (in) {
+  if (b0 < nb) {
     load8(bcnt + boff + b0, c);
 #pragma unroll
     for (int j = 0; j < kBinPer; j += 2) {
@@ -197,67 +257,73 @@ __global__ __launch_bounds__(kBinThreads) void k_bin_starts(
       w[j + 1] = a.y;
     }
   }
+  if (threadIdx.x == 0) {
+    const QuadInfo qi = *qinfo;
+    make_filter_plan(qi, counts, chunk_count, log2nb, sP);
+    if (blockIdx.x == 0) *plan_out = sP;
+  }
+  __syncthreads();
+  const bool active = sP.spa.m[r] != 0;  // CTA-uniform; idle CTAs still meet the barriers
+  const bool in = active && b0 < nb;
+  // phase 1
   u32 x = 0;
 #pragma unroll
   for (int j = 0; j < kBinPer; ++j) x += c[j];
   u32 tot;
   const u32 ex = block_excl_sum(x, sh, &tot);
-  __syncthreads();  // s_base
+  if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+  grid_barrier(bar, 0);
+  // phase 2
+  if (warp == 0) {
+    u32 y = 0;
+    for (u32 i = lane; i < t; i += 32) y += __ldcg(tsum + r * tiles + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (lane == 0) s_base = y;
+  }
+  __syncthreads();
   const u32 s0 = s_base + ex;
-  const u32 cs = (u32)P.spa.chunk_size[r];  // ranks and sizes fit 32 bits (n < 2^32)
+  const u32 cs = (u32)sP.spa.chunk_size[r];  // ranks and sizes fit 32 bits (n < 2^32)
   SegMax e[kBinPer];
-  seg_elems(c, w, s0, cs, e);
+  u32 straddle;
+  seg_elems(c, w, s0, cs, e, &straddle);
   SegMax agg{kNone, 0};
 #pragma unroll
   for (int j = 0; j < kBinPer; ++j) agg = seg_combine(agg, e[j]);
   SegMax tagg;
-  block_excl_segmax(agg, sseg, sval, &tagg);
+  SegMax run = block_excl_segmax(agg, sseg, sval, &tagg);
   if (threadIdx.x == 0) {
     agg_seg[blockIdx.x] = tagg.seg;
     agg_val[blockIdx.x] = tagg.val;
   }
-  if (!in) return;
-  const u32 cbase = P.spa.chunk_begin[r];
-  u32 s = s0;
-  u32 so[kBinPer];
+  if (in) {
+    // bin starts, and the bin holding each chunk's first rank
+    const u32 cbase = sP.spa.chunk_begin[r];
+    ChunkCursor cc(s0, cs);
+    u32 so[kBinPer];
+    u32 q = s0;
 #pragma unroll
-  for (int j = 0; j < kBinPer; ++j) {
-    so[j] = s;
-    if (c[j]) {
-      const u32 chi = (s + c[j] - 1) / cs;
-      for (u32 q = (s + cs - 1) / cs; q <= chi; ++q) first_bin[cbase + q] = b0 + j;
+    for (int j = 0; j < kBinPer; ++j) {
+      so[j] = q;
+      if (c[j]) {
+        const u32 clo = cc.at(q), chi = cc.peek(q + c[j] - 1);
+        for (u32 k = ((u64)clo * cs == q) ? clo : clo + 1; k <= chi; ++k) first_bin[cbase + k] = b0 + j;
+      }
+      q += c[j];
     }
-    s += c[j];
+    uint4* o = reinterpret_cast<uint4*>(bstart + boff + b0);
+    o[0] = make_uint4(so[0], so[1], so[2], so[3]);
+    o[1] = make_uint4(so[4], so[5], so[6], so[7]);
   }
-  uint4* o = reinterpret_cast<uint4*>(bstart + boff + b0);
-  o[0] = make_uint4(so[0], so[1], so[2], so[3]);
-  o[1] = make_uint4(so[4], so[5], so[6], so[7]);
-}
-
-// T_b for every bin: max(seed of its chunk, exclusive segmented max of w
-// over the chunk's inner bins); 0 for straddling and empty bins. The carry
-// into a tile folds the aggregates of the region's earlier tiles.
-__global__ __launch_bounds__(kBinThreads) void k_bin_thresholds(
-    const u32* __restrict__ bcnt, const u64* __restrict__ bw, const u32* __restrict__ bstart,
-    const FilterPlan* __restrict__ P_p, const u32* __restrict__ agg_seg, const u64* __restrict__ agg_val,
-    u64* __restrict__ bthr) {
-  const FilterPlan& P = *P_p;
-  __shared__ u32 sseg[kBinThreads / 32];
-  __shared__ u64 sval[kBinThreads / 32];
-  __shared__ u32 c_seg;
-  __shared__ u64 c_val;
-  const u32 nb = 1u << P.log2nb;
-  const u32 tiles = bin_tiles(P.log2nb);
-  const u32 r = blockIdx.x / tiles, t = blockIdx.x % tiles;
-  if (P.spa.m[r] == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  grid_barrier(bar, 1);
+  // phase 3
   if (warp == 0) {
     // ordered fold of tiles [0, t): lane L folds its contiguous share, then
     // an ordered warp scan
     const u32 per = (t + 31) / 32;
     SegMax a{kNone, 0};
     for (u32 i = lane * per; i < min(t, (lane + 1) * per); ++i)
-      a = seg_combine(a, SegMax{agg_seg[r * tiles + i], agg_val[r * tiles + i]});
+      a = seg_combine(a, SegMax{__ldcg(agg_seg + r * tiles + i), __ldcg(agg_val + r * tiles + i)});
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const SegMax y = shfl_up_seg(a, o);
@@ -268,48 +334,24 @@ __global__ __launch_bounds__(kBinThreads) void k_bin_thresholds(
       c_val = a.val;
     }
   }
-  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
-  const bool in = b0 < nb;
-  const size_t boff = (size_t)r << P.log2nb;
-  u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
-  u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
-  u32 s0 = 0;
-  if (in) {
-    load8(bcnt + boff + b0, c);
-    s0 = bstart[boff + b0];
-#pragma unroll
-    for (int j = 0; j < kBinPer; j += 2) {
-      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(bw + boff + b0 + j);
-      w[j] = a.x;
-      w[j + 1] = a.y;
-    }
-  }
-  const u32 cs = (u32)P.spa.chunk_size[r];
-  SegMax e[kBinPer];
-  seg_elems(c, w, s0, cs, e);
-  SegMax agg{kNone, 0};
-#pragma unroll
-  for (int j = 0; j < kBinPer; ++j) agg = seg_combine(agg, e[j]);
-  SegMax tagg;
-  SegMax run = block_excl_segmax(agg, sseg, sval, &tagg);
-  run = seg_combine(SegMax{c_seg, c_val}, run);  // c_* ready: block_excl_segmax synced
+  __syncthreads();
   if (!in) return;
-  const u64 seedw = P.seed_w[r];
+  run = seg_combine(SegMax{c_seg, c_val}, run);
+  const u64 seedw = sP.seed_w[r];
   u64 th[kBinPer];
-  u32 s = s0;
+  ChunkCursor cc(s0, cs);
+  u32 q = s0;
 #pragma unroll
   for (int j = 0; j < kBinPer; ++j) {
     th[j] = 0;
-    if (c[j]) {
-      const u32 clo = s / cs, chi = (s + c[j] - 1) / cs;
-      if (clo == chi) {
-        u64 tv = clo == 0 ? seedw : 0ull;
-        if (run.seg == clo && run.val > tv) tv = run.val;
-        th[j] = tv;
-      }
+    if (c[j] && !((straddle >> j) & 1u)) {
+      const u32 clo = cc.at(q);
+      u64 tv = clo == 0 ? seedw : 0ull;
+      if (run.seg == clo && run.val > tv) tv = run.val;
+      th[j] = tv;
     }
     run = seg_combine(run, e[j]);
-    s += c[j];
+    q += c[j];
   }
 #pragma unroll
   for (int j = 0; j < kBinPer; j += 2)
@@ -338,8 +380,8 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
     const double2* __restrict__ seg, const u64* __restrict__ segcnt, u32 nseg,
     const FilterPlan* __restrict__ P_p, const QuadInfo* __restrict__ qinfo,
     const u32* __restrict__ bstart, const u64* __restrict__ bthr, u32* __restrict__ bcur,
-    u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
-    unsigned long long* __restrict__ ncand) {
+    u32* __restrict__ bmap, u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big,
+    u32* __restrict__ nbig, unsigned long long* __restrict__ ncand) {
   // The plan's per-region values, read once into shared memory (the loop's
   // stores would otherwise force re-reads from global memory per item).
   __shared__ u64 s_off[4];
@@ -397,6 +439,7 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
         if ((ord_enc_z(gd) ^ vm) < th[j]) continue;  // (past tot: th = ~0)
         const int reg = (int)r + 1;
         const u32 pos = atomicAdd(bcur + bi[j], 1u);
+        if (pos == 0) atomicOr(bmap + (bi[j] >> 5), 1u << (bi[j] & 31));  // k_spa_chunks' index
         const u64 dst = s_off[r] + bstart[bi[j]] + pos;
         kout[dst] = k_of(reg, p[j].x, p[j].y);
         vout[dst] = v_of(reg, p[j].x, p[j].y);
@@ -567,148 +610,264 @@ __device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u6
   }
 }
 
-// One CTA per tile of 2048 bins: dense position of every bin's candidates
-// (global order: region, bin, record) and each chunk's first dense index.
-__global__ __launch_bounds__(kBinThreads) void k_cand_positions(
-    const u32* __restrict__ bcnt, const u32* __restrict__ bcur, const u32* __restrict__ bstart,
-    const u32* __restrict__ csum, const FilterPlan* __restrict__ P_p, u32* __restrict__ cpos, u32* __restrict__ first_cand,
-    u32* __restrict__ region_end) {
-  const FilterPlan& P = *P_p;
-  __shared__ u32 sh[kBinThreads / 32];
-  __shared__ u32 s_base;
-  const u32 nb = 1u << P.log2nb;
-  const u32 tiles = bin_tiles(P.log2nb);
-  const u32 gt = blockIdx.x, r = gt / tiles, t = gt % tiles;
-  if (P.spa.m[r] == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    u32 x = 0;
-    for (u32 i = lane; i < gt; i += 32) x += csum[i];
+// ------------------------------------------------------------------ chunk SPA
+//
+// One warp per SPA chunk (spa.cpp:109-163 over the chunk's candidates),
+// chunks taken in order from an atomic counter for the look-back. The
+// chunk's ranks [lo, hi) cover bins first_bin[c] .. first_bin[c + 1]; each
+// bin's candidates sit at its sparse slots (region offset + bin start),
+// sorted in place when above 32 (k_bin_sort_warp / _big), else batched with
+// their neighbours and sorted in registers by (bin, record). A candidate's
+// index inside its sorted bin is its rank offset whenever the bin straddles
+// a chunk boundary (T = 0 there: every record is a candidate), so clipping
+// to [lo - start, hi - start) gives the chunk's share; inner bins lie
+// wholly inside. The running extremum starts at the seed for chunk 0 and at
+// the identity otherwise; kept records go to scratch at the chunk's own
+// rank range, their count to chunk_kept[c] and to the sum of its group of
+// 256 chunks; k_spa_emit places them. (Chunks all finish their scans at
+// about the same time, so a decoupled look-back here would walk back
+// through thousands of aggregates before any prefix appears.)
+__global__ __launch_bounds__(256) void k_spa_chunks(
+    const u64* __restrict__ k, const u64* __restrict__ v, const u32* __restrict__ bcur,
+    const u32* __restrict__ bstart, const u32* __restrict__ bmap, const u32* __restrict__ first_bin,
+    const FilterPlan* __restrict__ P_p, u64* __restrict__ sk, u64* __restrict__ sv,
+    u32* __restrict__ chunk_kept, u32* __restrict__ group_kept,
+    unsigned long long* __restrict__ kept_counts) {
+  const SpaPlan& plan = P_p->spa;
+  const int lane = threadIdx.x & 31;
+  const u32 c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= plan.total_chunks) return;
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const int log2nb = P_p->log2nb;
+  const u32 cl = c - plan.chunk_begin[r];
+  const u32 nchunks = (r < 3 ? plan.chunk_begin[r + 1] : plan.total_chunks) - plan.chunk_begin[r];
+  const u32 cs = (u32)plan.chunk_size[r];
+  const u32 lo = cl * cs, hi = (u32)min((u64)lo + cs, plan.m[r]);
+  const size_t boff = (size_t)r << log2nb;
+  const u64 rbase = plan.off[r];
+  const u32 b_first = first_bin[c];
+  const u32 b_last = cl + 1 < nchunks ? first_bin[c + 1] : (1u << log2nb) - 1u;
+  const bool is_min = (region == 1 || region == 4);
+  const double ident = is_min ? INFINITY : -INFINITY;
+  double carry = (cl == 0) ? plan.seed[r] : ident;
+  u64* const kd = sk + rbase + lo;
+  u64* const vd = sv + rbase + lo;
+  u32 kept = 0;
+  __shared__ int s_mark[8][32];
+  __shared__ u64 s_pk[8][32], s_pv[8][32], s_pc[8][32];
+  const int warp = threadIdx.x >> 5;
+
+  // one SPA step over 32 lanes in lane order; inactive lanes are neutral
+  auto step = [&](bool active, u64 kk, u64 vv) {
+    const double g = active ? guarded_of(region, vv) : ident;
+    double incl = g;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_base = x;
-  }
-  const size_t boff = (size_t)r << P.log2nb;
-  const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
-  const bool in = b0 < nb;
-  u32 nc[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (in) load8(bcur + boff + b0, nc);
-  u32 x = 0;
-#pragma unroll
-  for (int j = 0; j < kBinPer; ++j) x += nc[j];
-  u32 tot;
-  const u32 ex = block_excl_sum(x, sh, &tot);
-  __syncthreads();  // s_base
-  if (!in) return;
-  u32 cp = s_base + ex;
-  u32 n[kBinPer], st[kBinPer], cps[kBinPer];
-  load8(bcnt + boff + b0, n);
-  load8(bstart + boff + b0, st);
-  const u32 cs = (u32)P.spa.chunk_size[r];
-  const u32 cbase = P.spa.chunk_begin[r];
-#pragma unroll
-  for (int j = 0; j < kBinPer; ++j) {
-    cps[j] = cp;
-    if (n[j]) {
-      // chunk starts in this bin: chunk 0 starts the region's candidates;
-      // a later chunk's first bin holds every one of its records
-      const u32 s = st[j], chi = (s + n[j] - 1) / cs;
-      for (u32 q = (s + cs - 1) / cs; q <= chi; ++q)
-        first_cand[cbase + q] = q == 0 ? cp : cp + (q * cs - s);
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = op_ext(is_min, y, incl);
     }
-    cp += nc[j];
+    double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) ex = ident;
+    const bool keep = active && !steps_back(is_min, g, op_ext(is_min, carry, ex));
+    carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, incl, 31));
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const u32 at = kept + __popc(km & lanemask_lt());
+      kd[at] = kk;
+      vd[at] = vv;
+    }
+    kept += __popc(km);
+  };
+
+  // The chunk's bins holding candidates, in order, from the filter's
+  // bitmap: 1024 bins per load round (a sparse stretch of a region can put
+  // thousands of empty bins in one chunk), then 32 of them per window.
+  __shared__ u32 s_list[8][1024];
+  const u32 gb0 = (u32)boff + b_first, gb1 = (u32)boff + b_last;  // inclusive
+  for (u32 w0 = gb0 >> 5; w0 <= (gb1 >> 5); w0 += 32) {
+    const u32 wi = w0 + lane;
+    u32 word = wi <= (gb1 >> 5) ? bmap[wi] : 0u;
+    if (wi == (gb0 >> 5)) word &= ~0u << (gb0 & 31);
+    if (wi == (gb1 >> 5) && (gb1 & 31) != 31) word &= (2u << (gb1 & 31)) - 1u;
+    const u32 cntw = __popc(word);
+    u32 at = cntw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, at, o);
+      if (lane >= o) at += y;
+    }
+    const u32 nlist = __shfl_sync(0xffffffffu, at, 31);
+    at -= cntw;
+    while (word) {
+      s_list[warp][at++] = (wi << 5) + (u32)(__ffs(word) - 1) - (u32)boff;
+      word &= word - 1;
+    }
+    __syncwarp();
+   for (u32 lb = 0; lb < nlist; lb += 32) {
+    const bool listed = lb + lane < nlist;
+    const u32 b = listed ? s_list[warp][lb + lane] : 0u;
+    u32 n = 0, s = 0;
+    if (listed) {
+      n = bcur[boff + b];
+      s = bstart[boff + b];
+    }
+    // the chunk's share of the bin, as indices into its sorted candidates
+    const u32 i0 = lo > s ? lo - s : 0u;
+    const u32 i1 = min(n, hi > s ? hi - s : 0u);
+    const bool act = n > 0 && i1 > i0;
+    const bool small = n <= 32;
+    unsigned todo = __ballot_sync(0xffffffffu, act);
+    while (todo) {
+      const int p = __ffs(todo) - 1;
+      if (!__shfl_sync(0xffffffffu, small, p)) {
+        // a bin sorted in place: its share in slices of 32
+        const u64 src = rbase + __shfl_sync(0xffffffffu, s, p);
+        const u32 a0 = __shfl_sync(0xffffffffu, i0, p), a1 = __shfl_sync(0xffffffffu, i1, p);
+        for (u32 t = a0; t < a1; t += 32) {
+          const bool on = t + lane < a1;
+          u64 kk = 0, vv = 0;
+          if (on) {
+            kk = k[src + t + lane];
+            vv = v[src + t + lane];
+          }
+          step(on, kk, vv);
+        }
+        todo &= todo - 1;
+        continue;
+      }
+      // consecutive small bins from p with at most 32 candidates in all
+      const u32 xx = (lane >= p && act) ? (small ? n : 64u) : 0u;
+      u32 incl = xx;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned over = __ballot_sync(0xffffffffu, incl > 32);
+      const int e = over ? __ffs(over) - 1 : 32;  // batch = active bins in [p, e)
+      const bool inb = lane >= p && lane < e && act;
+      const u32 excl = incl - xx;
+      const u32 total = __shfl_sync(0xffffffffu, incl, e - 1);
+      s_mark[warp][lane] = -1;
+      __syncwarp();
+      if (inb) s_mark[warp][excl] = lane;
+      __syncwarp();
+      int jj = s_mark[warp][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, jj, o);
+        if (lane >= o && y > jj) jj = y;
+      }
+      __syncwarp();
+      const bool has = (u32)lane < total;
+      const int src = has ? jj : 0;
+      const u32 bs = __shfl_sync(0xffffffffu, s, src);
+      const u32 bex = __shfl_sync(0xffffffffu, excl, src);
+      u64 kk = 0, vv = 0;
+      u32 g = ~0u;
+      if (has) {
+        const u64 a = rbase + bs + (lane - bex);
+        kk = k[a];
+        vv = v[a];
+        g = (u32)jj;
+      }
+      // bin g's records occupy lanes [gex, gex + gn); order each bin by
+      // (canon k, v, k) = rec_less: a record's new lane is gex + the number
+      // of its bin's records below it (ties by lane), gn compares each
+      const int gs = has ? (int)g : 0;
+      const u32 gex = __shfl_sync(0xffffffffu, excl, gs);
+      const u32 gn_all = __shfl_sync(0xffffffffu, n, gs);  // (all lanes shuffle)
+      const u32 gn = has ? gn_all : 1u;
+      u32 maxn = gn;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxn = max(maxn, __shfl_xor_sync(0xffffffffu, maxn, o));
+      if (maxn > 8) {
+        // a bin of many records: one bitonic pass over the batch, by (bin, record)
+        warp_sort_records(region, g, kk, vv);
+      } else if (maxn > 1) {
+        // few records per bin: rank by counting (canonical k first, the
+        // rest of rec_less only on a tie)
+        const u64 cc = canon_k(region, kk);
+        s_pc[warp][lane] = cc;
+        s_pk[warp][lane] = kk;
+        s_pv[warp][lane] = vv;
+        __syncwarp();
+        u32 rank = 0;
+        if (has) {
+          for (u32 j = 0; j < gn; ++j) {
+            const u32 o = gex + j;
+            const u64 oc = s_pc[warp][o];
+            bool less = oc < cc;
+            if (oc == cc && o != (u32)lane) {
+              const u64 ov = s_pv[warp][o], ok = s_pk[warp][o];
+              less = ov < vv || (ov == vv && (ok < kk || (ok == kk && o < (u32)lane)));
+            }
+            rank += less;
+          }
+        }
+        __syncwarp();
+        if (has) {
+          s_pk[warp][gex + rank] = kk;
+          s_pv[warp][gex + rank] = vv;
+        }
+        __syncwarp();
+        if (has) {
+          kk = s_pk[warp][lane];
+          vv = s_pv[warp][lane];
+        }
+        __syncwarp();
+      }
+      // lane order is now (bin, record); keep each bin's share
+      const u32 g0 = __shfl_sync(0xffffffffu, i0, gs), g1 = __shfl_sync(0xffffffffu, i1, gs);
+      const u32 idx = (u32)lane - gex;
+      step(has && idx >= g0 && idx < g1, kk, vv);
+      todo &= ~__ballot_sync(0xffffffffu, inb);
+    }
+   }
+    __syncwarp();  // s_list is rewritten next round
   }
-  uint4* o = reinterpret_cast<uint4*>(cpos + boff + b0);
-  o[0] = make_uint4(cps[0], cps[1], cps[2], cps[3]);
-  o[1] = make_uint4(cps[4], cps[5], cps[6], cps[7]);
-  if (b0 + kBinPer == nb) region_end[r] = cp;
+
+  if (lane == 0) {
+    chunk_kept[c] = kept;
+    if (kept) {
+      atomicAdd(&group_kept[c >> 8], kept);
+      atomicAdd(&kept_counts[r], (unsigned long long)kept);
+    }
+  }
 }
 
-// One warp per 32 consecutive bins: consecutive bins whose candidates fit
-// in 32 lanes form one batch, loaded one record per lane, sorted once by
-// (bin, record) and stored densely; bins above 32 candidates were sorted in
-// place and are copied.
-__global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
-                                                   const u64* __restrict__ v,
-                                                   const u32* __restrict__ bcur,
-                                                   const u32* __restrict__ bstart,
-                                                   const u32* __restrict__ cpos, const FilterPlan* __restrict__ P_p,
-                                                   u64* __restrict__ ck, u64* __restrict__ cv) {
-  const FilterPlan& P = *P_p;
-  __shared__ int s_mark[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u32 gb = (blockIdx.x * 8 + warp) * 32;  // first bin (all regions)
-  if (gb >= (4u << P.log2nb)) return;
-  const u32 r = gb >> P.log2nb;
-  if (P.spa.m[r] == 0) return;
-  const u32 b = gb + lane;
-  const u32 n = bcur[b];
-  unsigned todo = __ballot_sync(0xffffffffu, n > 0);
-  if (!todo) return;
-  const u32 s = bstart[b];
-  const u32 cp = cpos[b];
-  const bool act = n > 0;
-  const bool small = n <= 32;
-  const int region = (int)r + 1;
-  const u64 rbase = P.spa.off[r];
-  while (todo) {
-    const int p = __ffs(todo) - 1;
-    if (!__shfl_sync(0xffffffffu, small, p)) {
-      const u64 src = rbase + __shfl_sync(0xffffffffu, s, p);
-      const u32 dst = __shfl_sync(0xffffffffu, cp, p), len = __shfl_sync(0xffffffffu, n, p);
-      for (u32 i = lane; i < len; i += 32) {
-        ck[dst + i] = k[src + i];
-        cv[dst + i] = v[src + i];
-      }
-      todo &= todo - 1;
-      continue;
-    }
-    const u32 xx = (lane >= p && act) ? (small ? n : 64u) : 0u;
-    u32 incl = xx;
+// Places each chunk's kept records (from k_spa_chunks' scratch) at its
+// output offset: the kept counts of the earlier groups of 256 chunks plus
+// those of the earlier chunks of its own group. Decoded to points.
+__global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__ P_p,
+                                                  const u64* __restrict__ sk,
+                                                  const u64* __restrict__ sv,
+                                                  const u32* __restrict__ chunk_kept,
+                                                  const u32* __restrict__ group_kept,
+                                                  double2* __restrict__ out) {
+  const SpaPlan& plan = P_p->spa;
+  const int lane = threadIdx.x & 31;
+  const u32 c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= plan.total_chunks) return;
+  const u32 kept = chunk_kept[c];
+  if (kept == 0) return;
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const u32 lo = (c - plan.chunk_begin[r]) * (u32)plan.chunk_size[r];
+  const u32 g = c >> 8;
+  u32 x = 0;
+  for (u32 i = lane; i < g; i += 32) x += group_kept[i];
+  for (u32 i = (g << 8) + lane; i < c; i += 32) x += chunk_kept[i];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const unsigned over = __ballot_sync(0xffffffffu, incl > 32);
-    const int e = over ? __ffs(over) - 1 : 32;  // batch = active bins in [p, e)
-    const bool inb = lane >= p && lane < e && act;
-    const u32 excl = incl - xx;
-    const u32 total = __shfl_sync(0xffffffffu, incl, e - 1);
-    s_mark[warp][lane] = -1;
-    __syncwarp();
-    if (inb) s_mark[warp][excl] = lane;
-    __syncwarp();
-    int jj = s_mark[warp][lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, jj, o);
-      if (lane >= o && y > jj) jj = y;
-    }
-    __syncwarp();
-    const bool has = (u32)lane < total;
-    const int src = has ? jj : 0;
-    const u32 bs = __shfl_sync(0xffffffffu, s, src);
-    const u32 bex = __shfl_sync(0xffffffffu, excl, src);
-    u64 kk = 0, vv = 0;
-    u32 g = ~0u;
-    if (has) {
-      const u64 a = rbase + bs + (lane - bex);
-      kk = k[a];
-      vv = v[a];
-      g = (u32)jj;
-    }
-    // one record per bin: lane order is already (bin, record) order
-    if (__any_sync(0xffffffffu, inb && n > 1)) warp_sort_records(region, g, kk, vv);
-    // bin g's records now occupy lanes [excl_g, excl_g + n_g) in order
-    const int gs = has ? (int)g : 0;
-    const u32 gex = __shfl_sync(0xffffffffu, excl, gs);
-    const u32 gcp = __shfl_sync(0xffffffffu, cp, gs);
-    if (has) {
-      ck[gcp + (lane - gex)] = kk;
-      cv[gcp + (lane - gex)] = vv;
-    }
-    todo &= ~__ballot_sync(0xffffffffu, inb);
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const u64 src = plan.off[r] + lo;
+  for (u32 i = lane; i < kept; i += 32) {
+    double px, py;
+    decode_point(region, sk[src + i], sv[src + i], px, py);
+    out[x + i] = make_double2(px, py);
   }
 }
 
@@ -718,54 +877,24 @@ __global__ __launch_bounds__(256) void k_cand_copy(const u64* __restrict__ k,
 // counts and the quad, so the host enqueues the whole path without waiting
 // for K2. A degenerate frame (no SPA, pipeline.cpp:53-71) leaves every
 // region empty and the path idle.
-__global__ void k_filter_plan(const QuadInfo* __restrict__ qinfo, const u32* __restrict__ counts,
-                              u64 chunk_count, int log2nb, FilterPlan* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const QuadInfo qi = *qinfo;
-  FilterPlan P;
-  P.log2nb = log2nb;
-  u64 m[4];
-  for (int r = 0; r < 4; ++r) m[r] = qi.degenerate ? 0ull : (u64)counts[r];
-  u64 off = 0;
-  u32 chunks = 0;
-  for (int r = 0; r < 4; ++r) {
-    P.spa.off[r] = off;
-    off += m[r];
-    P.spa.m[r] = m[r];
-    P.spa.chunk_begin[r] = chunks;
-    const u64 cs = m[r] ? (m[r] + chunk_count - 1) / chunk_count : 1;  // spa.cpp:121
-    P.spa.chunk_size[r] = cs;
-    if (m[r]) chunks += (u32)((m[r] + cs - 1) / cs);                   // spa.cpp:122
-    // guarded(region, anchors.first): LL left.y, LR bottom.x, UR right.y, UL top.x
-    const double seed = (r == 0 || r == 2) ? qi.q[2 * r + 1] : qi.q[2 * r];
-    P.spa.seed[r] = seed;
-    const int reg = r + 1;
-    P.seed_w[r] = wkey(reg, (reg == 1 || reg == 4) ? ~ord_enc(seed) : ord_enc(seed));
-  }
-  P.spa.total_chunks = chunks;
-  *out = P;
-}
-
 // ------------------------------------------------------------------ launchers
 
-void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count,
-                        int log2nb, FilterPlan* out, cudaStream_t st) {
-  k_filter_plan<<<1, 32, 0, st>>>(qinfo, counts, chunk_count, log2nb, out);
-}
-
-void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
-                     u64* bthr, u32* first_bin, FilterAux aux, cudaStream_t st) {
+void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
+                     const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
+                     u32* first_bin, FilterAux aux, u32* bar, cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
-  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, log2nb, aux.tsum);
-  k_bin_starts<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, aux.tsum, P, bstart, first_bin,
-                                                  aux.agg_seg, aux.agg_val);
-  k_bin_thresholds<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bw, bstart, P, aux.agg_seg,
-                                                      aux.agg_val, bthr);
+  dim3 grid(4 * tiles), block(kBinThreads);
+  void* args[] = {(void*)&qinfo, (void*)&counts, (void*)&chunk_count, (void*)&log2nb,
+                  (void*)&bcnt, (void*)&bw, (void*)&plan, (void*)&bstart, (void*)&bthr,
+                  (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar};
+  // cooperative: the launch fails rather than run with a CTA not resident
+  cudaLaunchCooperativeKernel((const void*)k_bin_scan, grid, block, args, 0, st);
 }
 
 void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
-                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
-                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st) {
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
+                   u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
+                   cudaStream_t st) {
   if (nseg == 0) return;
   // one resident wave: the warp-stride loop then has no partial last wave
   static int resident = 0;
@@ -775,8 +904,8 @@ void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const Filter
   }
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
                                    (u32)resident);
-  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segcnt, nseg, P, qinfo, bstart, bthr, bcur, kout,
-                                              vout, big, nbig, ncand);
+  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segcnt, nseg, P, qinfo, bstart, bthr, bcur, bmap,
+                                              kout, vout, big, nbig, ncand);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
@@ -792,14 +921,17 @@ void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart,
                                                                 big + kBigListB, nbig + 1, overflow);
 }
 
-void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
-                         const u32* bstart, const FilterPlan* P, int log2nb, u64* ck, u64* cv,
-                         u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st) {
-  const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
-  k_bin_tile_sums<<<4 * tiles, kBinThreads, 0, st>>>(bcur, log2nb, aux.csum);
-  k_cand_positions<<<4 * tiles, kBinThreads, 0, st>>>(bcnt, bcur, bstart, aux.csum, P, cpos,
-                                                      first_cand, aux.region_end);
-  k_cand_copy<<<(4u << log2nb) / 256, 256, 0, st>>>(k, v, bcur, bstart, cpos, P, ck, cv);
+void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
+                       const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
+                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                       unsigned long long* kept_counts, double2* out, cudaStream_t st) {
+  if (max_chunks == 0) return;
+  const u32 blocks = (max_chunks + 7) / 8;
+  cudaMemsetAsync(group_kept, 0, ((max_chunks + 255) / 256) * sizeof(u32), st);
+  k_spa_chunks<<<blocks, 256, 0, st>>>(k, v, bcur, bstart, bmap, first_bin, P, sk, sv, chunk_kept,
+                                       group_kept, kept_counts);
+  k_spa_emit<<<blocks, 256, 0, st>>>(P, sk, sv, chunk_kept, group_kept, out);
 }
+
 
 }  // namespace chgpu

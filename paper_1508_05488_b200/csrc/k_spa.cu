@@ -25,12 +25,6 @@ constexpr int kSpaThreads = 256;
 constexpr int kSpaItems = 16;
 constexpr int kSpaTile = kSpaThreads * kSpaItems;
 
-__device__ __forceinline__ double op_ext(bool is_min, double a, double b) {
-  return is_min ? (b < a ? b : a) : (b > a ? b : a);
-}
-__device__ __forceinline__ bool steps_back(bool is_min, double g, double t) {
-  return is_min ? (g > t) : (g < t);  // spa.cpp:92-105
-}
 
 // Block-wide exclusive scan with op_ext; returns the exclusive value for
 // this thread and the block aggregate in *agg.
@@ -307,105 +301,6 @@ __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ 
   for (u32 i = lane; i < kc; i += 32) out[o + i] = scratch[begin + i];
 }
 
-// ------------------------------------------------------------------ SPA over dense candidates
-//
-// Same scan as k_spa_warp, over the pre-filter's candidates (k_filter.cu):
-// they are in region_less order in (ck, cv) and chunk c owns the dense
-// range [first_cand[c], first_cand[c + 1]) (the region's end for its last
-// chunk). One warp per chunk, 32 records per step, the running extremum in
-// a register. Chunks are taken in order from a counter; a chunk counts its
-// kept records, publishes the count, finds its output offset with a
-// decoupled look-back over the preceding chunks (the serial compaction of
-// spa.cpp:158-161, across all four regions), and rescans its candidates
-// writing the kept points, decoded, straight to their final place.
-__global__ __launch_bounds__(256) void k_spa_dense(const u64* __restrict__ ck,
-                                                   const u64* __restrict__ cv,
-                                                   const FilterPlan* __restrict__ P_p,
-                                                   const u32* __restrict__ first_cand,
-                                                   const u32* __restrict__ region_end,
-                                                   u64* __restrict__ status, u32 tag,
-                                                   u32* __restrict__ chunk_ctr,
-                                                   unsigned long long* __restrict__ kept_counts,
-                                                   double2* __restrict__ out) {
-  const SpaPlan& plan = P_p->spa;
-  const int lane = threadIdx.x & 31;
-  u32 c = 0;
-  if (lane == 0) c = atomicAdd(chunk_ctr, 1u);
-  c = __shfl_sync(0xffffffffu, c, 0);
-  if (c >= plan.total_chunks) return;
-  int r = 0;
-  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
-  const int region = r + 1;
-  const u32 cl = c - plan.chunk_begin[r];
-  const u32 nchunks = (r < 3 ? plan.chunk_begin[r + 1] : plan.total_chunks) - plan.chunk_begin[r];
-  const u32 beg = first_cand[c];
-  const u32 end = cl + 1 < nchunks ? first_cand[c + 1] : region_end[r];
-  const bool is_min = (region == 1 || region == 4);
-  const double ident = is_min ? INFINITY : -INFINITY;
-  const double seed = (cl == 0) ? plan.seed[r] : ident;
-
-  // One pass of the scan; emit(kk, vv, pos) for each kept record.
-  auto scan = [&](auto emit) -> u32 {
-    double carry = seed;
-    u32 kept = 0;
-    u64 nk = 0, nv = 0;
-    if (beg + lane < end) {
-      nk = ck[beg + lane];
-      nv = cv[beg + lane];
-    }
-    for (u32 t = beg; t < end; t += 32) {
-      const bool active = t + lane < end;
-      const u64 kk = nk, vv = nv;
-      if (t + 32 + lane < end) {  // next step's records in flight during this scan
-        nk = ck[t + 32 + lane];
-        nv = cv[t + 32 + lane];
-      }
-      const double g = active ? guarded_of(region, vv) : ident;
-      double incl = g;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = op_ext(is_min, y, incl);
-      }
-      double ex = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) ex = ident;
-      const double th = op_ext(is_min, carry, ex);
-      const bool keep = active && !steps_back(is_min, g, th);
-      carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, incl, 31));
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      if (keep) emit(kk, vv, kept + __popc(km & lanemask_lt()));
-      kept += __popc(km);
-    }
-    return kept;
-  };
-
-  const u32 kept = scan([](u64, u64, u32) {});
-  u32 excl = 0;
-  if (c == 0) {
-    if (lane == 0) store_status(status, make_status(tag, kFlagPrefix, kept));
-  } else {
-    if (lane == 0) store_status(status + c, make_status(tag, kFlagAgg, kept));
-    excl = warp_lookback(status, 1, (int)c, 0, tag);
-    if (lane == 0) store_status(status + c, make_status(tag, kFlagPrefix, excl + kept));
-  }
-  if (lane == 0 && kept) atomicAdd(&kept_counts[r], (unsigned long long)kept);
-  if (kept)
-    scan([&](u64 kk, u64 vv, u32 pos) {
-      double px, py;
-      decode_point(region, kk, vv, px, py);
-      out[excl + pos] = make_double2(px, py);
-    });
-}
-
-void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max_chunks,
-                      const u32* first_cand, const u32* region_end, u64* status, u32 tag,
-                      u32* chunk_ctr, unsigned long long* kept_counts, double2* out,
-                      cudaStream_t st) {
-  if (max_chunks == 0) return;
-  const u32 blocks = (max_chunks + 7) / 8;
-  k_spa_dense<<<blocks, 256, 0, st>>>(ck, cv, P, first_cand, region_end, status, tag, chunk_ctr,
-                                      kept_counts, out);
-}
 
 void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
                      double2* scratch, u32* chunk_kept, u32* offs,

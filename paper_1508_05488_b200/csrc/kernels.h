@@ -46,29 +46,23 @@ struct FilterPlan {
 // Small per-call scratch of the pre-filter (<= 512 bin tiles).
 struct FilterAux {
   u32* tsum;        // records per bin tile
-  u32* csum;        // candidates per bin tile
   u32* agg_seg;     // tile aggregates of the segmented max
   u64* agg_val;
-  u32* region_end;  // [4] dense end of each region's candidates
 };
 // The plan of the filter path on the device (from K2's counts).
-void launch_filter_plan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count,
-                        int log2nb, FilterPlan* out, cudaStream_t st);
-void launch_bin_scan(const u32* bcnt, const u64* bw, const FilterPlan* P, int log2nb, u32* bstart,
-                     u64* bthr, u32* first_bin, FilterAux aux, cudaStream_t st);
+void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
+                     const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
+                     u32* first_bin, FilterAux aux, u32* bar, cudaStream_t st);
+void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
+                       const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
+                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                       unsigned long long* kept_counts, double2* out, cudaStream_t st);
 void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
-                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u64* kout,
-                   u64* vout, u32* big, u32* nbig, unsigned long long* ncand, cudaStream_t st);
+                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
+                   u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
+                   cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
-void launch_cand_compact(const u64* k, const u64* v, const u32* bcnt, const u32* bcur,
-                         const u32* bstart, const FilterPlan* P, int log2nb, u64* ck, u64* cv,
-                         u32* first_cand, u32* cpos, FilterAux aux, cudaStream_t st);
-void launch_spa_dense(const u64* ck, const u64* cv, const FilterPlan* P, u32 max_chunks,
-                      const u32* first_cand, const u32* region_end, u64* status, u32 tag,
-                      u32* chunk_ctr, unsigned long long* kept_counts, double2* out,
-                      cudaStream_t st);
-
 // Melkman's convex-position trajectory on the device (k_convex.cu).
 int convex_blocks();
 void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInfo* qinfo, u32* ok,

@@ -52,6 +52,10 @@ struct Pinned {
 constexpr int kMaxFilterBits = 18;
 constexpr size_t kConvexMin = size_t(1) << 16;  // ring size from which k_convex.cu is tried  // SPA pre-filter: at most 2^18 bins per region
 
+// d_ftab: per bin a max w (u64), a record count and a candidate count
+// (u32 each), then the candidate-bin bitmap.
+size_t filter_tab_bytes(int log2nb) { return (size_t(4) << log2nb) * 16 + (size_t(4) << log2nb) / 8; }
+
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
@@ -106,7 +110,7 @@ struct chgpu_ctx {
   unsigned char* d_faux = nullptr;  // FilterAux scratch (bin-tile sums and aggregates)
   u64* d_ck = nullptr;       // dense candidates (k words)    [cap]
   u64* d_cv = nullptr;       // dense candidates (v words)    [cap]
-  u32* d_ffirst = nullptr;   // per-chunk first bin
+  u32* d_ffirst = nullptr;   // per-chunk first dense candidate
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
@@ -785,6 +789,7 @@ struct FilterTabs {
   u64* w;
   u32* cnt;
   u32* cur;
+  u32* bmap;  // one bit per bin: the bin holds a candidate
 };
 FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
   const size_t nbt = size_t(4) << log2nb;
@@ -792,6 +797,7 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
   t.w = reinterpret_cast<u64*>(ctx->d_ftab);
   t.cnt = reinterpret_cast<u32*>(t.w + nbt);
   t.cur = t.cnt + nbt;
+  t.bmap = t.cur + nbt;
   return t;
 }
 
@@ -807,45 +813,43 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
   cudaStream_t st = ctx->st;
   const FilterPlan* P = ctx->d_plan;
   const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
-  if (2 * (size_t)max_chunks > ctx->ffirst_cap) {
+  if ((size_t)max_chunks > ctx->ffirst_cap) {
     cudaFree(ctx->d_ffirst);
     ctx->d_ffirst = nullptr;
-    const size_t want = std::max<size_t>(2 * (size_t)max_chunks, 8192);
+    const size_t want = std::max<size_t>((size_t)max_chunks, 8192);
     CK(cudaMalloc(&ctx->d_ffirst, want * sizeof(u32)));
     ctx->ffirst_cap = want;
   }
   u32* first_bin = ctx->d_ffirst;
-  u32* first_cand = ctx->d_ffirst + max_chunks;
   FilterAux aux;
   aux.tsum = reinterpret_cast<u32*>(ctx->d_faux);
-  aux.csum = aux.tsum + 512;
-  aux.agg_seg = aux.csum + 512;
-  aux.region_end = aux.agg_seg + 512;
+  aux.agg_seg = aux.tsum + 512;
   aux.agg_val = reinterpret_cast<u64*>(ctx->d_faux + 8192);
   const FilterTabs t = filter_tabs(ctx, log2nb);
   const int nbig_slot = take_ctr(ctx), nbig2_slot = take_ctr(ctx);
   (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
   *ovf_slot = take_ctr(ctx);
-  launch_filter_plan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb,
-                     ctx->d_plan, st);
-  launch_bin_scan(t.cnt, t.w, P, log2nb, ctx->d_fstart, ctx->d_fthr, first_bin, aux, st);
+  // plan + bin starts + thresholds: one cooperative launch
+  launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
+                  ctx->d_plan, ctx->d_fstart, ctx->d_fthr, first_bin, aux, ctx->d_ctr + take_ctr(ctx),
+                  st);
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: points in kbuf, group sizes in vbuf
   launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf), ctx->d_vbuf,
                 (u32)((n + kSegPts - 1) / kSegPts), P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
-                t.cur, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot, ctx->d_u64 + 11, st);
+                t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
+                ctx->d_u64 + 11, st);
   CK(cudaEventRecord(ctx->ev[4], st));
   launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
                       ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, st);
-  // the bin thresholds are dead once the filter ran: their table holds the
-  // dense positions now
-  launch_cand_compact(ctx->d_ka, ctx->d_va, t.cnt, t.cur, ctx->d_fstart, P, log2nb, ctx->d_ck,
-                      ctx->d_cv, first_cand, reinterpret_cast<u32*>(ctx->d_fthr), aux, st);
   CK(cudaEventRecord(ctx->ev[5], st));
   CK(cudaEventRecord(ctx->ev[6], st));
-  launch_spa_dense(ctx->d_ck, ctx->d_cv, P, max_chunks, first_cand, aux.region_end, ctx->d_status,
-                   next_tag(ctx), ctx->d_ctr + take_ctr(ctx), ctx->d_u64, ctx->d_kept, st);
-  ctx->launches += 12;
+  // per-chunk SPA over the sparse candidates, kept records via d_ck / d_cv
+  // (raw scratch: per-chunk kept counts, then their sums per 256 chunks)
+  launch_spa_chunks(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, max_chunks,
+                    ctx->d_ck, ctx->d_cv, ctx->d_raw, ctx->d_raw + max_chunks, ctx->d_u64,
+                    ctx->d_kept, st);
+  ctx->launches += 6;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[8], st));
   return CHGPU_OK;
@@ -1058,7 +1062,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
        (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
   const int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
   if (want_filter)
-    CK(cudaMemsetAsync(ctx->d_ftab, 0, (size_t(4) << log2nb) * 16, st));
+    CK(cudaMemsetAsync(ctx->d_ftab, 0, filter_tab_bytes(log2nb), st));
   const FilterTabs ftabs = filter_tabs(ctx, log2nb);
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
@@ -1072,7 +1076,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
                             ctx->cap, ctx->d_ctr + cnt_slot, st);
   }
-  ctx->launches += 2;
+  ctx->launches += 1;  // K2 (K1 counted at its launch)
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[2], st));
   // The filter path is enqueued before the host sees K2's results (it idles
@@ -1333,7 +1337,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_bbase, (size_t(4) << kMaxBucketBits) * sizeof(u64))) ||
       bad(cudaMalloc(&ctx->d_bcur, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_big, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
-      bad(cudaMalloc(&ctx->d_ftab, (size_t(4) << kMaxFilterBits) * 16)) ||
+      bad(cudaMalloc(&ctx->d_ftab, filter_tab_bytes(kMaxFilterBits))) ||
       bad(cudaMalloc(&ctx->d_fstart, (size_t(4) << kMaxFilterBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_fthr, (size_t(4) << kMaxFilterBits) * sizeof(u64))) ||
       bad(cudaMalloc(&ctx->d_fbig, 2 * (size_t)kBigListB * sizeof(u32))) ||
@@ -1685,7 +1689,7 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     // The pre-filtered SPA against the global quad (the same kernels as
     // chgpu_hull), falling back to the full region sort on overflow.
     const int log2nb = filter_bits(n, chunk_count);
-    CK(cudaMemsetAsync(ctx->d_ftab, 0, (size_t(4) << log2nb) * 16, st));
+    CK(cudaMemsetAsync(ctx->d_ftab, 0, filter_tab_bytes(log2nb), st));
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
     ctx->ctr_used += 5;

@@ -1,19 +1,29 @@
 #!/bin/bash
-# Builds libchgpu variants of one .cu file with extra -D flags:
-#   tools/build_variants.sh k_filter "A:-DX=1 -DY=2" "B:-DX=2" ...
-# -> build/variants/libchgpu_A.so ... (swap in place of paper_1508_05488_b200/libchgpu.so to A/B).
+# Builds libchgpu variants with extra -D flags, for A/B timing on the GPU box:
+#   tools/build_variants.sh <src|ALL> "A:-DX=1 -DY=2" "B:-DX=2" ...
+# <src> (e.g. k_filter) recompiles that one .cu; ALL recompiles every .cu.
+# -> build/variants/libchgpu_A.so ... (tools/ab_variants.sh swaps them in).
 set -e
 cd "$(dirname "$0")/.."
 make -s >/dev/null
 src=$1; shift
 mkdir -p build/variants
-others=$(ls build/*.o | grep -v "/$src" | grep -v "/api_" | grep -v acceptance)
+NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a"
+FL="-O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_1508_05488_b200/csrc"
+CU="k_discard k_sort k_bucket k_spa k_filter k_convex pipeline"
 for v in "$@"; do
   name=${v%%:*}; flags=${v#*:}
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 \
-    -Xcompiler -fPIC -Iinclude -Ipaper_1508_05488_b200/csrc $flags -c -o build/variants/$src.$name.o \
-    paper_1508_05488_b200/csrc/$src.cu
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/libchgpu_$name.so \
-    build/variants/$src.$name.o $others -Xlinker -soname=libchgpu.so
+  if [ "$src" = ALL ]; then redo=$CU; else redo=$src; fi
+  objs=""
+  for c in $CU; do
+    if echo " $redo " | grep -q " $c "; then
+      $NV $FL $flags -c -o build/variants/$c.$name.o paper_1508_05488_b200/csrc/$c.cu
+      objs="$objs build/variants/$c.$name.o"
+    else
+      objs="$objs build/$c.o"
+    fi
+  done
+  $NV -shared -o build/variants/libchgpu_$name.so $objs build/finisher.o build/datasets.o \
+    -Xlinker -soname=libchgpu.so
   echo built $name
 done
