@@ -310,11 +310,18 @@ __device__ __forceinline__ double bin_scale(double span, int log2nb) {
 }
 
 // Bin of a record of region ri + 1 with primary coordinate p:
-// trunc(clamp((p - lo) * scale, 0, top)) in the region's sort direction.
-// The float->int conversion saturates (negative and NaN -> 0), then the top
-// clamps. One dependent multiply: this sits on K2's per-survivor path.
-__device__ __forceinline__ u32 bin_of(double lo, double scale, u32 top, u32 ri, double p) {
-  const u32 b = min((u32)__double2uint_rz(__dmul_rn(__dsub_rn(p, lo), scale)), top);
+// trunc(clamp((p - lo) * scale, 0, top)) in the region's sort direction
+// (NaN -> 0). One dependent multiply: this sits on K2's per-survivor path.
+//
+// The conversion runs on the FP64 pipe, not the (narrow) XU pipe: clamp to
+// [0, top] (fmax maps NaN to 0), then add 2^52 rounding toward zero, which
+// leaves trunc(t) in the low mantissa bits. Same bin as
+// min(__double2uint_rz(t), top) for every t.
+__device__ __forceinline__ u32 bin_of(double lo, double scale, u32 top, double topd, u32 ri,
+                                      double p) {
+  double t = __dmul_rn(__dsub_rn(p, lo), scale);
+  t = fmin(fmax(t, 0.0), topd);  // topd = (double)top, hoisted by the caller
+  const u32 b = (u32)__double_as_longlong(__dadd_rz(t, 4503599627370496.0));
   return ri >= 2 ? top - b : b;  // UR / UL sort descending
 }
 

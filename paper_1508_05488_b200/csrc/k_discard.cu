@@ -217,7 +217,9 @@ __device__ __forceinline__ int classify(const QuadEdges& e, double px, double py
                 (u32)(cross_edge(e.ax[1], e.ay[1], e.ex[1], e.ey[1], px, py) < 0.0) << 1 |
                 (u32)(cross_edge(e.ax[2], e.ay[2], e.ex[2], e.ey[2], px, py) < 0.0) << 2 |
                 (u32)(cross_edge(e.ax[3], e.ay[3], e.ex[3], e.ey[3], px, py) < 0.0) << 3;
-  return __ffs(m);  // 0 when no edge has the point on its right (Interior)
+  // lowest set bit + 1 (0: no edge has the point on its right, Interior)
+  // from a 16-entry table of 3-bit fields: ALU shifts, not the XU pipe's FLO
+  return (int)((0x28b28c28b288ull >> (3 * m)) & 7u);
 }
 
 // Two-ended stream layout: streams 1 and 2 share kbuf[0, ncap) growing
@@ -391,9 +393,9 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 sidx = blockIdx.x * (kK2Threads / 32) + warp;
   const u32 base = sidx * kSegPts;  // n < 2^32
-  double2 p[kK2Items];
+  double2 p[kSegItems];
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
+  for (int j = 0; j < kSegItems; ++j) {
     const u32 idx = base + j * 32 + lane;
     p[j] = idx < n ? ldg_stream(pts + idx) : make_double2(0.0, 0.0);
   }
@@ -414,7 +416,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   u32 codes = 0;  // 3 bits of stream id per item
   u64 cnt = 0;    // 16-bit count per stream
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
+  for (int j = 0; j < kSegItems; ++j) {
     const u32 idx = base + j * 32 + lane;
     int r = idx < n ? classify(e, p[j].x, p[j].y) : 0;
     if (lex && r != 0) r = 1;
@@ -441,7 +443,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     u32 pp = s_base + (u32)((incl - cnt) & 0xFFFFu);
     for (int w = 0; w < warp; ++w) pp += (u32)s_segT[w] & 0xFFFFu;
 #pragma unroll
-    for (int j = 0; j < kK2Items; ++j) {
+    for (int j = 0; j < kSegItems; ++j) {
       if (!((codes >> (3 * j)) & 7)) continue;
       kbuf[pp] = ord_enc(p[j].x);
       vbuf[pp] = ord_enc(p[j].y);
@@ -456,8 +458,9 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   u64 pos = (T << 16) + (T << 32) + (T << 48) + (incl - cnt);
   double2* out = seg + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
+  const double topd = (double)top;
 #pragma unroll
-  for (int j = 0; j < kK2Items; ++j) {
+  for (int j = 0; j < kSegItems; ++j) {
     const u32 r = (codes >> (3 * j)) & 7;
     if (!r) continue;
     const u32 ri = r - 1, sh = 16 * ri;
@@ -466,7 +469,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     out[slot] = p[j];
     const bool odd = (r & 1u) != 0;
     const double prim = odd ? p[j].x : p[j].y;  // LL, UR: x; LR, UL: y
-    const u32 b = (ri << log2nb) | bin_of(s_lo[ri], s_scale[ri], top, ri, prim);
+    const u32 b = (ri << log2nb) | bin_of(s_lo[ri], s_scale[ri], top, topd, ri, prim);
     atomicAdd(bcnt + b, 1u);
     // any subset of a bin's records gives a valid (lower) max: sample; w =
     // wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
@@ -572,7 +575,8 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, double2* seg,
                                u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
                                u32* bcnt, u64* bw, u32 wmask, cudaStream_t st) {
-  const u32 tiles = (n + kK2Tile - 1) / kK2Tile;
+  constexpr u32 tile = kK2Threads / 32 * kSegPts;  // one segment per warp
+  const u32 tiles = (n + tile - 1) / tile;
   if (tiles == 0) return;
   k_classify_survivors<<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, seg, segcnt, kbuf, vbuf,
                                                      counts_out, log2nb, bcnt, bw, wmask);

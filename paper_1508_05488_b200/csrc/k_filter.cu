@@ -401,6 +401,7 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
   }
   __syncthreads();
   const u32 lg = s_lg, top = (1u << lg) - 1u;
+  const double topd = (double)top;
   nseg = s_nseg;
   const int lane = threadIdx.x & 31;
   const u32 wstride = gridDim.x * (kFilterThreads / 32);
@@ -427,7 +428,7 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
         const u32 sl = s0 + j * 32 + lane;
         const u32 r = rr[j];
         const double prim = (r & 1u) ? p[j].y : p[j].x;  // LL, UR: x; LR, UL: y
-        bi[j] = (r << lg) | bin_of(s_lo[r], s_scale[r], top, r, prim);
+        bi[j] = (r << lg) | bin_of(s_lo[r], s_scale[r], top, topd, r, prim);
         th[j] = sl < tot ? __ldg(bthr + bi[j]) : ~0ull;
       }
 #pragma unroll
