@@ -359,7 +359,9 @@ def main():
                          "n_after_spa": r.stats.n_after_spa, "n_hull": r.stats.n_hull,
                          "frac_after_round1": r.stats.n_after_round1 / n}
         line["gpu_launches"] = d.launches * args.steps
-        d2h = 16 * (r.stats.n_after_spa + r.stats.n_hull)
+        # device -> host: the kept chains (the host finisher builds the hull),
+        # or on the convex fast path the finished hull alone
+        d2h = 16 * (r.stats.n_hull if d.convex_fast_path else sum(d.kept_counts))
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 16,
                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                        "h2d_ms": res_e2e.diag.times_ms["t_h2d_ms"]}

@@ -230,7 +230,7 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
     int log2nb, const u32* __restrict__ bcnt, const u64* __restrict__ bw,
     FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u64* __restrict__ bthr,
     u32* __restrict__ first_bin, u32* __restrict__ tsum, u32* __restrict__ agg_seg,
-    u64* __restrict__ agg_val, u32* __restrict__ bar) {
+    u64* __restrict__ agg_val, u32* __restrict__ bar, u32* __restrict__ overflow) {
   __shared__ FilterPlan sP;
   __shared__ u32 sh[kBinThreads / 32];
   __shared__ u32 sseg[kBinThreads / 32];
@@ -356,6 +356,12 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
 #pragma unroll
   for (int j = 0; j < kBinPer; j += 2)
     *reinterpret_cast<ulonglong2*>(bthr + boff + b0 + j) = make_ulonglong2(th[j], th[j + 1]);
+  // T = 0 passes every record: such a bin above kBinSortMax records is
+  // certain to overflow the bin sorts, so the filter can stand down now
+  bool certain = false;
+#pragma unroll
+  for (int j = 0; j < kBinPer; ++j) certain |= th[j] == 0 && c[j] > (u32)kBinSortMax;
+  if (certain) atomicOr(overflow, 1u);
 }
 
 // ------------------------------------------------------------------ filter
@@ -381,7 +387,8 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
     const FilterPlan* __restrict__ P_p, const QuadInfo* __restrict__ qinfo,
     const u32* __restrict__ bstart, const u64* __restrict__ bthr, u32* __restrict__ bcur,
     u32* __restrict__ bmap, u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big,
-    u32* __restrict__ nbig, unsigned long long* __restrict__ ncand) {
+    u32* __restrict__ nbig, unsigned long long* __restrict__ ncand,
+    const u32* __restrict__ overflow) {
   // The plan's per-region values, read once into shared memory (the loop's
   // stores would otherwise force re-reads from global memory per item).
   __shared__ u64 s_off[4];
@@ -395,7 +402,9 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
     s_scale[r] = bin_scale(qinfo->bspan[r], P_p->log2nb);
     if (r == 0) {
       s_lg = (u32)P_p->log2nb;
-      s_nseg = qinfo->degenerate ? 0u : nseg;  // no segments then (K2 wrote LEX records)
+      // no segments on a degenerate frame (K2 wrote LEX records), nothing to
+      // do once the bin scan saw a certain overflow
+      s_nseg = (qinfo->degenerate || *overflow) ? 0u : nseg;
       s_cand = 0;
     }
   }
@@ -882,12 +891,13 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 
 void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
-                     u32* first_bin, FilterAux aux, u32* bar, cudaStream_t st) {
+                     u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
   dim3 grid(4 * tiles), block(kBinThreads);
   void* args[] = {(void*)&qinfo, (void*)&counts, (void*)&chunk_count, (void*)&log2nb,
                   (void*)&bcnt, (void*)&bw, (void*)&plan, (void*)&bstart, (void*)&bthr,
-                  (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar};
+                  (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar,
+                  (void*)&overflow};
   // cooperative: the launch fails rather than run with a CTA not resident
   cudaLaunchCooperativeKernel((const void*)k_bin_scan, grid, block, args, 0, st);
 }
@@ -895,7 +905,7 @@ void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, 
 void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
                    const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
                    u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
-                   cudaStream_t st) {
+                   const u32* overflow, cudaStream_t st) {
   if (nseg == 0) return;
   // one resident wave: the warp-stride loop then has no partial last wave
   static int resident = 0;
@@ -906,7 +916,7 @@ void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const Filter
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
                                    (u32)resident);
   k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segcnt, nseg, P, qinfo, bstart, bthr, bcur, bmap,
-                                              kout, vout, big, nbig, ncand);
+                                              kout, vout, big, nbig, ncand, overflow);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,

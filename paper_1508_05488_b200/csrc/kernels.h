@@ -52,7 +52,7 @@ struct FilterAux {
 // The plan of the filter path on the device (from K2's counts).
 void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
-                     u32* first_bin, FilterAux aux, u32* bar, cudaStream_t st);
+                     u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st);
 void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
                        const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
                        u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
@@ -60,7 +60,7 @@ void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* b
 void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
                    const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
                    u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
-                   cudaStream_t st);
+                   const u32* overflow, cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
 // Melkman's convex-position trajectory on the device (k_convex.cu).

@@ -832,13 +832,13 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
   // plan + bin starts + thresholds: one cooperative launch
   launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
                   ctx->d_plan, ctx->d_fstart, ctx->d_fthr, first_bin, aux, ctx->d_ctr + take_ctr(ctx),
-                  st);
+                  ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: points in kbuf, group sizes in vbuf
   launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf), ctx->d_vbuf,
                 (u32)((n + kSegPts - 1) / kSegPts), P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
-                ctx->d_u64 + 11, st);
+                ctx->d_u64 + 11, ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[4], st));
   launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
                       ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, st);
@@ -1086,7 +1086,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   size_t spec = 0;
   if (want_filter) {
     TRY(enqueue_filter_spa(ctx, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
-    spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 4));
+    // (small chains only: a survivor-heavy call reads its result back once
+    // it knows the size, or not at all on the convex fast path)
+    if (ctx->kept_hint + 4 < kConvexMin)
+      spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 4));
     TRY(ensure_host_out(ctx, spec + 4));
     CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
@@ -1094,8 +1097,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
                        cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
                        cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
-                       st));
+    if (spec)
+      CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
+                         st));
     CK(cudaEventRecord(ctx->ev[9], st));
   }
   CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, st));

@@ -3,8 +3,9 @@ DRAM bytes (read + write) of each kernel, keyed like bench.py's per_kernel."""
 import csv, io, json, subprocess, sys
 
 KEYS = {"k_classify_survivors": "k2_classify_survivors", "k_filter": "k3_filter",
-        "k_extremes_partial": "k1_extremes", "k_cand_copy": "k3_cand_copy",
-        "k_spa_dense": "k4_spa_dense", "k_classify_compact": "k2_classify_compact"}
+        "k_extremes_partial": "k1_extremes", "k_bin_scan": "k3_bin_scan",
+        "k_spa_chunks": "k4_spa_chunks", "k_spa_emit": "k4_spa_emit",
+        "k_bin_sort_warp": "k3_bin_sort", "k_classify_compact": "k2_classify_compact"}
 out = {}
 for rep in sys.argv[2:]:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,

@@ -14,7 +14,7 @@ done
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/launches_uniform.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python tools/launch_summary.py $O/launches_uniform.csv > $O/launches_uniform.txt 2>&1
-for K in k_classify_survivors k_filter k_extremes_partial k_cand_copy k_spa_dense; do
+for K in k_classify_survivors k_filter k_extremes_partial k_bin_scan k_spa_chunks k_spa_emit k_bin_sort_warp; do
   ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 -o $O/full_$K \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_$K.log 2>&1
 done
