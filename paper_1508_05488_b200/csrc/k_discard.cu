@@ -430,9 +430,9 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     if (lane >= o) incl += y;
   }
   const u64 T = __shfl_sync(0xffffffffu, incl, 31);  // the segment's four group sizes
-  if (lane == 0) s_segT[warp] = T;
 
   if (lex) {  // uniform: dense stream 1 through a CTA reservation
+    if (lane == 0) s_segT[warp] = T;
     __syncthreads();
     if (tid == 0) {
       u32 sum = 0;
@@ -479,12 +479,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
       atomicMax(bw + b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     }
   }
-  __syncthreads();
-  if (tid < 4) {
-    u32 sum = 0;
-    for (int w = 0; w < kK2Threads / 32; ++w) sum += (u32)(s_segT[w] >> (16 * tid)) & 0xFFFFu;
-    if (sum) atomicAdd(&counts_out[tid + 1], sum);
-  }
+  // (region totals: the bin scan sums the bin counts)
 }
 
 // Labels only (the classify() stage tap, classify.cpp:9-33).

@@ -226,12 +226,13 @@ __device__ __forceinline__ void grid_barrier(u32* ctr, u32 g) {
 //             carry into a tile folds the aggregates of the region's earlier
 //             tiles.
 __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
-    const QuadInfo* __restrict__ qinfo, const u32* __restrict__ counts, u64 chunk_count,
+    const QuadInfo* __restrict__ qinfo, u32* __restrict__ counts, u64 chunk_count,
     int log2nb, const u32* __restrict__ bcnt, const u64* __restrict__ bw,
     FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u64* __restrict__ bthr,
     u32* __restrict__ first_bin, u32* __restrict__ tsum, u32* __restrict__ agg_seg,
     u64* __restrict__ agg_val, u32* __restrict__ bar, u32* __restrict__ overflow) {
   __shared__ FilterPlan sP;
+  __shared__ u32 s_m[4];
   __shared__ u32 sh[kBinThreads / 32];
   __shared__ u32 sseg[kBinThreads / 32];
   __shared__ u64 sval[kBinThreads / 32];
@@ -244,8 +245,7 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u32 b0 = t * kBinTile + threadIdx.x * kBinPer;
   const size_t boff = (size_t)r << log2nb;
-  // the bins first (an empty region's bins are all zero), the plan while
-  // they load
+  // the bins (an empty region's bins are all zero)
   u32 c[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
   u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (b0 < nb) {
@@ -257,14 +257,6 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
       w[j + 1] = a.y;
     }
   }
-  if (threadIdx.x == 0) {
-    const QuadInfo qi = *qinfo;
-    make_filter_plan(qi, counts, chunk_count, log2nb, sP);
-    if (blockIdx.x == 0) *plan_out = sP;
-  }
-  __syncthreads();
-  const bool active = sP.spa.m[r] != 0;  // CTA-uniform; idle CTAs still meet the barriers
-  const bool in = active && b0 < nb;
   // phase 1
   u32 x = 0;
 #pragma unroll
@@ -273,15 +265,35 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
   const u32 ex = block_excl_sum(x, sh, &tot);
   if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
   grid_barrier(bar, 0);
-  // phase 2
+  // phase 2: this tile's first rank, the region sizes (sums of the bin
+  // counts: K2 keeps no region totals of its own), then the plan
   if (warp == 0) {
     u32 y = 0;
     for (u32 i = lane; i < t; i += 32) y += __ldcg(tsum + r * tiles + i);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
     if (lane == 0) s_base = y;
+  } else if (warp <= 4) {
+    const u32 rr = warp - 1;
+    u32 y = 0;
+    for (u32 i = lane; i < tiles; i += 32) y += __ldcg(tsum + rr * tiles + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (lane == 0) s_m[rr] = y;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    const QuadInfo qi = *qinfo;
+    make_filter_plan(qi, s_m, chunk_count, log2nb, sP);
+    if (blockIdx.x == 0) {
+      *plan_out = sP;
+      if (!qi.degenerate)  // (a degenerate frame's K2 counted its LEX stream itself)
+        for (int q = 0; q < 4; ++q) counts[q] = s_m[q];
+    }
+  }
+  __syncthreads();
+  const bool active = sP.spa.m[r] != 0;  // CTA-uniform; idle CTAs still meet the barriers
+  const bool in = active && b0 < nb;
   const u32 s0 = s_base + ex;
   const u32 cs = (u32)sP.spa.chunk_size[r];  // ranks and sizes fit 32 bits (n < 2^32)
   SegMax e[kBinPer];
@@ -889,7 +901,7 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 // region empty and the path idle.
 // ------------------------------------------------------------------ launchers
 
-void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
+void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);

@@ -50,7 +50,7 @@ struct FilterAux {
   u64* agg_val;
 };
 // The plan of the filter path on the device (from K2's counts).
-void launch_bin_scan(const QuadInfo* qinfo, const u32* counts, u64 chunk_count, int log2nb,
+void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st);
 void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
