@@ -389,6 +389,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   __shared__ u64 s_segT[kK2Threads / 32];
   __shared__ u32 s_base;
   __shared__ int s_lex;
+  __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 sidx = blockIdx.x * (kK2Threads / 32) + warp;
@@ -456,26 +457,38 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   // exclusive position of this lane's next record of each group (16-bit
   // fields): the group's start in the segment plus the lanes before it
   u64 pos = (T << 16) + (T << 32) + (T << 48) + (incl - cnt);
-  double2* out = seg + (u64)base;
-  const u32 top = (1u << log2nb) - 1u;
-  const double topd = (double)top;
+  // Stage the segment in shared memory in slot order, then work on it with
+  // every lane busy: ~44% of the items survive, so the per-survivor code
+  // runs in ceil(count / 32) rounds instead of once per item, and the
+  // segment's global stores are coalesced.
+  double2* const ss = s_seg + warp * kSegPts;
 #pragma unroll
   for (int j = 0; j < kSegItems; ++j) {
     const u32 r = (codes >> (3 * j)) & 7;
     if (!r) continue;
-    const u32 ri = r - 1, sh = 16 * ri;
-    const u32 slot = (u32)(pos >> sh) & 0xFFFFu;
+    const u32 sh = 16 * (r - 1);
+    ss[(u32)(pos >> sh) & 0xFFFFu] = p[j];
     pos += 1ull << sh;
-    out[slot] = p[j];
-    const bool odd = (r & 1u) != 0;
-    const double prim = odd ? p[j].x : p[j].y;  // LL, UR: x; LR, UL: y
+  }
+  __syncwarp();
+  const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
+            c3 = c2 + ((u32)(T >> 32) & 0xFFFFu), tot = c3 + (u32)(T >> 48);
+  double2* out = seg + (u64)base;
+  const u32 top = (1u << log2nb) - 1u;
+  const double topd = (double)top;
+  for (u32 slot = lane; slot < tot; slot += 32) {
+    const double2 q = ss[slot];
+    out[slot] = q;
+    const u32 ri = (u32)(slot >= c1) + (u32)(slot >= c2) + (u32)(slot >= c3);
+    const bool odd = (ri & 1u) == 0;  // LL, UR (ri 0, 2): primary x
+    const double prim = odd ? q.x : q.y;
     const u32 b = (ri << log2nb) | bin_of(s_lo[ri], s_scale[ri], top, topd, ri, prim);
     atomicAdd(bcnt + b, 1u);
     // any subset of a bin's records gives a valid (lower) max: sample; w =
     // wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
     // complemented for the min-regions LL and UL
     if ((slot & wmask) == 0) {
-      const double g = odd ? p[j].y : p[j].x;
+      const double g = odd ? q.y : q.x;
       atomicMax(bw + b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     }
   }
