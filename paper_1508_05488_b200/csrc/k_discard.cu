@@ -419,7 +419,8 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
 #pragma unroll
   for (int j = 0; j < kSegItems; ++j) {
     const u32 idx = base + j * 32 + lane;
-    int r = idx < n ? classify(e, p[j].x, p[j].y) : 0;
+    int r = classify(e, p[j].x, p[j].y);  // unconditional: no per-item branch
+    r = idx < n ? r : 0;
     if (lex && r != 0) r = 1;
     codes |= (u32)r << (3 * j);
     cnt += r ? 1ull << (16 * (r - 1)) : 0ull;
@@ -463,12 +464,11 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   // segment's global stores are coalesced.
   double2* const ss = s_seg + warp * kSegPts;
 #pragma unroll
-  for (int j = 0; j < kSegItems; ++j) {
+  for (int j = 0; j < kSegItems; ++j) {  // branch-free: a predicated store
     const u32 r = (codes >> (3 * j)) & 7;
-    if (!r) continue;
-    const u32 sh = 16 * (r - 1);
-    ss[(u32)(pos >> sh) & 0xFFFFu] = p[j];
-    pos += 1ull << sh;
+    const u32 sh = 16 * ((r - 1) & 3);
+    if (r) ss[(u32)(pos >> sh) & 0xFFFFu] = p[j];
+    pos += (u64)(r != 0) << sh;
   }
   __syncwarp();
   const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
