@@ -364,7 +364,7 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
 }
 
 #ifndef CHGPU_K2_MINB
-#define CHGPU_K2_MINB 3
+#define CHGPU_K2_MINB 4
 #endif
 // K2 of the pre-filtered path (k_filter.cu): classify, count, and for
 // every survivor one fire-and-forget increment of its SPA bin's count and
@@ -384,11 +384,8 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     double2* __restrict__ seg, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
     u64* __restrict__ bw, u32 wmask) {
-  __shared__ QuadEdges s_edges;
-  __shared__ double s_lo[4], s_scale[4];
-  __shared__ u64 s_segT[kK2Threads / 32];
+  __shared__ u64 s_segT[kK2Threads / 32];  // (degenerate frame only)
   __shared__ u32 s_base;
-  __shared__ int s_lex;
   __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -400,19 +397,20 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     const u32 idx = base + j * 32 + lane;
     p[j] = idx < n ? ldg_stream(pts + idx) : make_double2(0.0, 0.0);
   }
-  if (tid < 4) {  // while the loads fly
-    const int c = tid;
-    s_edges.ax[c] = qinfo->q[2 * c];
-    s_edges.ay[c] = qinfo->q[2 * c + 1];
-    s_edges.ex[c] = qinfo->ex[c];
-    s_edges.ey[c] = qinfo->ey[c];
-    s_lo[c] = qinfo->blo[c];
-    s_scale[c] = bin_scale(qinfo->bspan[c], log2nb);
-    if (c == 0) s_lex = qinfo->degenerate;
+  // the quad's edges by uniform loads (one transaction per warp, L1 hits
+  // after the first warp), the bin map of region `lane` in lanes 0..3:
+  // no CTA barrier between the point loads and the classification
+  QuadEdges e;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    e.ax[c] = __ldg(&qinfo->q[2 * c]);
+    e.ay[c] = __ldg(&qinfo->q[2 * c + 1]);
+    e.ex[c] = __ldg(&qinfo->ex[c]);
+    e.ey[c] = __ldg(&qinfo->ey[c]);
   }
-  __syncthreads();
-  const bool lex = s_lex != 0;
-  const QuadEdges e = s_edges;
+  const bool lex = __ldg(&qinfo->degenerate) != 0;
+  const double my_lo = __ldg(&qinfo->blo[lane & 3]);
+  const double my_scale = bin_scale(__ldg(&qinfo->bspan[lane & 3]), log2nb);
 
   u32 codes = 0;  // 3 bits of stream id per item
   u64 cnt = 0;    // 16-bit count per stream
@@ -476,13 +474,18 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   double2* out = seg + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
   const double topd = (double)top;
-  for (u32 slot = lane; slot < tot; slot += 32) {
-    const double2 q = ss[slot];
-    out[slot] = q;
+  for (u32 s0 = 0; s0 < tot; s0 += 32) {  // warp-uniform trip count
+    const u32 slot = s0 + lane;
+    const bool on = slot < tot;
+    const double2 q = on ? ss[slot] : make_double2(0.0, 0.0);
     const u32 ri = (u32)(slot >= c1) + (u32)(slot >= c2) + (u32)(slot >= c3);
     const bool odd = (ri & 1u) == 0;  // LL, UR (ri 0, 2): primary x
     const double prim = odd ? q.x : q.y;
-    const u32 b = (ri << log2nb) | bin_of(s_lo[ri], s_scale[ri], top, topd, ri, prim);
+    const double blo = __shfl_sync(0xffffffffu, my_lo, (int)(ri & 3));
+    const double bsc = __shfl_sync(0xffffffffu, my_scale, (int)(ri & 3));
+    if (!on) continue;
+    out[slot] = q;
+    const u32 b = (ri << log2nb) | bin_of(blo, bsc, top, topd, ri, prim);
     atomicAdd(bcnt + b, 1u);
     // any subset of a bin's records gives a valid (lower) max: sample; w =
     // wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
