@@ -52,6 +52,12 @@ struct Pinned {
 constexpr int kMaxFilterBits = 18;
 constexpr size_t kConvexMin = size_t(1) << 16;  // ring size from which k_convex.cu is tried  // SPA pre-filter: at most 2^18 bins per region
 
+// The bin tables must be zero when K2 starts. They are cleared right after
+// a call's counters come back (the GPU is otherwise idle while the host
+// finishes the hull), so the next call usually finds them clean.
+int ftab_prepare(chgpu_ctx* ctx, int log2nb, cudaStream_t st);
+int ftab_clear_behind(chgpu_ctx* ctx);
+
 // d_ftab: per bin a max w (u64), a record count and a candidate count
 // (u32 each), then the candidate-bin bitmap.
 size_t filter_tab_bytes(int log2nb) { return (size_t(4) << log2nb) * 16 + (size_t(4) << log2nb) / 8; }
@@ -104,6 +110,8 @@ struct chgpu_ctx {
   // d_ftab holds [max w: u64 x nbt][count: u32 x nbt][candidates: u32 x nbt],
   // cleared by one memset per call.
   unsigned char* d_ftab = nullptr;
+  size_t ftab_zero = 0;   // leading bytes of d_ftab known to be zero
+  size_t ftab_dirty = 0;  // bytes the current call's K2 may have written
   u32* d_fstart = nullptr;   // per-bin first rank          [4 << kMaxFilterBits]
   u64* d_fthr = nullptr;     // per-bin threshold            [4 << kMaxFilterBits]
   u32* d_fbig = nullptr;     // bins queued for the big sorts [2 * kBigListB]
@@ -170,6 +178,23 @@ int fail(chgpu_ctx* ctx, int code, const char* msg) {
 }
 
 // A fresh zeroed device counter for this call.
+int ftab_prepare(chgpu_ctx* ctx, int log2nb, cudaStream_t st) {
+  const size_t need = filter_tab_bytes(log2nb);
+  if (ctx->ftab_zero < need) CK(cudaMemsetAsync(ctx->d_ftab, 0, need, st));
+  ctx->ftab_zero = 0;
+  ctx->ftab_dirty = need;
+  return CHGPU_OK;
+}
+
+int ftab_clear_behind(chgpu_ctx* ctx) {
+  if (ctx->ftab_dirty) {
+    CK(cudaMemsetAsync(ctx->d_ftab, 0, ctx->ftab_dirty, ctx->st));
+    ctx->ftab_zero = ctx->ftab_dirty;
+    ctx->ftab_dirty = 0;
+  }
+  return CHGPU_OK;
+}
+
 int take_ctr(chgpu_ctx* ctx) {
   if (ctx->ctr_used >= kCtrSlots) return kCtrSlots - 1;  // never reached for sane inputs
   return ctx->ctr_used++;
@@ -1062,7 +1087,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
        (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
   const int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
   if (want_filter)
-    CK(cudaMemsetAsync(ctx->d_ftab, 0, filter_tab_bytes(log2nb), st));
+    TRY(ftab_prepare(ctx, log2nb, st));
   const FilterTabs ftabs = filter_tabs(ctx, log2nb);
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
@@ -1109,6 +1134,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     CK(cudaMemcpyAsync(&ctx->h->ctr[nonfinite_slot], ctx->d_ctr + nonfinite_slot, sizeof(u32),
                        cudaMemcpyDeviceToHost, st));
   TRY(sync(ctx));
+  if (want_filter) TRY(ftab_clear_behind(ctx));  // K2 and the filter path are done with them
   // read_points rejects the file before convex_hull runs (io.cpp:38-42)
   if (from_file && ctx->h->ctr[nonfinite_slot])
     return fail(ctx, CHGPU_NONFINITE, "non-finite coordinate");
@@ -1693,7 +1719,7 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     // The pre-filtered SPA against the global quad (the same kernels as
     // chgpu_hull), falling back to the full region sort on overflow.
     const int log2nb = filter_bits(n, chunk_count);
-    CK(cudaMemsetAsync(ctx->d_ftab, 0, filter_tab_bytes(log2nb), st));
+    TRY(ftab_prepare(ctx, log2nb, st));
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
     ctx->ctr_used += 5;
