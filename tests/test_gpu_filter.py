@@ -176,3 +176,26 @@ def test_paths_interleaved_on_one_context(product):
             assert _counts(r) == run["counts"], (case["dist"], case["n"], run)
             assert sha(r.hull.vertices) == run["hull_sha"]
     ctx.close()
+
+
+def test_filter_tables_across_sizes(product, oracle):
+    """One context, filter path, calls whose bin-table sizes (log2nb) and
+    chunk counts change every time: the tables are cleared behind each call
+    for the next one, and a call after a certain overflow (circle) or a
+    degenerate frame must still start on clean tables."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = product.Context(0)
+    ctx.set_spa_path(product.SPA_FILTER)
+    cases = [("uniform_square", 3_000_000, 1, 1024), ("uniform_disk", 200_000, 2, 7),
+             ("circle", 1_000_000, 3, 1024), ("uniform_square", 5_000_000, 4, 64),
+             ("collinear", 100_000, 5, 1024), ("gaussian", 2_000_000, 6, 1024),
+             ("uniform_square", 300_000, 7, 2048), ("uniform_disk", 4_000_000, 8, 1024)]
+    for dist, n, seed, cc in cases + cases[::-1]:
+        pts = product.generate(dist, n, seed)
+        want = oracle.convex_hull(pts, cc)
+        r = ctx.convex_hull(pts, product.PipelineConfig(chunk_count=cc))
+        assert _counts(r) == want.counts.tolist(), (dist, n, cc)
+        assert np.array_equal(r.hull.vertices, want.hull), (dist, n, cc)
+    ctx.close()
