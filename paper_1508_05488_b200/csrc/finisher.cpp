@@ -289,13 +289,63 @@ int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corner
   for (int sgi = 0; sgi <= cut_seg; ++sgi) {
     const size_t end = sgi == cut_seg ? cut_idx : seg_len[sgi];
     const Pt* p = seg_ptr[sgi];
-    for (size_t j = 0; j < end; ++j) {
+    size_t j = 0;
+    for (; j < end && phase != 2; ++j) {
       if (have_prev && same(prev, p[j])) continue;
       prev = p[j];
       have_prev = true;
       ++ring_n;
       feed(p[j]);
     }
+    if (j == end) continue;
+    // The deque loop proper, with every piece of state in locals that no
+    // store through the deque pointers can alias (the lambda's captures
+    // would be reloaded after each deque store).
+    Pt* h = head;
+    Pt* t = tail;
+    double h_ax = hax, h_ay = hay, h_ex = hex, h_ey = hey;
+    double t_ax = tax, t_ay = tay, t_ex = tex, t_ey = tey;
+    double qx = prev.x, qy = prev.y;  // have_prev holds in phase 2
+    size_t fed = 0;
+    for (; j < end; ++j) {
+      const double vx = p[j].x, vy = p[j].y;
+      if (vx == qx && vy == qy) continue;  // consecutive duplicate (polygon.cpp:16-18)
+      qx = vx;
+      qy = vy;
+      ++fed;
+      const bool left_head = h_ex * (vy - h_ay) - h_ey * (vx - h_ax) > 0.0;
+      const bool left_tail = t_ex * (vy - t_ay) - t_ey * (vx - t_ax) > 0.0;
+      if (left_head & left_tail) continue;  // inside the hull so far: ~70% of chain points
+      if (!left_tail && t - h >= 2) {
+        --t;
+        while (t - h >= 2) {
+          const Pt a = t[-2], b = t[-1];
+          if ((b.x - a.x) * (vy - a.y) - (b.y - a.y) * (vx - a.x) > 0.0) break;
+          --t;
+        }
+      }
+      *t++ = Pt{vx, vy};
+      while (t - h >= 2) {
+        const Pt a = h[0], b = h[1];
+        if ((a.x - vx) * (b.y - vy) - (a.y - vy) * (b.x - vx) > 0.0) break;
+        ++h;
+      }
+      *--h = Pt{vx, vy};
+      h_ax = vx;
+      h_ay = vy;
+      h_ex = h[1].x - vx;
+      h_ey = h[1].y - vy;
+      t_ax = t[-2].x;
+      t_ay = t[-2].y;
+      t_ex = t[-1].x - t_ax;
+      t_ey = t[-1].y - t_ay;
+    }
+    head = h;
+    tail = t;
+    hax = h_ax, hay = h_ay, hex = h_ex, hey = h_ey;
+    tax = t_ax, tay = t_ay, tex = t_ex, tey = t_ey;
+    prev = Pt{qx, qy};
+    ring_n += fed;
   }
   // the trailing run: one vertex unless it repeats the previous one or
   // closes the ring onto corner 0 (when the ring has more than one vertex)
