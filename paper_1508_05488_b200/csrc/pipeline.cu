@@ -49,6 +49,24 @@ struct Pinned {
   unsigned long long ncand;
 };
 
+// The per-call counters the host reads after K2 and the filter path: the
+// quad, K2's region counts (cnt_slot + 1 .. 4), the overflow and
+// non-finite flags, the kept counts and the candidate count. ctx->h is
+// pinned host memory, mapped into the device address space (UVA).
+__global__ void k_readback(const QuadInfo* __restrict__ qinfo, const u32* __restrict__ ctr,
+                           int cnt_slot, int ovf_slot, int nonfinite_slot,
+                           const unsigned long long* __restrict__ u64s, Pinned* h) {
+  const int t = threadIdx.x;
+  const u32* q = reinterpret_cast<const u32*>(qinfo);
+  u32* hq = reinterpret_cast<u32*>(&h->qi);
+  for (int i = t; i < (int)(sizeof(QuadInfo) / 4); i += blockDim.x) hq[i] = q[i];
+  if (t < 5) h->ctr[cnt_slot + t] = ctr[cnt_slot + t];
+  if (t == 5 && ovf_slot >= 0) h->ctr[ovf_slot] = ctr[ovf_slot];
+  if (t == 6 && nonfinite_slot >= 0) h->ctr[nonfinite_slot] = ctr[nonfinite_slot];
+  if (t >= 8 && t < 12) h->kept[t - 8] = u64s[t - 8];
+  if (t == 12) h->ncand = u64s[11];
+}
+
 constexpr int kMaxFilterBits = 18;
 constexpr size_t kConvexMin = size_t(1) << 16;  // ring size from which k_convex.cu is tried  // SPA pre-filter: at most 2^18 bins per region
 
@@ -1116,23 +1134,17 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     if (ctx->kept_hint + 4 < kConvexMin)
       spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 4));
     TRY(ensure_host_out(ctx, spec + 4));
-    CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ctx->h->ncand, ctx->d_u64 + 11, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
-                       cudaMemcpyDeviceToHost, st));
     if (spec)
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
                          st));
-    CK(cudaEventRecord(ctx->ev[9], st));
   }
-  CK(cudaMemcpyAsync(&ctx->h->qi, ctx->d_qinfo, sizeof(QuadInfo), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&ctx->h->ctr[cnt_slot], ctx->d_ctr + cnt_slot, 5 * sizeof(u32),
-                     cudaMemcpyDeviceToHost, st));
-  if (from_file)
-    CK(cudaMemcpyAsync(&ctx->h->ctr[nonfinite_slot], ctx->d_ctr + nonfinite_slot, sizeof(u32),
-                       cudaMemcpyDeviceToHost, st));
+  // every counter the host needs, in one launch straight into the pinned
+  // (device-mapped) host block instead of one DMA per value
+  k_readback<<<1, 64, 0, st>>>(ctx->d_qinfo, ctx->d_ctr, cnt_slot, ovf_slot,
+                               from_file ? nonfinite_slot : -1, ctx->d_u64, ctx->h);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  if (want_filter) CK(cudaEventRecord(ctx->ev[9], st));
   TRY(sync(ctx));
   if (want_filter) TRY(ftab_clear_behind(ctx));  // K2 and the filter path are done with them
   // read_points rejects the file before convex_hull runs (io.cpp:38-42)
