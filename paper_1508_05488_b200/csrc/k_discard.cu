@@ -381,12 +381,13 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
 // like k_classify_compact.
 __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivors(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
-    double2* __restrict__ seg, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
+    u64* __restrict__ seg, u32* __restrict__ segidx, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
     u64* __restrict__ bw, u32 wmask) {
   __shared__ u64 s_segT[kK2Threads / 32];  // (degenerate frame only)
   __shared__ u32 s_base;
   __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
+  __shared__ u32 s_sidx[kK2Threads / 32 * kSegPts];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 sidx = blockIdx.x * (kK2Threads / 32) + warp;
@@ -461,17 +462,23 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   // runs in ceil(count / 32) rounds instead of once per item, and the
   // segment's global stores are coalesced.
   double2* const ss = s_seg + warp * kSegPts;
+  u32* const si = s_sidx + warp * kSegPts;
 #pragma unroll
-  for (int j = 0; j < kSegItems; ++j) {  // branch-free: a predicated store
+  for (int j = 0; j < kSegItems; ++j) {  // branch-free: predicated stores
     const u32 r = (codes >> (3 * j)) & 7;
     const u32 sh = 16 * ((r - 1) & 3);
-    if (r) ss[(u32)(pos >> sh) & 0xFFFFu] = p[j];
+    const u32 sl = (u32)(pos >> sh) & 0xFFFFu;
+    if (r) {
+      ss[sl] = p[j];
+      si[sl] = base + j * 32 + lane;
+    }
     pos += (u64)(r != 0) << sh;
   }
   __syncwarp();
   const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
             c3 = c2 + ((u32)(T >> 32) & 0xFFFFu), tot = c3 + (u32)(T >> 48);
-  double2* out = seg + (u64)base;
+  u64* const out = seg + (u64)base;
+  u32* const out_idx = segidx + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
   const double topd = (double)top;
   for (u32 s0 = 0; s0 < tot; s0 += 32) {  // warp-uniform trip count
@@ -484,16 +491,16 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     const double blo = __shfl_sync(0xffffffffu, my_lo, (int)(ri & 3));
     const double bsc = __shfl_sync(0xffffffffu, my_scale, (int)(ri & 3));
     if (!on) continue;
-    out[slot] = q;
     const u32 b = (ri << log2nb) | bin_of(blo, bsc, top, topd, ri, prim);
     atomicAdd(bcnt + b, 1u);
-    // any subset of a bin's records gives a valid (lower) max: sample; w =
-    // wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
-    // complemented for the min-regions LL and UL
-    if ((slot & wmask) == 0) {
-      const double g = odd ? q.y : q.x;
-      atomicMax(bw + b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
-    }
+    // w = wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
+    // complemented for the min-regions LL and UL; kept as w >> kWShift
+    const double g = odd ? q.y : q.x;
+    const u64 key = filter_key(b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
+    // any subset of a bin's records gives a valid (lower) max: sample
+    if ((slot & wmask) == 0) atomicMax(bw + b, key & kWMask);
+    out[slot] = key;            // the filter reads 8 B per survivor
+    out_idx[slot] = si[slot];   // ... and the point only for candidates
   }
   // (region totals: the bin scan sums the bin counts)
 }
@@ -583,13 +590,13 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                                                                kbuf, vbuf, ncap, counts_out);
 }
 
-void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, double2* seg,
-                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
+                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
                                u32* bcnt, u64* bw, u32 wmask, cudaStream_t st) {
   constexpr u32 tile = kK2Threads / 32 * kSegPts;  // one segment per warp
   const u32 tiles = (n + tile - 1) / tile;
   if (tiles == 0) return;
-  k_classify_survivors<<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, seg, segcnt, kbuf, vbuf,
+  k_classify_survivors<<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, seg, segidx, segcnt, kbuf, vbuf,
                                                      counts_out, log2nb, bcnt, bw, wmask);
 }
 

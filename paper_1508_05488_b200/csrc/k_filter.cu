@@ -189,7 +189,8 @@ __device__ void make_filter_plan(const QuadInfo& qi, const u32* __restrict__ cou
     const double seed = (r == 0 || r == 2) ? qi.q[2 * r + 1] : qi.q[2 * r];
     P.spa.seed[r] = seed;
     const int reg = r + 1;
-    P.seed_w[r] = wkey(reg, (reg == 1 || reg == 4) ? ~ord_enc(seed) : ord_enc(seed));
+    // (w >> kWShift, like the filter keys and the bin maxima)
+    P.seed_w[r] = wkey(reg, (reg == 1 || reg == 4) ? ~ord_enc(seed) : ord_enc(seed)) >> kWShift;
   }
   P.spa.total_chunks = chunks;
 }
@@ -391,27 +392,25 @@ constexpr int kFilterThreads = 256;
 constexpr int kFilterItems = CHGPU_FILTER_ITEMS;
 
 // Warp-stride over K2's survivor segments (k_classify_survivors: 256
-// slots each, groups LL | LR | UR | UL sized by segcnt). A candidate takes
-// the next slot of its bin; the bin's 33rd candidate queues the bin for
-// k_bin_sort_warp, its 257th for k_bin_sort_big.
+// slots each): per survivor one 8-byte key, its global bin over w >> kWShift
+// (filter_key). A survivor with (w >> kWShift) < T_b is dropped: since the
+// shift is monotone, that implies w < the bin's lower bound of the running
+// max. A candidate fetches its point from the input (its index from K2),
+// takes the next slot of its bin and writes its sort record; the bin's 33rd
+// candidate queues it for k_bin_sort_warp, its 257th for k_bin_sort_big.
 __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
-    const double2* __restrict__ seg, const u64* __restrict__ segcnt, u32 nseg,
-    const FilterPlan* __restrict__ P_p, const QuadInfo* __restrict__ qinfo,
-    const u32* __restrict__ bstart, const u64* __restrict__ bthr, u32* __restrict__ bcur,
-    u32* __restrict__ bmap, u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big,
-    u32* __restrict__ nbig, unsigned long long* __restrict__ ncand,
-    const u32* __restrict__ overflow) {
-  // The plan's per-region values, read once into shared memory (the loop's
-  // stores would otherwise force re-reads from global memory per item).
+    const u64* __restrict__ seg, const u32* __restrict__ segidx, const u64* __restrict__ segcnt,
+    u32 nseg, const double2* __restrict__ pts, const FilterPlan* __restrict__ P_p,
+    const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
+    const u64* __restrict__ bthr, u32* __restrict__ bcur, u32* __restrict__ bmap,
+    u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
+    unsigned long long* __restrict__ ncand, const u32* __restrict__ overflow) {
   __shared__ u64 s_off[4];
-  __shared__ double s_lo[4], s_scale[4];
   __shared__ u32 s_lg, s_nseg;
   __shared__ u32 s_cand;
   if (threadIdx.x < 4) {
     const int r = threadIdx.x;
     s_off[r] = P_p->spa.off[r];
-    s_lo[r] = qinfo->blo[r];
-    s_scale[r] = bin_scale(qinfo->bspan[r], P_p->log2nb);
     if (r == 0) {
       s_lg = (u32)P_p->log2nb;
       // no segments on a degenerate frame (K2 wrote LEX records), nothing to
@@ -421,52 +420,44 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
     }
   }
   __syncthreads();
-  const u32 lg = s_lg, top = (1u << lg) - 1u;
-  const double topd = (double)top;
+  const u32 lg = s_lg;
   nseg = s_nseg;
   const int lane = threadIdx.x & 31;
   const u32 wstride = gridDim.x * (kFilterThreads / 32);
   u32 mine = 0;
   for (u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5); sg < nseg; sg += wstride) {
     const u64 T = __ldg(segcnt + sg);
-    const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
-              c3 = c2 + ((u32)(T >> 32) & 0xFFFFu), tot = c3 + (u32)(T >> 48);
-    const double2* sp = seg + (u64)sg * kSegPts;
+    const u32 tot = ((u32)T & 0xFFFFu) + ((u32)(T >> 16) & 0xFFFFu) + ((u32)(T >> 32) & 0xFFFFu) +
+                    (u32)(T >> 48);
+    const u64* sp = seg + (u64)sg * kSegPts;
     for (u32 s0 = 0; s0 < tot; s0 += 32 * kFilterItems) {
-      double2 p[kFilterItems];
-      u32 rr[kFilterItems];
+      u64 key[kFilterItems];
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
         const u32 sl = s0 + j * 32 + lane;
-        rr[j] = (u32)(sl >= c1) + (u32)(sl >= c2) + (u32)(sl >= c3);
-        p[j] = sl < tot ? __ldcs(sp + sl) : make_double2(0.0, 0.0);
+        key[j] = sl < tot ? __ldcs(sp + sl) : 0ull;
       }
       // all threshold loads in flight before any test
-      u32 bi[kFilterItems];
       u64 th[kFilterItems];
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
         const u32 sl = s0 + j * 32 + lane;
-        const u32 r = rr[j];
-        const double prim = (r & 1u) ? p[j].y : p[j].x;  // LL, UR: x; LR, UL: y
-        bi[j] = (r << lg) | bin_of(s_lo[r], s_scale[r], top, topd, r, prim);
-        th[j] = sl < tot ? __ldg(bthr + bi[j]) : ~0ull;
+        th[j] = sl < tot ? __ldg(bthr + (key[j] >> (64 - kWShift))) : ~0ull;
       }
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
-        const u32 r = rr[j];
-        const double gd = (r & 1u) ? p[j].x : p[j].y;  // the guarded coordinate
-        // wkey(v): -0.0 folded onto +0.0, complemented for LL / UL
-        const u64 vm = (r == 0 || r == 3) ? ~0ull : 0ull;
-        if ((ord_enc_z(gd) ^ vm) < th[j]) continue;  // (past tot: th = ~0)
+        if ((key[j] & kWMask) < th[j]) continue;  // (past tot: th = ~0)
+        const u32 bi = (u32)(key[j] >> (64 - kWShift));
+        const u32 r = bi >> lg;
         const int reg = (int)r + 1;
-        const u32 pos = atomicAdd(bcur + bi[j], 1u);
-        if (pos == 0) atomicOr(bmap + (bi[j] >> 5), 1u << (bi[j] & 31));  // k_spa_chunks' index
-        const u64 dst = s_off[r] + bstart[bi[j]] + pos;
-        kout[dst] = k_of(reg, p[j].x, p[j].y);
-        vout[dst] = v_of(reg, p[j].x, p[j].y);
-        if (pos == 32) big[atomicAdd(nbig, 1u)] = bi[j];                       // > 32: by a warp
-        if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi[j];  // > 256: a CTA
+        const double2 p = __ldg(pts + segidx[(u64)sg * kSegPts + s0 + j * 32 + lane]);
+        const u32 pos = atomicAdd(bcur + bi, 1u);
+        if (pos == 0) atomicOr(bmap + (bi >> 5), 1u << (bi & 31));  // k_spa_chunks' index
+        const u64 dst = s_off[r] + bstart[bi] + pos;
+        kout[dst] = k_of(reg, p.x, p.y);
+        vout[dst] = v_of(reg, p.x, p.y);
+        if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: by a warp
+        if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: a CTA
         ++mine;
       }
     }
@@ -914,10 +905,11 @@ void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int lo
   cudaLaunchCooperativeKernel((const void*)k_bin_scan, grid, block, args, 0, st);
 }
 
-void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
-                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
-                   u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
-                   const u32* overflow, cudaStream_t st) {
+void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
+                   const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
+                   const u32* bstart, const u64* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
+                   u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
+                   cudaStream_t st) {
   if (nseg == 0) return;
   // one resident wave: the warp-stride loop then has no partial last wave
   static int resident = 0;
@@ -927,8 +919,8 @@ void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const Filter
   }
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
                                    (u32)resident);
-  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segcnt, nseg, P, qinfo, bstart, bthr, bcur, bmap,
-                                              kout, vout, big, nbig, ncand, overflow);
+  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segidx, segcnt, nseg, pts, P, qinfo, bstart, bthr,
+                                              bcur, bmap, kout, vout, big, nbig, ncand, overflow);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,

@@ -57,10 +57,11 @@ void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* b
                        const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
                        u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
                        unsigned long long* kept_counts, double2* out, cudaStream_t st);
-void launch_filter(const double2* seg, const u64* segcnt, u32 nseg, const FilterPlan* P,
-                   const QuadInfo* qinfo, const u32* bstart, const u64* bthr, u32* bcur, u32* bmap,
-                   u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
-                   const u32* overflow, cudaStream_t st);
+void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
+                   const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
+                   const u32* bstart, const u64* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
+                   u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
+                   cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
 // Melkman's convex-position trajectory on the device (k_convex.cu).
@@ -86,9 +87,9 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf, u64* vbuf,
                              u64 ncap, u32* counts_out, cudaStream_t st);
 // K2 of the pre-filtered path: raw survivor points + bin statistics.
-void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, double2* seg,
-                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
-                               u32* bcnt, u64* bw, u32 wmask, cudaStream_t st);
+void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
+                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out,
+                               int log2nb, u32* bcnt, u64* bw, u32 wmask, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

@@ -851,8 +851,8 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
 // exactly as run_spa leaves them and the kept counts in d_u64[0..3].
 // Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
 // *ovf_slot / *ncand land in the counters for the caller's read-back.
-int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb, int cnt_slot,
-                       int* ovf_slot) {
+int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chunk_count,
+                       int log2nb, int cnt_slot, int* ovf_slot) {
   cudaStream_t st = ctx->st;
   const FilterPlan* P = ctx->d_plan;
   const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
@@ -877,9 +877,10 @@ int enqueue_filter_spa(chgpu_ctx* ctx, size_t n, size_t chunk_count, int log2nb,
                   ctx->d_plan, ctx->d_fstart, ctx->d_fthr, first_bin, aux, ctx->d_ctr + take_ctr(ctx),
                   ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[3], st));
-  // K2's survivor segments: points in kbuf, group sizes in vbuf
-  launch_filter(reinterpret_cast<const double2*>(ctx->d_kbuf), ctx->d_vbuf,
-                (u32)((n + kSegPts - 1) / kSegPts), P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
+  // K2's survivor segments: filter keys in kbuf, input indices in the upper
+  // half of vbuf, group sizes in its lower part
+  launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+                (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
                 ctx->d_u64 + 11, ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[4], st));
@@ -1112,8 +1113,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   if (want_filter) {
     // raw survivor points + bin statistics (a degenerate frame writes the
     // LEX records of stream 1 instead)
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, reinterpret_cast<double2*>(ctx->d_kbuf),
-                              ctx->d_vbuf, ctx->d_kbuf, ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
+                              reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+                              ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
   } else {
     launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
@@ -1128,7 +1130,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   int ovf_slot = -1;
   size_t spec = 0;
   if (want_filter) {
-    TRY(enqueue_filter_spa(ctx, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
+    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
     // (small chains only: a survivor-heavy call reads its result back once
     // it knows the size, or not at all on the convex fast path)
     if (ctx->kept_hint + 4 < kConvexMin)
@@ -1735,12 +1737,13 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
     ctx->ctr_used += 5;
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, reinterpret_cast<double2*>(ctx->d_kbuf),
-                              ctx->d_vbuf, ctx->d_kbuf, ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
+                              reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+                              ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
     CK(cudaGetLastError());
     int ovf_slot = -1;
-    TRY(enqueue_filter_spa(ctx, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
+    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
     CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
