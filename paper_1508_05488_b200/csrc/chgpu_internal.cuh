@@ -366,13 +366,15 @@ constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
 #endif
 constexpr int kSegItems = CHGPU_SEG_ITEMS;        // points per lane of the filter path's K2
 constexpr int kSegPts = 32 * kSegItems;           // one K2 warp's survivor segment
-// A survivor's filter key: its global SPA bin (< 4 * 2^18) over the top 20
-// bits, w >> kWShift below. w >> kWShift is monotone in w, so maxima and
-// threshold tests on it are valid lower bounds / drops (k_filter.cu).
-constexpr int kWShift = 20;
-constexpr u64 kWMask = (1ull << (64 - kWShift)) - 1;
+// A survivor's filter key: its global SPA bin (< 4 * 2^18) in the high
+// word, w >> 32 (sign, exponent and 20 mantissa bits of the guarded
+// coordinate) in the low word. w >> 32 is monotone in w, so maxima and
+// threshold tests on it are valid lower bounds / drops (k_filter.cu), and
+// the bin tables of maxima and thresholds are 32-bit.
+constexpr int kWShift = 32;
+constexpr u64 kWMask = 0xFFFFFFFFull;
 __host__ __device__ __forceinline__ u64 filter_key(u32 gbin, u64 w) {
-  return ((u64)gbin << (64 - kWShift)) | (w >> kWShift);
+  return ((u64)gbin << 32) | (w >> kWShift);
 }
 
 }  // namespace chgpu

@@ -383,7 +383,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     u64* __restrict__ seg, u32* __restrict__ segidx, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
-    u64* __restrict__ bw, u32 wmask) {
+    u32* __restrict__ bw, u32 wmask) {
   __shared__ u64 s_segT[kK2Threads / 32];  // (degenerate frame only)
   __shared__ u32 s_base;
   __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
@@ -498,7 +498,7 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     const double g = odd ? q.y : q.x;
     const u64 key = filter_key(b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     // any subset of a bin's records gives a valid (lower) max: sample
-    if ((slot & wmask) == 0) atomicMax(bw + b, key & kWMask);
+    if ((slot & wmask) == 0) atomicMax(bw + b, (u32)key);
     out[slot] = key;            // the filter reads 8 B per survivor
     out_idx[slot] = si[slot];   // ... and the point only for candidates
   }
@@ -592,7 +592,7 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
 
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
                                u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
-                               u32* bcnt, u64* bw, u32 wmask, cudaStream_t st) {
+                               u32* bcnt, u32* bw, u32 wmask, cudaStream_t st) {
   constexpr u32 tile = kK2Threads / 32 * kSegPts;  // one segment per warp
   const u32 tiles = (n + tile - 1) / tile;
   if (tiles == 0) return;

@@ -228,8 +228,8 @@ __device__ __forceinline__ void grid_barrier(u32* ctr, u32 g) {
 //             tiles.
 __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
     const QuadInfo* __restrict__ qinfo, u32* __restrict__ counts, u64 chunk_count,
-    int log2nb, const u32* __restrict__ bcnt, const u64* __restrict__ bw,
-    FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u64* __restrict__ bthr,
+    int log2nb, const u32* __restrict__ bcnt, const u32* __restrict__ bw,
+    FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u32* __restrict__ bthr,
     u32* __restrict__ first_bin, u32* __restrict__ tsum, u32* __restrict__ agg_seg,
     u64* __restrict__ agg_val, u32* __restrict__ bar, u32* __restrict__ overflow) {
   __shared__ FilterPlan sP;
@@ -251,12 +251,10 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
   u64 w[kBinPer] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (b0 < nb) {
     load8(bcnt + boff + b0, c);
+    u32 w32[kBinPer];
+    load8(bw + boff + b0, w32);
 #pragma unroll
-    for (int j = 0; j < kBinPer; j += 2) {
-      const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(bw + boff + b0 + j);
-      w[j] = a.x;
-      w[j + 1] = a.y;
-    }
+    for (int j = 0; j < kBinPer; ++j) w[j] = w32[j];
   }
   // phase 1
   u32 x = 0;
@@ -366,9 +364,9 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
     run = seg_combine(run, e[j]);
     q += c[j];
   }
-#pragma unroll
-  for (int j = 0; j < kBinPer; j += 2)
-    *reinterpret_cast<ulonglong2*>(bthr + boff + b0 + j) = make_ulonglong2(th[j], th[j + 1]);
+  uint4* const to = reinterpret_cast<uint4*>(bthr + boff + b0);
+  to[0] = make_uint4((u32)th[0], (u32)th[1], (u32)th[2], (u32)th[3]);
+  to[1] = make_uint4((u32)th[4], (u32)th[5], (u32)th[6], (u32)th[7]);
   // T = 0 passes every record: such a bin above kBinSortMax records is
   // certain to overflow the bin sorts, so the filter can stand down now
   bool certain = false;
@@ -402,7 +400,7 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
     const u64* __restrict__ seg, const u32* __restrict__ segidx, const u64* __restrict__ segcnt,
     u32 nseg, const double2* __restrict__ pts, const FilterPlan* __restrict__ P_p,
     const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
-    const u64* __restrict__ bthr, u32* __restrict__ bcur, u32* __restrict__ bmap,
+    const u32* __restrict__ bthr, u32* __restrict__ bcur, u32* __restrict__ bmap,
     u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
     unsigned long long* __restrict__ ncand, const u32* __restrict__ overflow) {
   __shared__ u64 s_off[4];
@@ -438,16 +436,16 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
         key[j] = sl < tot ? __ldcs(sp + sl) : 0ull;
       }
       // all threshold loads in flight before any test
-      u64 th[kFilterItems];
+      u32 th[kFilterItems];
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
         const u32 sl = s0 + j * 32 + lane;
-        th[j] = sl < tot ? __ldg(bthr + (key[j] >> (64 - kWShift))) : ~0ull;
+        th[j] = sl < tot ? __ldg(bthr + (key[j] >> 32)) : ~0u;
       }
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
-        if ((key[j] & kWMask) < th[j]) continue;  // (past tot: th = ~0)
-        const u32 bi = (u32)(key[j] >> (64 - kWShift));
+        if ((u32)key[j] < th[j]) continue;  // (past tot: key 0 < th ~0)
+        const u32 bi = (u32)(key[j] >> 32);
         const u32 r = bi >> lg;
         const int reg = (int)r + 1;
         const double2 p = __ldg(pts + segidx[(u64)sg * kSegPts + s0 + j * 32 + lane]);
@@ -893,7 +891,7 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 // ------------------------------------------------------------------ launchers
 
 void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
-                     const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
+                     const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
   dim3 grid(4 * tiles), block(kBinThreads);
@@ -907,7 +905,7 @@ void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int lo
 
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
-                   const u32* bstart, const u64* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
+                   const u32* bstart, const u32* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
                    u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
                    cudaStream_t st) {
   if (nseg == 0) return;

@@ -51,7 +51,7 @@ struct FilterAux {
 };
 // The plan of the filter path on the device (from K2's counts).
 void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
-                     const u32* bcnt, const u64* bw, FilterPlan* plan, u32* bstart, u64* bthr,
+                     const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st);
 void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
                        const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
@@ -59,7 +59,7 @@ void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* b
                        unsigned long long* kept_counts, double2* out, cudaStream_t st);
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
-                   const u32* bstart, const u64* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
+                   const u32* bstart, const u32* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
                    u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
                    cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
@@ -89,7 +89,7 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
 // K2 of the pre-filtered path: raw survivor points + bin statistics.
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
                                u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out,
-                               int log2nb, u32* bcnt, u64* bw, u32 wmask, cudaStream_t st);
+                               int log2nb, u32* bcnt, u32* bw, u32 wmask, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

@@ -829,7 +829,7 @@ u32 filter_wmask() {
 }
 
 struct FilterTabs {
-  u64* w;
+  u32* w;  // (in the first half of its 8-byte-per-bin slot range)
   u32* cnt;
   u32* cur;
   u32* bmap;  // one bit per bin: the bin holds a candidate
@@ -837,8 +837,8 @@ struct FilterTabs {
 FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
   const size_t nbt = size_t(4) << log2nb;
   FilterTabs t;
-  t.w = reinterpret_cast<u64*>(ctx->d_ftab);
-  t.cnt = reinterpret_cast<u32*>(t.w + nbt);
+  t.w = reinterpret_cast<u32*>(ctx->d_ftab);
+  t.cnt = t.w + 2 * nbt;
   t.cur = t.cnt + nbt;
   t.bmap = t.cur + nbt;
   return t;
@@ -874,13 +874,15 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   *ovf_slot = take_ctr(ctx);
   // plan + bin starts + thresholds: one cooperative launch
   launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
-                  ctx->d_plan, ctx->d_fstart, ctx->d_fthr, first_bin, aux, ctx->d_ctr + take_ctr(ctx),
+                  ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), first_bin, aux,
+                  ctx->d_ctr + take_ctr(ctx),
                   ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
   // half of vbuf, group sizes in its lower part
   launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
-                (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart, ctx->d_fthr,
+                (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart,
+                reinterpret_cast<const u32*>(ctx->d_fthr),
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
                 ctx->d_u64 + 11, ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[4], st));
