@@ -53,9 +53,9 @@ struct Pinned {
 // quad, K2's region counts (cnt_slot + 1 .. 4), the overflow and
 // non-finite flags, the kept counts and the candidate count. ctx->h is
 // pinned host memory, mapped into the device address space (UVA).
-__global__ void k_readback(const QuadInfo* __restrict__ qinfo, const u32* __restrict__ ctr,
+__global__ void k_readback(const QuadInfo* __restrict__ qinfo, u32* __restrict__ ctr,
                            int cnt_slot, int ovf_slot, int nonfinite_slot,
-                           const unsigned long long* __restrict__ u64s, Pinned* h) {
+                           unsigned long long* __restrict__ u64s, Pinned* h) {
   const int t = threadIdx.x;
   const u32* q = reinterpret_cast<const u32*>(qinfo);
   u32* hq = reinterpret_cast<u32*>(&h->qi);
@@ -65,6 +65,12 @@ __global__ void k_readback(const QuadInfo* __restrict__ qinfo, const u32* __rest
   if (t == 6 && nonfinite_slot >= 0) h->ctr[nonfinite_slot] = ctr[nonfinite_slot];
   if (t >= 8 && t < 12) h->kept[t - 8] = u64s[t - 8];
   if (t == 12) h->ncand = u64s[11];
+  // ... then clear every counter for what follows (later stages of this
+  // call take fresh slots; a call that ends here leaves them clean for the
+  // next one, which then skips its clearing memsets)
+  __syncthreads();
+  for (int i = t; i < kCtrSlots; i += blockDim.x) ctr[i] = 0;
+  if (t < 16) u64s[t] = 0;
 }
 
 constexpr int kMaxFilterBits = 18;
@@ -129,6 +135,7 @@ struct chgpu_ctx {
   // cleared by one memset per call.
   unsigned char* d_ftab = nullptr;
   size_t ftab_zero = 0;   // leading bytes of d_ftab known to be zero
+  bool counters_clean = false;  // d_ctr and d_u64 are all zero
   size_t ftab_dirty = 0;  // bytes the current call's K2 may have written
   u32* d_fstart = nullptr;   // per-bin first rank          [4 << kMaxFilterBits]
   u64* d_fthr = nullptr;     // per-bin threshold            [4 << kMaxFilterBits]
@@ -947,8 +954,11 @@ int begin_call(chgpu_ctx* ctx) {
   ctx->stage_used = 0;
   ctx->launches = 0;
   ctx->ctr_used = 0;
-  CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
-  CK(cudaMemsetAsync(ctx->d_u64, 0, 16 * sizeof(unsigned long long), ctx->st));
+  if (!ctx->counters_clean) {  // (k_readback cleared them at the end of the last call)
+    CK(cudaMemsetAsync(ctx->d_ctr, 0, kCtrSlots * sizeof(u32), ctx->st));
+    CK(cudaMemsetAsync(ctx->d_u64, 0, 16 * sizeof(unsigned long long), ctx->st));
+  }
+  ctx->counters_clean = false;
   return CHGPU_OK;
 }
 
@@ -1303,6 +1313,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     const int mk = chgpu::host::finish_chains(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
                                               corners, ctx->hull);
     if (mk) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon/melkman: degenerate polygon");
+    // the filter path touched no counter after k_readback cleared them
+    if (filtered) ctx->counters_clean = true;
     D.t_host_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
     ctx->hull_ptr = ctx->hull.data();
