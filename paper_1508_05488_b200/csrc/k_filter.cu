@@ -18,7 +18,7 @@
 //   * a bin straddling a chunk boundary: T = 0, every record is a candidate,
 //     so after sorting a record's rank inside the bin is its position.
 // The first bin of every chunk c > 0 has T = 0 (seed = identity) as well,
-// so each chunk's first candidate sits at a known dense position.
+// so each chunk's first candidate sits at a known rank.
 //
 // Kernels:
 //   K2 (k_discard.cu)  per survivor: bin count += 1, bin max(w); the
@@ -590,7 +590,7 @@ __global__ __launch_bounds__(kBigThreads) void k_bin_sort_big(u64* __restrict__ 
   }
 }
 
-// ------------------------------------------------------------------ dense candidates
+// ------------------------------------------------------------------ in-register batch order
 
 // Ascending bitonic sort of one record per lane by (g, canon k, v, k), g a
 // small group id (the bin's lane); lanes without a record carry g = ~0 and

@@ -141,9 +141,9 @@ struct chgpu_ctx {
   u64* d_fthr = nullptr;     // per-bin threshold            [4 << kMaxFilterBits]
   u32* d_fbig = nullptr;     // bins queued for the big sorts [2 * kBigListB]
   unsigned char* d_faux = nullptr;  // FilterAux scratch (bin-tile sums and aggregates)
-  u64* d_ck = nullptr;       // dense candidates (k words)    [cap]
-  u64* d_cv = nullptr;       // dense candidates (v words)    [cap]
-  u32* d_ffirst = nullptr;   // per-chunk first dense candidate
+  u64* d_ck = nullptr;       // kept records per chunk, k words (scratch) [cap]
+  u64* d_cv = nullptr;       // ... v words                             [cap]
+  u32* d_ffirst = nullptr;   // per-chunk first bin
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
@@ -853,7 +853,7 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
 
 // Enqueues the pre-filtered SPA (k_filter.cu) right behind K2, with no
 // host round trip: the plan is built on the device from K2's counts
-// (cnt_slot + 1 .. 4), then bin scan, filter, big-bin sorts, dense
+// (cnt_slot + 1 .. 4), then bin scan, filter, big-bin sorts, per-chunk
 // compaction and the SPA over the candidates; kept chains land in d_kept
 // exactly as run_spa leaves them and the kept counts in d_u64[0..3].
 // Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
