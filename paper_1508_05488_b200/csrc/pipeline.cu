@@ -852,10 +852,11 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
 }
 
 // Enqueues the pre-filtered SPA (k_filter.cu) right behind K2, with no
-// host round trip: the plan is built on the device from K2's counts
-// (cnt_slot + 1 .. 4), then bin scan, filter, big-bin sorts, per-chunk
-// compaction and the SPA over the candidates; kept chains land in d_kept
-// exactly as run_spa leaves them and the kept counts in d_u64[0..3].
+// host round trip: the bin scan builds the plan on the device from the bin
+// counts (and writes the region sizes to cnt_slot + 1 .. 4), then the
+// filter, the big-bin sorts and the per-chunk SPA over the candidates;
+// kept chains land in d_kept exactly as run_spa leaves them and the kept
+// counts in d_u64[0..3].
 // Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
 // *ovf_slot / *ncand land in the counters for the caller's read-back.
 int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chunk_count,
