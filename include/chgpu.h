@@ -205,6 +205,13 @@ void chgpu_fold_extremes(const double* quads, const uint64_t* idxs, size_t k, do
  * are the kept points of the 4 regions concatenated; kept_counts[4]. */
 int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
                        size_t chunk_count, const double** chains_xy, size_t* kept_counts);
+/* Same, with the chains copied into a caller's device buffer of cap_points
+ * points (on the context's device; CHGPU_TOO_LARGE if they do not fit): the
+ * multi-GPU merge gathers them over NCCL without a host round trip. A shard
+ * of n points never has more than n chain points. */
+int chgpu_shard_chains_device(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
+                              size_t chunk_count, double* d_chains, size_t cap_points,
+                              size_t* kept_counts);
 
 #ifdef __cplusplus
 }

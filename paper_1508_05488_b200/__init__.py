@@ -208,6 +208,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_fold_extremes.restype = None
         L.chgpu_shard_chains.argtypes = [vp, C.c_void_p, C.c_size_t, _dp, C.c_size_t,
                                          C.POINTER(_dp), _sz]
+        L.chgpu_shard_chains_device.argtypes = [vp, C.c_void_p, C.c_size_t, _dp, C.c_size_t,
+                                                C.c_void_p, C.c_size_t, _sz]
         _lib = L
         return L
 
@@ -397,6 +399,17 @@ class Context:
         chains = np.ctypeslib.as_array(out, shape=(total * 2,)).reshape(-1, 2).copy() \
             if total else np.empty((0, 2))
         return chains, [int(c) for c in kc]
+
+    def shard_chains_device(self, ptr: int, n: int, quad, chunk_count: int, out_ptr: int,
+                            cap_points: int):
+        """shard_chains with the chains written to the device buffer at
+        out_ptr (cap_points points); returns the kept counts."""
+        q = np.ascontiguousarray(np.asarray(quad, np.float64).reshape(8))
+        kc = (C.c_size_t * 4)()
+        self._check(self.lib.chgpu_shard_chains_device(self.h, C.c_void_p(ptr), n, _p(q),
+                                                       chunk_count, C.c_void_p(out_ptr),
+                                                       cap_points, kc))
+        return [int(c) for c in kc]
 
 
 _tls = threading.local()

@@ -1730,10 +1730,30 @@ void chgpu_fold_extremes(const double* quads, const uint64_t* idxs, size_t k, do
   }
 }
 
-int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
-                       size_t chunk_count, const double** chains_xy, size_t* kept_counts) {
+namespace {
+// Shard chains (see include/chgpu.h), delivered to the context's pinned host
+// buffer (d_dst == nullptr) or to a caller's device buffer of d_cap points.
+int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
+                      size_t chunk_count, const double** chains_xy, double* d_dst, size_t d_cap,
+                      size_t* kept_counts) {
+  // the chains: D2D into the caller's buffer, or D2H into the context's
+  auto deliver = [&](size_t total) -> int {
+    if (d_dst) {
+      if (total > d_cap) return fail(ctx, CHGPU_TOO_LARGE, "shard chains exceed the output buffer");
+      CK(cudaMemcpyAsync(d_dst, ctx->d_kept, total * sizeof(double2), cudaMemcpyDeviceToDevice,
+                         ctx->st));
+      TRY(sync(ctx));
+      return CHGPU_OK;
+    }
+    TRY(ensure_host_out(ctx, total + 4));
+    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, total * sizeof(double2), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    TRY(sync(ctx));
+    *chains_xy = reinterpret_cast<const double*>(ctx->h_out);
+    return CHGPU_OK;
+  };
   for (int r = 0; r < 4; ++r) kept_counts[r] = 0;
-  *chains_xy = nullptr;
+  if (chains_xy) *chains_xy = nullptr;
   if (n == 0) return CHGPU_OK;
   if (n >= (size_t(1) << 32)) return fail(ctx, CHGPU_TOO_LARGE, "shard too large");
   cudaSetDevice(ctx->device);
@@ -1764,15 +1784,10 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
                        cudaMemcpyDeviceToHost, st));
     TRY(sync(ctx));
+    TRY(ftab_clear_behind(ctx));  // (for the next call, while the host exchanges)
     if (!ctx->h->ctr[ovf_slot]) {
       for (int r = 0; r < 4; ++r) kept_counts[r] = (size_t)ctx->h->kept[r];
-      const size_t total = kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3];
-      TRY(ensure_host_out(ctx, total + 4));
-      CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, total * sizeof(double2),
-                         cudaMemcpyDeviceToHost, st));
-      TRY(sync(ctx));
-      *chains_xy = reinterpret_cast<const double*>(ctx->h_out);
-      return CHGPU_OK;
+      return deliver(kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3]);
     }
   }
   const int cnt_slot = ctx->ctr_used;
@@ -1806,12 +1821,20 @@ int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const doubl
     TRY(sync(ctx));
     for (int r = 0; r < 4; ++r) kept_counts[r] = (size_t)ctx->h->kept[r];
   }
-  const size_t total = kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3];
-  TRY(ensure_host_out(ctx, total + 4));
-  CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, total * sizeof(double2), cudaMemcpyDeviceToHost, st));
-  TRY(sync(ctx));
-  *chains_xy = reinterpret_cast<const double*>(ctx->h_out);
-  return CHGPU_OK;
+  return deliver(kept_counts[0] + kept_counts[1] + kept_counts[2] + kept_counts[3]);
+}
+}  // namespace
+
+int chgpu_shard_chains(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
+                       size_t chunk_count, const double** chains_xy, size_t* kept_counts) {
+  return shard_chains_impl(ctx, d_xy, n, quad, chunk_count, chains_xy, nullptr, 0, kept_counts);
+}
+
+int chgpu_shard_chains_device(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
+                              size_t chunk_count, double* d_chains, size_t cap_points,
+                              size_t* kept_counts) {
+  return shard_chains_impl(ctx, d_xy, n, quad, chunk_count, nullptr, d_chains, cap_points,
+                           kept_counts);
 }
 
 }  // extern "C"

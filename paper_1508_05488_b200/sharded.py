@@ -88,18 +88,32 @@ class GpuShardOps(ShardOps):
 
     def __init__(self, ctx, points: torch.Tensor, base_index: int):
         self.ctx, self.t, self.base = ctx, points, int(base_index)
+        self.out = None  # chain buffer (device), reused across calls
 
     def extremes(self):
         q, idx = self.ctx.shard_extremes(self.t.data_ptr(), self.t.shape[0], self.base)
         return q.reshape(4, 2), idx.astype(np.int64)
 
     def chains(self, quad, chunk_count):
-        pts, _ = self.ctx.shard_chains(self.t.data_ptr(), self.t.shape[0], quad, chunk_count)
-        return pts
+        # device-resident chains (a shard never keeps more than its points):
+        # the gather and the merge read them without a host round trip
+        n = self.t.shape[0]
+        if self.out is None or self.out.shape[0] < n:
+            self.out = torch.empty((max(n, 1), 2), dtype=torch.float64, device=self.t.device)
+        kc = self.ctx.shard_chains_device(self.t.data_ptr(), n, quad, chunk_count,
+                                          self.out.data_ptr(), self.out.shape[0])
+        return self.out[: sum(kc)]
 
     def finish(self, points, chunk_count):
         from . import PipelineConfig
-        return self.ctx.convex_hull(points, PipelineConfig(chunk_count=chunk_count)).hull.vertices
+        cfg = PipelineConfig(chunk_count=chunk_count)
+        if isinstance(points, torch.Tensor) and points.is_cuda:
+            p = points.contiguous()
+            torch.cuda.current_stream(p.device).synchronize()  # the merge reads it on ctx's stream
+            return self.ctx.convex_hull_device(p.data_ptr(), p.shape[0], cfg).hull.vertices
+        if isinstance(points, torch.Tensor):
+            points = points.numpy()
+        return self.ctx.convex_hull(points, cfg).hull.vertices
 
 
 def _device_for(group) -> torch.device:
@@ -125,18 +139,21 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
     arr = torch.stack(allq).cpu().numpy()
     quad = fold_extremes(arr[:, :8], arr[:, 8:].astype(np.int64))
 
-    # per-rank discard + sort + SPA against the global quad
-    ch = np.ascontiguousarray(ops.chains(quad, chunk_count), np.float64).reshape(-1, 2)
+    # per-rank discard + sort + SPA against the global quad (a CUDA tensor
+    # from GpuShardOps, numpy from the CPU ops of the tests)
+    ch = ops.chains(quad, chunk_count)
+    ch = (ch if isinstance(ch, torch.Tensor)
+          else torch.from_numpy(np.ascontiguousarray(ch, np.float64))).reshape(-1, 2)
 
     # exchange 2: chains to rank 0 (sizes first, then padded payloads)
-    cnt = torch.tensor([len(ch)], dtype=torch.int64, device=dev)
+    cnt = torch.tensor([ch.shape[0]], dtype=torch.int64, device=dev)
     counts = [torch.empty_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
     counts = [int(c.item()) for c in counts]
     width = max(max(counts), 1)
     buf = torch.zeros((width, 2), dtype=torch.float64, device=dev)
-    if len(ch):
-        buf[: len(ch)] = torch.from_numpy(ch).to(dev)
+    if ch.shape[0]:
+        buf[: ch.shape[0]] = ch.to(dev)
     gathered = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
     if dist.get_backend(group) == "nccl":
         # NCCL gather: emulate with all_gather (the payload is tiny)
@@ -147,6 +164,6 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
         dist.gather(buf, gathered, dst=0, group=group)
     if rank != 0:
         return None
-    parts = [g[:c].cpu().numpy() for g, c in zip(gathered, counts)]
-    union = np.concatenate(parts + [frame_vertices(quad)], axis=0)
-    return ops.finish(union, chunk_count)
+    frame = torch.from_numpy(frame_vertices(quad)).to(dev)
+    union = torch.cat([g[:c] for g, c in zip(gathered, counts)] + [frame], dim=0)
+    return ops.finish(union.numpy() if dev.type == "cpu" else union, chunk_count)
