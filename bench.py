@@ -298,14 +298,18 @@ def main():
         hbm, src = peaks()
         t = d.times_ms
         n = args.n
-        disc_bytes = 32 * n + 16 * s1
+        # K2 writes each survivor as an 8-byte filter key + a 4-byte input
+        # index on the pre-filtered path, as a 16-byte (k, v) record on the
+        # sort path
+        surv_b = 12 if d.spa_path == 1 else 16
+        disc_bytes = 32 * n + surv_b * s1
         disc_ms = t["t_k1_ms"] + t["t_k2_ms"]
         kernels = {
             "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n,
                             "basis": "16 B/pt read"},
             ("k2_classify_survivors" if d.spa_path == 1 else "k2_classify_compact"):
-                {"ms": t["t_k2_ms"], "bytes": 16 * n + 16 * s1,
-                                    "basis": "16 B/pt read + 16 B/survivor write"},
+                {"ms": t["t_k2_ms"], "bytes": 16 * n + surv_b * s1,
+                 "basis": f"16 B/pt read + {surv_b} B/survivor write"},
         }
         if d.spa_path == 1:
             lb = d.filter_log2nb
@@ -314,8 +318,9 @@ def main():
             kernels.update({
                 "k3_bin_scan": {"ms": t["t_binscan_ms"], "bytes": 24 * nb,
                                 "basis": "12 B/bin read + 12 B/bin write"},
-                "k3_filter": {"ms": t["t_filter_ms"], "bytes": 16 * s1 + 16 * nc,
-                              "basis": "16 B/survivor read + 16 B/candidate write",
+                "k3_filter": {"ms": t["t_filter_ms"], "bytes": 8 * s1 + 36 * nc,
+                              "basis": "8 B/survivor key read + per candidate 4 B index "
+                                       "+ 16 B point read, 16 B record write",
                               "candidates": nc},
                 "k3_bin_sort": {"ms": t["t_binsort_ms"],
                                 "basis": "bins above 32 candidates sorted in place"},
