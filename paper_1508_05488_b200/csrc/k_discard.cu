@@ -366,28 +366,32 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
 #ifndef CHGPU_K2_MINB
 #define CHGPU_K2_MINB 4
 #endif
+#ifndef CHGPU_K2_ABL  // ablation bits, A/B timing only (results are invalid when set)
+#define CHGPU_K2_ABL 0
+#endif
 // K2 of the pre-filtered path (k_filter.cu): classify, count, and for
 // every survivor one fire-and-forget increment of its SPA bin's count and
 // (for one record in 2^k, wmask) a running max of its guarded key w.
 //
 // Survivor layout: each warp owns the 256-slot segment of its 256 input
-// points (seg + 256 * warp index) and writes its survivors there as raw
-// points, grouped LL | LR | UR | UL, with the four group sizes packed in
-// segcnt[warp index] (16-bit fields). Positions come from one warp scan,
-// so no CTA barrier or global reservation sits between the loads and the
-// stores; the filter reads the segments back (its order within a bin is
-// re-established by the bin sort). A degenerate frame (pipeline.cpp:53-71)
-// writes LEX records into dense stream 1 of (kbuf, vbuf) instead, exactly
-// like k_classify_compact.
+// points (seg + 256 * warp index) and writes its survivors there in any
+// order (the filter re-establishes the order inside a bin by the bin sort,
+// and a key names its region through its bin), with the survivor count in
+// segcnt[warp index]. Positions come from one 32-bit warp scan, so no CTA
+// barrier or global reservation sits between the loads and the stores. A
+// degenerate frame (pipeline.cpp:53-71) writes LEX records into dense
+// stream 1 of (kbuf, vbuf) instead, exactly like k_classify_compact.
 __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivors(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
     u64* __restrict__ seg, u32* __restrict__ segidx, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
     u32* __restrict__ bw, u32 wmask) {
-  __shared__ u64 s_segT[kK2Threads / 32];  // (degenerate frame only)
+  __shared__ u32 s_segT[kK2Threads / 32];  // (degenerate frame only)
   __shared__ u32 s_base;
   __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
   __shared__ u32 s_sidx[kK2Threads / 32 * kSegPts];
+  __shared__ unsigned char s_sreg[kK2Threads / 32 * kSegPts];
+  __shared__ double2 s_bmap[kK2Threads / 32][4];  // (lo, scale) per region, per warp
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const u32 sidx = blockIdx.x * (kK2Threads / 32) + warp;
@@ -399,8 +403,9 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     p[j] = idx < n ? ldg_stream(pts + idx) : make_double2(0.0, 0.0);
   }
   // the quad's edges by uniform loads (one transaction per warp, L1 hits
-  // after the first warp), the bin map of region `lane` in lanes 0..3:
-  // no CTA barrier between the point loads and the classification
+  // after the first warp), the bin map of region `lane` in lanes 0..3 into
+  // the warp's own table: no CTA barrier between the point loads and the
+  // classification
   QuadEdges e;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -410,39 +415,38 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     e.ey[c] = __ldg(&qinfo->ey[c]);
   }
   const bool lex = __ldg(&qinfo->degenerate) != 0;
-  const double my_lo = __ldg(&qinfo->blo[lane & 3]);
-  const double my_scale = bin_scale(__ldg(&qinfo->bspan[lane & 3]), log2nb);
+  if (lane < 4)
+    s_bmap[warp][lane] = make_double2(__ldg(&qinfo->blo[lane]), bin_scale(__ldg(&qinfo->bspan[lane]), log2nb));
 
   u32 codes = 0;  // 3 bits of stream id per item
-  u64 cnt = 0;    // 16-bit count per stream
+  u32 cnt = 0;    // survivors of this lane
 #pragma unroll
   for (int j = 0; j < kSegItems; ++j) {
     const u32 idx = base + j * 32 + lane;
     int r = classify(e, p[j].x, p[j].y);  // unconditional: no per-item branch
-    r = idx < n ? r : 0;
-    if (lex && r != 0) r = 1;
+    r = idx < n ? r : 0;  // (a degenerate frame only asks r != 0)
     codes |= (u32)r << (3 * j);
-    cnt += r ? 1ull << (16 * (r - 1)) : 0ull;
+    cnt += r != 0;
   }
-  u64 incl = cnt;
+  u32 incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  const u64 T = __shfl_sync(0xffffffffu, incl, 31);  // the segment's four group sizes
+  const u32 tot = __shfl_sync(0xffffffffu, incl, 31);  // the segment's survivors
 
   if (lex) {  // uniform: dense stream 1 through a CTA reservation
-    if (lane == 0) s_segT[warp] = T;
+    if (lane == 0) s_segT[warp] = tot;
     __syncthreads();
     if (tid == 0) {
       u32 sum = 0;
-      for (int w = 0; w < kK2Threads / 32; ++w) sum += (u32)s_segT[w] & 0xFFFFu;
+      for (int w = 0; w < kK2Threads / 32; ++w) sum += s_segT[w];
       s_base = sum ? atomicAdd(&counts_out[1], sum) : 0u;
     }
     __syncthreads();
-    u32 pp = s_base + (u32)((incl - cnt) & 0xFFFFu);
-    for (int w = 0; w < warp; ++w) pp += (u32)s_segT[w] & 0xFFFFu;
+    u32 pp = s_base + (incl - cnt);
+    for (int w = 0; w < warp; ++w) pp += s_segT[w];
 #pragma unroll
     for (int j = 0; j < kSegItems; ++j) {
       if (!((codes >> (3 * j)) & 7)) continue;
@@ -453,54 +457,59 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     return;
   }
 
-  if (lane == 0) segcnt[sidx] = T;
-  // exclusive position of this lane's next record of each group (16-bit
-  // fields): the group's start in the segment plus the lanes before it
-  u64 pos = (T << 16) + (T << 32) + (T << 48) + (incl - cnt);
+  if (lane == 0) segcnt[sidx] = tot;
   // Stage the segment in shared memory in slot order, then work on it with
   // every lane busy: ~44% of the items survive, so the per-survivor code
   // runs in ceil(count / 32) rounds instead of once per item, and the
   // segment's global stores are coalesced.
   double2* const ss = s_seg + warp * kSegPts;
   u32* const si = s_sidx + warp * kSegPts;
+  unsigned char* const sr = s_sreg + warp * kSegPts;
+  {
+    // shared-window addresses held in registers and predicated stores:
+    // no per-item branch and no re-derived shared base per item
+    const u32 a_pt = (u32)__cvta_generic_to_shared(ss), a_ix = (u32)__cvta_generic_to_shared(si),
+              a_rg = (u32)__cvta_generic_to_shared(sr);
+    u32 pos = incl - cnt;
 #pragma unroll
-  for (int j = 0; j < kSegItems; ++j) {  // branch-free: predicated stores
-    const u32 r = (codes >> (3 * j)) & 7;
-    const u32 sh = 16 * ((r - 1) & 3);
-    const u32 sl = (u32)(pos >> sh) & 0xFFFFu;
-    if (r) {
-      ss[sl] = p[j];
-      si[sl] = base + j * 32 + lane;
+    for (int j = 0; j < kSegItems; ++j) {
+      const u32 r = (codes >> (3 * j)) & 7;
+      asm volatile(
+          "{\n\t.reg .pred q;\n\t"
+          "setp.ne.u32 q, %0, 0;\n\t"
+          "@q st.shared.v2.f64 [%1], {%2, %3};\n\t"
+          "@q st.shared.u32 [%4], %5;\n\t"
+          "@q st.shared.u8 [%6], %7;\n\t}" ::"r"(r),
+          "r"(a_pt + 16 * pos), "d"(p[j].x), "d"(p[j].y), "r"(a_ix + 4 * pos), "r"(base + j * 32 + lane),
+          "r"(a_rg + pos), "r"(r - 1)
+          : "memory");
+      pos += r != 0;
     }
-    pos += (u64)(r != 0) << sh;
   }
   __syncwarp();
-  const u32 c1 = (u32)T & 0xFFFFu, c2 = c1 + ((u32)(T >> 16) & 0xFFFFu),
-            c3 = c2 + ((u32)(T >> 32) & 0xFFFFu), tot = c3 + (u32)(T >> 48);
+  if (CHGPU_K2_ABL & 8) return;
   u64* const out = seg + (u64)base;
   u32* const out_idx = segidx + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
   const double topd = (double)top;
-  for (u32 s0 = 0; s0 < tot; s0 += 32) {  // warp-uniform trip count
-    const u32 slot = s0 + lane;
-    const bool on = slot < tot;
-    const double2 q = on ? ss[slot] : make_double2(0.0, 0.0);
-    const u32 ri = (u32)(slot >= c1) + (u32)(slot >= c2) + (u32)(slot >= c3);
+  for (u32 slot = lane; slot < tot; slot += 32) {
+    const double2 q = ss[slot];
+    const u32 ri = sr[slot];
     const bool odd = (ri & 1u) == 0;  // LL, UR (ri 0, 2): primary x
     const double prim = odd ? q.x : q.y;
-    const double blo = __shfl_sync(0xffffffffu, my_lo, (int)(ri & 3));
-    const double bsc = __shfl_sync(0xffffffffu, my_scale, (int)(ri & 3));
-    if (!on) continue;
-    const u32 b = (ri << log2nb) | bin_of(blo, bsc, top, topd, ri, prim);
-    atomicAdd(bcnt + b, 1u);
+    const double2 bm = s_bmap[warp][ri];
+    const u32 b = (ri << log2nb) | bin_of(bm.x, bm.y, top, topd, ri, prim);
+    if (!(CHGPU_K2_ABL & 1)) atomicAdd(bcnt + b, 1u);
     // w = wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
     // complemented for the min-regions LL and UL; kept as w >> kWShift
     const double g = odd ? q.y : q.x;
     const u64 key = filter_key(b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     // any subset of a bin's records gives a valid (lower) max: sample
-    if ((slot & wmask) == 0) atomicMax(bw + b, (u32)key);
-    out[slot] = key;            // the filter reads 8 B per survivor
-    out_idx[slot] = si[slot];   // ... and the point only for candidates
+    if (!(CHGPU_K2_ABL & 2) && (slot & wmask) == 0) atomicMax(bw + b, (u32)key);
+    if (!(CHGPU_K2_ABL & 4)) {
+      out[slot] = key;            // the filter reads 8 B per survivor
+      out_idx[slot] = si[slot];   // ... and the point only for candidates
+    }
   }
   // (region totals: the bin scan sums the bin counts)
 }

@@ -424,9 +424,7 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
   const u32 wstride = gridDim.x * (kFilterThreads / 32);
   u32 mine = 0;
   for (u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5); sg < nseg; sg += wstride) {
-    const u64 T = __ldg(segcnt + sg);
-    const u32 tot = ((u32)T & 0xFFFFu) + ((u32)(T >> 16) & 0xFFFFu) + ((u32)(T >> 32) & 0xFFFFu) +
-                    (u32)(T >> 48);
+    const u32 tot = (u32)__ldg(segcnt + sg);
     const u64* sp = seg + (u64)sg * kSegPts;
     for (u32 s0 = 0; s0 < tot; s0 += 32 * kFilterItems) {
       u64 key[kFilterItems];

@@ -829,7 +829,7 @@ int filter_bits(size_t n, size_t chunk_count) {
 u32 filter_wmask() {
   static const u32 m = [] {
     const char* e = std::getenv("CHGPU_FILTER_WSAMPLE_LOG2");
-    const int k = e ? std::max(0, std::min(8, std::atoi(e))) : 0;
+    const int k = e ? std::max(0, std::min(8, std::atoi(e))) : 1;
     return (1u << k) - 1u;
   }();
   return m;

@@ -176,3 +176,19 @@ def test_finish_chains_equals_assemble_then_melkman(product, oracle):
                 product.finish_chains(chains, kc, quad)
         else:
             assert np.array_equal(product.finish_chains(chains, kc, quad), want), trial
+    # long chains (the finisher tests blocks of 8 points at once): runs of
+    # duplicates, collinear grids and points inside the hull so far
+    for trial in range(1500):
+        span = (3, 7, 50)[trial % 3]
+        quad = rng.integers(0, span, (4, 2)).astype(np.float64)
+        kc = [int(x) for x in rng.integers(0, 40, 4)]
+        chains = rng.integers(0, span, (sum(kc), 2)).astype(np.float64)
+        if sum(kc) > 2 and rng.random() < 0.5:  # runs of repeats
+            rep = rng.integers(0, sum(kc), sum(kc) // 3)
+            chains[rep] = chains[np.maximum(rep - 1, 0)]
+        want = _finish_reference(ref, chains, kc, quad)
+        if want is None:
+            with pytest.raises(product.DegenerateInput):
+                product.finish_chains(chains, kc, quad)
+        else:
+            assert np.array_equal(product.finish_chains(chains, kc, quad), want), ("long", trial)
