@@ -79,7 +79,13 @@ __device__ __forceinline__ void empty_quad(QuadCand& a) {
 }
 
 constexpr int kK1Threads = 256;
-constexpr int kK1Unroll = 4;
+#ifndef CHGPU_K1_UNROLL
+#define CHGPU_K1_UNROLL 8
+#endif
+constexpr int kK1Unroll = CHGPU_K1_UNROLL;  // points per lane per warp tile
+#ifndef CHGPU_K1_MINB
+#define CHGPU_K1_MINB 3
+#endif
 
 // Block-wide merge of nparts partials and the QuadInfo (with
 // frame_vertices, extremes.cpp:49-57). Ties fall back to the global index,
@@ -141,29 +147,37 @@ __device__ void merge_partials_block(const QuadCand* __restrict__ partials, int 
 // kCheck (file ingestion): also flags any non-finite coordinate
 // (io.cpp:38-42 require_finite; the reference rejects them before hulling).
 template <bool kCheck>
-__global__ __launch_bounds__(kK1Threads, 3) void k_extremes_partial(
+__global__ __launch_bounds__(kK1Threads, CHGPU_K1_MINB) void k_extremes_partial(
     const double2* __restrict__ pts, u64 n, u64 base_index, QuadCand* __restrict__ partials,
     u32 part_base, u32* __restrict__ ticket, u32 total_parts, QuadInfo* __restrict__ out,
     u32* __restrict__ nonfinite) {
   QuadCand acc;
   empty_quad(acc);
   bool finite = true;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (kK1Unroll - 1) * stride < n; i += kK1Unroll * stride) {
+  // Warp tiles of 32 * kK1Unroll contiguous points (every load of a tile
+  // in flight before the fold), grid-strided over the warps; a lane visits
+  // its points in increasing index order, as the fold requires.
+  constexpr u64 kTile = 32 * kK1Unroll;
+  const int ln = threadIdx.x & 31;
+  const u64 tw = (u64)gridDim.x * (kK1Threads / 32);
+  u64 t = (u64)blockIdx.x * (kK1Threads / 32) + (threadIdx.x >> 5);
+  for (; (t + 1) * kTile <= n; t += tw) {
+    const u64 i0 = t * kTile + ln;
     double2 p[kK1Unroll];
 #pragma unroll
-    for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i + u * stride);
+    for (int u = 0; u < kK1Unroll; ++u) p[u] = ldg_stream(pts + i0 + 32 * u);
 #pragma unroll
     for (int u = 0; u < kK1Unroll; ++u) {
       if (kCheck) finite &= isfinite(p[u].x) && isfinite(p[u].y);
-      fold_point(acc, p[u].x, p[u].y, base_index + i + u * stride);
+      fold_point(acc, p[u].x, p[u].y, base_index + i0 + 32 * u);
     }
   }
-  for (; i < n; i += stride) {
-    const double2 p = ldg_stream(pts + i);
-    if (kCheck) finite &= isfinite(p.x) && isfinite(p.y);
-    fold_point(acc, p.x, p.y, base_index + i);
+  if (t * kTile < n) {  // the one partial tile
+    for (u64 i = t * kTile + ln; i < n; i += 32) {
+      const double2 p = ldg_stream(pts + i);
+      if (kCheck) finite &= isfinite(p.x) && isfinite(p.y);
+      fold_point(acc, p.x, p.y, base_index + i);
+    }
   }
   if (kCheck && !__all_sync(0xffffffffu, finite) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 #pragma unroll
