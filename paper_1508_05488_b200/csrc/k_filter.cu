@@ -383,11 +383,16 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
 #ifndef CHGPU_FILTER_WAVES
 #define CHGPU_FILTER_WAVES 1
 #endif
+#ifndef CHGPU_FILTER_PIPE
+#define CHGPU_FILTER_PIPE 1
+#endif
 #ifndef CHGPU_FILTER_MINB
 #define CHGPU_FILTER_MINB 8
 #endif
 constexpr int kFilterThreads = 256;
+#if !CHGPU_FILTER_PIPE
 constexpr int kFilterItems = CHGPU_FILTER_ITEMS;
+#endif
 
 // Warp-stride over K2's survivor segments (k_classify_survivors: 256
 // slots each): per survivor one 8-byte key, its global bin over w >> kWShift
@@ -423,6 +428,59 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
   const int lane = threadIdx.x & 31;
   const u32 wstride = gridDim.x * (kFilterThreads / 32);
   u32 mine = 0;
+  // One candidate's work (its point, bin slot, sort record, big-bin queue).
+  auto take = [&](u64 key, u32 sg, u32 sl) {
+    const u32 bi = (u32)(key >> 32);
+    const u32 r = bi >> lg;
+    const int reg = (int)r + 1;
+    const double2 p = __ldg(pts + segidx[(u64)sg * kSegPts + sl]);
+    const u32 pos = atomicAdd(bcur + bi, 1u);
+    if (pos == 0) atomicOr(bmap + (bi >> 5), 1u << (bi & 31));  // k_spa_chunks' index
+    const u64 dst = s_off[r] + bstart[bi] + pos;
+    kout[dst] = k_of(reg, p.x, p.y);
+    vout[dst] = v_of(reg, p.x, p.y);
+    if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: by a warp
+    if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: a CTA
+    ++mine;
+  };
+#if CHGPU_FILTER_PIPE
+  // Software-pipelined over the warp's rounds of 32 survivors, across its
+  // segments: the key and the bin threshold of the next round are in flight
+  // while the current round is tested, so a warp keeps two dependent
+  // key -> threshold chains going instead of one.
+  {
+    u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5);
+    u32 tot = sg < nseg ? (u32)__ldg(segcnt + sg) : 0u;
+    u32 s0 = 0;
+    // advance (sg, s0, tot) to the next non-empty round
+    auto next_round = [&](u32& g, u32& o, u32& t) {
+      o += 32;
+      while (g < nseg && o >= t) {
+        g += wstride;
+        o = 0;
+        t = g < nseg ? (u32)__ldg(segcnt + g) : 0u;
+      }
+    };
+    if (sg < nseg && tot == 0) { s0 = 0; next_round(sg, s0, tot); s0 = 0; }
+    // (next_round skipped empty segments; s0 restarts at 0 there)
+    u32 c_sg = sg, c_s0 = 0, c_tot = tot;
+    u64 c_key = (c_sg < nseg && c_s0 + lane < c_tot) ? __ldcs(seg + (u64)c_sg * kSegPts + c_s0 + lane) : 0ull;
+    u32 c_th = (c_sg < nseg && c_s0 + lane < c_tot) ? __ldg(bthr + (c_key >> 32)) : ~0u;
+    u32 n_sg = c_sg, n_s0 = c_s0, n_tot = c_tot;
+    if (n_sg < nseg) next_round(n_sg, n_s0, n_tot);
+    u64 n_key = (n_sg < nseg && n_s0 + lane < n_tot) ? __ldcs(seg + (u64)n_sg * kSegPts + n_s0 + lane) : 0ull;
+    while (c_sg < nseg) {
+      const u32 n_th = (n_sg < nseg && n_s0 + lane < n_tot) ? __ldg(bthr + (n_key >> 32)) : ~0u;
+      u32 f_sg = n_sg, f_s0 = n_s0, f_tot = n_tot;
+      if (f_sg < nseg) next_round(f_sg, f_s0, f_tot);
+      const u64 f_key =
+          (f_sg < nseg && f_s0 + lane < f_tot) ? __ldcs(seg + (u64)f_sg * kSegPts + f_s0 + lane) : 0ull;
+      if (c_s0 + lane < c_tot && (u32)c_key >= c_th) take(c_key, c_sg, c_s0 + lane);
+      c_sg = n_sg, c_s0 = n_s0, c_tot = n_tot, c_key = n_key, c_th = n_th;
+      n_sg = f_sg, n_s0 = f_s0, n_tot = f_tot, n_key = f_key;
+    }
+  }
+#else
   for (u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5); sg < nseg; sg += wstride) {
     const u32 tot = (u32)__ldg(segcnt + sg);
     const u64* sp = seg + (u64)sg * kSegPts;
@@ -443,21 +501,11 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
 #pragma unroll
       for (int j = 0; j < kFilterItems; ++j) {
         if ((u32)key[j] < th[j]) continue;  // (past tot: key 0 < th ~0)
-        const u32 bi = (u32)(key[j] >> 32);
-        const u32 r = bi >> lg;
-        const int reg = (int)r + 1;
-        const double2 p = __ldg(pts + segidx[(u64)sg * kSegPts + s0 + j * 32 + lane]);
-        const u32 pos = atomicAdd(bcur + bi, 1u);
-        if (pos == 0) atomicOr(bmap + (bi >> 5), 1u << (bi & 31));  // k_spa_chunks' index
-        const u64 dst = s_off[r] + bstart[bi] + pos;
-        kout[dst] = k_of(reg, p.x, p.y);
-        vout[dst] = v_of(reg, p.x, p.y);
-        if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: by a warp
-        if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: a CTA
-        ++mine;
+        take(key[j], sg, s0 + j * 32 + lane);
       }
     }
   }
+#endif
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_cand, mine);
