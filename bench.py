@@ -353,7 +353,7 @@ def main():
             "peak_source": src, "frac": dom["gbs"] / hbm,
             "traffic": measured_traffic(dom_name),
             "algorithmic_bytes": f"{dom.get('basis', 'bytes moved')}: {dom['bytes']} B per launch",
-            "discard_kernels": {"kernels": "k_extremes_partial+final, k_classify_compact",
+            "discard_kernels": {"kernels": "k_extremes_partial (+ last-block merge), k_classify_survivors",
                                 "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
                                 "frac": disc_bytes / (disc_ms * 1e-3) / 1e9 / hbm,
                                 "bytes": disc_bytes, "ms": disc_ms},
