@@ -150,12 +150,23 @@ class Hull:
     vertices: np.ndarray = field(default_factory=lambda: np.empty((0, 2)))
 
 
-@dataclass
 class HullResult:
-    """pipeline.hpp:44-47 (+ GPU diagnostics)."""
-    hull: Hull
-    stats: StageStats
-    diag: Diag | None = None
+    """pipeline.hpp:44-47 (+ GPU diagnostics). `diag` is converted from the
+    C struct on first access (it is not needed on the hot path)."""
+
+    __slots__ = ("hull", "stats", "_diag", "_raw")
+
+    def __init__(self, hull: Hull, stats: StageStats, diag: "Diag | None" = None, raw=None):
+        self.hull, self.stats, self._diag, self._raw = hull, stats, diag, raw
+
+    @property
+    def diag(self) -> "Diag | None":
+        if self._diag is None and self._raw is not None:
+            self._diag = Diag._from(self._raw)
+        return self._diag
+
+    def __repr__(self) -> str:
+        return f"HullResult(hull={self.hull!r}, stats={self.stats!r})"
 
 
 _dp = C.POINTER(C.c_double)
@@ -292,7 +303,7 @@ class Context:
             if k.value else np.empty((0, 2))
         if copy:
             verts = verts.copy()
-        return HullResult(Hull(verts), StageStats._from(s), Diag._from(d))
+        return HullResult(Hull(verts), StageStats._from(s), raw=d)
 
     def convex_hull(self, points, config: PipelineConfig | None = None,
                     copy: bool = True) -> HullResult:
@@ -332,7 +343,7 @@ class Context:
             if k.value else np.empty((0, 2))
         if copy:
             verts = verts.copy()
-        return HullResult(Hull(verts), StageStats._from(s), Diag._from(d))
+        return HullResult(Hull(verts), StageStats._from(s), raw=d)
 
     # ---- stage taps -----------------------------------------------------
     def find_extremes(self, points) -> np.ndarray:
