@@ -151,13 +151,21 @@ class Hull:
 
 
 class HullResult:
-    """pipeline.hpp:44-47 (+ GPU diagnostics). `diag` is converted from the
-    C struct on first access (it is not needed on the hot path)."""
+    """pipeline.hpp:44-47 (+ GPU diagnostics). `stats` and `diag` are
+    converted from the C structs on first access (neither is needed on the
+    hot path)."""
 
-    __slots__ = ("hull", "stats", "_diag", "_raw")
+    __slots__ = ("hull", "_stats", "_rstats", "_diag", "_raw")
 
-    def __init__(self, hull: Hull, stats: StageStats, diag: "Diag | None" = None, raw=None):
-        self.hull, self.stats, self._diag, self._raw = hull, stats, diag, raw
+    def __init__(self, hull: Hull, stats: "StageStats | None" = None, diag: "Diag | None" = None,
+                 raw=None, raw_stats=None):
+        self.hull, self._stats, self._rstats, self._diag, self._raw = hull, stats, raw_stats, diag, raw
+
+    @property
+    def stats(self) -> StageStats:
+        if self._stats is None and self._rstats is not None:
+            self._stats = StageStats._from(self._rstats)
+        return self._stats
 
     @property
     def diag(self) -> "Diag | None":
@@ -303,7 +311,7 @@ class Context:
             if k.value else np.empty((0, 2))
         if copy:
             verts = verts.copy()
-        return HullResult(Hull(verts), StageStats._from(s), raw=d)
+        return HullResult(Hull(verts), raw=d, raw_stats=s)
 
     def convex_hull(self, points, config: PipelineConfig | None = None,
                     copy: bool = True) -> HullResult:
@@ -343,7 +351,7 @@ class Context:
             if k.value else np.empty((0, 2))
         if copy:
             verts = verts.copy()
-        return HullResult(Hull(verts), StageStats._from(s), raw=d)
+        return HullResult(Hull(verts), raw=d, raw_stats=s)
 
     # ---- stage taps -----------------------------------------------------
     def find_extremes(self, points) -> np.ndarray:
