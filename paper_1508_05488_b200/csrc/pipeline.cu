@@ -887,7 +887,7 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
                   ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
-  // half of vbuf, group sizes in its lower part
+  // half of vbuf, each segment's survivor count in its lower part
   launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
                 (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart,
                 reinterpret_cast<const u32*>(ctx->d_fthr),
