@@ -180,6 +180,11 @@ int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out);
  * reference stage throws DegenerateInput. */
 int chgpu_finish_chains(const double* chains, const size_t* kept_counts, const double* quad,
                         double* out, size_t* n_out);
+
+/* Counters of the split finisher (finisher.cpp finish_chains_split: chains
+ * 1-4 run concurrently and are verified before use): calls that took it,
+ * and calls whose checks fell back to the sequential pass. Diagnostics. */
+void chgpu_finish_split_stats(unsigned long long* taken, unsigned long long* fallback);
 /* canonicalize_ring (melkman.hpp:20), in place. */
 void chgpu_canonicalize_ring(double* ring, size_t n);
 /* hull_oracle (pipeline.hpp:62): host reference hull; out capacity n. */

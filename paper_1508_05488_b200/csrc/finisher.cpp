@@ -9,8 +9,16 @@
 #include "finisher.h"
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <mutex>
+#include <thread>
+
+#include <unistd.h>
 
 namespace chgpu {
 namespace host {
@@ -367,6 +375,350 @@ int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corner
   return kOk;
 }
 
+// ------------------------------------------------------------------
+// The split finisher: finish_chains with the four chain segments run
+// concurrently, bit-identical by construction.
+//
+// Segment A is the ring up to and including corner B (L, chain 1, B),
+// segment B is chain 2 and corner R, segment C is chain 3 and corner T,
+// segment D is chain 4 with the closing logic. A runs exactly like
+// finish_chains. B, C and D run Melkman's deque loop speculatively on a
+// local model of the deque they will meet: their own corner K at the back
+// (with an unknown vertex Y below it) and at the front (with the ring's first
+// vertex L and an unknown vertex X beyond it). Every predicate they evaluate
+// uses the same expression as finish_chains on the same values, except the
+// ones touching X or Y: those take the outcome "strictly left" (no pop), and
+// the point is recorded. Popping K or L aborts. Once A (and B, for C) are
+// done, X and Y are known: the recorded predicates are evaluated for real,
+// and the handover states are checked (A's deque is [B, L, X, …, Y, B]; B
+// ends as [R, L, …, R]). Only if every check holds is the merged deque the one
+// the sequential pass would hold after corner T; otherwise the sequential
+// pass runs. The checks cost a few predicates per chain.
+
+namespace {
+
+inline double turn_v(const Pt& a, const Pt& b, double vx, double vy) {  // turn(a, b, v)
+  return (b.x - a.x) * (vy - a.y) - (b.y - a.y) * (vx - a.x);
+}
+inline double turn_front(double vx, double vy, const Pt& a, const Pt& b) {  // turn(v, a, b)
+  return (a.x - vx) * (b.y - vy) - (a.y - vy) * (b.x - vx);
+}
+
+// Melkman's deque loop (melkman.cpp:62-80) over p[0, len), consecutive
+// duplicates of (qx, qy) dropped: the same steps as finish_chains' loop.
+void deque_loop(Pt*& hp, Pt*& tp, const Pt* p, size_t len, double& qx, double& qy) {
+  Pt* h = hp;
+  Pt* t = tp;
+  double h_ax = h[0].x, h_ay = h[0].y, h_ex = h[1].x - h_ax, h_ey = h[1].y - h_ay;
+  double t_ax = t[-2].x, t_ay = t[-2].y, t_ex = t[-1].x - t_ax, t_ey = t[-1].y - t_ay;
+  for (size_t j = 0; j < len; ++j) {
+    const double vx = p[j].x, vy = p[j].y;
+    if (vx == qx && vy == qy) continue;
+    qx = vx;
+    qy = vy;
+    const bool left_head = h_ex * (vy - h_ay) - h_ey * (vx - h_ax) > 0.0;
+    const bool left_tail = t_ex * (vy - t_ay) - t_ey * (vx - t_ax) > 0.0;
+    if (left_head & left_tail) continue;
+    if (!left_tail && t - h >= 2) {
+      --t;
+      while (t - h >= 2) {
+        const Pt a = t[-2], b = t[-1];
+        if ((b.x - a.x) * (vy - a.y) - (b.y - a.y) * (vx - a.x) > 0.0) break;
+        --t;
+      }
+    }
+    *t++ = Pt{vx, vy};
+    while (t - h >= 2) {
+      const Pt a = h[0], b = h[1];
+      if ((a.x - vx) * (b.y - vy) - (a.y - vy) * (b.x - vx) > 0.0) break;
+      ++h;
+    }
+    *--h = Pt{vx, vy};
+    h_ax = vx;
+    h_ay = vy;
+    h_ex = h[1].x - vx;
+    h_ey = h[1].y - vy;
+    t_ax = t[-2].x;
+    t_ay = t[-2].y;
+    t_ex = t[-1].x - t_ax;
+    t_ey = t[-1].y - t_ay;
+  }
+  hp = h;
+  tp = t;
+}
+
+// Segment A: phase A (collinear run, seed) then the deque loop, over the
+// ring points of `segs` (finish_chains' feed + loop). Returns false if the
+// deque was never seeded.
+bool run_prefix(const Pt* const* sp, const size_t* sl, int nseg, Pt*& head, Pt*& tail, double& qx,
+                double& qy) {
+  int phase = 0;
+  Pt lo{0, 0}, hi{0, 0}, last{0, 0};
+  bool have_prev = false;
+  for (int s = 0; s < nseg; ++s) {
+    const Pt* p = sp[s];
+    size_t j = 0;
+    for (; j < sl[s] && phase != 2; ++j) {
+      const Pt v = p[j];
+      if (have_prev && v.x == qx && v.y == qy) continue;
+      qx = v.x;
+      qy = v.y;
+      have_prev = true;
+      if (phase == 0) {
+        lo = hi = last = v;
+        phase = 1;
+        continue;
+      }
+      if (turn(lo, hi, v) == 0) {
+        if (lex_less(v, lo))
+          lo = v;
+        else if (lex_less(hi, v))
+          hi = v;
+        last = v;
+        continue;
+      }
+      const Pt second = last;
+      const Pt first = same(last, lo) ? hi : lo;
+      const bool ccw = turn(first, second, v) == kLeft;
+      *tail++ = v;
+      *tail++ = ccw ? first : second;
+      *tail++ = ccw ? second : first;
+      *tail++ = v;
+      phase = 2;
+    }
+    if (j < sl[s]) deque_loop(head, tail, p + j, sl[s] - j, qx, qy);
+  }
+  return phase == 2;
+}
+
+// Segments B / C: the deque loop on the local model (see above).
+struct SpecRun {
+  Pt K, L;               // own corner (back base, first front element), ring start
+  std::vector<Pt> bk;    // back stack above K (bk.back() = tail[-1])
+  std::vector<Pt> fr;    // front stack before L (fr.back() = head[0])
+  std::vector<Pt> xt;    // v with turn(v, L, X) taken as > 0
+  std::vector<Pt> yt;    // v with turn(Y, K, v) taken as > 0
+  bool ok = true;
+
+  // chain p[0, len), then the next corner `end` (also a ring point) unless
+  // !with_end (chain 4 closing onto corner 0)
+  void run(const Pt* p, size_t len, const Pt& end, bool with_end = true) {
+    bk.clear();
+    fr.clear();
+    xt.clear();
+    yt.clear();
+    fr.push_back(K);
+    ok = true;
+    double qx = K.x, qy = K.y;
+    const size_t n = len + (with_end ? 1 : 0);
+    for (size_t j = 0; j < n; ++j) {
+      const double vx = j < len ? p[j].x : end.x, vy = j < len ? p[j].y : end.y;
+      if (vx == qx && vy == qy) continue;
+      qx = vx;
+      qy = vy;
+      const Pt& h0 = fr.back();
+      const Pt& h1 = fr.size() >= 2 ? fr[fr.size() - 2] : L;
+      const bool left_head = turn_v(h0, h1, vx, vy) > 0.0;
+      bool left_tail;
+      if (bk.empty()) {  // turn(Y, K, v)
+        yt.push_back(Pt{vx, vy});
+        left_tail = true;
+      } else {
+        const Pt& t1 = bk.back();
+        const Pt& t0 = bk.size() >= 2 ? bk[bk.size() - 2] : K;
+        left_tail = turn_v(t0, t1, vx, vy) > 0.0;
+      }
+      if (left_head & left_tail) continue;
+      if (!left_tail) {
+        bk.pop_back();  // (left_tail is false only with bk non-empty)
+        for (;;) {
+          if (bk.empty()) {
+            yt.push_back(Pt{vx, vy});
+            break;
+          }
+          const Pt& t1 = bk.back();
+          const Pt& t0 = bk.size() >= 2 ? bk[bk.size() - 2] : K;
+          if (turn_v(t0, t1, vx, vy) > 0.0) break;
+          bk.pop_back();
+        }
+      }
+      bk.push_back(Pt{vx, vy});
+      for (;;) {
+        if (fr.empty()) {  // turn(v, L, X)
+          xt.push_back(Pt{vx, vy});
+          break;
+        }
+        const Pt& a = fr.back();
+        const Pt& b = fr.size() >= 2 ? fr[fr.size() - 2] : L;
+        if (turn_front(vx, vy, a, b) > 0.0) break;
+        fr.pop_back();
+      }
+      fr.push_back(Pt{vx, vy});
+    }
+  }
+  // the recorded predicates with the real X and Y
+  bool verify(const Pt& X, const Pt& Y) const {
+    for (const Pt& v : xt)
+      if (!(turn_front(v.x, v.y, L, X) > 0.0)) return false;
+    for (const Pt& v : yt)
+      if (!(turn_v(Y, K, v.x, v.y) > 0.0)) return false;
+    return true;
+  }
+};
+
+// A worker thread for segment B, C or D. After a job it polls for the next one
+// for a while (calls come back to back in a serving loop, and a condition
+// variable wake-up costs tens of microseconds), then parks.
+struct Worker {
+  std::thread th;
+  std::mutex m;
+  std::condition_variable cv;
+  std::function<void()> job;
+  std::atomic<int> state{0};  // 0 idle, 1 job ready, 2 job done
+  std::atomic<bool> parked{false};
+  Worker() {
+    th = std::thread([this] {
+      for (;;) {
+        // poll ~2 ms, then park until the next submit
+        for (int i = 0; i < 20000 && state.load(std::memory_order_acquire) != 1; ++i)
+          for (int k = 0; k < 16; ++k) __builtin_ia32_pause();
+        if (state.load(std::memory_order_acquire) != 1) {
+          std::unique_lock<std::mutex> lk(m);
+          parked.store(true);
+          cv.wait(lk, [this] { return state.load(std::memory_order_acquire) == 1; });
+          parked.store(false);
+        }
+        job();
+        state.store(2, std::memory_order_release);
+      }
+    });
+  }
+  // (never destroyed: see WorkerPool)
+  void submit(std::function<void()> j) {
+    job = std::move(j);
+    {
+      std::lock_guard<std::mutex> lk(m);  // (orders the job before a parked wait re-checks)
+      state.store(1, std::memory_order_release);
+    }
+    if (parked.load()) cv.notify_all();
+  }
+  void wait() {
+    while (state.load(std::memory_order_acquire) != 2) __builtin_ia32_pause();
+    state.store(0, std::memory_order_relaxed);
+  }
+};
+
+// The process's three workers. Created on first use and never destroyed (the
+// threads end with the process); a forked child (whose copy has no threads)
+// makes its own.
+struct WorkerPool {
+  Worker b, c, d;
+  pid_t pid = getpid();
+};
+WorkerPool* worker_pool() {
+  static WorkerPool* pool = nullptr;
+  if (!pool || pool->pid != getpid()) pool = new WorkerPool;
+  return pool;
+}
+
+std::atomic<unsigned long long> g_split_taken{0}, g_split_fallback{0};
+
+size_t split_min() {
+  static const size_t v = [] {
+    const char* e = std::getenv("CHGPU_FINISH_SPLIT_MIN");
+    return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)2048;
+  }();
+  return v;
+}
+
+}  // namespace
+
+int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
+                        std::vector<Pt>& hull) {
+  for (int r = 0; r < 4; ++r)
+    if (kept_counts[r] < split_min() || kept_counts[r] < 8)
+      return finish_chains(chains, kept_counts, corners, hull);
+  const Pt* c[4];
+  c[0] = chains;
+  for (int r = 1; r < 4; ++r) c[r] = c[r - 1] + kept_counts[r - 1];
+  // the closing logic of finish_chains stays simple when chain 4's trailing
+  // run of its last point does not reach back to corner T
+  const Pt last_pt = c[3][kept_counts[3] - 1];
+  size_t cut = kept_counts[3] - 1;
+  while (cut > 0 && same(c[3][cut - 1], last_pt)) --cut;
+  if (cut == 0) return finish_chains(chains, kept_counts, corners, hull);
+
+  size_t total = 4;
+  for (int r = 0; r < 4; ++r) total += kept_counts[r];
+  thread_local Scratch deque_s;
+  Pt* buf = deque_s.get(2 * total + 8);
+  Pt* head = buf + total + 4;
+  Pt* tail = head;
+
+  // the workers serve one call at a time (concurrent calls on other
+  // contexts take the sequential pass)
+  static std::mutex busy;
+  std::unique_lock<std::mutex> own(busy, std::try_to_lock);
+  if (!own.owns_lock()) return finish_chains(chains, kept_counts, corners, hull);
+  WorkerPool* const pool = worker_pool();
+  static SpecRun sb, sc, sd;
+  sb.K = corners[1];
+  sc.K = corners[2];
+  sd.K = corners[3];
+  sb.L = sc.L = sd.L = corners[0];
+  // B: chain 2 then corner R; C: chain 3 then corner T; D: chain 4 up to
+  // its trailing run, then the run's one vertex unless it closes the ring
+  // onto corner 0 (finish_chains' closing logic; a repeat of the previous
+  // ring point drops as a consecutive duplicate)
+  const bool drop_last = same(last_pt, corners[0]);
+  pool->b.submit([&] { sb.run(c[1], kept_counts[1], corners[2]); });
+  pool->c.submit([&] { sc.run(c[2], kept_counts[2], corners[3]); });
+  pool->d.submit([&] { sd.run(c[3], cut, last_pt, !drop_last); });
+  double qx = 0, qy = 0;
+  const Pt* sp[3] = {&corners[0], c[0], &corners[1]};
+  const size_t sl[3] = {1, kept_counts[0], 1};
+  const bool seeded = run_prefix(sp, sl, 3, head, tail, qx, qy);
+  pool->b.wait();
+  pool->c.wait();
+  pool->d.wait();
+
+  // handover checks: A ends as [B, L, X, ..., Y, B]; B as [R, L, ..., R]; C as [T, L, ..., T]
+  bool ok = seeded && sb.ok && sc.ok && sd.ok && tail - head >= 5 && same(head[0], corners[1]) &&
+            same(head[1], corners[0]) && same(tail[-1], corners[1]);
+  ok = ok && sb.fr.size() == 1 && same(sb.fr[0], corners[2]) && !sb.bk.empty() &&
+       same(sb.bk.back(), corners[2]);
+  ok = ok && sc.fr.size() == 1 && same(sc.fr[0], corners[3]) && !sc.bk.empty() &&
+       same(sc.bk.back(), corners[3]);
+  if (ok) {
+    const Pt X = head[2], Y = tail[-2];
+    const Pt YC = sb.bk.size() >= 2 ? sb.bk[sb.bk.size() - 2] : corners[1];
+    const Pt YD = sc.bk.size() >= 2 ? sc.bk[sc.bk.size() - 2] : corners[2];
+    ok = sb.verify(X, Y) && sc.verify(X, YC) && sd.verify(X, YD);
+  }
+  if (!ok) {
+    g_split_fallback.fetch_add(1, std::memory_order_relaxed);
+    return finish_chains(chains, kept_counts, corners, hull);
+  }
+  g_split_taken.fetch_add(1, std::memory_order_relaxed);
+
+  // the final deque: D's front stack, then A's [L, X, ..., Y, B] (its front
+  // copy of B was popped by R's front pops), then the back stacks of B, C, D
+  Pt* h = head + 1 - (ptrdiff_t)sd.fr.size();
+  for (size_t i = 0; i < sd.fr.size(); ++i) h[i] = sd.fr[sd.fr.size() - 1 - i];
+  head = h;
+  for (const Pt& p : sb.bk) *tail++ = p;
+  for (const Pt& p : sc.bk) *tail++ = p;
+  for (const Pt& p : sd.bk) *tail++ = p;
+  const size_t m = (size_t)(tail - 1 - head);
+  size_t lo_i = 0;
+  for (size_t i = 1; i < m; ++i)
+    if (lex_less(head[i], head[lo_i])) lo_i = i;
+  hull.resize(m);
+  std::memcpy(hull.data(), head + lo_i, (m - lo_i) * sizeof(Pt));
+  std::memcpy(hull.data() + (m - lo_i), head, lo_i * sizeof(Pt));
+  return kOk;
+}
+
 int monotone_chain(const Pt* pts, size_t n, std::vector<Pt>& hull) {
   // oracle.cpp:19-37 over lexicographically sorted, duplicate-free points.
   hull.clear();
@@ -426,8 +778,8 @@ extern "C" int chgpu_assemble_polygon(const double* chains, const size_t* kept_c
 extern "C" int chgpu_finish_chains(const double* chains, const size_t* kept_counts,
                                    const double* quad, double* out, size_t* n_out) {
   std::vector<Pt> hull;
-  const int st = chgpu::host::finish_chains(reinterpret_cast<const Pt*>(chains), kept_counts,
-                                            reinterpret_cast<const Pt*>(quad), hull);
+  const int st = chgpu::host::finish_chains_split(reinterpret_cast<const Pt*>(chains), kept_counts,
+                                                  reinterpret_cast<const Pt*>(quad), hull);
   if (st) {
     *n_out = 0;
     return st;
@@ -435,6 +787,13 @@ extern "C" int chgpu_finish_chains(const double* chains, const size_t* kept_coun
   std::memcpy(out, hull.data(), hull.size() * sizeof(Pt));
   *n_out = hull.size();
   return 0;
+}
+
+// Split-finisher counters (tests): calls that took the concurrent path, and
+// calls whose checks sent them to the sequential pass.
+extern "C" void chgpu_finish_split_stats(unsigned long long* taken, unsigned long long* fallback) {
+  *taken = chgpu::host::g_split_taken.load();
+  *fallback = chgpu::host::g_split_fallback.load();
 }
 
 extern "C" int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out) {

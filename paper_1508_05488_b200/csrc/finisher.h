@@ -24,6 +24,9 @@ int melkman_ring(const Pt* ring, size_t n, std::vector<Pt>& hull);
 // assemble_ring + melkman_ring in one streaming pass (no ring copy).
 int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
                   std::vector<Pt>& hull);
+// finish_chains with the four chains run concurrently and verified; same result.
+int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
+                        std::vector<Pt>& hull);
 int monotone_chain(const Pt* sorted_unique, size_t n, std::vector<Pt>& hull);
 int sorted_hull(const Pt* pts, size_t n, std::vector<Pt>& hull);
 void insert_sorted_unique(std::vector<Pt>& sorted, const Pt& p);

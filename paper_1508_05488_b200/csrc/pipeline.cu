@@ -1311,8 +1311,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
     const auto t_host0 = std::chrono::steady_clock::now();
     // polygon.cpp:7-29 + melkman.cpp:17-86 in one streaming pass
-    const int mk = chgpu::host::finish_chains(reinterpret_cast<const Pt*>(ctx->h_out), kept_counts,
-                                              corners, ctx->hull);
+    // (the four chains concurrently when they are long, verified: finisher.cpp)
+    const int mk = chgpu::host::finish_chains_split(reinterpret_cast<const Pt*>(ctx->h_out),
+                                                    kept_counts, corners, ctx->hull);
     if (mk) return fail(ctx, CHGPU_DEGENERATE, "assemble_polygon/melkman: degenerate polygon");
     // the filter path touched no counter after k_readback cleared them
     if (filtered) ctx->counters_clean = true;

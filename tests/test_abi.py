@@ -4,6 +4,7 @@ with the reference's known answers. No GPU compute is called here."""
 import ctypes as C
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -192,3 +193,20 @@ def test_finish_chains_equals_assemble_then_melkman(product, oracle):
                 product.finish_chains(chains, kc, quad)
         else:
             assert np.array_equal(product.finish_chains(chains, kc, quad), want), ("long", trial)
+
+
+def test_split_finisher(product):
+    """finish_chains_split (the four chains concurrently, verified) is bit-identical
+    to the reference's assemble_polygon + melkman, takes the split path on
+    pipeline chains, and survives fork (tests/split_finisher_check.py runs
+    in its own process with the split threshold lowered to 8)."""
+    import subprocess
+    from pyoracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    env = dict(os.environ, CHGPU_FINISH_SPLIT_MIN="8")
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "split_finisher_check.py")],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    taken = int(out.stdout.split("taken=")[1].split()[0])
+    assert taken > 0, out.stdout
