@@ -16,6 +16,7 @@
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <new>
 #include <thread>
 
 #include <unistd.h>
@@ -576,7 +577,7 @@ struct Worker {
   std::function<void()> job;
   std::atomic<int> state{0};  // 0 idle, 1 job ready, 2 job done
   std::atomic<bool> parked{false};
-  Worker() {
+  void start() {
     th = std::thread([this] {
       for (;;) {
         // poll ~2 ms, then park until the next submit
@@ -615,9 +616,23 @@ struct WorkerPool {
   Worker b, c, d;
   pid_t pid = getpid();
 };
-WorkerPool* worker_pool() {
+WorkerPool* worker_pool() {  // nullptr if threads cannot be made here
   static WorkerPool* pool = nullptr;
-  if (!pool || pool->pid != getpid()) pool = new WorkerPool;
+  if (!pool || pool->pid != getpid()) {
+    // (a pool whose threads could not all start is kept alive, unused: its
+    // running threads still reference it)
+    WorkerPool* p = new (std::nothrow) WorkerPool;
+    try {
+      if (p) {
+        p->b.start();
+        p->c.start();
+        p->d.start();
+      }
+      pool = p;
+    } catch (...) {
+      pool = nullptr;
+    }
+  }
   return pool;
 }
 
@@ -661,6 +676,7 @@ int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt 
   std::unique_lock<std::mutex> own(busy, std::try_to_lock);
   if (!own.owns_lock()) return finish_chains(chains, kept_counts, corners, hull);
   WorkerPool* const pool = worker_pool();
+  if (!pool) return finish_chains(chains, kept_counts, corners, hull);
   static SpecRun sb, sc, sd;
   sb.K = corners[1];
   sc.K = corners[2];
