@@ -494,67 +494,80 @@ bool run_prefix(const Pt* const* sp, const size_t* sl, int nseg, Pt*& head, Pt*&
 
 // Segments B / C: the deque loop on the local model (see above).
 struct SpecRun {
-  Pt K, L;               // own corner (back base, first front element), ring start
-  std::vector<Pt> bk;    // back stack above K (bk.back() = tail[-1])
-  std::vector<Pt> fr;    // front stack before L (fr.back() = head[0])
-  std::vector<Pt> xt;    // v with turn(v, L, X) taken as > 0
-  std::vector<Pt> yt;    // v with turn(Y, K, v) taken as > 0
+  Pt K, L;                    // own corner (back base, first front element), ring start
+  Scratch bks, frs;           // stack storage (grows only)
+  Pt* bk = nullptr;           // back stack above K, bk[nb - 1] = tail[-1]
+  Pt* fr = nullptr;           // front stack before L, fr[nf - 1] = head[0]
+  size_t nb = 0, nf = 0;
+  std::vector<Pt> xt;         // v with turn(v, L, X) taken as > 0
+  std::vector<Pt> yt;         // v with turn(Y, K, v) taken as > 0
   bool ok = true;
 
   // chain p[0, len), then the next corner `end` (also a ring point) unless
-  // !with_end (chain 4 closing onto corner 0)
+  // !with_end (chain 4 closing onto corner 0). The end edges are cached as
+  // in deque_loop (same rounded differences as turn()).
   void run(const Pt* p, size_t len, const Pt& end, bool with_end = true) {
-    bk.clear();
-    fr.clear();
+    bk = bks.get(len + 2);
+    fr = frs.get(len + 3);
+    nb = 0;
+    nf = 0;
     xt.clear();
     yt.clear();
-    fr.push_back(K);
+    fr[nf++] = K;
     ok = true;
     double qx = K.x, qy = K.y;
+    double h_ax = K.x, h_ay = K.y, h_ex = L.x - K.x, h_ey = L.y - K.y;
+    double t_ax = 0, t_ay = 0, t_ex = 0, t_ey = 0;  // (unused while nb == 0: Y is unknown)
     const size_t n = len + (with_end ? 1 : 0);
     for (size_t j = 0; j < n; ++j) {
       const double vx = j < len ? p[j].x : end.x, vy = j < len ? p[j].y : end.y;
       if (vx == qx && vy == qy) continue;
       qx = vx;
       qy = vy;
-      const Pt& h0 = fr.back();
-      const Pt& h1 = fr.size() >= 2 ? fr[fr.size() - 2] : L;
-      const bool left_head = turn_v(h0, h1, vx, vy) > 0.0;
+      const bool left_head = h_ex * (vy - h_ay) - h_ey * (vx - h_ax) > 0.0;
       bool left_tail;
-      if (bk.empty()) {  // turn(Y, K, v)
+      if (nb == 0) {  // turn(Y, K, v)
         yt.push_back(Pt{vx, vy});
         left_tail = true;
       } else {
-        const Pt& t1 = bk.back();
-        const Pt& t0 = bk.size() >= 2 ? bk[bk.size() - 2] : K;
-        left_tail = turn_v(t0, t1, vx, vy) > 0.0;
+        left_tail = t_ex * (vy - t_ay) - t_ey * (vx - t_ax) > 0.0;
       }
       if (left_head & left_tail) continue;
       if (!left_tail) {
-        bk.pop_back();  // (left_tail is false only with bk non-empty)
+        --nb;  // (left_tail is false only with nb > 0)
         for (;;) {
-          if (bk.empty()) {
+          if (nb == 0) {
             yt.push_back(Pt{vx, vy});
             break;
           }
-          const Pt& t1 = bk.back();
-          const Pt& t0 = bk.size() >= 2 ? bk[bk.size() - 2] : K;
+          const Pt& t1 = bk[nb - 1];
+          const Pt& t0 = nb >= 2 ? bk[nb - 2] : K;
           if (turn_v(t0, t1, vx, vy) > 0.0) break;
-          bk.pop_back();
+          --nb;
         }
       }
-      bk.push_back(Pt{vx, vy});
+      const Pt t0 = nb >= 1 ? bk[nb - 1] : K;  // the new tail edge: (t0, v)
+      bk[nb++] = Pt{vx, vy};
       for (;;) {
-        if (fr.empty()) {  // turn(v, L, X)
+        if (nf == 0) {  // turn(v, L, X)
           xt.push_back(Pt{vx, vy});
           break;
         }
-        const Pt& a = fr.back();
-        const Pt& b = fr.size() >= 2 ? fr[fr.size() - 2] : L;
+        const Pt& a = fr[nf - 1];
+        const Pt& b = nf >= 2 ? fr[nf - 2] : L;
         if (turn_front(vx, vy, a, b) > 0.0) break;
-        fr.pop_back();
+        --nf;
       }
-      fr.push_back(Pt{vx, vy});
+      const Pt h1 = nf >= 1 ? fr[nf - 1] : L;  // the new front edge: (v, h1)
+      fr[nf++] = Pt{vx, vy};
+      h_ax = vx;
+      h_ay = vy;
+      h_ex = h1.x - vx;
+      h_ey = h1.y - vy;
+      t_ax = t0.x;
+      t_ay = t0.y;
+      t_ex = vx - t0.x;
+      t_ey = vy - t0.y;
     }
   }
   // the recorded predicates with the real X and Y
@@ -701,14 +714,14 @@ int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt 
   // handover checks: A ends as [B, L, X, ..., Y, B]; B as [R, L, ..., R]; C as [T, L, ..., T]
   bool ok = seeded && sb.ok && sc.ok && sd.ok && tail - head >= 5 && same(head[0], corners[1]) &&
             same(head[1], corners[0]) && same(tail[-1], corners[1]);
-  ok = ok && sb.fr.size() == 1 && same(sb.fr[0], corners[2]) && !sb.bk.empty() &&
-       same(sb.bk.back(), corners[2]);
-  ok = ok && sc.fr.size() == 1 && same(sc.fr[0], corners[3]) && !sc.bk.empty() &&
-       same(sc.bk.back(), corners[3]);
+  ok = ok && sb.nf == 1 && same(sb.fr[0], corners[2]) && sb.nb > 0 &&
+       same(sb.bk[sb.nb - 1], corners[2]);
+  ok = ok && sc.nf == 1 && same(sc.fr[0], corners[3]) && sc.nb > 0 &&
+       same(sc.bk[sc.nb - 1], corners[3]);
   if (ok) {
     const Pt X = head[2], Y = tail[-2];
-    const Pt YC = sb.bk.size() >= 2 ? sb.bk[sb.bk.size() - 2] : corners[1];
-    const Pt YD = sc.bk.size() >= 2 ? sc.bk[sc.bk.size() - 2] : corners[2];
+    const Pt YC = sb.nb >= 2 ? sb.bk[sb.nb - 2] : corners[1];
+    const Pt YD = sc.nb >= 2 ? sc.bk[sc.nb - 2] : corners[2];
     ok = sb.verify(X, Y) && sc.verify(X, YC) && sd.verify(X, YD);
   }
   if (!ok) {
@@ -719,12 +732,13 @@ int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt 
 
   // the final deque: D's front stack, then A's [L, X, ..., Y, B] (its front
   // copy of B was popped by R's front pops), then the back stacks of B, C, D
-  Pt* h = head + 1 - (ptrdiff_t)sd.fr.size();
-  for (size_t i = 0; i < sd.fr.size(); ++i) h[i] = sd.fr[sd.fr.size() - 1 - i];
+  Pt* h = head + 1 - (ptrdiff_t)sd.nf;
+  for (size_t i = 0; i < sd.nf; ++i) h[i] = sd.fr[sd.nf - 1 - i];
   head = h;
-  for (const Pt& p : sb.bk) *tail++ = p;
-  for (const Pt& p : sc.bk) *tail++ = p;
-  for (const Pt& p : sd.bk) *tail++ = p;
+  for (const SpecRun* sr : {&sb, &sc, &sd}) {
+    std::memcpy(tail, sr->bk, sr->nb * sizeof(Pt));
+    tail += sr->nb;
+  }
   const size_t m = (size_t)(tail - 1 - head);
   size_t lo_i = 0;
   for (size_t i = 1; i < m; ++i)
