@@ -5,31 +5,49 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one full convex_hull of a synthetic point set (the reference's own
-generator, bit-identical): extremes -> classify/discard -> region sort ->
-SPA -> chains to host -> Melkman, result on the host.
+generator, bit-identical): extremes -> classify/discard -> SPA pre-filter ->
+chunk SPA -> chains to host -> Melkman, the hull on the host.
 
-* value: Mpoints/s with the input already resident in HBM (chgpu_hull_device),
-  timed with CUDA events on the library's stream, max over ranks.
-* e2e: the same metric through the C ABI with the input in pinned HOST
-  memory (chgpu_hull), host->device copy and the chain/hull read-back inside
-  the timed region.
-* roofline: the dominant kernel (the onesweep radix pass) plus the discard
-  kernels (K1 + K2), algorithmic bytes / CUDA-event time, against
-  MEASURED_PEAKS.json hbm_gbs.
-* cpu_baseline: the reference C++ path (oracle/_ref, compiled from the
-  unmodified sources) on this host's cores, on the same input.
+Workloads (identical `config` in both arms):
+* N = 1: BASELINE configs[1], 20M uniform_square points, seed 42.
+* N > 1 (torchrun, one rank per GPU): BASELINE configs[4], the 1B-point
+  uniform_square set (seed 42) split into N contiguous index ranges; rank r
+  generates exactly its range (chgpu_generate_range). The step is the sharded
+  hull (paper_1508_05488_b200/sharded.py: NCCL exchange of the extreme
+  candidates, per-rank discard + SPA against the global quad, chains gathered,
+  rank-0 merge); value counts all 1B points ("scaling": "strong").
 
-N > 1 (torchrun): weak scaling, each rank owns a 20M-point shard of one
-global set (shard r = generate(dist, n, seed + r)); the step is the sharded
-hull (paper_1508_05488_b200/sharded.py) and value counts all ranks' points.
-The input is 320 MB per rank, larger than the 126 MB L2, so no L2 flush is
+Keys of our line:
+* value: Mpoints/s with the input resident in HBM (chgpu_hull_device), CUDA
+  events on the library's stream around K steps, max over ranks.
+* e2e: the same metric through the C ABI with the input in pinned HOST memory
+  (chgpu_hull: H2D inside the timed region, overlapped with K1), and
+  e2e.pageable the same through the C++ drop-in chainhull::convex_hull
+  (libchainhull.so) on pageable host memory, as a std::vector caller has it.
+* roofline: the kernel with the largest time (K2) against MEASURED_PEAKS.json
+  hbm_gbs, algorithmic bytes / its in-step CUDA-event time, plus the discard
+  kernels K1 + K2 on SURVEY §8(d)'s basis (32 n + 16 s1).
+* parity: the measured step's hull and counters against the reference's own
+  outputs (tests/golden/big.json, big_1b.json), outside the timed region.
+* cpu_baseline: the reference C++ path (oracle/_ref, the unmodified sources)
+  on this host's cores, median of 5 after one warm-up, with
+  mallopt(M_MMAP_THRESHOLD, 256 MB) as tests/acceptance.cpp:376 does.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref) on the
+same config; it imports nothing from the product (inputs come from the
+reference's own generate()). Under torchrun only rank 0 runs it.
+
+The input (320 MB per 20M points) exceeds the 126 MB L2, so no L2 flush is
 needed between steps.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
+import hashlib
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -42,6 +60,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Mpoints/s end-to-end hull (20M uniform pts)"
 UNIT = "Mpoints/s"
+N_SINGLE = 20_000_000        # BASELINE configs[1]
+N_SHARDED = 1_000_000_000    # BASELINE configs[4]
+REF_SAMPLE_SHARDED = 50_000_000  # reference arm's bounded sample of configs[4]
 
 
 def peaks():
@@ -53,6 +74,79 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def workload(args, world):
+    """The config dict both arms print (identical by construction)."""
+    n = args.n if args.n else (N_SHARDED if world > 1 else N_SINGLE)
+    shards = world if world > 1 else 1
+    name = ("BASELINE configs[4]" if world > 1 and n == N_SHARDED and args.dist == "uniform_square"
+            else "BASELINE configs[1]" if world == 1 and n == N_SINGLE and args.dist == "uniform_square"
+            else "custom")
+    return {"workload": f"{n} {args.dist} points, seed {args.seed}"
+                        + (f", {shards} contiguous shards" if shards > 1 else ""),
+            "baseline_config": name, "n_points": n, "distribution": args.dist, "seed": args.seed,
+            "chunk_count": args.chunk_count, "shards": shards,
+            "parallelism": f"shard{shards}" if shards > 1 else "single",
+            "l2": (f"input {16 * n // shards // 1_000_000} MB per GPU > 126 MB L2 (no flush needed)"
+                   if 16 * n // shards > 126_000_000 else "input fits in L2 (not flushed)")}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def set_mallopt():
+    """mallopt(M_MMAP_THRESHOLD, 256 MB), as the reference's acceptance
+    harness does before timing (tests/acceptance.cpp:376)."""
+    try:
+        libc = ctypes.CDLL("libc.so.6")
+        return bool(libc.mallopt(-3, 256 << 20))  # M_MMAP_THRESHOLD = -3
+    except OSError:
+        return False
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+def golden_for(n, dist, seed, chunk_count):
+    """The reference's own hull + counters for this input (tests/golden)."""
+    gdir = os.path.join(ROOT, "tests", "golden")
+    try:
+        with open(os.path.join(gdir, "big.json")) as f:
+            for g in json.load(f):
+                if (g["n"], g["dist"], g["seed"], g["chunk_count"]) == (n, dist, seed, chunk_count):
+                    return g
+        with open(os.path.join(gdir, "big_1b.json")) as f:
+            g = json.load(f)
+            if (g["n"], g["dist"], g["seed"], g["chunk_count"]) == (n, dist, seed, chunk_count):
+                return g
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
+def check_parity(hull, counts, n, dist, seed, chunk_count, sharded):
+    """'bit-exact' when the hull bytes (and, on one GPU, all four counters)
+    equal the reference's; raises on a mismatch; 'unpinned' without a golden."""
+    g = golden_for(n, dist, seed, chunk_count)
+    if g is None:
+        return "unpinned (no golden for this input)"
+    if sha(hull) != g["hull_sha"] or len(hull) != g["hull_n"]:
+        raise SystemExit(f"PARITY FAILURE: hull differs from the reference ({len(hull)} vs "
+                         f"{g['hull_n']} vertices)")
+    if not sharded and list(counts) != list(g["counts"]):
+        raise SystemExit(f"PARITY FAILURE: counters {list(counts)} != reference {g['counts']}")
+    return ("bit-exact (hull sha256 == reference)" if sharded
+            else "bit-exact (hull sha256 and n_input/n_after_round1/n_after_spa/n_hull == reference)")
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -62,21 +156,22 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.out = ""
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.2)
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
         if self.p:
-            time.sleep(0.25)
+            time.sleep(0.1)
             self.p.terminate()
             try:
                 self.out, _ = self.p.communicate(timeout=5)
@@ -99,84 +194,118 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of
-# the pipeline's kernels from the committed ncu --set full captures of this
-# workload (profiles/, tools/round_measure.sh); None when absent.
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "round1", "traffic.json")
+# Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the
+# pipeline's kernels from the committed ncu --set full captures of this
+# workload (profiles/); None when absent.
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "round2", "traffic.json")
 
 
 def measured_traffic(kernel_key: str):
     try:
         with open(TRAFFIC_FILE) as f:
-            t = json.load(f)
-        return t.get(kernel_key)
+            return json.load(f).get(kernel_key)
     except Exception:
         return None
 
 
-def cpu_baseline(pts: np.ndarray, steps: int = 3):
-    """The reference CPU path (oracle/_ref) on this host; port if absent."""
+def ref_lib():
+    """The reference (oracle/_ref) or, where it was not built, the C port."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import Oracle, RefLib
-    cores = os.cpu_count() or 1
     if RefLib.available():
-        ref = RefLib()
-        kind = "reference"
-        run = lambda par: ref.convex_hull(pts, 1024, par)  # noqa: E731
-    else:
-        orc = Oracle()
-        kind, cores = "port", 1
-        run = lambda par: orc.convex_hull(pts, 1024)  # noqa: E731
-    run(0)  # warm-up (page faults, allocator)
-    ts = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        run(0)
-        ts.append(time.perf_counter() - t0)
-    t_all = statistics.median(ts)
-    t0 = time.perf_counter()
-    run(1)
-    t_one = time.perf_counter() - t0
+        return RefLib(), "reference"
+    return Oracle(), "port"
+
+
+def ref_step(lib, kind, pts, chunk_count, parallelism):
+    if kind == "reference":
+        return lib.convex_hull(pts, chunk_count, parallelism)[0]
+    return lib.convex_hull(pts, chunk_count)
+
+
+def cpu_baseline(pts: np.ndarray, chunk_count: int):
+    """The reference CPU path (oracle/_ref) on this host, same input: median
+    of 5 after one warm-up at parallelism = 0 (all host threads), and at
+    parallelism = 1 (median of 3), generation excluded."""
+    lib, kind = ref_lib()
+    mall = set_mallopt()
+    cores = os.cpu_count() or 1
+
+    def timed(par, reps):
+        ref_step(lib, kind, pts, chunk_count, par)  # warm-up (page faults, allocator)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ref_step(lib, kind, pts, chunk_count, par)
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    t_all = timed(0, 5)
+    t_one = timed(1, 3)
     n = len(pts)
-    return {"value": n / t_all / 1e6, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{n} points, convex_hull chunk_count=1024, median of {steps} runs "
-                      f"(parallelism=0 = all {cores} host threads), generation excluded",
+    return {"value": n / t_all / 1e6, "unit": UNIT, "cores": cores if kind == "reference" else 1,
+            "kind": kind, "cpu_model": cpu_model(), "nproc": cores,
+            "sample": f"the same {n} points, convex_hull chunk_count={chunk_count}, "
+                      f"parallelism=0 (all {cores} host threads), median of 5 after 1 warm-up; "
+                      f"mallopt(M_MMAP_THRESHOLD, 256 MB) {'applied' if mall else 'unavailable'}; "
+                      f"generation excluded",
             "value_1thread": n / t_one / 1e6, "ms_all_cores": t_all * 1e3,
             "ms_1thread": t_one * 1e3}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU implementation of the path."""
-    import paper_1508_05488_b200 as P
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, the unmodified sources) on this host's cores. Imports
+    nothing from the product: the input comes from the reference's own
+    generate()."""
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import Oracle, RefLib
-    pts = P.generate(args.dist, args.n, args.seed)
+    cfg = workload(args, world)
+    n = cfg["n_points"]
+    lib, kind = ref_lib()
+    mall = set_mallopt()
     cores = os.cpu_count() or 1
-    if RefLib.available():
-        ref, kind = RefLib(), "reference"
-        step = lambda: ref.convex_hull(pts, args.chunk_count, 0)  # noqa: E731
-    else:
-        orc, kind, cores = Oracle(), "port", 1
-        step = lambda: orc.convex_hull(pts, args.chunk_count)  # noqa: E731
+    # a bounded sample of configs[4]: its first REF_SAMPLE_SHARDED points
+    # (uniform_square draws two values per point in order, so the prefix of
+    # the 1B set is generate(m)); configs[1] runs whole
+    m = min(n, REF_SAMPLE_SHARDED) if world > 1 else n
+    pts = lib.generate(args.dist, m, args.seed)
     for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
+        ref_step(lib, kind, pts, args.chunk_count, 0)
+    ts = []
     for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    v = args.n / dt / 1e6
+        t0 = time.perf_counter()
+        ref_step(lib, kind, pts, args.chunk_count, 0)
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
+    v = m / dt / 1e6
+    sample = (f"{m} points per step" + (f" (the first {m} of the {n}-point set)" if m < n else "")
+              + f", convex_hull chunk_count={args.chunk_count}, parallelism=0 (all {cores} host "
+              f"threads), mean of {args.steps} steps after {args.warmup} warm-up; "
+              f"mallopt(M_MMAP_THRESHOLD, 256 MB) {'applied' if mall else 'unavailable'}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"{args.n} {args.dist} points seed {args.seed}",
-                       "chunk_count": args.chunk_count, "parallelism": "cpu threads"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{args.n} points per step, all host threads"},
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (the reference's generate())", "impl": "reference",
+            "config": cfg,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores if kind == "reference" else 1,
+                             "kind": kind, "cpu_model": cpu_model(), "nproc": cores,
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def capi_lib():
+    """libchainhull.so (the C++ drop-in) through its C entry
+    (include/chainhull_capi.h)."""
+    import paper_1508_05488_b200 as P
+    P.load_library()  # libchgpu.so first (libchainhull.so's dependency)
+    L = ctypes.CDLL(os.path.join(ROOT, "paper_1508_05488_b200", "libchainhull.so"))
+    sz = ctypes.c_size_t
+    L.chainhull_capi_convex_hull.argtypes = [ctypes.c_void_p, sz, sz, sz, ctypes.c_int,
+                                             ctypes.c_void_p, sz, ctypes.POINTER(sz),
+                                             ctypes.POINTER(sz)]
+    return L
 
 
 def main():
@@ -186,12 +315,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dist", default="uniform_square")
-    ap.add_argument("--n", type=int, default=20_000_000)
+    ap.add_argument("--npoints", dest="n", type=int, default=0, help="points in the whole set (default: the "
+                    "BASELINE config for the GPU count)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--chunk-count", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
-                    help="exchange backend for N > 1 (gloo: testing several ranks on one GPU)")
+                    help="exchange backend for N > 1 (gloo: several ranks on one GPU, testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -208,6 +339,8 @@ def main():
     import paper_1508_05488_b200 as P
     from paper_1508_05488_b200.sharded import GpuShardOps, sharded_convex_hull
 
+    cfg = workload(args, world)
+    n_total = cfg["n_points"]
     local = local % max(1, torch.cuda.device_count())  # gloo testing: ranks may share a GPU
     torch.cuda.set_device(local)
     if world > 1:
@@ -216,32 +349,33 @@ def main():
         else:
             dist.init_process_group("gloo")
     ctx = P.Context(local)
-    cfg = P.PipelineConfig(chunk_count=args.chunk_count)
+    pcfg = P.PipelineConfig(chunk_count=args.chunk_count)
 
-    # Input: this rank's shard, generated on the host (bit-identical to the
-    # reference generator), resident in HBM and in pinned host memory.
-    pts = P.generate(args.dist, args.n, args.seed + rank)
-    d_pts = torch.from_numpy(pts).to(f"cuda:{local}")
-    h_pin = torch.empty((args.n, 2), dtype=torch.float64, pin_memory=True)
-    h_pin.numpy()[:] = pts
-    ctx.reserve(args.n)
+    # This rank's contiguous shard of the set, generated on the host
+    # (bit-identical to the reference generator) straight into pinned memory,
+    # then resident in HBM.
+    begin = n_total * rank // world
+    n = n_total * (rank + 1) // world - begin
+    h_pin = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    P.generate(args.dist, n_total, args.seed, begin=begin, count=n, out=h_pin.numpy())
+    d_pts = h_pin.to(f"cuda:{local}")
+    ctx.reserve(n)
     torch.cuda.synchronize()
-
     stream = torch.cuda.ExternalStream(ctx.stream)
+    ops = GpuShardOps(ctx, d_pts, begin) if world > 1 else None
 
     def step_device():
         if world == 1:
-            return ctx.convex_hull_device(d_pts.data_ptr(), args.n, cfg, copy=False)
-        ops = GpuShardOps(ctx, d_pts, rank * args.n)
+            return ctx.convex_hull_device(d_pts.data_ptr(), n, pcfg, copy=False)
         return sharded_convex_hull(ops, args.chunk_count)
 
     def step_host():
         if world == 1:
-            return ctx.convex_hull(h_pin.numpy(), cfg, copy=False)
-        # host-resident shard: copy in, then the sharded step
-        d_pts.copy_(h_pin, non_blocking=True)
-        torch.cuda.synchronize()
-        ops = GpuShardOps(ctx, d_pts, rank * args.n)
+            return ctx.convex_hull(h_pin.numpy(), pcfg, copy=False)
+        # host-resident shard: copy it in on the library stream, then the
+        # sharded step
+        with torch.cuda.stream(stream):
+            d_pts.copy_(h_pin, non_blocking=True)
         return sharded_convex_hull(ops, args.chunk_count)
 
     def timed(fn, steps):
@@ -266,57 +400,53 @@ def main():
         return ms, out
 
     for _ in range(args.warmup):
-        last = step_device()
-    # correctness guard for the measured configuration (single GPU)
-    diag = last.diag if world == 1 else None
-
+        step_device()
     with ClockSampler(local) as clk:
         ms, res = timed(step_device, args.steps)
-    for _ in range(2):
-        step_host()
-    ms_e2e, res_e2e = timed(step_host, args.steps)
+        # parity of the measured configuration, outside the timed region
+        if world == 1:
+            r = res
+            counts = [r.stats.n_input, r.stats.n_after_round1, r.stats.n_after_spa, r.stats.n_hull]
+            parity = check_parity(r.hull.vertices, counts, n_total, args.dist, args.seed,
+                                  args.chunk_count, sharded=False)
+        elif rank == 0:
+            parity = check_parity(res, [n_total, None, None, len(res)], n_total, args.dist,
+                                  args.seed, args.chunk_count, sharded=True)
+        for _ in range(2):
+            step_host()
+        ms_e2e, res_e2e = timed(step_host, args.steps)
     clocks = clk.summary()
 
-    total_pts = args.n * world
-    value = total_pts / (ms * 1e-3) / 1e6
-    e2e_value = total_pts / (ms_e2e * 1e-3) / 1e6
-
+    value = n_total / (ms * 1e-3) / 1e6
+    e2e_value = n_total / (ms_e2e * 1e-3) / 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generator, bit-identical)",
-            "config": {"workload": f"{args.n} {args.dist} points per GPU, seed {args.seed}",
-                       "chunk_count": args.chunk_count, "input_bytes": args.n * 16,
-                       "l2": "input 320 MB > 126 MB L2 (no flush needed)",
-                       "parallelism": f"shard{world}" if world > 1 else "single"},
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, bit-identical)", "config": cfg,
             "clocks": clocks}
 
     if rank == 0 and world == 1:
         r = res
         d = r.diag
+        line["parity"] = parity
         s1 = sum(d.region_counts[1:])
         hbm, src = peaks()
         t = d.times_ms
-        n = args.n
         # K2 writes each survivor as an 8-byte filter key + a 4-byte input
         # index on the pre-filtered path, as a 16-byte (k, v) record on the
         # sort path
         surv_b = 12 if d.spa_path == 1 else 16
-        disc_bytes = 32 * n + surv_b * s1
         disc_ms = t["t_k1_ms"] + t["t_k2_ms"]
         kernels = {
-            "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n,
-                            "basis": "16 B/pt read"},
+            "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n, "basis": "16 B/pt read"},
             ("k2_classify_survivors" if d.spa_path == 1 else "k2_classify_compact"):
                 {"ms": t["t_k2_ms"], "bytes": 16 * n + surv_b * s1,
                  "basis": f"16 B/pt read + {surv_b} B/survivor write"},
         }
         if d.spa_path == 1:
-            lb = d.filter_log2nb
-            nb = 4 * (1 << lb)
             nc = d.n_candidates
             kernels.update({
-                "k3_bin_scan": {"ms": t["t_binscan_ms"], "bytes": 24 * nb,
+                "k3_bin_scan": {"ms": t["t_binscan_ms"], "bytes": 24 * 4 * (1 << d.filter_log2nb),
                                 "basis": "12 B/bin read + 12 B/bin write"},
                 "k3_filter": {"ms": t["t_filter_ms"], "bytes": 8 * s1 + 36 * nc,
                               "basis": "8 B/survivor key read + per candidate 4 B index "
@@ -336,8 +466,8 @@ def main():
                 "k3_radix_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": 32 * s1,
                                   "basis": "16 B/record read + 16 B/record write"},
                 "k3_ties": {"ms": t["t_ties_ms"]},
-                "k4_spa": {"ms": t["t_spa_kernel_ms"], "bytes": 8 * s1 + 2 * s1
-                           + 16 * sum(d.kept_counts),
+                "k4_spa": {"ms": t["t_spa_kernel_ms"],
+                           "bytes": 8 * s1 + 2 * s1 + 16 * sum(d.kept_counts),
                            "basis": "8 B/record read + 16 B/kept write (+ flags)"},
             })
         for kv in kernels.values():
@@ -347,16 +477,23 @@ def main():
         kernels["host_melkman_ms"] = t["t_host_ms"]
         dom_name, dom = max(((k, v) for k, v in kernels.items()
                              if isinstance(v, dict) and v.get("gbs")), key=lambda kv: kv[1]["ms"])
+        # SURVEY §8(d) basis of the discard kernels: 32 n + 16 s1
+        disc_bytes = 32 * n + 16 * s1
+        disc_bytes_written = 32 * n + surv_b * s1
         line["roofline"] = {
             "bound": "hbm", "kernel": dom_name,
             "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s",
             "peak_source": src, "frac": dom["gbs"] / hbm,
             "traffic": measured_traffic(dom_name),
             "algorithmic_bytes": f"{dom.get('basis', 'bytes moved')}: {dom['bytes']} B per launch",
-            "discard_kernels": {"kernels": "k_extremes_partial (+ last-block merge), k_classify_survivors",
-                                "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
-                                "frac": disc_bytes / (disc_ms * 1e-3) / 1e9 / hbm,
-                                "bytes": disc_bytes, "ms": disc_ms},
+            "discard_kernels": {
+                "kernels": "k_extremes_partial (+ last-block merge), k_classify_survivors",
+                "basis": "SURVEY 8(d): 32 B/pt + 16 B/survivor",
+                "bytes": disc_bytes, "ms": disc_ms,
+                "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
+                "frac": disc_bytes / (disc_ms * 1e-3) / 1e9 / hbm,
+                "bytes_moved": disc_bytes_written,
+                "frac_bytes_moved": disc_bytes_written / (disc_ms * 1e-3) / 1e9 / hbm},
             "spa_path": ["sort", "prefilter", "prefilter->sort"][d.spa_path],
             "per_kernel": kernels,
         }
@@ -367,14 +504,46 @@ def main():
         # device -> host: the kept chains (the host finisher builds the hull),
         # or on the convex fast path the finished hull alone
         d2h = 16 * (r.stats.n_hull if d.convex_fast_path else sum(d.kept_counts))
-        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 16,
-                       "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-                       "h2d_ms": res_e2e.diag.times_ms["t_h2d_ms"]}
+        e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 16,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+               "h2d_ms": res_e2e.diag.times_ms["t_h2d_ms"],
+               "source": "pinned host memory through the C ABI (chgpu_hull)"}
+        if not args.no_pageable:
+            # the C++ drop-in chainhull::convex_hull on pageable memory (a
+            # std::vector's), timed on the host clock (synchronous API)
+            L = capi_lib()
+            h_page = np.array(h_pin.numpy(), copy=True)  # pageable
+            nh = ctypes.c_size_t()
+            cnt = (ctypes.c_size_t * 4)()
+
+            def page_step():
+                st = L.chainhull_capi_convex_hull(h_page.ctypes.data, n, args.chunk_count, 0, 1,
+                                                  None, 0, ctypes.byref(nh), cnt)
+                if st:
+                    raise SystemExit(f"chainhull_capi_convex_hull failed ({st})")
+            for _ in range(2):
+                page_step()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                page_step()
+            ms_page = (time.perf_counter() - t0) * 1e3 / args.steps
+            if list(cnt) != [r.stats.n_input, r.stats.n_after_round1, r.stats.n_after_spa,
+                             r.stats.n_hull]:
+                raise SystemExit("PARITY FAILURE: C++ drop-in counters differ")
+            e2e["pageable"] = {"value": n / (ms_page * 1e-3) / 1e6, "unit": UNIT,
+                               "ms_per_step": ms_page, "h2d_bytes_per_step": n * 16,
+                               "d2h_bytes_per_step": d2h,
+                               "source": "pageable host memory through the C++ drop-in "
+                                         "chainhull::convex_hull (libchainhull.so), host clock"}
+        line["e2e"] = e2e
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(pts)
+            line["cpu_baseline"] = cpu_baseline(h_pin.numpy(), args.chunk_count)
     elif rank == 0:
-        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": args.n * 16,
-                       "d2h_bytes_per_step": 0, "ms_per_step": ms_e2e}
+        line["parity"] = parity
+        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_total * 16,
+                       "d2h_bytes_per_step": 16 * len(res_e2e), "ms_per_step": ms_e2e,
+                       "source": "each rank's shard from pinned host memory, copied in inside "
+                                 "the timed region, then the sharded step"}
         line["hull_vertices"] = int(len(res)) if res is not None else None
     if rank == 0:
         print(json.dumps(line), flush=True)

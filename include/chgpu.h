@@ -96,7 +96,9 @@ typedef struct {
 
 /* Options (chgpu_ctx_set_option). */
 enum {
-  CHGPU_OPT_SPA_PATH = 1  /* value: one of the CHGPU_SPA_* below */
+  CHGPU_OPT_SPA_PATH = 1,   /* value: one of the CHGPU_SPA_* below */
+  CHGPU_OPT_CHAINS_TAP = 2  /* value 1: keep each hull call's SPA chains for
+                               chgpu_last_chains (a parity tap; costs one D2H) */
 };
 enum {
   CHGPU_SPA_AUTO = 0,     /* pre-filter when chunks average >= 16 records (default) */
@@ -143,6 +145,14 @@ int chgpu_hull_xy_binary(chgpu_ctx* ctx, const char* path, size_t chunk_count,
 int chgpu_hull_device(chgpu_ctx* ctx, const double* d_xy, size_t n, size_t chunk_count,
                       int degenerate_fallback, const double** hull_xy, size_t* n_hull,
                       chgpu_stats* stats, chgpu_diag* diag);
+
+/* The SPA chains of the last chgpu_hull* call on ctx (the kept points of
+ * spa_filter per region, spa.cpp:109-163, concatenated LL|LR|UR|UL, as
+ * the device pipeline produced them), when CHGPU_OPT_CHAINS_TAP is set:
+ * *chains_xy (owned by ctx, valid until the next call) and kept_counts[4].
+ * CHGPU_INVALID_ARG when the tap is off; all-zero counts on the degenerate
+ * branch (it has no chains). */
+int chgpu_last_chains(chgpu_ctx* ctx, const double** chains_xy, size_t* kept_counts);
 
 /* ---- stage taps (the reference stage API, used by the C++ shim) -------- */
 
@@ -195,6 +205,12 @@ int chgpu_hull_oracle(const double* xy, size_t n, double* out, size_t* n_out);
 /* generate (datasets.hpp:35): bit-identical to the reference's
  * mt19937_64-based generator. dist follows datasets.hpp:13-21. */
 int chgpu_generate(int dist, size_t n, uint64_t seed, double* out_xy);
+/* Points [begin, begin + count) of generate(dist, n, seed) into out_xy
+ * (2*count doubles): the contiguous shard of one rank of the sharded run,
+ * without materialising the whole set (draws before `begin` are discarded;
+ * datasets.cpp:17-106 consumes a fixed number per point). */
+int chgpu_generate_range(int dist, size_t n, uint64_t seed, size_t begin, size_t count,
+                         double* out_xy);
 
 /* ---- sharded path (multi-GPU, one rank per GPU) ------------------------- */
 

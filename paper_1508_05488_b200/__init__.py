@@ -95,6 +95,7 @@ class _Diag(C.Structure):
 
 # chgpu_ctx_set_option (include/chgpu.h)
 OPT_SPA_PATH = 1
+OPT_CHAINS_TAP = 2
 SPA_AUTO, SPA_SORT, SPA_FILTER = 0, 1, 2
 
 
@@ -202,6 +203,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_ctx_stream.restype = vp
         L.chgpu_reserve.argtypes = [vp, C.c_size_t]
         L.chgpu_ctx_set_option.argtypes = [vp, C.c_int, C.c_longlong]
+        L.chgpu_last_chains.argtypes = [vp, C.POINTER(_dp), _sz]
         hull_args = [vp, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
                      C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_hull.argtypes = hull_args
@@ -221,6 +223,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_canonicalize_ring.restype = None
         L.chgpu_hull_oracle.argtypes = [_dp, C.c_size_t, _dp, _sz]
         L.chgpu_generate.argtypes = [C.c_int, C.c_size_t, C.c_uint64, _dp]
+        L.chgpu_generate_range.argtypes = [C.c_int, C.c_size_t, C.c_uint64, C.c_size_t,
+                                           C.c_size_t, _dp]
         L.chgpu_shard_extremes.argtypes = [vp, C.c_void_p, C.c_size_t, C.c_uint64, _dp,
                                            C.POINTER(C.c_uint64)]
         L.chgpu_fold_extremes.argtypes = [_dp, C.POINTER(C.c_uint64), C.c_size_t, _dp]
@@ -297,6 +301,22 @@ class Context:
     def set_spa_path(self, mode: int):
         """SPA_AUTO (default), SPA_SORT (sort every survivor) or SPA_FILTER."""
         self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_SPA_PATH, mode))
+
+    def set_chains_tap(self, on: bool = True):
+        """Keep each hull call's SPA chains for last_chains() (parity tap)."""
+        self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_CHAINS_TAP, int(bool(on))))
+
+    def last_chains(self):
+        """(chains (k, 2) float64 copy, kept_counts[4]) of the last hull call:
+        the kept points of spa_filter per region (spa.cpp:109-163), LL|LR|UR|UL."""
+        out = _dp()
+        kc = (C.c_size_t * 4)()
+        self._check(self.lib.chgpu_last_chains(self.h, C.byref(out), kc))
+        counts = [int(c) for c in kc]
+        k = sum(counts)
+        a = (np.ctypeslib.as_array(out, shape=(2 * k,)).reshape(-1, 2).copy() if k
+             else np.empty((0, 2)))
+        return a, counts
 
     def _hull(self, fn, ptr, n, config, copy=True):
         config = config or PipelineConfig()
@@ -531,13 +551,22 @@ def hull_oracle(points) -> np.ndarray:
     return out[:k.value]
 
 
-def generate(distribution: str | int, n: int, seed: int) -> np.ndarray:
-    """datasets.hpp:35, bit-identical to the reference generator."""
+def generate(distribution: str | int, n: int, seed: int, begin: int = 0,
+             count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+    """datasets.hpp:35, bit-identical to the reference generator; with
+    begin/count, only points [begin, begin + count) of the n-point set (a
+    contiguous shard), written into `out` when given (e.g. pinned memory)."""
     L = load_library()
     d = DISTRIBUTIONS.index(distribution) if isinstance(distribution, str) else int(distribution)
     if n <= 0:
         raise ValueError("generate: n must be positive")
-    out = np.empty((n, 2), np.float64)
-    if L.chgpu_generate(d, n, seed, _p(out)):
+    count = n - begin if count is None else count
+    if begin < 0 or count < 0 or begin + count > n:
+        raise ValueError("generate: slice outside the set")
+    if out is None:
+        out = np.empty((count, 2), np.float64)
+    elif out.shape != (count, 2) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("generate: out must be a contiguous (count, 2) float64 array")
+    if count and L.chgpu_generate_range(d, n, seed, begin, count, _p(out)):
         raise ValueError("generate: unknown distribution")
     return out

@@ -17,6 +17,7 @@
 
 #include "chainhull/api.hpp"
 #include "chgpu.h"
+#include "chainhull_capi.h"
 
 namespace chainhull {
 
@@ -308,3 +309,40 @@ Distribution parse_distribution(const std::string& name) {
 }
 
 }  // namespace chainhull
+
+// ---------------------------------------------------------------- C entry (include/chainhull_capi.h)
+
+extern "C" int chainhull_capi_convex_hull(const double* xy, std::size_t n, std::size_t chunk_count,
+                                          std::size_t parallelism, int degenerate_fallback,
+                                          double* hull_out, std::size_t hull_cap,
+                                          std::size_t* n_hull, std::size_t* counts) {
+  try {
+    chainhull::PipelineConfig cfg;
+    cfg.chunk_count = chunk_count;
+    cfg.parallelism = parallelism;
+    cfg.degenerate_fallback = degenerate_fallback != 0;
+    const chainhull::HullResult r = chainhull::convex_hull(
+        std::span<const chainhull::Point2>(reinterpret_cast<const chainhull::Point2*>(xy), n), cfg);
+    const std::size_t k = r.hull.vertices.size();
+    *n_hull = k;
+    if (hull_out) {
+      if (k > hull_cap) return CHGPU_TOO_LARGE;
+      std::memcpy(hull_out, r.hull.vertices.data(), k * sizeof(chainhull::Point2));
+    }
+    if (counts) {
+      counts[0] = r.stats.n_input;
+      counts[1] = r.stats.n_after_round1;
+      counts[2] = r.stats.n_after_spa;
+      counts[3] = r.stats.n_hull;
+    }
+    return CHGPU_OK;
+  } catch (const chainhull::EmptyInput&) {
+    return CHGPU_EMPTY;
+  } catch (const chainhull::DegenerateInput&) {
+    return CHGPU_DEGENERATE;
+  } catch (const std::invalid_argument&) {
+    return CHGPU_INVALID_ARG;
+  } catch (...) {
+    return CHGPU_CUDA_ERR;
+  }
+}

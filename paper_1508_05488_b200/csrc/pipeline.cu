@@ -146,6 +146,9 @@ struct chgpu_ctx {
   u32* d_ffirst = nullptr;   // per-chunk first bin
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
+  bool chains_tap = false;   // CHGPU_OPT_CHAINS_TAP
+  std::vector<Pt> tap;       // the last call's chains (tap on)
+  size_t tap_counts[4] = {0, 0, 0, 0};
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
   size_t kept_hint = 0;          // chain points of the previous call (speculative D2H size)
   // Pinned staging arena for host->device uploads of small host-built
@@ -1031,6 +1034,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   S.n_input = n;
   cudaStream_t st = ctx->st;
   TRY(begin_call(ctx));
+  ctx->tap.clear();
+  for (auto& c : ctx->tap_counts) c = 0;
   CK(cudaEventRecord(ctx->ev[0], st));
 
   // ---- K1: extremes (extremes.cpp:28-47).
@@ -1286,6 +1291,13 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       kept += kept_counts[r];
     }
     S.n_after_spa = kept + qi.frame_size;  // pipeline.cpp:96
+    if (ctx->chains_tap) {  // parity tap: the chains as the device left them
+      ctx->tap.resize(kept);
+      CK(cudaMemcpyAsync(ctx->tap.data(), ctx->d_kept, kept * sizeof(double2),
+                         cudaMemcpyDeviceToHost, st));
+      TRY(sync(ctx));
+      for (int r = 0; r < 4; ++r) ctx->tap_counts[r] = kept_counts[r];
+    }
 
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
@@ -1466,6 +1478,10 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
       if (value < CHGPU_SPA_AUTO || value > CHGPU_SPA_FILTER) break;
       ctx->spa_mode = (int)value;
       return CHGPU_OK;
+    case CHGPU_OPT_CHAINS_TAP:
+      if (value != 0 && value != 1) break;
+      ctx->chains_tap = value != 0;
+      return CHGPU_OK;
     default:
       break;
   }
@@ -1473,6 +1489,15 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
 }
 
 void* chgpu_ctx_stream(chgpu_ctx* ctx) { return ctx ? (void*)ctx->st : nullptr; }
+
+int chgpu_last_chains(chgpu_ctx* ctx, const double** chains_xy, size_t* kept_counts) {
+  if (!ctx || !ctx->chains_tap)
+    return ctx ? fail(ctx, CHGPU_INVALID_ARG, "chgpu_last_chains: CHGPU_OPT_CHAINS_TAP is off")
+               : CHGPU_INVALID_ARG;
+  *chains_xy = reinterpret_cast<const double*>(ctx->tap.data());
+  for (int r = 0; r < 4; ++r) kept_counts[r] = ctx->tap_counts[r];
+  return CHGPU_OK;
+}
 
 int chgpu_reserve(chgpu_ctx* ctx, size_t n) {
   cudaSetDevice(ctx->device);

@@ -26,6 +26,16 @@ def test_header_symbols_exported(product):
         assert hasattr(lib, s), f"{s} declared in include/chgpu.h but not exported"
 
 
+def test_capi_header_symbols_exported(product):
+    product.load_library()
+    lib = C.CDLL(os.path.join(ROOT, "paper_1508_05488_b200", "libchainhull.so"))
+    src = open(os.path.join(ROOT, "include", "chainhull_capi.h")).read()
+    syms = sorted(set(re.findall(r"\b(chainhull_capi_[a-z_0-9]+)\s*\(", src)))
+    assert syms
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/chainhull_capi.h but not exported"
+
+
 def test_no_device_fails_loudly(product):
     import torch
     if torch.cuda.is_available():

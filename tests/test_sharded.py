@@ -124,15 +124,16 @@ def test_fold_extremes_python_and_c_agree(product):
         assert np.array_equal(out.reshape(4, 2), want)
 
 
-def _gpu_worker(rank, world, port, results, mode=0):
+def _gpu_worker(rank, world, port, results, mode=0, backend="gloo"):
     import sys
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
     import paper_1508_05488_b200 as P
     from paper_1508_05488_b200.sharded import GpuShardOps, sharded_convex_hull
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
-                            world_size=world)
+    kw = {"device_id": torch.device("cuda", 0)} if backend == "nccl" else {}
+    dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world, **kw)
     ctx = P.Context(0)
     ctx.set_spa_path(mode)
     for i, (dist_name, n, seed) in enumerate(DATASETS):
@@ -161,6 +162,26 @@ def test_sharded_hull_gpu_ranks(oracle, mode):
     results = mgr.dict()
     port = _free_port()
     mp.spawn(_gpu_worker, args=(2, port, results, mode), nprocs=2, join=True)
+    for i, (dist_name, n, seed) in enumerate(DATASETS):
+        pts = oracle.generate(dist_name, n, seed)
+        want = oracle.convex_hull(pts, 1024)
+        for cc in (1, 1024):
+            got = np.frombuffer(results[(i, cc)], np.float64).reshape(-1, 2)
+            assert np.array_equal(got, want.hull), (dist_name, n, cc)
+
+
+@pytest.mark.gpu
+def test_sharded_hull_nccl_one_rank(oracle):
+    """The NCCL branch of sharded_convex_hull (device-resident exchange
+    buffers, all_gather of the chains) at world size 1 on the one GPU: the
+    hull equals the reference's."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mgr = mp.Manager()
+    results = mgr.dict()
+    port = _free_port()
+    mp.spawn(_gpu_worker, args=(1, port, results, 0, "nccl"), nprocs=1, join=True)
     for i, (dist_name, n, seed) in enumerate(DATASETS):
         pts = oracle.generate(dist_name, n, seed)
         want = oracle.convex_hull(pts, 1024)
