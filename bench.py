@@ -76,16 +76,18 @@ def peaks():
 
 def workload(args, world):
     """The config dict both arms print (identical by construction)."""
-    n = args.n if args.n else (N_SHARDED if world > 1 else N_SINGLE)
-    shards = world if world > 1 else 1
-    name = ("BASELINE configs[4]" if world > 1 and n == N_SHARDED and args.dist == "uniform_square"
-            else "BASELINE configs[1]" if world == 1 and n == N_SINGLE and args.dist == "uniform_square"
-            else "custom")
+    sharded = world > 1 or args.sharded
+    n = args.n if args.n else (N_SHARDED if sharded else N_SINGLE)
+    shards = world
+    name = ("BASELINE configs[4]" if sharded and n == N_SHARDED and args.dist == "uniform_square"
+            else "BASELINE configs[1]" if not sharded and n == N_SINGLE
+            and args.dist == "uniform_square" else "custom")
     return {"workload": f"{n} {args.dist} points, seed {args.seed}"
-                        + (f", {shards} contiguous shards" if shards > 1 else ""),
+                        + (f", {shards} contiguous shard{'s' if shards > 1 else ''}"
+                           if sharded else ""),
             "baseline_config": name, "n_points": n, "distribution": args.dist, "seed": args.seed,
             "chunk_count": args.chunk_count, "shards": shards,
-            "parallelism": f"shard{shards}" if shards > 1 else "single",
+            "parallelism": f"shard{shards}" if sharded else "single",
             "l2": (f"input {16 * n // shards // 1_000_000} MB per GPU > 126 MB L2 (no flush needed)"
                    if 16 * n // shards > 126_000_000 else "input fits in L2 (not flushed)")}
 
@@ -268,7 +270,7 @@ def run_reference(args, rank, world):
     # a bounded sample of configs[4]: its first REF_SAMPLE_SHARDED points
     # (uniform_square draws two values per point in order, so the prefix of
     # the 1B set is generate(m)); configs[1] runs whole
-    m = min(n, REF_SAMPLE_SHARDED) if world > 1 else n
+    m = min(n, REF_SAMPLE_SHARDED) if (world > 1 or args.sharded) else n
     pts = lib.generate(args.dist, m, args.seed)
     for _ in range(args.warmup):
         ref_step(lib, kind, pts, args.chunk_count, 0)
@@ -285,8 +287,8 @@ def run_reference(args, rank, world):
               f"mallopt(M_MMAP_THRESHOLD, 256 MB) {'applied' if mall else 'unavailable'}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (the reference's generate())", "impl": "reference",
+            "scaling": "strong" if (world > 1 or args.sharded) else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (the reference's generate())", "impl": "reference",
             "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores if kind == "reference" else 1,
                              "kind": kind, "cpu_model": cpu_model(), "nproc": cores,
@@ -321,6 +323,8 @@ def main():
     ap.add_argument("--chunk-count", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pageable", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the N > 1 code path (NCCL exchanges, rank-0 merge) even at one rank")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="exchange backend for N > 1 (gloo: several ranks on one GPU, testing)")
     args = ap.parse_args()
@@ -329,6 +333,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    sharded = world > 1 or args.sharded
+    if sharded and "MASTER_ADDR" not in os.environ:  # --sharded without torchrun
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29500 + os.getpid() % 2000),
+                          RANK="0", WORLD_SIZE="1")
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -343,7 +351,7 @@ def main():
     n_total = cfg["n_points"]
     local = local % max(1, torch.cuda.device_count())  # gloo testing: ranks may share a GPU
     torch.cuda.set_device(local)
-    if world > 1:
+    if sharded:
         if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -362,15 +370,15 @@ def main():
     ctx.reserve(n)
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
-    ops = GpuShardOps(ctx, d_pts, begin) if world > 1 else None
+    ops = GpuShardOps(ctx, d_pts, begin) if sharded else None
 
     def step_device():
-        if world == 1:
+        if not sharded:
             return ctx.convex_hull_device(d_pts.data_ptr(), n, pcfg, copy=False)
         return sharded_convex_hull(ops, args.chunk_count)
 
     def step_host():
-        if world == 1:
+        if not sharded:
             return ctx.convex_hull(h_pin.numpy(), pcfg, copy=False)
         # host-resident shard: copy it in on the library stream, then the
         # sharded step
@@ -379,7 +387,7 @@ def main():
         return sharded_convex_hull(ops, args.chunk_count)
 
     def timed(fn, steps):
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -392,7 +400,7 @@ def main():
         e1.synchronize()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        if world > 1:
+        if sharded:
             t = torch.tensor([ms], dtype=torch.float64,
                              device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -404,7 +412,7 @@ def main():
     with ClockSampler(local) as clk:
         ms, res = timed(step_device, args.steps)
         # parity of the measured configuration, outside the timed region
-        if world == 1:
+        if not sharded:
             r = res
             counts = [r.stats.n_input, r.stats.n_after_round1, r.stats.n_after_spa, r.stats.n_hull]
             parity = check_parity(r.hull.vertices, counts, n_total, args.dist, args.seed,
@@ -421,11 +429,11 @@ def main():
     e2e_value = n_total / (ms_e2e * 1e-3) / 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, bit-identical)", "config": cfg,
             "clocks": clocks}
 
-    if rank == 0 and world == 1:
+    if rank == 0 and not sharded:
         r = res
         d = r.diag
         line["parity"] = parity
@@ -547,7 +555,7 @@ def main():
         line["hull_vertices"] = int(len(res)) if res is not None else None
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
