@@ -5,6 +5,8 @@
 #                                          + host finisher + generator
 #   paper_1508_05488_b200/libchainhull.so  the reference's C++ API
 #                                          (include/chainhull/*.hpp) over libchgpu
+#   build/chainhull                        the reference CLI (hull/gen/verify/bench)
+#                                          over libchainhull
 #   build/acceptance_b200                  the reference acceptance gate relinked
 #                                          against libchainhull (only when
 #                                          /root/reference is present)
@@ -25,7 +27,7 @@ CXXFLAGS := -O3 -std=gnu++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$
             -I/usr/local/cuda/include
 REF      ?= /root/reference/proj
 
-CU_SRCS  := $(CSRC)/k_discard.cu $(CSRC)/k_sort.cu $(CSRC)/k_bucket.cu $(CSRC)/k_spa.cu \
+CU_SRCS  := $(CSRC)/k_discard.cu $(CSRC)/k_sort.cu $(CSRC)/k_spa.cu \
             $(CSRC)/k_filter.cu $(CSRC)/k_convex.cu \
             $(CSRC)/pipeline.cu
 CXX_SRCS := $(CSRC)/finisher.cpp $(CSRC)/datasets.cpp
@@ -37,7 +39,7 @@ API_SRCS := $(wildcard $(PKG)/cpp/*.cpp)
 API_OBJS := $(patsubst $(PKG)/cpp/%.cpp,$(BUILD)/api_%.o,$(API_SRCS))
 API_HDRS := $(wildcard include/chainhull/*.hpp)
 
-all: $(PKG)/libchgpu.so $(PKG)/libchainhull.so acceptance $(BUILD)/io_probe_b200
+all: $(PKG)/libchgpu.so $(PKG)/libchainhull.so acceptance $(BUILD)/io_probe_b200 $(BUILD)/chainhull
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -70,6 +72,11 @@ endif
 # I/O parity probe against the drop-in (tests/test_io_parity.py).
 $(BUILD)/io_probe_b200: tests/io_probe.cpp $(PKG)/libchainhull.so $(API_HDRS)
 	$(CXX) -O2 -std=gnu++20 -ffp-contract=off -Iinclude -o $@ $< \
+	  -L$(PKG) -lchainhull -lchgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)' -lpthread
+
+# The reference command line (tools/src/main.cpp) over the drop-in.
+$(BUILD)/chainhull: $(PKG)/tools/chainhull_cli.cpp $(PKG)/libchainhull.so $(API_HDRS)
+	$(CXX) -O2 -std=gnu++20 -Wall -Wextra -Iinclude -o $@ $< \
 	  -L$(PKG) -lchainhull -lchgpu -Wl,-rpath,'$$ORIGIN/../$(PKG)' -lpthread
 
 sass: $(PKG)/libchgpu.so

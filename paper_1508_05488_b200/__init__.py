@@ -501,11 +501,20 @@ def melkman(polygon) -> np.ndarray:
     return out[:k.value]
 
 
+def _kept_counts(kept_counts, n_chain_points):
+    """The four chain lengths as a C array, checked against the chains."""
+    kc = [int(c) for c in kept_counts]
+    if len(kc) != 4 or any(c < 0 for c in kc) or sum(kc) != n_chain_points:
+        raise ValueError(f"kept_counts must be 4 non-negative counts summing to the "
+                         f"{n_chain_points} chain points, got {list(kept_counts)}")
+    return (C.c_size_t * 4)(*kc)
+
+
 def assemble_polygon(chains, kept_counts, quad) -> np.ndarray:
     """polygon.hpp:25: chains = the 4 kept chains concatenated."""
     L = load_library()
     a = _pts(chains)
-    kc = (C.c_size_t * 4)(*[int(c) for c in kept_counts])
+    kc = _kept_counts(kept_counts, len(a))
     q = np.ascontiguousarray(np.asarray(quad, np.float64).reshape(8))
     out = np.empty((len(a) + 4, 2), np.float64)
     k = C.c_size_t()
@@ -520,7 +529,7 @@ def finish_chains(chains, kept_counts, quad) -> np.ndarray:
     streaming pass (the hull path's finisher)."""
     L = load_library()
     a = _pts(chains)
-    kc = (C.c_size_t * 4)(*[int(c) for c in kept_counts])
+    kc = _kept_counts(kept_counts, len(a))
     q = np.ascontiguousarray(np.asarray(quad, np.float64).reshape(8))
     out = np.empty((len(a) + 4, 2), np.float64)
     k = C.c_size_t()

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -580,9 +581,32 @@ struct SpecRun {
   }
 };
 
-// A worker thread for segment B, C or D. After a job it polls for the next one
-// for a while (calls come back to back in a serving loop, and a condition
-// variable wake-up costs tens of microseconds), then parks.
+// One pause of a spin loop (x86 PAUSE, aarch64 YIELD).
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#elif defined(__aarch64__) || defined(__arm__)
+  asm volatile("yield" ::: "memory");
+#endif
+}
+
+using Clock = std::chrono::steady_clock;
+
+// How long a worker spins for a job before it parks: after a job, and after
+// finisher_prewake() (a call on its way to the finisher). A wake-up from the
+// parked state costs tens of microseconds; a spin costs a core.
+Clock::duration spin_budget() {
+  static const Clock::duration d = [] {
+    const char* e = std::getenv("CHGPU_FINISH_SPIN_US");  // tuning knob
+    return std::chrono::duration_cast<Clock::duration>(
+        std::chrono::microseconds(e ? std::strtol(e, nullptr, 10) : 1000));
+  }();
+  return d;
+}
+
+// A worker thread for segment B, C or D: parked on a condition variable
+// while idle; spins (bounded by a steady_clock deadline) only after a job
+// or a pre-wake, so an idle library burns no host cores.
 struct Worker {
   std::thread th;
   std::mutex m;
@@ -590,24 +614,41 @@ struct Worker {
   std::function<void()> job;
   std::atomic<int> state{0};  // 0 idle, 1 job ready, 2 job done
   std::atomic<bool> parked{false};
+  std::atomic<long long> spin_until{0};  // steady_clock ticks: spin (not park) until then
   void start() {
     th = std::thread([this] {
       for (;;) {
-        // poll ~2 ms, then park until the next submit
-        for (int i = 0; i < 20000 && state.load(std::memory_order_acquire) != 1; ++i)
-          for (int k = 0; k < 16; ++k) __builtin_ia32_pause();
-        if (state.load(std::memory_order_acquire) != 1) {
-          std::unique_lock<std::mutex> lk(m);
-          parked.store(true);
-          cv.wait(lk, [this] { return state.load(std::memory_order_acquire) == 1; });
-          parked.store(false);
+        for (unsigned i = 0; state.load(std::memory_order_acquire) != 1; ++i) {
+          if ((i & 63) == 0 &&
+              Clock::now().time_since_epoch().count() >= spin_until.load(std::memory_order_relaxed)) {
+            std::unique_lock<std::mutex> lk(m);
+            parked.store(true);
+            cv.wait(lk, [this] {
+              return state.load(std::memory_order_acquire) == 1 ||
+                     Clock::now().time_since_epoch().count() <
+                         spin_until.load(std::memory_order_relaxed);
+            });
+            parked.store(false);
+            continue;
+          }
+          cpu_relax();
         }
         job();
+        spin_until.store((Clock::now() + spin_budget()).time_since_epoch().count(),
+                         std::memory_order_relaxed);
         state.store(2, std::memory_order_release);
       }
     });
   }
   // (never destroyed: see WorkerPool)
+  void wake() {  // spin from now on for a while: a job is on its way
+    spin_until.store((Clock::now() + spin_budget()).time_since_epoch().count(),
+                     std::memory_order_relaxed);
+    if (parked.load()) {
+      std::lock_guard<std::mutex> lk(m);
+      cv.notify_all();
+    }
+  }
   void submit(std::function<void()> j) {
     job = std::move(j);
     {
@@ -617,34 +658,39 @@ struct Worker {
     if (parked.load()) cv.notify_all();
   }
   void wait() {
-    while (state.load(std::memory_order_acquire) != 2) __builtin_ia32_pause();
+    while (state.load(std::memory_order_acquire) != 2) cpu_relax();
     state.store(0, std::memory_order_relaxed);
   }
 };
 
 // The process's three workers. Created on first use and never destroyed (the
 // threads end with the process); a forked child (whose copy has no threads)
-// makes its own.
+// makes its own. If the threads cannot be started, the failure is
+// remembered for this process and every call takes the sequential pass.
 struct WorkerPool {
   Worker b, c, d;
   pid_t pid = getpid();
 };
 WorkerPool* worker_pool() {  // nullptr if threads cannot be made here
+  static std::mutex mu;
   static WorkerPool* pool = nullptr;
-  if (!pool || pool->pid != getpid()) {
-    // (a pool whose threads could not all start is kept alive, unused: its
-    // running threads still reference it)
-    WorkerPool* p = new (std::nothrow) WorkerPool;
-    try {
-      if (p) {
-        p->b.start();
-        p->c.start();
-        p->d.start();
-      }
-      pool = p;
-    } catch (...) {
-      pool = nullptr;
-    }
+  static pid_t failed_pid = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  const pid_t me = getpid();
+  if (pool && pool->pid == me) return pool;
+  if (failed_pid == me) return nullptr;
+  // (a pool whose threads could not all start is kept alive, unused: its
+  // running threads still reference it)
+  WorkerPool* p = new (std::nothrow) WorkerPool;
+  try {
+    if (!p) throw std::bad_alloc();
+    p->b.start();
+    p->c.start();
+    p->d.start();
+    pool = p;
+  } catch (...) {
+    failed_pid = me;
+    pool = nullptr;
   }
   return pool;
 }
@@ -660,6 +706,15 @@ size_t split_min() {
 }
 
 }  // namespace
+
+void finisher_prewake(size_t expected_chain_points) {
+  if (expected_chain_points < 4 * split_min()) return;
+  if (WorkerPool* pool = worker_pool()) {
+    pool->b.wake();
+    pool->c.wake();
+    pool->d.wake();
+  }
+}
 
 int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
                         std::vector<Pt>& hull) {

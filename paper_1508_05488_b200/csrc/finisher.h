@@ -27,6 +27,9 @@ int finish_chains(const Pt* chains, const size_t kept_counts[4], const Pt corner
 // finish_chains with the four chains run concurrently and verified; same result.
 int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt corners[4],
                         std::vector<Pt>& hull);
+// A call expecting about this many chain points is on its way to
+// finish_chains_split: let the worker threads spin instead of parking.
+void finisher_prewake(size_t expected_chain_points);
 int monotone_chain(const Pt* sorted_unique, size_t n, std::vector<Pt>& hull);
 int sorted_hull(const Pt* pts, size_t n, std::vector<Pt>& hull);
 void insert_sorted_unique(std::vector<Pt>& sorted, const Pt& p);

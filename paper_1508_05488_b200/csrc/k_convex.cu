@@ -160,7 +160,7 @@ __global__ __launch_bounds__(256) void k_convex_emit(const double2* __restrict__
   }
 }
 
-int convex_blocks() { return 148 * 4; }
+int convex_blocks() { return device_limits().sms * 4; }
 
 void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInfo* qinfo, u32* ok,
                          u64* block_best, cudaStream_t st) {

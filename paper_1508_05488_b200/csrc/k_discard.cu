@@ -570,15 +570,13 @@ __global__ void k_classify_labels(const double2* __restrict__ pts, u64 n,
 int extremes_blocks(int requested) {
   // One resident wave at most: a grid-stride kernel gains nothing from a
   // second partial wave, it only adds a tail.
-  static int wave = 0;
-  if (!wave) {
-    int occ = 0, sms = 0, dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_extremes_partial<true>, kK1Threads, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    wave = std::max(1, occ) * std::max(1, sms);
-  }
-  return std::max(1, std::min(requested, wave));
+  return std::max(1, std::min(requested, device_limits().k1_wave));
+}
+
+int extremes_wave(int sms) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_extremes_partial<true>, kK1Threads, 0);
+  return std::max(1, occ) * std::max(1, sms);
 }
 
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,

@@ -936,7 +936,7 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 // region empty and the path idle.
 // ------------------------------------------------------------------ launchers
 
-void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
+cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
@@ -946,8 +946,12 @@ void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int lo
                   (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar,
                   (void*)&overflow};
   // cooperative: the launch fails rather than run with a CTA not resident
-  cudaLaunchCooperativeKernel((const void*)k_bin_scan, grid, block, args, 0, st);
+  // (the caller checked bin_scan_blocks against the device's residency and
+  // checks the launch status)
+  return cudaLaunchCooperativeKernel((const void*)k_bin_scan, grid, block, args, 0, st);
 }
+
+u32 bin_scan_blocks(int log2nb) { return 4 * std::max(1u, (1u << log2nb) / kBinTile); }
 
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
@@ -956,11 +960,7 @@ void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nse
                    cudaStream_t st) {
   if (nseg == 0) return;
   // one resident wave: the warp-stride loop then has no partial last wave
-  static int resident = 0;
-  if (resident == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_filter, kFilterThreads, 0);
-    resident = std::max(resident, 1) * 148 * CHGPU_FILTER_WAVES;
-  }
+  const int resident = device_limits().filter_resident;
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
                                    (u32)resident);
   k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segidx, segcnt, nseg, pts, P, qinfo, bstart, bthr,
@@ -969,14 +969,9 @@ void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nse
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_bin_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(BigSmem));
-    configured = true;
-  }
-  k_bin_sort_warp<<<148 * 4, 32 * kWarpSortWarps, 0, st>>>(k, v, P, bstart, bcur, big, nbig);
-  k_bin_sort_big<<<148 * 2, kBigThreads, sizeof(BigSmem), st>>>(k, v, P, bstart, bcur,
+  const int sms = device_limits().sms;
+  k_bin_sort_warp<<<sms * 4, 32 * kWarpSortWarps, 0, st>>>(k, v, P, bstart, bcur, big, nbig);
+  k_bin_sort_big<<<sms * 2, kBigThreads, sizeof(BigSmem), st>>>(k, v, P, bstart, bcur,
                                                                 big + kBigListB, nbig + 1, overflow);
 }
 
@@ -992,5 +987,22 @@ void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* b
   k_spa_emit<<<blocks, 256, 0, st>>>(P, sk, sv, chunk_kept, group_kept, out);
 }
 
+
+// Dynamic shared memory opt-in and residency of the filter kernels for the
+// current device (device_limits()).
+cudaError_t configure_filter_kernels(DeviceLimits* lim) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_bin_sort_big,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem));
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter, kFilterThreads, 0)) != cudaSuccess)
+    return e;
+  lim->filter_resident = std::max(occ, 1) * lim->sms * CHGPU_FILTER_WAVES;
+  occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bin_scan, kBinThreads, 0)) != cudaSuccess)
+    return e;
+  lim->binscan_coop = occ * lim->sms;
+  return cudaSuccess;
+}
 
 }  // namespace chgpu

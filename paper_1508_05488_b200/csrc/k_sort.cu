@@ -566,12 +566,6 @@ static void onesweep_launch(const u64* kin, const u64* vin, u64* kout, u64* vout
                             const SegDesc* segs, int nseg, u32 total_tiles, int use_src,
                             const u32* digit_excl, int pass, u64* status, u32 tag, u32* tile_ctr,
                             u32* rows, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_onesweep<kMode, kScan>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(OnesweepSmem));
-    configured = true;
-  }
   k_onesweep<kMode, kScan><<<total_tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
       kin, vin, kout, vout, segs, nseg, use_src, digit_excl, pass, status, tag, tile_ctr,
       total_tiles, rows);
@@ -705,12 +699,6 @@ void launch_seg_copy(const u64* kin, const u64* vin, u64* kout, u64* vout, const
 void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_tiles, int eqmode,
                        void* medium, u32* nmedium, unsigned long long* ngroups, cudaStream_t st) {
   if (total_tiles == 0) return;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_group_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(GroupSmem));
-    configured = true;
-  }
   k_group_scan<<<total_tiles, 256, sizeof(GroupSmem), st>>>(k, v, segs, nseg, eqmode,
                                                            (GroupRun*)medium, nmedium,
                                             ngroups);
@@ -723,5 +711,20 @@ void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* me
 }
 
 size_t group_run_bytes() { return sizeof(GroupRun); }
+
+// Dynamic shared memory opt-ins of the sort kernels (per device: called by
+// device_limits() once for each device).
+cudaError_t configure_sort_kernels() {
+  const int os = (int)sizeof(OnesweepSmem);
+  const void* fns[] = {(const void*)k_onesweep<kDigitQ, false>, (const void*)k_onesweep<kDigitV, false>,
+                       (const void*)k_onesweep<kDigitK, false>, (const void*)k_onesweep<kDigitQ, true>,
+                       (const void*)k_onesweep<kDigitV, true>, (const void*)k_onesweep<kDigitK, true>};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, os);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaFuncSetAttribute((const void*)k_group_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(GroupSmem));
+}
 
 }  // namespace chgpu

@@ -8,23 +8,6 @@
 
 namespace chgpu {
 
-// Bucket sort (k_bucket.cu).
-constexpr int kLocalBits = 10;     // low bits of q sorted inside a bucket
-constexpr u32 kBucketCap = 2048;   // largest bucket sorted in shared memory (< 65536)
-constexpr int kMaxBucketBits = 13;
-
-struct BucketPlan {
-  int nseg;
-  int bbits;            // buckets per segment = 2^bbits
-  u64 src_off[4];       // segment start in the source layout (K2 streams)
-  u64 dst_off[4];       // segment start in the sorted layout
-  u64 cum[5];           // prefix of segment lengths
-  int region[4];
-  double qlo[4], qscale[4];
-  double qmax;          // 2^(bbits + kLocalBits) - 1
-  u32 tile_begin[5];    // scatter tiles per segment
-};
-
 struct SpaPlan {
   u64 off[4];         // region offset in the sorted array
   u64 m[4];           // region size
@@ -50,9 +33,11 @@ struct FilterAux {
   u64* agg_val;
 };
 // The plan of the filter path on the device (from K2's counts).
-void launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
+cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
                      u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st);
+// CTAs of the cooperative k_bin_scan launch for log2nb bins per region.
+u32 bin_scan_blocks(int log2nb);
 void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
                        const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
                        u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
@@ -71,9 +56,27 @@ void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInf
 void launch_convex_emit(const double2* chains, const u64 kept[4], const QuadInfo* qinfo,
                         const u64* block_best, double2* out, cudaStream_t st);
 
+// Per-device launch limits. device_limits() configures the kernels'
+// attributes (dynamic shared memory opt-ins are per device) and measures
+// residency once per device, thread-safely; chgpu_ctx_create calls it after
+// cudaSetDevice so a failure surfaces there. Launchers read it for the
+// current device.
+struct DeviceLimits {
+  cudaError_t status = cudaSuccess;
+  int sms = 0;              // multiprocessors
+  int k1_wave = 0;          // K1 CTAs in one resident wave
+  int filter_resident = 0;  // k_filter CTAs in one resident wave
+  int binscan_coop = 0;     // k_bin_scan CTAs that can be co-resident (cooperative launch bound)
+};
+const DeviceLimits& device_limits();
+cudaError_t configure_sort_kernels();
+cudaError_t configure_filter_kernels(DeviceLimits* lim);
+
 // K1
 // Blocks launch_extremes_partial will use for a request of `requested`.
 int extremes_blocks(int requested);
+// K1 CTAs in one resident wave on a device with `sms` multiprocessors.
+int extremes_wave(int sms);
 // With a ticket counter (zeroed) and the call's total partial count, the
 // last block merges every partial into *out: no launch_extremes_final.
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
@@ -113,14 +116,6 @@ void launch_group_scan(u64* k, u64* v, const SegDesc* segs, int nseg, u32 total_
 void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* medium,
                              const u32* nmedium, void* longr, u32* nlong, cudaStream_t st);
 size_t group_run_bytes();
-void launch_bucket_hist(const u64* kbuf, const BucketPlan& P, u32* hist, cudaStream_t st);
-void launch_bucket_scan(const u32* hist, const BucketPlan& P, u64* base, u32* cursor, u32* big,
-                        u32* nbig, cudaStream_t st);
-u32 bucket_scatter_tiles(BucketPlan& P);
-void launch_bucket_scatter(const u64* kin, const u64* vin, u64* kout, u64* vout, const BucketPlan& P,
-                           u32 tiles, u32* cursor, cudaStream_t st);
-void launch_bucket_sort(u64* k, u64* v, const BucketPlan& P, const u64* base, const u32* hist,
-                        unsigned long long* ngroups, cudaStream_t st);
 // K4/K5
 void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
                      double2* scratch, u32* chunk_kept, u32* offs,

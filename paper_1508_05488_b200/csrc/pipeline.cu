@@ -2,7 +2,7 @@
 //
 // Mirrors convex_hull (reference pipeline.cpp:25-106) stage for stage:
 //   K1 extremes -> frame -> K2 classify+discard -> [degenerate branch]
-//   -> K3 region sort (bucket passes + group fix-up) -> K4/K5 SPA + chain
+//   -> K3 region sort (quantised LSD passes + group fix-up) -> K4/K5 SPA + chain
 //   compaction -> D2H chains -> host assemble + Melkman (finisher.cpp).
 // Host syncs happen only where the host must size the next launch: after
 // K2 (region counts), after the histogram (which digit passes move data),
@@ -16,11 +16,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -124,10 +126,6 @@ struct chgpu_ctx {
   unsigned long long* d_u64 = nullptr;  // [0..3] kept counts, [4] unique total, [5..9] label counts
   u32* d_hist = nullptr;
   u32* d_digit_excl = nullptr;
-  u32* d_bhist = nullptr;   // bucket counts   [4 << kMaxBucketBits]
-  u64* d_bbase = nullptr;   // bucket bases    [4 << kMaxBucketBits]
-  u32* d_bcur = nullptr;    // scatter cursors [4 << kMaxBucketBits]
-  u32* d_big = nullptr;     // oversized buckets
   SegDesc* d_segs = nullptr;
   size_t seg_cap = 0;
   // SPA pre-filter tables (k_filter.cu), nbt = 4 << log2nb bins per call:
@@ -473,17 +471,14 @@ struct Run {
 
 // Groups left for the host to resolve after the in-place fix-up.
 struct PendingLong {
-  int slot = -1;      // device counter of pending items (groups or buckets)
+  int slot = -1;      // device counter of pending groups
   int eqmode = 0;
   int depth = 0;
-  bool buckets = false;  // items are oversized buckets of a bucket sort
-  int bbits = 0;
   std::vector<int> regions;
   u64 *kF = nullptr, *vF = nullptr, *kS = nullptr, *vS = nullptr;
 };
 
 int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long);
-int resolve_big_buckets(chgpu_ctx* ctx, const PendingLong& p, bool* had);
 
 // Orders every group of the sorted layout (segments in ctx->h_segs, at
 // dst_off of (kF, vF)) by (canon k, v), in place. eqmode kEqQ: groups of
@@ -524,7 +519,6 @@ int fix_groups(chgpu_ctx* ctx, int nseg, u64* kF, u64* vF, u64* kS, u64* vS, int
 int resolve_long(chgpu_ctx* ctx, const PendingLong& p, bool* had_long) {
   *had_long = false;
   if (p.slot < 0) return CHGPU_OK;
-  if (p.buckets) return resolve_big_buckets(ctx, p, had_long);
   u32 nlong = 0;
   TRY(read_ctr(ctx, p.slot, &nlong));
   if (nlong == 0) return CHGPU_OK;
@@ -597,136 +591,15 @@ int sort_segments(chgpu_ctx* ctx, int nseg, int qbits, bool timed, bool defer_lo
   return CHGPU_OK;
 }
 
-// Bucket sort of nseg (<= 4) segments of the K2 two-ended layout (src_off
-// into kbuf/vbuf) into contiguous region order in (ka, va): see k_bucket.cu.
-// lo/hi bound each segment's primary coordinate (the quantizer range).
-// Buckets too large for shared memory are left in *pend (resolved now
-// unless `defer`).
-int bucket_sort(chgpu_ctx* ctx, int nseg, const u64* src_off, const u64* m, const int* region,
-                const double* lo, const double* hi, bool timed, bool defer, Sorted* out) {
-  BucketPlan P{};
-  P.nseg = nseg;
-  u64 mmax = 0, total = 0;
-  for (int s = 0; s < nseg; ++s) mmax = std::max(mmax, m[s]);
-  int bb = 1;
-  while (bb < kMaxBucketBits && (mmax >> bb) > 1024) ++bb;
-  P.bbits = bb;
-  P.qmax = std::ldexp(1.0, bb + kLocalBits) - 1.0;
-  for (int s = 0; s < nseg; ++s) {
-    P.src_off[s] = src_off[s];
-    P.dst_off[s] = total;
-    P.cum[s] = total;
-    P.region[s] = region[s];
-    P.qlo[s] = lo[s];
-    const double span = hi[s] - lo[s];
-    double scale = span > 0.0 ? P.qmax / span : 0.0;
-    if (!std::isfinite(scale)) scale = 0.0;
-    P.qscale[s] = scale;
-    total += m[s];
-  }
-  P.cum[nseg] = total;
-  out->kF = ctx->d_ka;
-  out->vF = ctx->d_va;
-  out->kS = ctx->d_kbuf;
-  out->vS = ctx->d_vbuf;
-  out->passes = 0;
-  out->pend = PendingLong{};
-  if (total == 0) return CHGPU_OK;
-  const int nbig_slot = take_ctr(ctx);
-  cudaStream_t st = ctx->st;
-  CK(cudaMemsetAsync(ctx->d_bhist, 0, (sizeof(u32) * nseg) << bb, st));
-  launch_bucket_hist(ctx->d_kbuf, P, ctx->d_bhist, st);
-  launch_bucket_scan(ctx->d_bhist, P, ctx->d_bbase, ctx->d_bcur, ctx->d_big, ctx->d_ctr + nbig_slot,
-                     st);
-  if (timed) CK(cudaEventRecord(ctx->ev[3], st));
-  const u32 tiles = bucket_scatter_tiles(P);
-  if (timed) CK(cudaEventRecord(ctx->ev[4], st));
-  launch_bucket_scatter(ctx->d_kbuf, ctx->d_vbuf, ctx->d_ka, ctx->d_va, P, tiles, ctx->d_bcur, st);
-  if (timed) CK(cudaEventRecord(ctx->ev[5], st));
-  launch_bucket_sort(ctx->d_ka, ctx->d_va, P, ctx->d_bbase, ctx->d_bhist, ctx->d_u64 + 10, st);
-  ctx->launches += 4;
-  CK(cudaGetLastError());
-  out->passes = 1;
-  PendingLong& p = out->pend;
-  p.slot = nbig_slot;
-  p.buckets = true;
-  p.bbits = bb;
-  p.regions.assign(region, region + nseg);
-  p.kF = out->kF;
-  p.vF = out->vF;
-  p.kS = out->kS;
-  p.vS = out->vS;
-  if (defer) return CHGPU_OK;
-  bool had = false;
-  return resolve_long(ctx, p, &had);
-}
-
-// Oversized buckets: each is sorted completely with the onesweep engine on
-// k, then its ==-primary runs are ordered by v (fix_groups).
-int resolve_big_buckets(chgpu_ctx* ctx, const PendingLong& p, bool* had) {
-  *had = false;
-  u32 nbig = 0;
-  TRY(read_ctr(ctx, p.slot, &nbig));
-  if (nbig == 0) return CHGPU_OK;
-  *had = true;
-  const size_t nb = size_t(1) << p.bbits;
-  const size_t nall = nb * p.regions.size();
-  std::vector<u32> ids(nbig), cnt(nall);
-  std::vector<u64> base(nall);
-  CK(cudaMemcpyAsync(ids.data(), ctx->d_big, nbig * sizeof(u32), cudaMemcpyDeviceToHost, ctx->st));
-  CK(cudaMemcpyAsync(cnt.data(), ctx->d_bhist, nall * sizeof(u32), cudaMemcpyDeviceToHost, ctx->st));
-  CK(cudaMemcpyAsync(base.data(), ctx->d_bbase, nall * sizeof(u64), cudaMemcpyDeviceToHost, ctx->st));
-  TRY(sync(ctx));
-  std::sort(ids.begin(), ids.end());
-  TRY(ensure_segs(ctx, nbig));
-  auto load = [&]() {
-    for (u32 i = 0; i < nbig; ++i)
-      ctx->h_segs[i] = make_seg(base[ids[i]], base[ids[i]], cnt[ids[i]], p.regions[ids[i] / nb]);
-  };
-  load();
-  bool in_a = true;
-  int passes = 0;
-  TRY(radix_sort(ctx, (int)nbig, p.kF, p.vF, p.kS, p.vS, p.kF, p.vF, kDigitK, kPasses, &in_a,
-                 &passes));
-  if (passes % 2 == 1) {
-    const u32 t2 = plan_tiles(ctx->h_segs, (int)nbig);
-    launch_seg_copy(p.kS, p.vS, p.kF, p.vF, ctx->d_segs, (int)nbig, t2, 0, ctx->st);
-    ++ctx->launches;
-  }
-  CK(cudaGetLastError());
-  load();
-  PendingLong inner;
-  return fix_groups(ctx, (int)nbig, p.kF, p.vF, p.kS, p.vS, kEqPrim, &inner, false, 1);
-}
-
 int plan_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, int* qbits);
-
-// Which engine sorts the regions: the segmented onesweep passes on the
-// quantized primary (default) or the experimental bucket sort
-// (CHGPU_SORT=bucket).
-bool use_bucket_sort() {
-  static const bool b = [] {
-    const char* e = std::getenv("CHGPU_SORT");
-    return e && std::strcmp(e, "bucket") == 0;
-  }();
-  return b;
-}
 
 // The four region streams of K2 (two-ended layout), sorted into region
 // order LL | LR | UR | UL.
 int sort_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, bool timed, bool defer,
                  Sorted* out) {
-  if (!use_bucket_sort()) {
-    int qbits = 0;
-    TRY(plan_regions(ctx, m, quad, &qbits));
-    return sort_segments(ctx, 4, qbits, timed, defer, out);
-  }
-  const u64 cap = ctx->cap;
-  const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
-  const int region[4] = {1, 2, 3, 4};
-  double lo[4], hi[4];
-  for (int s = 0; s < 4; ++s) region_range(quad, s + 1, &lo[s], &hi[s]);
-  return bucket_sort(ctx, 4, src_off, m, region, lo, hi, timed, defer, out);
+  int qbits = 0;
+  TRY(plan_regions(ctx, m, quad, &qbits));
+  return sort_segments(ctx, 4, qbits, timed, defer, out);
 }
 
 // Region segments of the K2 two-ended layout, with quantizers.
@@ -773,17 +646,11 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
   double lo, hi;
   region_range(quad, 0, &lo, &hi);
   Sorted so{};
-  if (use_bucket_sort()) {
-    const u64 src_off[1] = {0}, m[1] = {s1};
-    const int region[1] = {0};
-    TRY(bucket_sort(ctx, 1, src_off, m, region, &lo, &hi, false, false, &so));
-  } else {
-    TRY(ensure_segs(ctx, 1));
-    ctx->h_segs[0] = make_seg(0, 0, s1, 0);
-    const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
-    set_quantizer(ctx->h_segs[0], lo, hi, qbits);
-    TRY(sort_segments(ctx, 1, qbits, false, false, &so));
-  }
+  TRY(ensure_segs(ctx, 1));
+  ctx->h_segs[0] = make_seg(0, 0, s1, 0);
+  const int qbits = s1 <= (u64(1) << 22) ? 24 : 32;
+  set_quantizer(ctx->h_segs[0], lo, hi, qbits);
+  TRY(sort_segments(ctx, 1, qbits, false, false, &so));
   *passes = so.passes;
   *groups = 0;
   const int slot = take_ctr(ctx);
@@ -884,10 +751,9 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
   *ovf_slot = take_ctr(ctx);
   // plan + bin starts + thresholds: one cooperative launch
-  launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
-                  ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), first_bin, aux,
-                  ctx->d_ctr + take_ctr(ctx),
-                  ctx->d_ctr + *ovf_slot, st);
+  CK(launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
+                     ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), first_bin, aux,
+                     ctx->d_ctr + take_ctr(ctx), ctx->d_ctr + *ovf_slot, st));
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
   // half of vbuf, each segment's survivor count in its lower part
@@ -1037,6 +903,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   ctx->tap.clear();
   for (auto& c : ctx->tap_counts) c = 0;
   CK(cudaEventRecord(ctx->ev[0], st));
+  // a call like the last one will reach the split finisher in a few hundred
+  // microseconds: its worker threads spin instead of parking
+  chgpu::host::finisher_prewake(ctx->kept_hint);
 
   // ---- K1: extremes (extremes.cpp:28-47).
   int nparts = 0;
@@ -1118,11 +987,16 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
   // pre-filter's per-bin statistics when that path is taken.
-  const bool want_filter =
+  bool want_filter =
       chunk_count >= 1 &&
       (ctx->spa_mode == CHGPU_SPA_FILTER ||
        (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
-  const int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
+  int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
+  // the bin scan is one cooperative launch: every CTA must be resident
+  if (want_filter && bin_scan_blocks(log2nb) > (u32)device_limits().binscan_coop) {
+    want_filter = false;
+    log2nb = 0;
+  }
   if (want_filter)
     TRY(ftab_prepare(ctx, log2nb, st));
   const FilterTabs ftabs = filter_tabs(ctx, log2nb);
@@ -1379,6 +1253,32 @@ int upload_quad(chgpu_ctx* ctx, const double* quad) {
 
 }  // namespace
 
+namespace chgpu {
+
+const DeviceLimits& device_limits() {
+  constexpr int kMaxDevices = 64;
+  static std::once_flag once[kMaxDevices];
+  static DeviceLimits lim[kMaxDevices];
+  static DeviceLimits none = [] {
+    DeviceLimits d;
+    d.status = cudaErrorInvalidDevice;
+    return d;
+  }();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return none;
+  std::call_once(once[dev], [dev] {
+    DeviceLimits& d = lim[dev];
+    cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = configure_sort_kernels();
+    if (e == cudaSuccess) e = configure_filter_kernels(&d);
+    if (e == cudaSuccess) d.k1_wave = extremes_wave(d.sms);
+    d.status = e;
+  });
+  return lim[dev];
+}
+
+}  // namespace chgpu
+
 // ====================================================================== C ABI
 
 extern "C" {
@@ -1394,6 +1294,10 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
     delete ctx;
     return CHGPU_NO_DEVICE;
   }
+  if (device_limits().status != cudaSuccess) {  // kernel attributes of this device
+    delete ctx;
+    return CHGPU_CUDA_ERR;
+  }
   auto bad = [&](cudaError_t e) {
     ctx->err = cudaGetErrorString(e);
     return e != cudaSuccess;
@@ -1405,10 +1309,6 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
       bad(cudaMalloc(&ctx->d_rawquad, sizeof(QuadCand))) ||
       bad(cudaMalloc(&ctx->d_ctr, kCtrSlots * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_u64, 16 * sizeof(unsigned long long))) ||
-      bad(cudaMalloc(&ctx->d_bhist, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
-      bad(cudaMalloc(&ctx->d_bbase, (size_t(4) << kMaxBucketBits) * sizeof(u64))) ||
-      bad(cudaMalloc(&ctx->d_bcur, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
-      bad(cudaMalloc(&ctx->d_big, (size_t(4) << kMaxBucketBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_ftab, filter_tab_bytes(kMaxFilterBits))) ||
       bad(cudaMalloc(&ctx->d_fstart, (size_t(4) << kMaxFilterBits) * sizeof(u32))) ||
       bad(cudaMalloc(&ctx->d_fthr, (size_t(4) << kMaxFilterBits) * sizeof(u64))) ||
@@ -1444,10 +1344,6 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_u64);
   cudaFree(ctx->d_segs);
   cudaFree(ctx->d_hist);
-  cudaFree(ctx->d_bhist);
-  cudaFree(ctx->d_bbase);
-  cudaFree(ctx->d_bcur);
-  cudaFree(ctx->d_big);
   cudaFree(ctx->d_ftab);
   cudaFree(ctx->d_fstart);
   cudaFree(ctx->d_fthr);
