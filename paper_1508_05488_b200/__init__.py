@@ -28,7 +28,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchgpu.so")
+# (CHGPU_LIB: an alternative in-tree build of the same library, for A/B timing)
+LIB_PATH = os.environ.get("CHGPU_LIB") or os.path.join(HERE, "libchgpu.so")
 DISTRIBUTIONS = ["uniform_square", "uniform_disk", "circle", "gaussian", "collinear",
                  "duplicates_heavy"]
 

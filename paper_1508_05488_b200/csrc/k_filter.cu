@@ -66,6 +66,15 @@ __device__ __forceinline__ SegMax shfl_up_seg(SegMax x, int o) {
 
 constexpr int kBinThreads = 256;
 constexpr int kBinPer = 8;
+// Bins per entry of the coarse threshold table (min T of the group), which
+// the filter keeps in shared memory: kCoarseBins / kBinPer bin-scan
+// threads' bins.
+#ifndef CHGPU_COARSE_LOG2
+#define CHGPU_COARSE_LOG2 5
+#endif
+constexpr int kCoarseLog2 = CHGPU_COARSE_LOG2;
+constexpr int kCoarseBins = 1 << kCoarseLog2;
+static_assert(kCoarseBins >= kBinPer && kCoarseBins <= 32 * kBinPer, "coarse group = whole threads of a warp");
 constexpr int kBinTile = kBinThreads * kBinPer;  // 2048 bins
 
 __device__ __forceinline__ u32 bin_tiles(int log2nb) { return max(1u, (1u << log2nb) / kBinTile); }
@@ -230,8 +239,9 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
     const QuadInfo* __restrict__ qinfo, u32* __restrict__ counts, u64 chunk_count,
     int log2nb, const u32* __restrict__ bcnt, const u32* __restrict__ bw,
     FilterPlan* __restrict__ plan_out, u32* __restrict__ bstart, u32* __restrict__ bthr,
-    u32* __restrict__ first_bin, u32* __restrict__ tsum, u32* __restrict__ agg_seg,
-    u64* __restrict__ agg_val, u32* __restrict__ bar, u32* __restrict__ overflow) {
+    u32* __restrict__ tcoarse, u32* __restrict__ first_bin, u32* __restrict__ tsum,
+    u32* __restrict__ agg_seg, u64* __restrict__ agg_val, u32* __restrict__ bar,
+    u32* __restrict__ overflow) {
   __shared__ FilterPlan sP;
   __shared__ u32 s_m[4];
   __shared__ u32 sh[kBinThreads / 32];
@@ -346,12 +356,12 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
     }
   }
   __syncthreads();
-  if (!in) return;
   run = seg_combine(SegMax{c_seg, c_val}, run);
   const u64 seedw = sP.seed_w[r];
   u64 th[kBinPer];
   ChunkCursor cc(s0, cs);
   u32 q = s0;
+  u32 gmin = ~0u;  // min T over this thread's bins holding records
 #pragma unroll
   for (int j = 0; j < kBinPer; ++j) {
     th[j] = 0;
@@ -361,9 +371,15 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
       if (run.seg == clo && run.val > tv) tv = run.val;
       th[j] = tv;
     }
+    if (c[j]) gmin = min(gmin, (u32)th[j]);
     run = seg_combine(run, e[j]);
     q += c[j];
   }
+  // the coarse table: min T over each group of kCoarseBins bins
+#pragma unroll
+  for (int o = 1; o < kCoarseBins / kBinPer; o <<= 1) gmin = min(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+  if (in && (threadIdx.x & (kCoarseBins / kBinPer - 1)) == 0) tcoarse[(boff + b0) >> kCoarseLog2] = gmin;
+  if (!in) return;
   uint4* const to = reinterpret_cast<uint4*>(bthr + boff + b0);
   to[0] = make_uint4((u32)th[0], (u32)th[1], (u32)th[2], (u32)th[3]);
   to[1] = make_uint4((u32)th[4], (u32)th[5], (u32)th[6], (u32)th[7]);
@@ -377,40 +393,42 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
 
 // ------------------------------------------------------------------ filter
 
-#ifndef CHGPU_FILTER_ITEMS
-#define CHGPU_FILTER_ITEMS 1
+#ifndef CHGPU_FILTER_DIST
+#define CHGPU_FILTER_DIST 1
 #endif
-#ifndef CHGPU_FILTER_WAVES
-#define CHGPU_FILTER_WAVES 1
+#ifndef CHGPU_FILTER_ABL
+#define CHGPU_FILTER_ABL 0
 #endif
-#ifndef CHGPU_FILTER_PIPE
-#define CHGPU_FILTER_PIPE 1
-#endif
-#ifndef CHGPU_FILTER_MINB
-#define CHGPU_FILTER_MINB 8
-#endif
-constexpr int kFilterThreads = 256;
-#if !CHGPU_FILTER_PIPE
-constexpr int kFilterItems = CHGPU_FILTER_ITEMS;
-#endif
+constexpr int kFilterThreads = 1024;  // one CTA per SM (the coarse table fills shared memory)
+
+// Bytes of k_filter's dynamic shared memory (the coarse threshold table).
+size_t filter_smem_bytes(int log2nb) { return ((size_t)4 << log2nb) / kCoarseBins * sizeof(u32); }
 
 // Warp-stride over K2's survivor segments (k_classify_survivors: 256
 // slots each): per survivor one 8-byte key, its global bin over w >> kWShift
 // (filter_key). A survivor with (w >> kWShift) < T_b is dropped: since the
 // shift is monotone, that implies w < the bin's lower bound of the running
-// max. A candidate fetches its point from the input (its index from K2),
-// takes the next slot of its bin and writes its sort record; the bin's 33rd
+// max. The bins' thresholds are random 4-byte lookups, so they are tested in
+// two steps: first against the min T of the bin's group of kCoarseBins bins,
+// from a copy of the coarse table in shared memory (a key below it is below
+// T_b: dropped without touching L2), and only the rest against T_b itself.
+// A candidate fetches its point from the input (its index from K2), takes
+// the next slot of its bin and writes its sort record; the bin's 33rd
 // candidate queues it for k_bin_sort_warp, its 257th for k_bin_sort_big.
-__global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
+__global__ __launch_bounds__(kFilterThreads, 1) void k_filter(
     const u64* __restrict__ seg, const u32* __restrict__ segidx, const u64* __restrict__ segcnt,
     u32 nseg, const double2* __restrict__ pts, const FilterPlan* __restrict__ P_p,
     const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
-    const u32* __restrict__ bthr, u32* __restrict__ bcur, u32* __restrict__ bmap,
-    u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big, u32* __restrict__ nbig,
-    unsigned long long* __restrict__ ncand, const u32* __restrict__ overflow) {
+    const u32* __restrict__ bthr, const u32* __restrict__ tcoarse, u32* __restrict__ bcur,
+    u32* __restrict__ bmap, u64* __restrict__ kout, u64* __restrict__ vout, u32* __restrict__ big,
+    u32* __restrict__ nbig, unsigned long long* __restrict__ ncand, const u32* __restrict__ overflow) {
+  extern __shared__ __align__(16) u32 s_tc[];  // coarse thresholds, (4 << log2nb) / kCoarseBins
   __shared__ u64 s_off[4];
   __shared__ u32 s_lg, s_nseg;
   __shared__ u32 s_cand;
+  // candidate queue, per warp (see push)
+  __shared__ u64 s_qkey[kFilterThreads / 32][64];
+  __shared__ u32 s_qat[kFilterThreads / 32][64];
   if (threadIdx.x < 4) {
     const int r = threadIdx.x;
     s_off[r] = P_p->spa.off[r];
@@ -425,87 +443,129 @@ __global__ __launch_bounds__(kFilterThreads, CHGPU_FILTER_MINB) void k_filter(
   __syncthreads();
   const u32 lg = s_lg;
   nseg = s_nseg;
-  const int lane = threadIdx.x & 31;
+  if (nseg) {
+    const u32 ntc4 = (u32)(((size_t)4 << lg) / kCoarseBins / 4);  // uint4 words
+    const uint4* src = reinterpret_cast<const uint4*>(tcoarse);
+    uint4* dst = reinterpret_cast<uint4*>(s_tc);
+    for (u32 i = threadIdx.x; i < ntc4; i += kFilterThreads) dst[i] = __ldcg(src + i);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u32 wstride = gridDim.x * (kFilterThreads / 32);
   u32 mine = 0;
-  // One candidate's work (its point, bin slot, sort record, big-bin queue).
-  auto take = [&](u64 key, u32 sg, u32 sl) {
+  // One candidate's work (its point, bin slot, sort record, big-bin queue);
+  // `at` = its survivor slot in K2's segments.
+  auto take = [&](u64 key, u32 at) {
     const u32 bi = (u32)(key >> 32);
     const u32 r = bi >> lg;
     const int reg = (int)r + 1;
-    const double2 p = __ldg(pts + segidx[(u64)sg * kSegPts + sl]);
+    const u32 bs = bstart[bi];
+    const double2 p = __ldg(pts + segidx[at]);
     const u32 pos = atomicAdd(bcur + bi, 1u);
     if (pos == 0) atomicOr(bmap + (bi >> 5), 1u << (bi & 31));  // k_spa_chunks' index
-    const u64 dst = s_off[r] + bstart[bi] + pos;
+    const u64 dst = s_off[r] + bs + pos;
     kout[dst] = k_of(reg, p.x, p.y);
     vout[dst] = v_of(reg, p.x, p.y);
     if (pos == 32) big[atomicAdd(nbig, 1u)] = bi;                       // > 32: by a warp
     if (pos == kWarpSortMax) big[kBigListB + atomicAdd(nbig + 1, 1u)] = bi;  // > 256: a CTA
+#if !(CHGPU_FILTER_ABL & 1)
     ++mine;
-  };
-#if CHGPU_FILTER_PIPE
-  // Software-pipelined over the warp's rounds of 32 survivors, across its
-  // segments: the key and the bin threshold of the next round are in flight
-  // while the current round is tested, so a warp keeps two dependent
-  // key -> threshold chains going instead of one.
-  {
-    u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5);
-    u32 tot = sg < nseg ? (u32)__ldg(segcnt + sg) : 0u;
-    u32 s0 = 0;
-    // advance (sg, s0, tot) to the next non-empty round
-    auto next_round = [&](u32& g, u32& o, u32& t) {
-      o += 32;
-      while (g < nseg && o >= t) {
-        g += wstride;
-        o = 0;
-        t = g < nseg ? (u32)__ldg(segcnt + g) : 0u;
-      }
-    };
-    if (sg < nseg && tot == 0) { s0 = 0; next_round(sg, s0, tot); s0 = 0; }
-    // (next_round skipped empty segments; s0 restarts at 0 there)
-    u32 c_sg = sg, c_s0 = 0, c_tot = tot;
-    u64 c_key = (c_sg < nseg && c_s0 + lane < c_tot) ? __ldcs(seg + (u64)c_sg * kSegPts + c_s0 + lane) : 0ull;
-    u32 c_th = (c_sg < nseg && c_s0 + lane < c_tot) ? __ldg(bthr + (c_key >> 32)) : ~0u;
-    u32 n_sg = c_sg, n_s0 = c_s0, n_tot = c_tot;
-    if (n_sg < nseg) next_round(n_sg, n_s0, n_tot);
-    u64 n_key = (n_sg < nseg && n_s0 + lane < n_tot) ? __ldcs(seg + (u64)n_sg * kSegPts + n_s0 + lane) : 0ull;
-    while (c_sg < nseg) {
-      const u32 n_th = (n_sg < nseg && n_s0 + lane < n_tot) ? __ldg(bthr + (n_key >> 32)) : ~0u;
-      u32 f_sg = n_sg, f_s0 = n_s0, f_tot = n_tot;
-      if (f_sg < nseg) next_round(f_sg, f_s0, f_tot);
-      const u64 f_key =
-          (f_sg < nseg && f_s0 + lane < f_tot) ? __ldcs(seg + (u64)f_sg * kSegPts + f_s0 + lane) : 0ull;
-      if (c_s0 + lane < c_tot && (u32)c_key >= c_th) take(c_key, c_sg, c_s0 + lane);
-      c_sg = n_sg, c_s0 = n_s0, c_tot = n_tot, c_key = n_key, c_th = n_th;
-      n_sg = f_sg, n_s0 = f_s0, n_tot = f_tot, n_key = f_key;
-    }
-  }
-#else
-  for (u32 sg = blockIdx.x * (kFilterThreads / 32) + (threadIdx.x >> 5); sg < nseg; sg += wstride) {
-    const u32 tot = (u32)__ldg(segcnt + sg);
-    const u64* sp = seg + (u64)sg * kSegPts;
-    for (u32 s0 = 0; s0 < tot; s0 += 32 * kFilterItems) {
-      u64 key[kFilterItems];
-#pragma unroll
-      for (int j = 0; j < kFilterItems; ++j) {
-        const u32 sl = s0 + j * 32 + lane;
-        key[j] = sl < tot ? __ldcs(sp + sl) : 0ull;
-      }
-      // all threshold loads in flight before any test
-      u32 th[kFilterItems];
-#pragma unroll
-      for (int j = 0; j < kFilterItems; ++j) {
-        const u32 sl = s0 + j * 32 + lane;
-        th[j] = sl < tot ? __ldg(bthr + (key[j] >> 32)) : ~0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kFilterItems; ++j) {
-        if ((u32)key[j] < th[j]) continue;  // (past tot: key 0 < th ~0)
-        take(key[j], sg, s0 + j * 32 + lane);
-      }
-    }
-  }
 #endif
+  };
+  // Candidates are rare (~1.6% of survivors on spread-out inputs): the scan
+  // queues them in a warp-private list and takes them 32 at a time, every
+  // lane busy, instead of stalling a whole round on one lane's
+  // index -> point -> slot chain.
+  u32 qn = 0;  // warp-uniform queue length (< 32 between rounds)
+  auto push = [&](bool cand, u64 key, u32 at) {
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    if (!m) return;
+    if (cand) {
+      const u32 q = qn + __popc(m & lanemask_lt());
+      s_qkey[warp][q] = key;
+      s_qat[warp][q] = at;
+    }
+    qn += __popc(m);
+    if (qn < 32) return;
+    __syncwarp();
+    take(s_qkey[warp][lane], s_qat[warp][lane]);
+    const u32 rest = qn - 32;
+    u64 k2 = 0;
+    u32 a2 = 0;
+    if ((u32)lane < rest) {
+      k2 = s_qkey[warp][32 + lane];
+      a2 = s_qat[warp][32 + lane];
+    }
+    __syncwarp();
+    if ((u32)lane < rest) {
+      s_qkey[warp][lane] = k2;
+      s_qat[warp][lane] = a2;
+    }
+    __syncwarp();
+    qn = rest;
+  };
+  // A segment at a time, software-pipelined: while one segment's keys are
+  // tested (coarse table, then the exact threshold of the few that pass),
+  // the next segment's keys (up to kR rounds of 32) and the count of the one
+  // after are in flight. K2 fills ~44% of a segment's 256 slots on uniform
+  // inputs; rounds beyond kR (fuller segments) are loaded on the spot.
+  constexpr int kR = 4;
+  auto load_keys = [&](u32 g, u32 t, u64* k) {
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const u32 sl = 32 * j + lane;
+      k[j] = (g < nseg && sl < t) ? __ldcs(seg + (u64)g * kSegPts + sl) : 0ull;
+    }
+  };
+  auto test = [&](u32 g, u32 sl, u32 t, u64 key, u32 th) {
+    push(sl < t && (u32)key >= th, key, g * kSegPts + sl);
+  };
+  auto coarse = [&](u32 sl, u32 t, u64 key) -> u32 {
+    const u32 bi = (u32)(key >> 32);
+    const bool pass = sl < t && (u32)key >= s_tc[bi >> kCoarseLog2];
+#if CHGPU_FILTER_ABL & 1  // (diagnostic: count the coarse passes instead of the candidates)
+    mine += pass;
+#endif
+    return pass ? __ldcg(bthr + bi) : ~0u;
+  };
+  // kDist segments of keys in flight ahead of the one being tested (a
+  // register ring), each segment's count loaded one step before its keys.
+  constexpr int kDist = CHGPU_FILTER_DIST;
+  u32 sg = blockIdx.x * (kFilterThreads / 32) + warp;
+  u64 kr[kDist + 1][kR];
+  u32 tr[kDist + 2];
+#pragma unroll
+  for (int d = 0; d <= kDist + 1; ++d) {
+    const u32 g = sg + d * wstride;
+    tr[d] = g < nseg ? (u32)__ldg(segcnt + g) : 0u;
+  }
+#pragma unroll
+  for (int d = 0; d < kDist; ++d) load_keys(sg + d * wstride, tr[d], kr[d]);
+  for (; sg < nseg; sg += wstride) {
+    const u32 gl = sg + (kDist + 2) * wstride;
+    const u32 tl = gl < nseg ? (u32)__ldg(segcnt + gl) : 0u;
+    load_keys(sg + kDist * wstride, tr[kDist], kr[kDist]);
+    const u32 tot = tr[0];
+    u32 th[kR];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) th[j] = coarse(32 * j + lane, tot, kr[0][j]);
+#pragma unroll
+    for (int j = 0; j < kR; ++j) test(sg, 32 * j + lane, tot, kr[0][j], th[j]);
+    for (u32 s0 = 32 * kR; s0 < tot; s0 += 32) {  // a fuller segment's remaining rounds
+      const u32 sl = s0 + lane;
+      const u64 key = sl < tot ? __ldcs(seg + (u64)sg * kSegPts + sl) : 0ull;
+      test(sg, sl, tot, key, coarse(sl, tot, key));
+    }
+#pragma unroll
+    for (int d = 0; d < kDist; ++d)
+#pragma unroll
+      for (int j = 0; j < kR; ++j) kr[d][j] = kr[d + 1][j];
+#pragma unroll
+    for (int d = 0; d <= kDist; ++d) tr[d] = tr[d + 1];
+    tr[kDist + 1] = tl;
+  }
+  __syncwarp();
+  if ((u32)lane < qn) take(s_qkey[warp][lane], s_qat[warp][lane]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_cand, mine);
@@ -938,12 +998,13 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 
 cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
-                     u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st) {
+                     u32* tcoarse, u32* first_bin, FilterAux aux, u32* bar, u32* overflow,
+                     cudaStream_t st) {
   const u32 tiles = std::max(1u, (1u << log2nb) / kBinTile);
   dim3 grid(4 * tiles), block(kBinThreads);
   void* args[] = {(void*)&qinfo, (void*)&counts, (void*)&chunk_count, (void*)&log2nb,
                   (void*)&bcnt, (void*)&bw, (void*)&plan, (void*)&bstart, (void*)&bthr,
-                  (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar,
+                  (void*)&tcoarse, (void*)&first_bin, (void*)&aux.tsum, (void*)&aux.agg_seg, (void*)&aux.agg_val, (void*)&bar,
                   (void*)&overflow};
   // cooperative: the launch fails rather than run with a CTA not resident
   // (the caller checked bin_scan_blocks against the device's residency and
@@ -955,16 +1016,17 @@ u32 bin_scan_blocks(int log2nb) { return 4 * std::max(1u, (1u << log2nb) / kBinT
 
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
-                   const u32* bstart, const u32* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
-                   u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
-                   cudaStream_t st) {
+                   const u32* bstart, const u32* bthr, const u32* tcoarse, int log2nb, u32* bcur,
+                   u32* bmap, u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
+                   const u32* overflow, cudaStream_t st) {
   if (nseg == 0) return;
-  // one resident wave: the warp-stride loop then has no partial last wave
-  const int resident = device_limits().filter_resident;
+  // one persistent CTA per SM (the warp-stride loop then has no partial
+  // last wave)
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
-                                   (u32)resident);
-  k_filter<<<blocks, kFilterThreads, 0, st>>>(seg, segidx, segcnt, nseg, pts, P, qinfo, bstart, bthr,
-                                              bcur, bmap, kout, vout, big, nbig, ncand, overflow);
+                                   (u32)device_limits().filter_resident);
+  k_filter<<<blocks, kFilterThreads, filter_smem_bytes(log2nb), st>>>(
+      seg, segidx, segcnt, nseg, pts, P, qinfo, bstart, bthr, tcoarse, bcur, bmap, kout, vout, big,
+      nbig, ncand, overflow);
 }
 
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
@@ -994,10 +1056,14 @@ cudaError_t configure_filter_kernels(DeviceLimits* lim) {
   cudaError_t e = cudaFuncSetAttribute((const void*)k_bin_sort_big,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem));
   if (e != cudaSuccess) return e;
-  int occ = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter, kFilterThreads, 0)) != cudaSuccess)
+  const int fsm = (int)filter_smem_bytes(kMaxFilterLog2);
+  if ((e = cudaFuncSetAttribute((const void*)k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm)) !=
+      cudaSuccess)
     return e;
-  lim->filter_resident = std::max(occ, 1) * lim->sms * CHGPU_FILTER_WAVES;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter, kFilterThreads, fsm)) != cudaSuccess)
+    return e;
+  lim->filter_resident = std::max(occ, 1) * lim->sms;
   occ = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bin_scan, kBinThreads, 0)) != cudaSuccess)
     return e;

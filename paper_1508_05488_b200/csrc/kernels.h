@@ -20,7 +20,8 @@ struct SpaPlan {
 // SPA pre-filter (k_filter.cu + k_spa.cu k_spa_bins).
 constexpr int kBinSortMax = 4096;   // candidates of one bin sorted in shared memory (a CTA)
 constexpr int kWarpSortMax = 256;   // ... by one warp
-constexpr u32 kBigListB = 4u << 18; // offset of the CTA-sort list in the big-bin lists
+constexpr int kMaxFilterLog2 = 18;  // bins per region at most 2^18
+constexpr u32 kBigListB = 4u << kMaxFilterLog2; // offset of the CTA-sort list in the big-bin lists
 struct FilterPlan {
   SpaPlan spa;          // chunk geometry, region offsets of the sorted layout
   u64 seed_w[4];        // wkey of guarded(anchors.first)
@@ -35,7 +36,8 @@ struct FilterAux {
 // The plan of the filter path on the device (from K2's counts).
 cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
                      const u32* bcnt, const u32* bw, FilterPlan* plan, u32* bstart, u32* bthr,
-                     u32* first_bin, FilterAux aux, u32* bar, u32* overflow, cudaStream_t st);
+                     u32* tcoarse, u32* first_bin, FilterAux aux, u32* bar, u32* overflow,
+                     cudaStream_t st);
 // CTAs of the cooperative k_bin_scan launch for log2nb bins per region.
 u32 bin_scan_blocks(int log2nb);
 void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
@@ -44,9 +46,9 @@ void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* b
                        unsigned long long* kept_counts, double2* out, cudaStream_t st);
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
-                   const u32* bstart, const u32* bthr, u32* bcur, u32* bmap, u64* kout, u64* vout,
-                   u32* big, u32* nbig, unsigned long long* ncand, const u32* overflow,
-                   cudaStream_t st);
+                   const u32* bstart, const u32* bthr, const u32* tcoarse, int log2nb, u32* bcur,
+                   u32* bmap, u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
+                   const u32* overflow, cudaStream_t st);
 void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
                          const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
 // Melkman's convex-position trajectory on the device (k_convex.cu).

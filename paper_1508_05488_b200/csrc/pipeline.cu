@@ -75,7 +75,7 @@ __global__ void k_readback(const QuadInfo* __restrict__ qinfo, u32* __restrict__
   if (t < 16) u64s[t] = 0;
 }
 
-constexpr int kMaxFilterBits = 18;
+constexpr int kMaxFilterBits = kMaxFilterLog2;
 constexpr size_t kConvexMin = size_t(1) << 16;  // ring size from which k_convex.cu is tried  // SPA pre-filter: at most 2^18 bins per region
 
 // The bin tables must be zero when K2 starts. They are cleared right after
@@ -751,15 +751,17 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   (void)nbig2_slot;  // nbig_slot + 1: the CTA-sort list count
   *ovf_slot = take_ctr(ctx);
   // plan + bin starts + thresholds: one cooperative launch
+  // (the coarse threshold table lives in the upper half of d_fthr)
+  u32* const tcoarse = reinterpret_cast<u32*>(ctx->d_fthr) + (size_t(4) << kMaxFilterBits);
   CK(launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
-                     ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), first_bin, aux,
-                     ctx->d_ctr + take_ctr(ctx), ctx->d_ctr + *ovf_slot, st));
+                     ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), tcoarse,
+                     first_bin, aux, ctx->d_ctr + take_ctr(ctx), ctx->d_ctr + *ovf_slot, st));
   CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
   // half of vbuf, each segment's survivor count in its lower part
   launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
                 (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart,
-                reinterpret_cast<const u32*>(ctx->d_fthr),
+                reinterpret_cast<const u32*>(ctx->d_fthr), tcoarse, log2nb,
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
                 ctx->d_u64 + 11, ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[4], st));
