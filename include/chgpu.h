@@ -103,7 +103,9 @@ enum {
 enum {
   CHGPU_SPA_AUTO = 0,     /* pre-filter when chunks average >= 16 records (default) */
   CHGPU_SPA_SORT = 1,     /* always sort every survivor (the reference's sort_region) */
-  CHGPU_SPA_FILTER = 2    /* always pre-filter (falls back to the sort on overflow) */
+  CHGPU_SPA_FILTER = 2,   /* always pre-filter (falls back to the sort on overflow) */
+  CHGPU_SPA_FILTER_SORTED = 3  /* pre-filter, every chunk through the bin sorts and the
+                                  sorted chunk SPA (the path k_spa_small defers to) */
 };
 
 typedef struct chgpu_ctx chgpu_ctx;

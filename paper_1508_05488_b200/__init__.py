@@ -97,7 +97,7 @@ class _Diag(C.Structure):
 # chgpu_ctx_set_option (include/chgpu.h)
 OPT_SPA_PATH = 1
 OPT_CHAINS_TAP = 2
-SPA_AUTO, SPA_SORT, SPA_FILTER = 0, 1, 2
+SPA_AUTO, SPA_SORT, SPA_FILTER, SPA_FILTER_SORTED = 0, 1, 2, 3
 
 
 @dataclass
@@ -300,7 +300,9 @@ class Context:
         self._check(self.lib.chgpu_reserve(self.h, n))
 
     def set_spa_path(self, mode: int):
-        """SPA_AUTO (default), SPA_SORT (sort every survivor) or SPA_FILTER."""
+        """SPA_AUTO (default), SPA_SORT (sort every survivor), SPA_FILTER, or
+        SPA_FILTER_SORTED (pre-filter with every chunk through the bin sorts and
+        the sorted chunk SPA, the path large chunks take)."""
         self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_SPA_PATH, mode))
 
     def set_chains_tap(self, on: bool = True):

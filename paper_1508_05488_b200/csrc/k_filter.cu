@@ -40,6 +40,7 @@
 // bin tables are ~40 B per bin and stay in L2.
 
 #include <algorithm>
+#include <cstdio>
 
 #include "chgpu_internal.cuh"
 #include "kernels.h"
@@ -393,6 +394,12 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
 
 // ------------------------------------------------------------------ filter
 
+#ifndef CHGPU_SPA_CLOCKS
+#define CHGPU_SPA_CLOCKS 0
+#endif
+#if CHGPU_SPA_CLOCKS  // (diagnostic build: per-chunk clocks of k_spa_chunks)
+__device__ unsigned long long g_spa_clk[40];
+#endif
 #ifndef CHGPU_FILTER_DIST
 #define CHGPU_FILTER_DIST 1
 #endif
@@ -609,21 +616,20 @@ __device__ __forceinline__ void bitonic_smem(u64* sc, u64* sv, u64* sk, u32 Pn, 
 
 constexpr int kWarpSortWarps = 8;
 
-__global__ __launch_bounds__(32 * kWarpSortWarps) void k_bin_sort_warp(
-    u64* __restrict__ k, u64* __restrict__ v, const FilterPlan* __restrict__ P_p, const u32* __restrict__ bstart,
-    const u32* __restrict__ bcur, const u32* __restrict__ big, const u32* __restrict__ nbig_p) {
-  const FilterPlan& P = *P_p;
-  __shared__ u64 sh[kWarpSortWarps][3][kWarpSortMax];
+// Bins of 33..kWarpSortMax candidates, one warp each (sh: the warp's 3 x
+// kWarpSortMax words of shared memory); items strided over nvb virtual
+// blocks of kWarpSortWarps warps.
+__device__ void bin_sort_warp_body(u64* __restrict__ k, u64* __restrict__ v, const FilterPlan& P,
+                                   const u32* __restrict__ bstart, const u32* __restrict__ bcur,
+                                   const u32* __restrict__ big, u32 nbig, u64* sh, u32 vb, u32 nvb) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u64* sc = sh[wid][0];
-  u64* sv = sh[wid][1];
-  u64* sk = sh[wid][2];
-  const u32 nbig = *nbig_p;
-  for (u32 item = blockIdx.x * kWarpSortWarps + wid; item < nbig;
-       item += gridDim.x * kWarpSortWarps) {
+  u64* sc = sh;
+  u64* sv = sh + kWarpSortMax;
+  u64* sk = sh + 2 * kWarpSortMax;
+  for (u32 item = vb * kWarpSortWarps + wid; item < nbig; item += nvb * kWarpSortWarps) {
     const u32 bi = big[item];
     const u32 len = bcur[bi];
-    if (len > (u32)kWarpSortMax) continue;  // the CTA kernel's
+    if (len > (u32)kWarpSortMax) continue;  // the CTA sort's
     const int r = (int)(bi >> P.log2nb);
     const u64 base = P.spa.off[r] + bstart[bi];
     u32 Pn = 64;
@@ -654,18 +660,13 @@ struct BigSmem {
   u64 c[kBinSortMax], v[kBinSortMax], k[kBinSortMax];
 };
 
-__global__ __launch_bounds__(kBigThreads) void k_bin_sort_big(u64* __restrict__ k,
-                                                              u64* __restrict__ v, const FilterPlan* __restrict__ P_p,
-                                                              const u32* __restrict__ bstart,
-                                                              const u32* __restrict__ bcur,
-                                                              const u32* __restrict__ big,
-                                                              const u32* __restrict__ nbig_p,
-                                                              u32* __restrict__ overflow) {
-  const FilterPlan& P = *P_p;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  BigSmem& S = *reinterpret_cast<BigSmem*>(smem_raw);
-  const u32 nbig = *nbig_p;
-  for (u32 item = blockIdx.x; item < nbig; item += gridDim.x) {
+// Bins of kWarpSortMax+1..kBinSortMax candidates, one CTA each; above that
+// *overflow (the caller falls back to the full region sort).
+__device__ void bin_sort_big_body(u64* __restrict__ k, u64* __restrict__ v, const FilterPlan& P,
+                                  const u32* __restrict__ bstart, const u32* __restrict__ bcur,
+                                  const u32* __restrict__ big, u32 nbig, u32* __restrict__ overflow,
+                                  BigSmem& S, u32 vb, u32 nvb) {
+  for (u32 item = vb; item < nbig; item += nvb) {
     const u32 bi = big[item];
     const int r = (int)(bi >> P.log2nb);
     const u32 len = bcur[bi];
@@ -727,6 +728,241 @@ __device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u6
   }
 }
 
+// ------------------------------------------------------------------ chunk SPA, small chunks
+//
+// One warp per SPA chunk whose candidates fit kSmallCap (every chunk of a
+// spread-out input): spa_filter (spa.cpp:109-163) over the chunk's
+// candidates without any bin having been sorted. The chunk's candidate bins
+// are listed in order from the filter's bitmap and their candidates
+// gathered bin after bin into shared memory; a candidate's rank inside its
+// bin, #{y in the bin: rec_less(y, x)} (ties by slot), places it at its
+// sorted position (bins are contiguous runs of the sorted order). In a bin
+// straddling a chunk boundary (T = 0 there: all its records are
+// candidates) the bin's start rank + that rank decides whether it belongs to
+// this chunk, exactly as in k_spa_chunks. The scan then keeps a record iff
+// its w is >= the running max (the seed's for chunk 0): spa_filter's
+// threshold is the max over every earlier record of the chunk, and the
+// record holding it is never dropped by the filter. Kept records go to the
+// chunk's scratch range and counters exactly like k_spa_chunks. A chunk with
+// more candidates (or more than 32 x kSmallRounds candidate bins) is listed
+// for k_spa_chunks, which then runs after the bin sorts.
+constexpr int kSmallCap = kSpaSmallCap;
+static_assert(kSmallCap <= 256, "bin slots are bytes");
+constexpr int kSmallWarps = 8;
+
+__global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
+    const u64* __restrict__ k, const u64* __restrict__ v, const u32* __restrict__ bcur,
+    const u32* __restrict__ bstart, const u32* __restrict__ bmap, const u32* __restrict__ first_bin,
+    const FilterPlan* __restrict__ P_p, u64* __restrict__ sk, u64* __restrict__ sv,
+    u32* __restrict__ chunk_kept, u32* __restrict__ group_kept,
+    unsigned long long* __restrict__ kept_counts, u32* __restrict__ defer, u32* __restrict__ ndefer,
+    u32 cap) {
+  const SpaPlan& plan = P_p->spa;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 c = blockIdx.x * kSmallWarps + warp;
+  if (c >= plan.total_chunks) return;
+#if CHGPU_SPA_CLOCKS
+  const long long t0 = clock64();
+#endif
+  int r = 0;
+  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
+  const int region = r + 1;
+  const int log2nb = P_p->log2nb;
+  const u32 cl = c - plan.chunk_begin[r];
+  const u32 nchunks = (r < 3 ? plan.chunk_begin[r + 1] : plan.total_chunks) - plan.chunk_begin[r];
+  const u32 cs = (u32)plan.chunk_size[r];
+  const u32 lo = cl * cs, hi = (u32)min((u64)lo + cs, plan.m[r]);
+  const size_t boff = (size_t)r << log2nb;
+  const u64 rbase = plan.off[r];
+  const u32 b_first = first_bin[c];
+  const u32 b_last = cl + 1 < nchunks ? first_bin[c + 1] : (1u << log2nb) - 1u;
+
+  // gathered records (bin after bin): v, k, bin slot
+  __shared__ u64 s_v[kSmallWarps][kSmallCap], s_k[kSmallWarps][kSmallCap];
+  __shared__ unsigned char s_b[kSmallWarps][kSmallCap];
+  // per bin (in order): first gathered slot, candidates, start rank
+  __shared__ u32 s_bex[kSmallWarps][kSmallCap], s_bn[kSmallWarps][kSmallCap], s_bst[kSmallWarps][kSmallCap];
+  // sorted records and their in-chunk flags
+  __shared__ u64 s_ok[kSmallWarps][kSmallCap], s_ov[kSmallWarps][kSmallCap];
+  __shared__ unsigned char s_oin[kSmallWarps][kSmallCap];
+  __shared__ u32 s_list[kSmallWarps][32];
+  u64* const V = s_v[warp];
+  u64* const K = s_k[warp];
+  unsigned char* const B = s_b[warp];
+  u32* const BEX = s_bex[warp];
+  u32* const BN = s_bn[warp];
+  u32* const BST = s_bst[warp];
+
+  // 1. the chunk's candidate bins in order, 32 bitmap words per round
+  u32 m = 0, nbins = 0;
+  bool over = cap == 0;
+  const u32 gb0 = (u32)boff + b_first, gb1 = (u32)boff + b_last;  // inclusive
+  for (u32 w0 = gb0 >> 5; w0 <= (gb1 >> 5) && !over; w0 += 32) {
+    const u32 wi = w0 + lane;
+    u32 word = wi <= (gb1 >> 5) ? bmap[wi] : 0u;
+    if (wi == (gb0 >> 5)) word &= ~0u << (gb0 & 31);
+    if (wi == (gb1 >> 5) && (gb1 & 31) != 31) word &= (2u << (gb1 & 31)) - 1u;
+    const u32 cntw = __popc(word);
+    u32 at = cntw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, at, o);
+      if (lane >= o) at += y;
+    }
+    const u32 nlist = __shfl_sync(0xffffffffu, at, 31);
+    if (nbins + nlist > (u32)kSmallCap) {
+      over = true;
+      break;
+    }
+    // this round's bins in order, 32 at a time: their counts and starts
+    for (u32 lb = 0; lb < nlist; lb += 32) {
+      // list the bins [lb, lb + 32) of this round (lanes holding them write)
+      {
+        u32 idx = at - cntw;
+        u32 wd = word;
+        while (wd) {
+          const u32 b = (wi << 5) + (u32)(__ffs(wd) - 1);
+          if (idx >= lb && idx < lb + 32) s_list[warp][idx - lb] = b;
+          ++idx;
+          wd &= wd - 1;
+        }
+      }
+      __syncwarp();
+      const bool listed = lb + lane < nlist;
+      const u32 gb = listed ? s_list[warp][lane] : 0u;
+      u32 n = 0, st = 0;
+      if (listed) {
+        n = bcur[gb];
+        st = bstart[gb];
+      }
+      u32 incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (m + tot > cap) {
+        over = true;
+        break;
+      }
+      const u32 bi = nbins + lane;
+      if (listed) {
+        BEX[bi] = m + incl - n;
+        BN[bi] = n;
+        BST[bi] = st;
+      }
+      __syncwarp();
+      // gather: slot e of this batch belongs to the first listed lane whose
+      // end exceeds it
+      for (u32 e = m + lane; e < m + tot; e += 32) {
+        int a = 0, z = (int)min(31u, nlist - lb - 1);
+        while (a < z) {
+          const int mid = (a + z) >> 1;
+          if (BEX[nbins + mid] + BN[nbins + mid] > e) z = mid; else a = mid + 1;
+        }
+        const u64 src = rbase + BST[nbins + a] + (e - BEX[nbins + a]);
+        const u64 kk = k[src];
+        K[e] = kk;
+        V[e] = v[src];
+        B[e] = (unsigned char)(nbins + a);  // < kSmallCap <= 256
+      }
+      __syncwarp();
+      m += tot;
+      nbins += min(32u, nlist - lb);
+    }
+  }
+  if (__any_sync(0xffffffffu, over)) {
+    if (lane == 0) defer[atomicAdd(ndefer, 1u)] = c;
+#if CHGPU_SPA_CLOCKS
+    if (lane == 0) atomicAdd(&g_spa_clk[7], 1ull);
+#endif
+    return;
+  }
+#if CHGPU_SPA_CLOCKS
+  const long long t1 = clock64();
+#endif
+  // 2. each record's rank inside its bin -> its sorted position; the
+  // in-chunk test of straddling bins' records
+  for (u32 e = lane; e < m; e += 32) {
+    const u32 b = B[e];
+    const u32 ex = BEX[b], n = BN[b], st = BST[b];
+    const u64 ve = V[e], ke = K[e], ce = canon_k(region, ke);
+    u32 rank = 0;
+    for (u32 y = ex; y < ex + n; ++y) {
+      const u64 vy = V[y], ky = K[y], cy = canon_k(region, ky);
+      rank += (cy < ce || (cy == ce && (vy < ve || (vy == ve && (ky < ke || (ky == ke && y < e))))));
+    }
+    const bool partial = st < lo || st + n > hi;
+    const u32 rk = st + rank;
+    s_ok[warp][ex + rank] = ke;
+    s_ov[warp][ex + rank] = ve;
+    s_oin[warp][ex + rank] = (unsigned char)(!partial || (rk >= lo && rk < hi));
+  }
+  __syncwarp();
+#if CHGPU_SPA_CLOCKS
+  const long long t2 = clock64();
+#endif
+  // 3. the scan in sorted order, 32 records per round
+  const u64 seedw = (cl == 0) ? wkey(region, (region == 1 || region == 4) ? ~ord_enc(plan.seed[r])
+                                                                          : ord_enc(plan.seed[r]))
+                              : 0ull;  // (no finite point has w = 0)
+  u64 carry = seedw;
+  u64* const kd = sk + rbase + lo;
+  u64* const vd = sv + rbase + lo;
+  u32 kept = 0;
+  for (u32 base = 0; base < m; base += 32) {
+    const u32 e = base + lane;
+    const bool in = e < m && s_oin[warp][e];
+    u64 kk = 0, vv = 0, w = 0;
+    if (e < m) {
+      kk = s_ok[warp][e];
+      vv = s_ov[warp][e];
+      w = in ? wkey(region, vv) : 0ull;
+    }
+    u64 incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = y > incl ? y : incl;
+    }
+    u64 ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) ex = 0ull;
+    const u64 before = ex > carry ? ex : carry;
+    const bool keep = in && w >= before;
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const u32 at = kept + __popc(km & lanemask_lt());
+      kd[at] = kk;
+      vd[at] = vv;
+    }
+    kept += __popc(km);
+    const u64 rmax = __shfl_sync(0xffffffffu, incl, 31);
+    carry = rmax > carry ? rmax : carry;
+  }
+  if (lane == 0) {
+    chunk_kept[c] = kept;
+    if (kept) {
+      atomicAdd(&group_kept[c >> 8], kept);
+      atomicAdd(&kept_counts[r], (unsigned long long)kept);
+    }
+  }
+#if CHGPU_SPA_CLOCKS
+  if (lane == 0) {
+    const long long t3 = clock64();
+    atomicMax(&g_spa_clk[20], (u64)(t1 - t0));
+    atomicMax(&g_spa_clk[21], (u64)(t2 - t1));
+    atomicMax(&g_spa_clk[22], (u64)(t3 - t2));
+    atomicAdd(&g_spa_clk[23], (u64)(t1 - t0));
+    atomicAdd(&g_spa_clk[24], (u64)(t2 - t1));
+    atomicAdd(&g_spa_clk[25], (u64)(t3 - t2));
+    atomicAdd(&g_spa_clk[26], 1ull);
+    atomicMax(&g_spa_clk[27], (u64)m);
+    atomicAdd(&g_spa_clk[28], (u64)m);
+  }
+#endif
+}
+
 // ------------------------------------------------------------------ chunk SPA
 //
 // One warp per SPA chunk (spa.cpp:109-163 over the chunk's candidates),
@@ -744,16 +980,26 @@ __device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u6
 // 256 chunks; k_spa_emit places them. (Chunks all finish their scans at
 // about the same time, so a decoupled look-back here would walk back
 // through thousands of aggregates before any prefix appears.)
-__global__ __launch_bounds__(256) void k_spa_chunks(
-    const u64* __restrict__ k, const u64* __restrict__ v, const u32* __restrict__ bcur,
+// Smem of one warp of spa_chunk_warp.
+struct SpaWarpSmem {
+  u32 list[1024];
+  u64 pk[32], pv[32], pc[32];
+  int mark[32];
+};
+
+__device__ void spa_chunk_warp(
+    u32 c, const u64* __restrict__ k, const u64* __restrict__ v, const u32* __restrict__ bcur,
     const u32* __restrict__ bstart, const u32* __restrict__ bmap, const u32* __restrict__ first_bin,
     const FilterPlan* __restrict__ P_p, u64* __restrict__ sk, u64* __restrict__ sv,
     u32* __restrict__ chunk_kept, u32* __restrict__ group_kept,
-    unsigned long long* __restrict__ kept_counts) {
+    unsigned long long* __restrict__ kept_counts, SpaWarpSmem& W) {
   const SpaPlan& plan = P_p->spa;
   const int lane = threadIdx.x & 31;
-  const u32 c = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= plan.total_chunks) return;
+#if CHGPU_SPA_CLOCKS
+  const long long t_start = clock64();
+  u32 n_batches = 0, n_listed = 0;
+#endif
   int r = 0;
   while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
   const int region = r + 1;
@@ -772,9 +1018,6 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
   u64* const kd = sk + rbase + lo;
   u64* const vd = sv + rbase + lo;
   u32 kept = 0;
-  __shared__ int s_mark[8][32];
-  __shared__ u64 s_pk[8][32], s_pv[8][32], s_pc[8][32];
-  const int warp = threadIdx.x >> 5;
 
   // one SPA step over 32 lanes in lane order; inactive lanes are neutral
   auto step = [&](bool active, u64 kk, u64 vv) {
@@ -801,7 +1044,6 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
   // The chunk's bins holding candidates, in order, from the filter's
   // bitmap: 1024 bins per load round (a sparse stretch of a region can put
   // thousands of empty bins in one chunk), then 32 of them per window.
-  __shared__ u32 s_list[8][1024];
   const u32 gb0 = (u32)boff + b_first, gb1 = (u32)boff + b_last;  // inclusive
   for (u32 w0 = gb0 >> 5; w0 <= (gb1 >> 5); w0 += 32) {
     const u32 wi = w0 + lane;
@@ -816,15 +1058,18 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
       if (lane >= o) at += y;
     }
     const u32 nlist = __shfl_sync(0xffffffffu, at, 31);
+#if CHGPU_SPA_CLOCKS
+    n_listed += nlist;
+#endif
     at -= cntw;
     while (word) {
-      s_list[warp][at++] = (wi << 5) + (u32)(__ffs(word) - 1) - (u32)boff;
+      W.list[at++] = (wi << 5) + (u32)(__ffs(word) - 1) - (u32)boff;
       word &= word - 1;
     }
     __syncwarp();
    for (u32 lb = 0; lb < nlist; lb += 32) {
     const bool listed = lb + lane < nlist;
-    const u32 b = listed ? s_list[warp][lb + lane] : 0u;
+    const u32 b = listed ? W.list[lb + lane] : 0u;
     u32 n = 0, s = 0;
     if (listed) {
       n = bcur[boff + b];
@@ -837,6 +1082,9 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
     const bool small = n <= 32;
     unsigned todo = __ballot_sync(0xffffffffu, act);
     while (todo) {
+#if CHGPU_SPA_CLOCKS
+      ++n_batches;
+#endif
       const int p = __ffs(todo) - 1;
       if (!__shfl_sync(0xffffffffu, small, p)) {
         // a bin sorted in place: its share in slices of 32
@@ -867,11 +1115,11 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
       const bool inb = lane >= p && lane < e && act;
       const u32 excl = incl - xx;
       const u32 total = __shfl_sync(0xffffffffu, incl, e - 1);
-      s_mark[warp][lane] = -1;
+      W.mark[lane] = -1;
       __syncwarp();
-      if (inb) s_mark[warp][excl] = lane;
+      if (inb) W.mark[excl] = lane;
       __syncwarp();
-      int jj = s_mark[warp][lane];
+      int jj = W.mark[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, jj, o);
@@ -907,18 +1155,18 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
         // few records per bin: rank by counting (canonical k first, the
         // rest of rec_less only on a tie)
         const u64 cc = canon_k(region, kk);
-        s_pc[warp][lane] = cc;
-        s_pk[warp][lane] = kk;
-        s_pv[warp][lane] = vv;
+        W.pc[lane] = cc;
+        W.pk[lane] = kk;
+        W.pv[lane] = vv;
         __syncwarp();
         u32 rank = 0;
         if (has) {
           for (u32 j = 0; j < gn; ++j) {
             const u32 o = gex + j;
-            const u64 oc = s_pc[warp][o];
+            const u64 oc = W.pc[o];
             bool less = oc < cc;
             if (oc == cc && o != (u32)lane) {
-              const u64 ov = s_pv[warp][o], ok = s_pk[warp][o];
+              const u64 ov = W.pv[o], ok = W.pk[o];
               less = ov < vv || (ov == vv && (ok < kk || (ok == kk && o < (u32)lane)));
             }
             rank += less;
@@ -926,13 +1174,13 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
         }
         __syncwarp();
         if (has) {
-          s_pk[warp][gex + rank] = kk;
-          s_pv[warp][gex + rank] = vv;
+          W.pk[gex + rank] = kk;
+          W.pv[gex + rank] = vv;
         }
         __syncwarp();
         if (has) {
-          kk = s_pk[warp][lane];
-          vv = s_pv[warp][lane];
+          kk = W.pk[lane];
+          vv = W.pv[lane];
         }
         __syncwarp();
       }
@@ -953,20 +1201,41 @@ __global__ __launch_bounds__(256) void k_spa_chunks(
       atomicAdd(&kept_counts[r], (unsigned long long)kept);
     }
   }
+#if CHGPU_SPA_CLOCKS
+  if (lane == 0) {
+    const u64 d = (u64)(clock64() - t_start);
+    atomicMax(&g_spa_clk[0], d);
+    atomicAdd(&g_spa_clk[1], d);
+    atomicAdd(&g_spa_clk[2], 1ull);
+    atomicAdd(&g_spa_clk[8 + min(31, (int)(d / 2000))], 1ull);
+    if (d == g_spa_clk[0]) { g_spa_clk[3] = c; g_spa_clk[4] = n_batches; g_spa_clk[5] = n_listed; g_spa_clk[6] = kept; }
+  }
+#endif
 }
+
+#if CHGPU_SPA_CLOCKS
+__global__ void k_spa_clocks_report() {
+  printf("spa_chunks clocks: max %llu mean %llu chunks %llu | slowest c=%llu batches %llu listed %llu kept %llu\n",
+         g_spa_clk[0], g_spa_clk[1] / max(1ull, g_spa_clk[2]), g_spa_clk[2], g_spa_clk[3], g_spa_clk[4], g_spa_clk[5], g_spa_clk[6]);
+  printf("  hist(2000 clk buckets):");
+  for (int i = 0; i < 32; ++i) printf(" %llu", g_spa_clk[8 + i]);
+  printf("\n");
+  const unsigned long long ns = max(1ull, g_spa_clk[26]);
+  printf("spa_small: chunks %llu deferred %llu | gather max %llu mean %llu | sort max %llu mean %llu | scan max %llu mean %llu | m max %llu mean %llu\n",
+         g_spa_clk[26], g_spa_clk[7], g_spa_clk[20], g_spa_clk[23] / ns, g_spa_clk[21], g_spa_clk[24] / ns,
+         g_spa_clk[22], g_spa_clk[25] / ns, g_spa_clk[27], g_spa_clk[28] / ns);
+  for (int i = 0; i < 40; ++i) g_spa_clk[i] = 0;
+}
+#endif
 
 // Places each chunk's kept records (from k_spa_chunks' scratch) at its
 // output offset: the kept counts of the earlier groups of 256 chunks plus
 // those of the earlier chunks of its own group. Decoded to points.
-__global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__ P_p,
-                                                  const u64* __restrict__ sk,
-                                                  const u64* __restrict__ sv,
-                                                  const u32* __restrict__ chunk_kept,
-                                                  const u32* __restrict__ group_kept,
-                                                  double2* __restrict__ out) {
+__device__ void spa_emit_warp(u32 c, const FilterPlan* __restrict__ P_p, const u64* __restrict__ sk,
+                              const u64* __restrict__ sv, const u32* __restrict__ chunk_kept,
+                              const u32* __restrict__ group_kept, double2* __restrict__ out) {
   const SpaPlan& plan = P_p->spa;
   const int lane = threadIdx.x & 31;
-  const u32 c = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= plan.total_chunks) return;
   const u32 kept = chunk_kept[c];
   if (kept == 0) return;
@@ -994,6 +1263,51 @@ __global__ __launch_bounds__(256) void k_spa_emit(const FilterPlan* __restrict__
 // counts and the quad, so the host enqueues the whole path without waiting
 // for K2. A degenerate frame (no SPA, pipeline.cpp:53-71) leaves every
 // region empty and the path idle.
+// ------------------------------------------------------------------ chunk SPA finish
+
+constexpr int kFinishThreads = 256;
+constexpr size_t kFinishSmem =
+    sizeof(BigSmem) > 8 * sizeof(SpaWarpSmem) ? sizeof(BigSmem) : 8 * sizeof(SpaWarpSmem);
+static_assert(kFinishSmem >= (size_t)kWarpSortWarps * 3 * kWarpSortMax * sizeof(u64), "warp sorts fit");
+
+// Everything after k_spa_small in one cooperative launch (every CTA
+// resident): if it deferred any chunk, the bin sorts (bins of 33..256
+// candidates by a warp, up to kBinSortMax by a CTA), a grid barrier, the
+// sorted chunk SPA (spa_chunk_warp) over the deferred chunks, a grid
+// barrier; then always the emit (spa_emit_warp) of every chunk. With no
+// deferred chunk this is a single pass of the emit.
+__global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
+    u64* __restrict__ k, u64* __restrict__ v, const u32* __restrict__ bcur,
+    const u32* __restrict__ bstart, const u32* __restrict__ bmap, const u32* __restrict__ first_bin,
+    const FilterPlan* __restrict__ P_p, const u32* __restrict__ big, const u32* __restrict__ nbig_p,
+    u32* __restrict__ overflow, const u32* __restrict__ defer, const u32* __restrict__ ndefer_p,
+    u64* __restrict__ sk, u64* __restrict__ sv, u32* __restrict__ chunk_kept,
+    u32* __restrict__ group_kept, unsigned long long* __restrict__ kept_counts,
+    double2* __restrict__ out, u32* __restrict__ bar) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const u32 nwarps = gridDim.x * (kFinishThreads / 32);
+  const u32 gw = blockIdx.x * (kFinishThreads / 32) + warp;
+  const u32 nd = *ndefer_p;
+  if (nd) {
+    const FilterPlan& P = *P_p;
+    bin_sort_warp_body(k, v, P, bstart, bcur, big, nbig_p[0],
+                       reinterpret_cast<u64*>(smem) + (size_t)warp * 3 * kWarpSortMax, blockIdx.x,
+                       gridDim.x);
+    __syncthreads();
+    bin_sort_big_body(k, v, P, bstart, bcur, big + kBigListB, nbig_p[1], overflow,
+                      *reinterpret_cast<BigSmem*>(smem), blockIdx.x, gridDim.x);
+    grid_barrier(bar, 0);
+    SpaWarpSmem& W = reinterpret_cast<SpaWarpSmem*>(smem)[warp];
+    for (u32 i = gw; i < nd; i += nwarps)
+      spa_chunk_warp(defer[i], k, v, bcur, bstart, bmap, first_bin, P_p, sk, sv, chunk_kept,
+                     group_kept, kept_counts, W);
+    grid_barrier(bar, 1);
+  }
+  const u32 total = P_p->spa.total_chunks;
+  for (u32 c = gw; c < total; c += nwarps) spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out);
+}
+
 // ------------------------------------------------------------------ launchers
 
 cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count, int log2nb,
@@ -1029,33 +1343,53 @@ void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nse
       nbig, ncand, overflow);
 }
 
-void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
-                         const u32* big, const u32* nbig, u32* overflow, cudaStream_t st) {
-  const int sms = device_limits().sms;
-  k_bin_sort_warp<<<sms * 4, 32 * kWarpSortWarps, 0, st>>>(k, v, P, bstart, bcur, big, nbig);
-  k_bin_sort_big<<<sms * 2, kBigThreads, sizeof(BigSmem), st>>>(k, v, P, bstart, bcur,
-                                                                big + kBigListB, nbig + 1, overflow);
+// The chunk SPA: k_spa_small over every chunk, then (after the caller's
+// bin sorts) k_spa_chunks over the chunks it deferred, then k_spa_emit.
+void launch_spa_small(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
+                      const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
+                      u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                      unsigned long long* kept_counts, u32* defer, u32* ndefer, u32 cap,
+                      cudaStream_t st) {
+  if (max_chunks == 0) return;
+  cudaMemsetAsync(group_kept, 0, ((max_chunks + 255) / 256) * sizeof(u32), st);
+  k_spa_small<<<(max_chunks + kSmallWarps - 1) / kSmallWarps, 32 * kSmallWarps, 0, st>>>(
+      k, v, bcur, bstart, bmap, first_bin, P, sk, sv, chunk_kept, group_kept, kept_counts, defer,
+      ndefer, std::min<u32>(cap, (u32)kSmallCap));
 }
 
-void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
-                       const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
-                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
-                       unsigned long long* kept_counts, double2* out, cudaStream_t st) {
-  if (max_chunks == 0) return;
-  const u32 blocks = (max_chunks + 7) / 8;
-  cudaMemsetAsync(group_kept, 0, ((max_chunks + 255) / 256) * sizeof(u32), st);
-  k_spa_chunks<<<blocks, 256, 0, st>>>(k, v, bcur, bstart, bmap, first_bin, P, sk, sv, chunk_kept,
-                                       group_kept, kept_counts);
-  k_spa_emit<<<blocks, 256, 0, st>>>(P, sk, sv, chunk_kept, group_kept, out);
+cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart, const u32* bmap,
+                              const u32* first_bin, const FilterPlan* P, const u32* big,
+                              const u32* nbig, u32* overflow, const u32* defer, const u32* ndefer,
+                              u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                              unsigned long long* kept_counts, double2* out, u32* bar,
+                              u32 max_chunks, cudaStream_t st) {
+  if (max_chunks == 0) return cudaSuccess;
+  const u32 blocks = std::max(1u, std::min<u32>((u32)device_limits().finish_coop,
+                                                (max_chunks + 7) / 8));
+  void* args[] = {(void*)&k, (void*)&v, (void*)&bcur, (void*)&bstart, (void*)&bmap,
+                  (void*)&first_bin, (void*)&P, (void*)&big, (void*)&nbig, (void*)&overflow,
+                  (void*)&defer, (void*)&ndefer, (void*)&sk, (void*)&sv, (void*)&chunk_kept,
+                  (void*)&group_kept, (void*)&kept_counts, (void*)&out, (void*)&bar};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_spa_finish, dim3(blocks),
+                                                    dim3(kFinishThreads), args, kFinishSmem, st);
+#if CHGPU_SPA_CLOCKS
+  k_spa_clocks_report<<<1, 1, 0, st>>>();
+#endif
+  return e;
 }
 
 
 // Dynamic shared memory opt-in and residency of the filter kernels for the
 // current device (device_limits()).
 cudaError_t configure_filter_kernels(DeviceLimits* lim) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_bin_sort_big,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem));
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_spa_finish,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinishSmem);
   if (e != cudaSuccess) return e;
+  int fo = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fo, k_spa_finish, kFinishThreads, kFinishSmem)) !=
+      cudaSuccess)
+    return e;
+  lim->finish_coop = fo * lim->sms;
   const int fsm = (int)filter_smem_bytes(kMaxFilterLog2);
   if ((e = cudaFuncSetAttribute((const void*)k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm)) !=
       cudaSuccess)

@@ -20,7 +20,8 @@ struct SpaPlan {
 // SPA pre-filter (k_filter.cu + k_spa.cu k_spa_bins).
 constexpr int kBinSortMax = 4096;   // candidates of one bin sorted in shared memory (a CTA)
 constexpr int kWarpSortMax = 256;   // ... by one warp
-constexpr int kMaxFilterLog2 = 18;  // bins per region at most 2^18
+constexpr int kMaxFilterLog2 = 18;
+constexpr u32 kSpaSmallCap = 128;   // candidates of one chunk k_spa_small takes (else deferred)  // bins per region at most 2^18
 constexpr u32 kBigListB = 4u << kMaxFilterLog2; // offset of the CTA-sort list in the big-bin lists
 struct FilterPlan {
   SpaPlan spa;          // chunk geometry, region offsets of the sorted layout
@@ -40,17 +41,23 @@ cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count,
                      cudaStream_t st);
 // CTAs of the cooperative k_bin_scan launch for log2nb bins per region.
 u32 bin_scan_blocks(int log2nb);
-void launch_spa_chunks(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
-                       const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
-                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
-                       unsigned long long* kept_counts, double2* out, cudaStream_t st);
+cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart, const u32* bmap,
+                              const u32* first_bin, const FilterPlan* P, const u32* big,
+                              const u32* nbig, u32* overflow, const u32* defer, const u32* ndefer,
+                              u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                              unsigned long long* kept_counts, double2* out, u32* bar,
+                              u32 max_chunks, cudaStream_t st);
+void launch_spa_small(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
+                      const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
+                      u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
+                      unsigned long long* kept_counts, u32* defer, u32* ndefer, u32 cap,
+                      cudaStream_t st);
 void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
                    const u32* bstart, const u32* bthr, const u32* tcoarse, int log2nb, u32* bcur,
                    u32* bmap, u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
                    const u32* overflow, cudaStream_t st);
-void launch_bin_sort_big(u64* k, u64* v, const FilterPlan* P, const u32* bstart, const u32* bcur,
-                         const u32* big, const u32* nbig, u32* overflow, cudaStream_t st);
+
 // Melkman's convex-position trajectory on the device (k_convex.cu).
 int convex_blocks();
 void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInfo* qinfo, u32* ok,
@@ -69,6 +76,7 @@ struct DeviceLimits {
   int k1_wave = 0;          // K1 CTAs in one resident wave
   int filter_resident = 0;  // k_filter CTAs in one resident wave
   int binscan_coop = 0;     // k_bin_scan CTAs that can be co-resident (cooperative launch bound)
+  int finish_coop = 0;      // k_spa_finish CTAs that can be co-resident
 };
 const DeviceLimits& device_limits();
 cudaError_t configure_sort_kernels();

@@ -142,6 +142,7 @@ struct chgpu_ctx {
   u64* d_ck = nullptr;       // kept records per chunk, k words (scratch) [cap]
   u64* d_cv = nullptr;       // ... v words                             [cap]
   u32* d_ffirst = nullptr;   // per-chunk first bin
+  u32* d_fdefer = nullptr;   // chunks k_spa_small deferred to k_spa_chunks
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
   bool chains_tap = false;   // CHGPU_OPT_CHAINS_TAP
@@ -736,9 +737,11 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
   if ((size_t)max_chunks > ctx->ffirst_cap) {
     cudaFree(ctx->d_ffirst);
-    ctx->d_ffirst = nullptr;
+    cudaFree(ctx->d_fdefer);
+    ctx->d_ffirst = ctx->d_fdefer = nullptr;
     const size_t want = std::max<size_t>((size_t)max_chunks, 8192);
     CK(cudaMalloc(&ctx->d_ffirst, want * sizeof(u32)));
+    CK(cudaMalloc(&ctx->d_fdefer, want * sizeof(u32)));
     ctx->ffirst_cap = want;
   }
   u32* first_bin = ctx->d_ffirst;
@@ -765,16 +768,23 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
                 ctx->d_u64 + 11, ctx->d_ctr + *ovf_slot, st);
   CK(cudaEventRecord(ctx->ev[4], st));
-  launch_bin_sort_big(ctx->d_ka, ctx->d_va, P, ctx->d_fstart, t.cur, ctx->d_fbig,
-                      ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, st);
+  // the chunk SPA over the sparse candidates, kept records via d_ck / d_cv
+  // (raw scratch: per-chunk kept counts, then their sums per 256 chunks):
+  // k_spa_small per chunk; chunks over its capacity are deferred to the
+  // bin sorts + k_spa_chunks (both idle when none was)
+  const int ndefer_slot = take_ctr(ctx);
+  launch_spa_small(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, max_chunks,
+                   ctx->d_ck, ctx->d_cv, ctx->d_raw, ctx->d_raw + max_chunks, ctx->d_u64,
+                   ctx->d_fdefer, ctx->d_ctr + ndefer_slot,
+                   ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ? 0u : kSpaSmallCap, st);
   CK(cudaEventRecord(ctx->ev[5], st));
+  CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
+                       ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
+                       ctx->d_ctr + ndefer_slot, ctx->d_ck, ctx->d_cv, ctx->d_raw,
+                       ctx->d_raw + max_chunks, ctx->d_u64, ctx->d_kept, ctx->d_ctr + take_ctr(ctx),
+                       max_chunks, st));
   CK(cudaEventRecord(ctx->ev[6], st));
-  // per-chunk SPA over the sparse candidates, kept records via d_ck / d_cv
-  // (raw scratch: per-chunk kept counts, then their sums per 256 chunks)
-  launch_spa_chunks(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, max_chunks,
-                    ctx->d_ck, ctx->d_cv, ctx->d_raw, ctx->d_raw + max_chunks, ctx->d_u64,
-                    ctx->d_kept, st);
-  ctx->launches += 6;
+  ctx->launches += 5;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[8], st));
   return CHGPU_OK;
@@ -991,7 +1001,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   // pre-filter's per-bin statistics when that path is taken.
   bool want_filter =
       chunk_count >= 1 &&
-      (ctx->spa_mode == CHGPU_SPA_FILTER ||
+      (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ||
        (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
   int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
   // the bin scan is one cooperative launch: every CTA must be resident
@@ -1110,12 +1120,14 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       filtered = !overflow;
       if (!filtered) t_sort_ms = ms_between(ctx->ev[2], ctx->ev[8]);  // the attempt
       if (filtered) {
-        t_sort_ms = ms_between(ctx->ev[2], ctx->ev[6]);
-        t_spa_ms = ms_between(ctx->ev[6], ctx->ev[8]);
+        // sort = bin scan + filter (what replaces sort_region); spa = the
+        // chunk SPA (k_spa_small, deferred bin sorts + k_spa_chunks, emit)
+        t_sort_ms = ms_between(ctx->ev[2], ctx->ev[4]);
+        t_spa_ms = ms_between(ctx->ev[4], ctx->ev[8]);
         D.t_spa_kernel_ms = t_spa_ms;
         D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
         D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
-        D.t_binsort_ms = ms_between(ctx->ev[4], ctx->ev[5]);
+        D.t_binsort_ms = ms_between(ctx->ev[5], ctx->ev[6]);
       }
     }
     if (!filtered) {
@@ -1325,6 +1337,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
   if (const char* e = std::getenv("CHGPU_SPA")) {
     if (std::strcmp(e, "sort") == 0) ctx->spa_mode = CHGPU_SPA_SORT;
     if (std::strcmp(e, "filter") == 0) ctx->spa_mode = CHGPU_SPA_FILTER;
+    if (std::strcmp(e, "filter_sorted") == 0) ctx->spa_mode = CHGPU_SPA_FILTER_SORTED;
   }
   if (ensure_segs(ctx, 64) != CHGPU_OK) {
     chgpu_ctx_destroy(ctx);
@@ -1353,6 +1366,7 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_faux);
   cudaFree(ctx->d_plan);
   cudaFree(ctx->d_ffirst);
+  cudaFree(ctx->d_fdefer);
   cudaFree(ctx->d_digit_excl);
   cudaFreeHost(ctx->h);
   cudaFreeHost(ctx->h_segs);
@@ -1373,7 +1387,7 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
   if (!ctx) return CHGPU_INVALID_ARG;
   switch (option) {
     case CHGPU_OPT_SPA_PATH:
-      if (value < CHGPU_SPA_AUTO || value > CHGPU_SPA_FILTER) break;
+      if (value < CHGPU_SPA_AUTO || value > CHGPU_SPA_FILTER_SORTED) break;
       ctx->spa_mode = (int)value;
       return CHGPU_OK;
     case CHGPU_OPT_CHAINS_TAP:
@@ -1688,7 +1702,7 @@ int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double
   const bool degenerate = ctx->h->qi.degenerate != 0;
   const double2* pts = reinterpret_cast<const double2*>(d_xy);
   if (!degenerate && chunk_count >= 1 && ctx->spa_mode != CHGPU_SPA_SORT &&
-      (ctx->spa_mode == CHGPU_SPA_FILTER || chunk_count <= n / 64)) {
+      (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED || chunk_count <= n / 64)) {
     // The pre-filtered SPA against the global quad (the same kernels as
     // chgpu_hull), falling back to the full region sort on overflow.
     const int log2nb = filter_bits(n, chunk_count);

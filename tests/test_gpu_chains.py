@@ -53,14 +53,15 @@ def _check(chains, counts, want_regions, label):
 
 
 @pytest.mark.parametrize("case", CHAINS, ids=lambda c: f"{c['dist']}-{c['n']}-cc{c['chunk_count']}")
-@pytest.mark.parametrize("path", ["auto", "filter", "sort"])
+@pytest.mark.parametrize("path", ["auto", "filter", "filter_sorted", "sort"])
 def test_chains_match_reference(product, tap_ctx, case, path):
     if path == "sort" and case["n"] >= 20_000_000 and case["chunk_count"] == 1024 \
             and case["dist"] == "circle":
         pytest.skip("same kernels as the other circle cases")
     pts = _points(product, case["dist"], case["n"], case["seed"])
     assert sha(pts) == case["input_sha"]
-    mode = {"auto": product.SPA_AUTO, "filter": product.SPA_FILTER, "sort": product.SPA_SORT}[path]
+    mode = {"auto": product.SPA_AUTO, "filter": product.SPA_FILTER, "sort": product.SPA_SORT,
+            "filter_sorted": product.SPA_FILTER_SORTED}[path]
     tap_ctx.set_spa_path(mode)
     try:
         r = tap_ctx.convex_hull(pts, product.PipelineConfig(chunk_count=case["chunk_count"]))
@@ -68,17 +69,18 @@ def test_chains_match_reference(product, tap_ctx, case, path):
         tap_ctx.set_spa_path(product.SPA_AUTO)
     assert list(r.diag.region_counts) == case["region_counts"]
     chains, counts = tap_ctx.last_chains()
-    if path == "filter" or (path == "auto" and case["chunk_count"] <= case["n"] // 64):
+    if path in ("filter", "filter_sorted") or (path == "auto" and case["chunk_count"] <= case["n"] // 64):
         # the pre-filtered path really ran (no overflow fallback) where it applies
         assert r.diag.spa_path in (1, 2)
     _check(chains, counts, case["kept"], f"{case['dist']} cc={case['chunk_count']} {path}")
 
 
-@pytest.mark.parametrize("path", ["filter", "sort"])
+@pytest.mark.parametrize("path", ["filter", "filter_sorted", "sort"])
 def test_stage_chains_small_inputs(product, tap_ctx, path):
     """Every stages.json case (8 inputs x up to 8 chunk counts): the chains
     point by point against the reference's kept arrays."""
-    mode = {"filter": product.SPA_FILTER, "sort": product.SPA_SORT}[path]
+    mode = {"filter": product.SPA_FILTER, "sort": product.SPA_SORT,
+            "filter_sorted": product.SPA_FILTER_SORTED}[path]
     tap_ctx.set_spa_path(mode)
     checked = 0
     try:

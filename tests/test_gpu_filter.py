@@ -11,14 +11,15 @@ from conftest import load_golden, sha
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["sort", "filter"])
+@pytest.fixture(scope="module", params=["sort", "filter", "filter_sorted"])
 def path_ctx(request):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1508_05488_b200 as P
     ctx = P.Context(0)
-    ctx.set_spa_path(P.SPA_SORT if request.param == "sort" else P.SPA_FILTER)
+    ctx.set_spa_path({"sort": P.SPA_SORT, "filter": P.SPA_FILTER,
+                      "filter_sorted": P.SPA_FILTER_SORTED}[request.param])
     ctx.path = request.param
     yield ctx
     ctx.close()
