@@ -236,6 +236,31 @@ int chgpu_shard_chains_device(chgpu_ctx* ctx, const double* d_xy, size_t n, cons
                               size_t chunk_count, double* d_chains, size_t cap_points,
                               size_t* kept_counts);
 
+/* convex_hull (pipeline.hpp:55) of the concatenation shard[0], shard[1],
+ * ... (global point index = position in that concatenation) with several
+ * contexts, one per GPU, in one process: the multi-GPU drop-in for
+ * chainhull::convex_hull, and its route for spans of 2^32 points or more.
+ * on_device = 0: shards are host memory; shard s runs on ctxs[s % nctx],
+ *   in slices of at most 2^30 points (any size: a span too large for one
+ *   device is processed slice by slice).
+ * on_device = 1: shard s is device memory on ctxs[s]'s device (nshards ==
+ *   nctx, each under 2^32 points).
+ * Steps: each slice's extreme candidates with global indices,
+ * folded in index order into the quad find_extremes returns for the whole
+ * set; per slice the round-1 discard, region sort and SPA against that
+ * quad; the chains copied to ctxs[0]'s device (cudaMemcpyPeerAsync, NVLink
+ * between GPUs) with the frame; the single-GPU pipeline over that union.
+ * The hull equals the reference's for the whole set bit for bit; stats
+ * n_input and n_hull are the whole set's, the other counters the merge's
+ * (not comparable with a single-device run). The hull is owned by ctxs[0]
+ * until its next call. Contexts on the same device are allowed. */
+/* CUDA devices visible to this process (0 without a GPU). */
+int chgpu_device_count(void);
+int chgpu_hull_sharded(chgpu_ctx* const* ctxs, int nctx, const double* const* shards,
+                       const size_t* counts, int nshards, int on_device, size_t chunk_count,
+                       int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+                       chgpu_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

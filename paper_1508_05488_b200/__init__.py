@@ -209,6 +209,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                      C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_hull.argtypes = hull_args
         L.chgpu_hull_device.argtypes = hull_args
+        L.chgpu_device_count.argtypes = []
+        L.chgpu_hull_sharded.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(_dp), _sz, C.c_int,
+                                         C.c_int, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
+                                         C.POINTER(_Stats)]
         L.chgpu_hull_xy_binary.argtypes = [vp, C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
                                            C.POINTER(_Stats), C.POINTER(_Diag)]
         L.chgpu_find_extremes.argtypes = [vp, _dp, C.c_size_t, _dp]
@@ -468,6 +472,41 @@ def _ctx() -> Context:
 def convex_hull(points, config: PipelineConfig | None = None) -> HullResult:
     """chainhull::convex_hull (pipeline.hpp:55) on the GPU."""
     return _ctx().convex_hull(points, config)
+
+
+def hull_sharded(contexts, shards, config: PipelineConfig | None = None,
+                 on_device: bool = False) -> HullResult:
+    """convex_hull of the concatenation of `shards` with several contexts
+    (one per GPU) in one process: chgpu_hull_sharded (include/chgpu.h).
+    Host shards: (n, 2) float64 arrays, shard s on contexts[s % len]; device
+    shards (on_device=True): (ptr, n) pairs, shard s on contexts[s]'s device.
+    stats: n_input and n_hull of the whole set, the rest the merge's."""
+    config = config or PipelineConfig()
+    L = load_library()
+    keep = []
+    ptrs, counts = [], []
+    for sh in shards:
+        if on_device:
+            p, n = sh
+        else:
+            a = _pts(sh)
+            keep.append(a)
+            p, n = a.ctypes.data, len(a)
+        ptrs.append(p)
+        counts.append(n)
+    ctxs = (C.c_void_p * len(contexts))(*[c.h for c in contexts])
+    parr = (_dp * len(ptrs))(*[C.cast(C.c_void_p(p), _dp) for p in ptrs])
+    carr = (C.c_size_t * len(counts))(*counts)
+    out = _dp()
+    k = C.c_size_t()
+    s = _Stats()
+    st = L.chgpu_hull_sharded(ctxs, len(contexts), parr, carr, len(ptrs), int(bool(on_device)),
+                              config.chunk_count, int(bool(config.degenerate_fallback)),
+                              C.byref(out), C.byref(k), C.byref(s))
+    contexts[0]._check(st)
+    verts = np.ctypeslib.as_array(out, shape=(k.value * 2,)).reshape(-1, 2).copy() \
+        if k.value else np.empty((0, 2))
+    return HullResult(Hull(verts), raw_stats=s)
 
 
 def find_extremes(points) -> np.ndarray:

@@ -9,6 +9,8 @@
 // fallback for the preprocessing path. Status codes are mapped back to the
 // reference's exception types on the same branches (include/chgpu.h).
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -31,8 +33,10 @@ namespace {
 static_assert(sizeof(Point2) == 16, "Point2 must be two packed doubles");
 static_assert(sizeof(StageStats) == sizeof(chgpu_stats), "StageStats layout");
 
+// One pool per device (-1: the calling thread's current device).
 class ContextPool {
  public:
+  explicit ContextPool(int device = -1) : device_(device) {}
   ~ContextPool() {
     for (chgpu_ctx* c : free_) chgpu_ctx_destroy(c);
   }
@@ -46,7 +50,7 @@ class ContextPool {
       }
     }
     chgpu_ctx* c = nullptr;
-    const int st = chgpu_ctx_create(-1, &c);
+    const int st = chgpu_ctx_create(device_, &c);
     if (st != CHGPU_OK || !c)
       throw Error(st == CHGPU_NO_DEVICE ? "chainhull: no CUDA device (the GPU path has no CPU fallback)"
                                         : "chainhull: CUDA context creation failed");
@@ -58,22 +62,37 @@ class ContextPool {
   }
 
  private:
+  int device_;
   std::mutex mu_;
   std::vector<chgpu_ctx*> free_;
 };
 
-ContextPool& pool() {
-  static ContextPool p;
-  return p;
+ContextPool& pool(int device = -1) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<ContextPool>> per_device;  // [device + 1]
+  std::lock_guard<std::mutex> lock(mu);
+  const size_t i = (size_t)(device + 1);
+  if (per_device.size() <= i) per_device.resize(i + 1);
+  if (!per_device[i]) per_device[i] = std::make_unique<ContextPool>(device);
+  return *per_device[i];
 }
 
 struct Lease {
+  int device;
   chgpu_ctx* ctx;
-  Lease() : ctx(pool().acquire()) {}
-  ~Lease() { pool().release(ctx); }
+  explicit Lease(int dev = -1) : device(dev), ctx(pool(dev).acquire()) {}
+  ~Lease() { pool(device).release(ctx); }
   Lease(const Lease&) = delete;
   Lease& operator=(const Lease&) = delete;
 };
+
+// Shards of convex_hull for a span of 2^32 points or more (beyond one call
+// of the single-device path), or CHAINHULL_SHARDS=k (k > 1) to force k
+// shards: one per visible device, round robin.
+std::size_t forced_shards() {
+  const char* e = std::getenv("CHAINHULL_SHARDS");
+  return e ? (std::size_t)std::strtoull(e, nullptr, 10) : 0;
+}
 
 [[noreturn]] void raise(int status, const std::string& msg) {
   switch (status) {
@@ -101,13 +120,40 @@ std::array<double, 8> quad_array(const ExtremeQuad& q) {
 
 HullResult convex_hull(std::span<const Point2> points, const PipelineConfig& config) {
   if (points.empty()) throw EmptyInput("convex_hull: no points");
-  Lease lease;
   const double* hull_xy = nullptr;
   std::size_t n_hull = 0;
   chgpu_stats st{};
-  check(chgpu_hull(lease.ctx, raw(points), points.size(), config.chunk_count,
-                   config.degenerate_fallback ? 1 : 0, &hull_xy, &n_hull, &st, nullptr),
-        lease.ctx);
+  const std::size_t n = points.size();
+  const std::size_t forced = forced_shards();
+  std::unique_ptr<Lease> lease;
+  std::vector<std::unique_ptr<Lease>> leases;
+  if (n >= (std::size_t(1) << 32) || forced > 1) {
+    // several GPUs (or slices of one): chgpu_hull_sharded over contiguous
+    // host shards, one context per device
+    const int ndev = std::max(1, chgpu_device_count());
+    const std::size_t k = std::max<std::size_t>(forced > 1 ? forced : (std::size_t)ndev, 1);
+    std::vector<chgpu_ctx*> ctxs;
+    for (int d = 0; d < (int)std::min<std::size_t>(k, (std::size_t)ndev); ++d) {
+      leases.push_back(std::make_unique<Lease>(d));
+      ctxs.push_back(leases.back()->ctx);
+    }
+    std::vector<const double*> shards;
+    std::vector<std::size_t> counts;
+    for (std::size_t s = 0; s < k; ++s) {
+      const std::size_t b = n * s / k, e = n * (s + 1) / k;
+      shards.push_back(raw(points) + 2 * b);
+      counts.push_back(e - b);
+    }
+    check(chgpu_hull_sharded(ctxs.data(), (int)ctxs.size(), shards.data(), counts.data(), (int)k, 0,
+                             config.chunk_count, config.degenerate_fallback ? 1 : 0, &hull_xy,
+                             &n_hull, &st),
+          ctxs[0]);
+  } else {
+    lease = std::make_unique<Lease>();
+    check(chgpu_hull(lease->ctx, raw(points), n, config.chunk_count,
+                     config.degenerate_fallback ? 1 : 0, &hull_xy, &n_hull, &st, nullptr),
+          lease->ctx);
+  }
   HullResult r;
   const Point2* h = reinterpret_cast<const Point2*>(hull_xy);
   r.hull.vertices.assign(h, h + n_hull);

@@ -749,6 +749,14 @@ __device__ __forceinline__ void warp_sort_records(int region, u32& g, u64& k, u6
 constexpr int kSmallCap = kSpaSmallCap;
 static_assert(kSmallCap <= 256, "bin slots are bytes");
 constexpr int kSmallWarps = 8;
+struct SmallSmem {
+  u64 c[kSmallCap], v[kSmallCap], k[kSmallCap];  // gathered records
+  u64 ok[kSmallCap], ov[kSmallCap];              // sorted records
+  u32 bex[kSmallCap], bn[kSmallCap], bst[kSmallCap];
+  u32 list[32];
+  unsigned char b[kSmallCap], oin[kSmallCap];
+};
+constexpr size_t kSmallSmem = kSmallWarps * sizeof(SmallSmem);
 
 __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
     const u64* __restrict__ k, const u64* __restrict__ v, const u32* __restrict__ bcur,
@@ -777,21 +785,15 @@ __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
   const u32 b_first = first_bin[c];
   const u32 b_last = cl + 1 < nchunks ? first_bin[c + 1] : (1u << log2nb) - 1u;
 
-  // gathered records (bin after bin): v, k, bin slot
-  __shared__ u64 s_v[kSmallWarps][kSmallCap], s_k[kSmallWarps][kSmallCap];
-  __shared__ unsigned char s_b[kSmallWarps][kSmallCap];
-  // per bin (in order): first gathered slot, candidates, start rank
-  __shared__ u32 s_bex[kSmallWarps][kSmallCap], s_bn[kSmallWarps][kSmallCap], s_bst[kSmallWarps][kSmallCap];
-  // sorted records and their in-chunk flags
-  __shared__ u64 s_ok[kSmallWarps][kSmallCap], s_ov[kSmallWarps][kSmallCap];
-  __shared__ unsigned char s_oin[kSmallWarps][kSmallCap];
-  __shared__ u32 s_list[kSmallWarps][32];
-  u64* const V = s_v[warp];
-  u64* const K = s_k[warp];
-  unsigned char* const B = s_b[warp];
-  u32* const BEX = s_bex[warp];
-  u32* const BN = s_bn[warp];
-  u32* const BST = s_bst[warp];
+  extern __shared__ __align__(16) unsigned char small_smem[];
+  SmallSmem& S = reinterpret_cast<SmallSmem*>(small_smem)[warp];
+  u64* const C = S.c;  // gathered records (bin after bin): canon k, v, k, bin slot
+  u64* const V = S.v;
+  u64* const K = S.k;
+  unsigned char* const B = S.b;
+  u32* const BEX = S.bex;  // per bin (in order): first gathered slot, candidates, start rank
+  u32* const BN = S.bn;
+  u32* const BST = S.bst;
 
   // 1. the chunk's candidate bins in order, 32 bitmap words per round
   u32 m = 0, nbins = 0;
@@ -822,14 +824,14 @@ __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
         u32 wd = word;
         while (wd) {
           const u32 b = (wi << 5) + (u32)(__ffs(wd) - 1);
-          if (idx >= lb && idx < lb + 32) s_list[warp][idx - lb] = b;
+          if (idx >= lb && idx < lb + 32) S.list[idx - lb] = b;
           ++idx;
           wd &= wd - 1;
         }
       }
       __syncwarp();
       const bool listed = lb + lane < nlist;
-      const u32 gb = listed ? s_list[warp][lane] : 0u;
+      const u32 gb = listed ? S.list[lane] : 0u;
       u32 n = 0, st = 0;
       if (listed) {
         n = bcur[gb];
@@ -865,6 +867,7 @@ __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
         const u64 kk = k[src];
         K[e] = kk;
         V[e] = v[src];
+        C[e] = canon_k(region, kk);
         B[e] = (unsigned char)(nbins + a);  // < kSmallCap <= 256
       }
       __syncwarp();
@@ -887,17 +890,26 @@ __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
   for (u32 e = lane; e < m; e += 32) {
     const u32 b = B[e];
     const u32 ex = BEX[b], n = BN[b], st = BST[b];
-    const u64 ve = V[e], ke = K[e], ce = canon_k(region, ke);
+    const u64 ce = C[e];
     u32 rank = 0;
+    bool tie = false;
     for (u32 y = ex; y < ex + n; ++y) {
-      const u64 vy = V[y], ky = K[y], cy = canon_k(region, ky);
-      rank += (cy < ce || (cy == ce && (vy < ve || (vy == ve && (ky < ke || (ky == ke && y < e))))));
+      const u64 cy = C[y];
+      rank += cy < ce;
+      tie |= cy == ce && y != e;
+    }
+    if (tie) {  // (rare: an equal primary coordinate in the bin) the rest of rec_less
+      const u64 ve = V[e], ke = K[e];
+      for (u32 y = ex; y < ex + n; ++y) {
+        const u64 vy = V[y], ky = K[y];
+        rank += C[y] == ce && (vy < ve || (vy == ve && (ky < ke || (ky == ke && y < e))));
+      }
     }
     const bool partial = st < lo || st + n > hi;
     const u32 rk = st + rank;
-    s_ok[warp][ex + rank] = ke;
-    s_ov[warp][ex + rank] = ve;
-    s_oin[warp][ex + rank] = (unsigned char)(!partial || (rk >= lo && rk < hi));
+    S.ok[ex + rank] = K[e];
+    S.ov[ex + rank] = V[e];
+    S.oin[ex + rank] = (unsigned char)(!partial || (rk >= lo && rk < hi));
   }
   __syncwarp();
 #if CHGPU_SPA_CLOCKS
@@ -913,11 +925,11 @@ __global__ __launch_bounds__(32 * kSmallWarps) void k_spa_small(
   u32 kept = 0;
   for (u32 base = 0; base < m; base += 32) {
     const u32 e = base + lane;
-    const bool in = e < m && s_oin[warp][e];
+    const bool in = e < m && S.oin[e];
     u64 kk = 0, vv = 0, w = 0;
     if (e < m) {
-      kk = s_ok[warp][e];
-      vv = s_ov[warp][e];
+      kk = S.ok[e];
+      vv = S.ov[e];
       w = in ? wkey(region, vv) : 0ull;
     }
     u64 incl = w;
@@ -1352,7 +1364,7 @@ void launch_spa_small(const u64* k, const u64* v, const u32* bcur, const u32* bs
                       cudaStream_t st) {
   if (max_chunks == 0) return;
   cudaMemsetAsync(group_kept, 0, ((max_chunks + 255) / 256) * sizeof(u32), st);
-  k_spa_small<<<(max_chunks + kSmallWarps - 1) / kSmallWarps, 32 * kSmallWarps, 0, st>>>(
+  k_spa_small<<<(max_chunks + kSmallWarps - 1) / kSmallWarps, 32 * kSmallWarps, kSmallSmem, st>>>(
       k, v, bcur, bstart, bmap, first_bin, P, sk, sv, chunk_kept, group_kept, kept_counts, defer,
       ndefer, std::min<u32>(cap, (u32)kSmallCap));
 }
@@ -1382,7 +1394,10 @@ cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart
 // Dynamic shared memory opt-in and residency of the filter kernels for the
 // current device (device_limits()).
 cudaError_t configure_filter_kernels(DeviceLimits* lim) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_spa_finish,
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_spa_small,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute((const void*)k_spa_finish,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFinishSmem);
   if (e != cudaSuccess) return e;
   int fo = 0;

@@ -98,6 +98,12 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
 
 struct chgpu_ctx {
   int device = 0;
+  // chgpu_hull_sharded: this context's shards' chains (device), and on the
+  // merging context the union of every shard's chains + the frame
+  double2* d_store = nullptr;
+  size_t store_cap = 0, store_n = 0;
+  double2* d_union = nullptr;
+  size_t union_cap = 0;
   cudaStream_t st = nullptr, st_copy = nullptr;
   std::string err;
   u32 tag = 0;
@@ -1367,6 +1373,8 @@ void chgpu_ctx_destroy(chgpu_ctx* ctx) {
   cudaFree(ctx->d_plan);
   cudaFree(ctx->d_ffirst);
   cudaFree(ctx->d_fdefer);
+  cudaFree(ctx->d_store);
+  cudaFree(ctx->d_union);
   cudaFree(ctx->d_digit_excl);
   cudaFreeHost(ctx->h);
   cudaFreeHost(ctx->h_segs);
@@ -1673,9 +1681,11 @@ namespace {
 // buffer (d_dst == nullptr) or to a caller's device buffer of d_cap points.
 int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double* quad,
                       size_t chunk_count, const double** chains_xy, double* d_dst, size_t d_cap,
-                      size_t* kept_counts) {
-  // the chains: D2D into the caller's buffer, or D2H into the context's
+                      size_t* kept_counts, bool keep_on_device = false) {
+  // the chains: left in ctx->d_kept, D2D into the caller's buffer, or D2H
+  // into the context's
   auto deliver = [&](size_t total) -> int {
+    if (keep_on_device) return sync(ctx);
     if (d_dst) {
       if (total > d_cap) return fail(ctx, CHGPU_TOO_LARGE, "shard chains exceed the output buffer");
       CK(cudaMemcpyAsync(d_dst, ctx->d_kept, total * sizeof(double2), cudaMemcpyDeviceToDevice,
@@ -1773,6 +1783,183 @@ int chgpu_shard_chains_device(chgpu_ctx* ctx, const double* d_xy, size_t n, cons
                               size_t* kept_counts) {
   return shard_chains_impl(ctx, d_xy, n, quad, chunk_count, nullptr, d_chains, cap_points,
                            kept_counts);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- one process, several GPUs
+
+namespace {
+
+// Grows a device buffer of double2 (on the current device), keeping `keep`
+// leading points.
+int grow(chgpu_ctx* ctx, double2** buf, size_t* cap, size_t want, size_t keep) {
+  if (want <= *cap) return CHGPU_OK;
+  const size_t ncap = std::max(want, *cap * 2);
+  double2* nb = nullptr;
+  CK(cudaMalloc(&nb, ncap * sizeof(double2)));
+  if (keep) CK(cudaMemcpyAsync(nb, *buf, keep * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->st));
+  TRY(sync(ctx));
+  cudaFree(*buf);
+  *buf = nb;
+  *cap = ncap;
+  return CHGPU_OK;
+}
+
+struct ShardSlice {
+  const double* xy;  // host or device (on its context's device)
+  size_t n;
+  u64 base;          // global index of its first point
+  int ctx;
+  bool host;
+};
+
+// Runs fn(i) for every context index, one host thread per context (the
+// contexts' devices work concurrently); the first failure wins.
+template <typename F>
+int for_each_ctx(int nctx, F fn) {
+  if (nctx == 1) return fn(0);
+  std::vector<int> st(nctx, CHGPU_OK);
+  std::vector<std::thread> th;
+  th.reserve(nctx);
+  for (int i = 0; i < nctx; ++i) th.emplace_back([&, i] { st[i] = fn(i); });
+  for (auto& t : th) t.join();
+  for (int x : st)
+    if (x != CHGPU_OK) return x;
+  return CHGPU_OK;
+}
+
+// Largest slice of a host shard one context holds at a time (a span of
+// 2^32 points or more is processed in slices; each slice's indices stay
+// below 2^32). CHGPU_SLICE_MAX (points) lowers it (tests).
+size_t slice_max() {
+  const char* e = std::getenv("CHGPU_SLICE_MAX");
+  const size_t v = e ? (size_t)std::strtoull(e, nullptr, 10) : 0;
+  return v ? std::min(v, size_t(1) << 30) : size_t(1) << 30;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int chgpu_hull_sharded(chgpu_ctx* const* ctxs, int nctx, const double* const* shards,
+                       const size_t* counts, int nshards, int on_device, size_t chunk_count,
+                       int degenerate_fallback, const double** hull_xy, size_t* n_hull,
+                       chgpu_stats* stats) {
+  *n_hull = 0;
+  if (nctx < 1 || !ctxs || nshards < 1 || !shards || !counts) return CHGPU_INVALID_ARG;
+  chgpu_ctx* const c0 = ctxs[0];
+  if (on_device && nshards != nctx)
+    return fail(c0, CHGPU_INVALID_ARG, "chgpu_hull_sharded: device shards need one context each");
+  const auto t_wall0 = std::chrono::steady_clock::now();
+  // slices in global index order
+  std::vector<ShardSlice> slices;
+  u64 total = 0;
+  for (int s = 0; s < nshards; ++s) {
+    const size_t per = on_device ? counts[s] : slice_max();
+    if (on_device && counts[s] >= (size_t(1) << 32))
+      return fail(c0, CHGPU_TOO_LARGE, "a device shard must hold fewer than 2^32 points");
+    for (size_t off = 0; off < counts[s]; off += per) {
+      const size_t n = std::min(per, counts[s] - off);
+      slices.push_back({shards[s] + 2 * off, n, total + off, s % nctx, !on_device});
+    }
+    total += counts[s];
+  }
+  if (total == 0) return fail(c0, CHGPU_EMPTY, "convex_hull: no points");
+  std::vector<std::vector<size_t>> mine(nctx);
+  for (size_t i = 0; i < slices.size(); ++i) mine[slices[i].ctx].push_back(i);
+  // a context with one host slice keeps it resident between the passes
+  auto place = [&](chgpu_ctx* ctx, const ShardSlice& sl) -> int {
+    if (!sl.host) return CHGPU_OK;
+    TRY(ensure_cap(ctx, sl.n));
+    CK(cudaMemcpyAsync(ctx->d_pts, sl.xy, sl.n * sizeof(double2), cudaMemcpyHostToDevice, ctx->st));
+    return CHGPU_OK;
+  };
+  auto dev_ptr = [&](chgpu_ctx* ctx, const ShardSlice& sl) {
+    return sl.host ? reinterpret_cast<const double*>(ctx->d_pts) : sl.xy;
+  };
+
+  // exchange 1: every slice's extreme candidates with global indices,
+  // folded in index order (extremes.cpp:39-46, lowest index on ties)
+  std::vector<double> quads(8 * slices.size());
+  std::vector<uint64_t> idxs(4 * slices.size());
+  TRY(for_each_ctx(nctx, [&](int i) -> int {
+    chgpu_ctx* ctx = ctxs[i];
+    cudaSetDevice(ctx->device);
+    for (size_t j : mine[i]) {
+      TRY(place(ctx, slices[j]));
+      TRY(chgpu_shard_extremes(ctx, dev_ptr(ctx, slices[j]), slices[j].n, slices[j].base,
+                               &quads[8 * j], &idxs[4 * j]));
+    }
+    return CHGPU_OK;
+  }));
+  double quad[8];
+  chgpu_fold_extremes(quads.data(), idxs.data(), slices.size(), quad);
+
+  // per slice: round-1 discard, region sort and SPA against the global quad
+  // (every dropped point lies inside the global quad or inside a triangle
+  // of kept points and global anchors, so no hull vertex is lost); each
+  // context appends its slices' chains to its device store
+  TRY(for_each_ctx(nctx, [&](int i) -> int {
+    chgpu_ctx* ctx = ctxs[i];
+    cudaSetDevice(ctx->device);
+    ctx->store_n = 0;
+    const bool resident = mine[i].size() == 1;
+    for (size_t j : mine[i]) {
+      if (!resident) TRY(place(ctx, slices[j]));
+      size_t kc[4];
+      TRY(shard_chains_impl(ctx, dev_ptr(ctx, slices[j]), slices[j].n, quad, chunk_count, nullptr,
+                            nullptr, 0, kc, /*keep_on_device=*/true));
+      const size_t k = kc[0] + kc[1] + kc[2] + kc[3];
+      TRY(grow(ctx, &ctx->d_store, &ctx->store_cap, ctx->store_n + k + 1, ctx->store_n));
+      if (k)
+        CK(cudaMemcpyAsync(ctx->d_store + ctx->store_n, ctx->d_kept, k * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, ctx->st));
+      ctx->store_n += k;
+    }
+    return sync(ctx);
+  }));
+
+  // exchange 2: the chains to the first context's device (peer copies over
+  // NVLink), plus the frame; then the single-GPU pipeline over the union:
+  // the hull of the union of chains is the hull of the whole set
+  cudaSetDevice(c0->device);
+  size_t nu = 0;
+  for (int i = 0; i < nctx; ++i) nu += ctxs[i]->store_n;
+  Pt fr[4];
+  int nf = 0;
+  frame_of(quad, fr, &nf);
+  TRY(grow(c0, &c0->d_union, &c0->union_cap, nu + 4, 0));
+  size_t off = 0;
+  for (int i = 0; i < nctx; ++i) {
+    chgpu_ctx* ctx = ctxs[i];
+    if (ctx->store_n)
+      CK(cudaMemcpyPeerAsync(c0->d_union + off, c0->device, ctx->d_store, ctx->device,
+                             ctx->store_n * sizeof(double2), c0->st));
+    off += ctx->store_n;
+  }
+  TRY(upload(c0, c0->d_union + off, fr, nf * sizeof(Pt)));
+  off += nf;
+  TRY(ensure_cap(c0, off));
+  chgpu_stats S{};
+  TRY(run_pipeline(c0, nullptr, c0->d_union, off, chunk_count, degenerate_fallback, hull_xy, n_hull,
+                   &S, nullptr));
+  if (stats) {
+    // n_input and n_hull are the whole set's; the stage counters and times
+    // are the merge's (a sharded run's intermediate counters are not
+    // comparable with a single-process run)
+    S.n_input = total;
+    S.t_total_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();
+    *stats = S;
+  }
+  return CHGPU_OK;
 }
 
 }  // extern "C"
