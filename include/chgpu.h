@@ -91,14 +91,16 @@ typedef struct {
   double t_filter_ms;       /* pre-filter: candidate selection */
   double t_binsort_ms;      /* pre-filter: sort of bins above 32 candidates */
   int convex_fast_path;     /* 1: Melkman's all-kept trajectory verified on the GPU (k_convex.cu) */
-  int pad3_;
+  int k1k2_overlapped;      /* 1: K2 launched programmatically behind K1; t_k1_ms covers both */
 } chgpu_diag;
 
 /* Options (chgpu_ctx_set_option). */
 enum {
   CHGPU_OPT_SPA_PATH = 1,   /* value: one of the CHGPU_SPA_* below */
-  CHGPU_OPT_CHAINS_TAP = 2  /* value 1: keep each hull call's SPA chains for
+  CHGPU_OPT_CHAINS_TAP = 2, /* value 1: keep each hull call's SPA chains for
                                chgpu_last_chains (a parity tap; costs one D2H) */
+  CHGPU_OPT_PDL = 3         /* value 1 (default): K2 launched programmatically behind
+                               K1 (overlapped; timed together); 0: separately timed */
 };
 enum {
   CHGPU_SPA_AUTO = 0,     /* pre-filter when chunks average >= 16 records (default) */

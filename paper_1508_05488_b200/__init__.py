@@ -92,11 +92,13 @@ class _Diag(C.Structure):
                 ("t_d2h_ms", C.c_double), ("t_host_ms", C.c_double),
                 ("spa_path", C.c_int), ("filter_log2nb", C.c_int), ("n_candidates", C.c_size_t),
                 ("t_binscan_ms", C.c_double), ("t_filter_ms", C.c_double),
-                ("t_binsort_ms", C.c_double), ("convex_fast_path", C.c_int), ("pad3_", C.c_int)]
+                ("t_binsort_ms", C.c_double), ("convex_fast_path", C.c_int),
+                ("k1k2_overlapped", C.c_int)]
 
 # chgpu_ctx_set_option (include/chgpu.h)
 OPT_SPA_PATH = 1
 OPT_CHAINS_TAP = 2
+OPT_PDL = 3
 SPA_AUTO, SPA_SORT, SPA_FILTER, SPA_FILTER_SORTED = 0, 1, 2, 3
 
 
@@ -135,6 +137,7 @@ class Diag:
     n_candidates: int = 0
     filter_log2nb: int = 0
     convex_fast_path: bool = False
+    k1k2_overlapped: bool = False  # K2 launched programmatically behind K1: t_k1_ms covers both
 
     @classmethod
     def _from(cls, d: _Diag) -> "Diag":
@@ -143,7 +146,7 @@ class Diag:
                    [int(c) for c in d.region_counts], [int(c) for c in d.kept_counts],
                    bool(d.degenerate_branch), int(d.sort_passes), int(d.tie_runs),
                    int(d.launches), times, int(d.spa_path), int(d.n_candidates),
-                   int(d.filter_log2nb), bool(d.convex_fast_path))
+                   int(d.filter_log2nb), bool(d.convex_fast_path), bool(d.k1k2_overlapped))
 
 
 @dataclass
@@ -308,6 +311,10 @@ class Context:
         SPA_FILTER_SORTED (pre-filter with every chunk through the bin sorts and
         the sorted chunk SPA, the path large chunks take)."""
         self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_SPA_PATH, mode))
+
+    def set_pdl(self, on: bool = True):
+        """CHGPU_OPT_PDL: K2 launched programmatically behind K1 (default)."""
+        self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_PDL, int(bool(on))))
 
     def set_chains_tap(self, on: bool = True):
         """Keep each hull call's SPA chains for last_chains() (parity tap)."""

@@ -249,6 +249,22 @@ __device__ __forceinline__ u32 warp_lookback(const u64* col, size_t stride, int 
 
 // ---------------------------------------------------------------- loads
 
+// Loads of data the previous kernel of a programmatic launch produced, after
+// griddepcontrol.wait: the default cached path (ld.global.ca), as asm
+// volatile so that it stays below the wait. Not ld.global.nc: ptxas hoists
+// those above the wait (the data counts as read-only for the kernel), which
+// reads a stale quad.
+__device__ __forceinline__ double ld_after_wait_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ u32 ld_after_wait_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
@@ -275,20 +291,36 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------------- shared structs
 
 // Device-resident result of the extremes reduction, consumed by the
-// classify kernel without a host round trip.
-struct QuadInfo {
+// classify kernel without a host round trip. Doubles first, 16-byte
+// aligned: K2 reads its constants with 16-byte uniform loads.
+struct __align__(16) QuadInfo {
   double q[8];       // left.x, left.y, bottom.x, bottom.y, right.x, right.y, top.x, top.y
-  u64 idx[4];        // index of each corner (earliest among == ties)
-  u32 frame_size;    // frame_vertices(quad).size()
-  u32 degenerate;    // frame_size <= 2
   // derived once per call (quad_derive)
   double ex[4], ey[4];     // edge c = corner (c + 1) & 3 - corner c (classify's cross products)
   double blo[4], bspan[4]; // SPA bin map of region r + 1: origin and span of its primary
+  double bscale[4];        // ... and its scale (bin_scale of bspan at the call's bin count)
+  u64 idx[4];        // index of each corner (earliest among == ties)
+  u32 frame_size;    // frame_vertices(quad).size()
+  u32 degenerate;    // frame_size <= 2
 };
 
-// Fills QuadInfo's derived fields from q (host and device: IEEE subtracts,
-// so both sides derive the same bits).
-__host__ __device__ inline void quad_derive(QuadInfo& qi) {
+// The bin scale nb / span of a region (0 for a null, negative or denormal
+// span: every record then falls in one bin). IEEE division on both sides,
+// so host and device derive the same bits.
+__host__ __device__ __forceinline__ double bin_scale(double span, int log2nb) {
+#ifdef __CUDA_ARCH__
+  double s = span > 0.0 ? __ddiv_rn((double)(1u << log2nb), span) : 0.0;
+#else
+  double s = span > 0.0 ? (double)(1u << log2nb) / span : 0.0;
+#endif
+  if (!(s < 1e300)) s = 0.0;  // inf / nan
+  return s;
+}
+
+// Fills QuadInfo's derived fields from q (host and device: IEEE subtracts
+// and divides, so both sides derive the same bits); log2nb = SPA bins per
+// region of the call (0 when no bins are used).
+__host__ __device__ inline void quad_derive(QuadInfo& qi, int log2nb) {
   for (int c = 0; c < 4; ++c) {
     const int d = (c + 1) & 3;
     qi.ex[c] = qi.q[2 * d] - qi.q[2 * c];
@@ -297,16 +329,8 @@ __host__ __device__ inline void quad_derive(QuadInfo& qi) {
     bin_range(qi.q, c + 1, &lo, &hi);
     qi.blo[c] = lo;
     qi.bspan[c] = hi - lo;
+    qi.bscale[c] = bin_scale(qi.bspan[c], log2nb);
   }
-}
-
-// The bin scale nb / span of a region (0 for a null, negative or denormal
-// span: every record then falls in one bin). Computed once per CTA by each
-// kernel that bins, from the same inputs, so all of them agree.
-__device__ __forceinline__ double bin_scale(double span, int log2nb) {
-  double s = span > 0.0 ? __ddiv_rn((double)(1u << log2nb), span) : 0.0;
-  if (!(s < 1e300)) s = 0.0;  // inf / nan
-  return s;
 }
 
 // Bin of a record of region ri + 1 with primary coordinate p:

@@ -91,7 +91,8 @@ constexpr int kK1Unroll = CHGPU_K1_UNROLL;  // points per lane per warp tile
 // frame_vertices, extremes.cpp:49-57). Ties fall back to the global index,
 // so the result is independent of the merge order.
 __device__ void merge_partials_block(const QuadCand* __restrict__ partials, int nparts,
-                                     QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
+                                     QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out,
+                                     int log2nb) {
   QuadCand acc;
   empty_quad(acc);
   for (int p = threadIdx.x; p < nparts; p += blockDim.x) merge_quad(acc, partials[p]);
@@ -132,7 +133,7 @@ __device__ void merge_partials_block(const QuadCand* __restrict__ partials, int 
       if (k > 1 && qi.q[0] == lx && qi.q[1] == ly) --k;
       qi.frame_size = k;
       qi.degenerate = k <= 2 ? 1u : 0u;
-      quad_derive(qi);
+      quad_derive(qi, log2nb);
       *out = qi;
     }
   }
@@ -150,7 +151,10 @@ template <bool kCheck>
 __global__ __launch_bounds__(kK1Threads, CHGPU_K1_MINB) void k_extremes_partial(
     const double2* __restrict__ pts, u64 n, u64 base_index, QuadCand* __restrict__ partials,
     u32 part_base, u32* __restrict__ ticket, u32 total_parts, QuadInfo* __restrict__ out,
-    u32* __restrict__ nonfinite) {
+    u32* __restrict__ nonfinite, int log2nb) {
+  // a programmatically launched K2 may start as K1's CTAs retire (it waits
+  // for K1's completion before reading the quad)
+  asm volatile("griddepcontrol.launch_dependents;");
   QuadCand acc;
   empty_quad(acc);
   bool finite = true;
@@ -204,13 +208,13 @@ __global__ __launch_bounds__(kK1Threads, CHGPU_K1_MINB) void k_extremes_partial(
   __syncthreads();
   if (s_last) {
     __threadfence();
-    merge_partials_block(partials, (int)total_parts, out, nullptr);
+    merge_partials_block(partials, (int)total_parts, out, nullptr, log2nb);
   }
 }
 
 __global__ __launch_bounds__(1024) void k_extremes_final(const QuadCand* __restrict__ partials, int nparts,
                                  QuadInfo* __restrict__ out, QuadCand* __restrict__ raw_out) {
-  merge_partials_block(partials, nparts, out, raw_out);
+  merge_partials_block(partials, nparts, out, raw_out, 0);
 }
 
 // ------------------------------------------------------------------ K2
@@ -416,21 +420,27 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     const u32 idx = base + j * 32 + lane;
     p[j] = idx < n ? ldg_stream(pts + idx) : make_double2(0.0, 0.0);
   }
+  // (launched programmatically behind K1: the point loads above are in
+  // flight; K1's quad is complete and visible past this point)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // the quad's edges by uniform loads (one transaction per warp, L1 hits
   // after the first warp), the bin map of region `lane` in lanes 0..3 into
   // the warp's own table: no CTA barrier between the point loads and the
   // classification
+  // (K1 may still be running when this CTA starts: its output is read with
+  // ordinary cached loads kept below the wait, not as read-only data)
   QuadEdges e;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    e.ax[c] = __ldg(&qinfo->q[2 * c]);
-    e.ay[c] = __ldg(&qinfo->q[2 * c + 1]);
-    e.ex[c] = __ldg(&qinfo->ex[c]);
-    e.ey[c] = __ldg(&qinfo->ey[c]);
+    e.ax[c] = ld_after_wait_f64(&qinfo->q[2 * c]);
+    e.ay[c] = ld_after_wait_f64(&qinfo->q[2 * c + 1]);
+    e.ex[c] = ld_after_wait_f64(&qinfo->ex[c]);
+    e.ey[c] = ld_after_wait_f64(&qinfo->ey[c]);
   }
-  const bool lex = __ldg(&qinfo->degenerate) != 0;
+  const bool lex = ld_after_wait_u32(&qinfo->degenerate) != 0;
+  // (the bin map's scale comes precomputed: quad_derive at the call's bin count)
   if (lane < 4)
-    s_bmap[warp][lane] = make_double2(__ldg(&qinfo->blo[lane]), bin_scale(__ldg(&qinfo->bspan[lane]), log2nb));
+    s_bmap[warp][lane] = make_double2(ld_after_wait_f64(&qinfo->blo[lane]), ld_after_wait_f64(&qinfo->bscale[lane]));
 
   u32 codes = 0;  // 3 bits of stream id per item
   u32 cnt = 0;    // survivors of this lane
@@ -581,14 +591,16 @@ int extremes_wave(int sms) {
 
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
                             int blocks, cudaStream_t st, u32 part_base, u32* ticket,
-                            u32 total_parts, QuadInfo* out, u32* nonfinite) {
+                            u32 total_parts, QuadInfo* out, u32* nonfinite, int log2nb) {
   blocks = extremes_blocks(blocks);
   if (nonfinite)
     k_extremes_partial<true><<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base,
-                                                            ticket, total_parts, out, nonfinite);
+                                                            ticket, total_parts, out, nonfinite,
+                                                            log2nb);
   else
     k_extremes_partial<false><<<blocks, kK1Threads, 0, st>>>(pts, n, base_index, partials, part_base,
-                                                             ticket, total_parts, out, nullptr);
+                                                             ticket, total_parts, out, nullptr,
+                                                             log2nb);
   return blocks;
 }
 
@@ -613,12 +625,21 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
 
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
                                u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
-                               u32* bcnt, u32* bw, u32 wmask, cudaStream_t st) {
+                               u32* bcnt, u32* bw, u32 wmask, bool programmatic, cudaStream_t st) {
   constexpr u32 tile = kK2Threads / 32 * kSegPts;  // one segment per warp
   const u32 tiles = (n + tile - 1) / tile;
   if (tiles == 0) return;
-  k_classify_survivors<<<tiles, kK2Threads, 0, st>>>(pts, n, qinfo, seg, segidx, segcnt, kbuf, vbuf,
-                                                     counts_out, log2nb, bcnt, bw, wmask);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles);
+  cfg.blockDim = dim3(kK2Threads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = programmatic ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_classify_survivors, pts, n, qinfo, seg, segidx, segcnt, kbuf, vbuf,
+                     counts_out, log2nb, bcnt, bw, wmask);
 }
 
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,

@@ -92,7 +92,7 @@ int extremes_wave(int sms);
 int launch_extremes_partial(const double2* pts, u64 n, u64 base_index, QuadCand* partials,
                             int blocks, cudaStream_t st, u32 part_base = 0,
                             u32* ticket = nullptr, u32 total_parts = 0, QuadInfo* out = nullptr,
-                            u32* nonfinite = nullptr);
+                            u32* nonfinite = nullptr, int log2nb = 0);
 void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out, QuadCand* raw_out,
                            cudaStream_t st);
 // K2
@@ -101,8 +101,8 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              u64 ncap, u32* counts_out, cudaStream_t st);
 // K2 of the pre-filtered path: raw survivor points + bin statistics.
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
-                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out,
-                               int log2nb, u32* bcnt, u32* bw, u32 wmask, cudaStream_t st);
+                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+                               u32* bcnt, u32* bw, u32 wmask, bool programmatic, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,
                             cudaStream_t st);

@@ -152,6 +152,7 @@ struct chgpu_ctx {
   size_t ffirst_cap = 0;
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
   bool chains_tap = false;   // CHGPU_OPT_CHAINS_TAP
+  bool pdl = true;           // CHGPU_OPT_PDL: K2 launched programmatically behind K1
   std::vector<Pt> tap;       // the last call's chains (tap on)
   size_t tap_counts[4] = {0, 0, 0, 0};
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
@@ -920,6 +921,19 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   TRY(begin_call(ctx));
   ctx->tap.clear();
   for (auto& c : ctx->tap_counts) c = 0;
+  // Which SPA path (decided before K1: K2 follows K1 with no stream
+  // operation in between, so it can launch programmatically)
+  bool want_filter =
+      chunk_count >= 1 &&
+      (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ||
+       (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
+  int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
+  // the bin scan is one cooperative launch: every CTA must be resident
+  if (want_filter && bin_scan_blocks(log2nb) > (u32)device_limits().binscan_coop) {
+    want_filter = false;
+    log2nb = 0;
+  }
+  if (want_filter) TRY(ftab_prepare(ctx, log2nb, st));
   CK(cudaEventRecord(ctx->ev[0], st));
   // a call like the last one will reach the split finisher in a few hundred
   // microseconds: its worker threads spin instead of parking
@@ -988,7 +1002,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       nparts += launch_extremes_partial(ctx->d_pts + off, cnt, off, ctx->d_partials, blocks, st,
                                         (u32)nparts, ctx->d_ctr + ticket, total_parts,
                                         ctx->d_qinfo,
-                                        from_file ? ctx->d_ctr + nonfinite_slot : nullptr);
+                                        from_file ? ctx->d_ctr + nonfinite_slot : nullptr, log2nb);
       ++ctx->launches;
     }
     CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
@@ -997,26 +1011,18 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     const int ticket = take_ctr(ctx);
     nparts = launch_extremes_partial(pts_dev, n, 0, ctx->d_partials, blocks, st, 0,
                                      ctx->d_ctr + ticket, (u32)extremes_blocks(blocks),
-                                     ctx->d_qinfo);
+                                     ctx->d_qinfo, nullptr, log2nb);
     ++ctx->launches;
   }
   const double2* pts = (h_src || from_file) ? ctx->d_pts : pts_dev;
-  CK(cudaEventRecord(ctx->ev[1], st));
+  // K2 on the filter path launches programmatically right behind K1 (its
+  // CTAs load their points while K1's last block merges the quad): no
+  // event between them, the two are timed together
+  const bool pdl = want_filter && ctx->pdl;
+  if (!pdl) CK(cudaEventRecord(ctx->ev[1], st));
 
   // ---- K2: classify + round-1 discard (classify.cpp:9-87), plus the SPA
   // pre-filter's per-bin statistics when that path is taken.
-  bool want_filter =
-      chunk_count >= 1 &&
-      (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ||
-       (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
-  int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
-  // the bin scan is one cooperative launch: every CTA must be resident
-  if (want_filter && bin_scan_blocks(log2nb) > (u32)device_limits().binscan_coop) {
-    want_filter = false;
-    log2nb = 0;
-  }
-  if (want_filter)
-    TRY(ftab_prepare(ctx, log2nb, st));
   const FilterTabs ftabs = filter_tabs(ctx, log2nb);
   const int cnt_slot = ctx->ctr_used;
   ctx->ctr_used += 5;
@@ -1026,7 +1032,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
                               reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
                               ctx->d_kbuf, ctx->d_vbuf,
-                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
+                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), pdl,
+                              st);
   } else {
     launch_classify_compact(pts, (u32)n, ctx->d_qinfo, nullptr, 0, ctx->d_kbuf, ctx->d_vbuf,
                             ctx->cap, ctx->d_ctr + cnt_slot, st);
@@ -1232,14 +1239,22 @@ finished:
   const auto t_end = std::chrono::steady_clock::now();
 
   S.n_hull = ctx->hull_n;
-  S.t_extremes_ms = ms_between(ctx->ev[0], ctx->ev[1]);
-  S.t_classify_ms = ms_between(ctx->ev[1], ctx->ev[2]);
+  if (pdl) {
+    // K1 and K2 overlap (programmatic launch): one interval for both, the
+    // discard stage, reported as extremes + classify
+    S.t_extremes_ms = ms_between(ctx->ev[0], ctx->ev[2]);
+    S.t_classify_ms = 0.0;
+  } else {
+    S.t_extremes_ms = ms_between(ctx->ev[0], ctx->ev[1]);
+    S.t_classify_ms = ms_between(ctx->ev[1], ctx->ev[2]);
+  }
+  D.k1k2_overlapped = pdl ? 1 : 0;
   S.t_partition_ms = 0.0;
   S.t_sort_ms = t_sort_ms;
   S.t_spa_ms = t_spa_ms;
   S.t_melkman_ms = std::chrono::duration<double, std::milli>(t_end - t_fin0).count();
   S.t_total_ms = std::chrono::duration<double, std::milli>(t_end - t_wall0).count();
-  D.t_k1_ms = S.t_extremes_ms;
+  D.t_k1_ms = S.t_extremes_ms;  // (K1 + K2 when k1k2_overlapped)
   D.t_k2_ms = S.t_classify_ms;
   if (h_src || from_file) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
   D.launches = ctx->launches;
@@ -1257,7 +1272,7 @@ int upload_points(chgpu_ctx* ctx, const double* xy, size_t n) {
   return CHGPU_OK;
 }
 
-int upload_quad(chgpu_ctx* ctx, const double* quad) {
+int upload_quad(chgpu_ctx* ctx, const double* quad, int log2nb = 0) {
   QuadInfo qi{};
   std::memcpy(qi.q, quad, sizeof qi.q);
   Pt fr[4];
@@ -1265,7 +1280,7 @@ int upload_quad(chgpu_ctx* ctx, const double* quad) {
   frame_of(quad, fr, &nf);
   qi.frame_size = (u32)nf;
   qi.degenerate = nf <= 2;
-  quad_derive(qi);
+  quad_derive(qi, log2nb);
   ctx->h->qi = qi;
   TRY(upload(ctx, ctx->d_qinfo, &ctx->h->qi, sizeof(QuadInfo)));
   return CHGPU_OK;
@@ -1340,6 +1355,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
     return CHGPU_CUDA_ERR;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  if (const char* e = std::getenv("CHGPU_PDL")) ctx->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("CHGPU_SPA")) {
     if (std::strcmp(e, "sort") == 0) ctx->spa_mode = CHGPU_SPA_SORT;
     if (std::strcmp(e, "filter") == 0) ctx->spa_mode = CHGPU_SPA_FILTER;
@@ -1401,6 +1417,10 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
     case CHGPU_OPT_CHAINS_TAP:
       if (value != 0 && value != 1) break;
       ctx->chains_tap = value != 0;
+      return CHGPU_OK;
+    case CHGPU_OPT_PDL:
+      if (value != 0 && value != 1) break;
+      ctx->pdl = value != 0;
       return CHGPU_OK;
     default:
       break;
@@ -1708,14 +1728,14 @@ int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double
   TRY(ensure_cap(ctx, n));
   cudaStream_t st = ctx->st;
   TRY(begin_call(ctx));
-  TRY(upload_quad(ctx, quad));
+  const int log2nb = filter_bits(n, chunk_count);
+  TRY(upload_quad(ctx, quad, log2nb));
   const bool degenerate = ctx->h->qi.degenerate != 0;
   const double2* pts = reinterpret_cast<const double2*>(d_xy);
   if (!degenerate && chunk_count >= 1 && ctx->spa_mode != CHGPU_SPA_SORT &&
       (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED || chunk_count <= n / 64)) {
     // The pre-filtered SPA against the global quad (the same kernels as
     // chgpu_hull), falling back to the full region sort on overflow.
-    const int log2nb = filter_bits(n, chunk_count);
     TRY(ftab_prepare(ctx, log2nb, st));
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
@@ -1723,7 +1743,8 @@ int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double
     launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
                               reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
                               ctx->d_kbuf, ctx->d_vbuf,
-                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), st);
+                              ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), false,
+                              st);
     CK(cudaGetLastError());
     int ovf_slot = -1;
     TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
