@@ -445,12 +445,23 @@ def main():
         # sort path
         surv_b = 12 if d.spa_path == 1 else 16
         disc_ms = t["t_k1_ms"] + t["t_k2_ms"]
-        kernels = {
-            "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n, "basis": "16 B/pt read"},
-            ("k2_classify_survivors" if d.spa_path == 1 else "k2_classify_compact"):
-                {"ms": t["t_k2_ms"], "bytes": 16 * n + surv_b * s1,
-                 "basis": f"16 B/pt read + {surv_b} B/survivor write"},
-        }
+        if d.k1k2_overlapped:
+            # K2 launched programmatically behind K1 (its CTAs start while
+            # K1's last block merges the quad): one CUDA-event interval for
+            # the discard stage
+            kernels = {
+                "k1k2_discard": {"ms": t["t_k1_ms"], "bytes": 32 * n + surv_b * s1,
+                                 "basis": f"K1 16 B/pt read + K2 16 B/pt read + {surv_b} B/survivor "
+                                          "write (k_extremes_partial + k_classify_survivors, "
+                                          "programmatically overlapped)"},
+            }
+        else:
+            kernels = {
+                "k1_extremes": {"ms": t["t_k1_ms"], "bytes": 16 * n, "basis": "16 B/pt read"},
+                ("k2_classify_survivors" if d.spa_path == 1 else "k2_classify_compact"):
+                    {"ms": t["t_k2_ms"], "bytes": 16 * n + surv_b * s1,
+                     "basis": f"16 B/pt read + {surv_b} B/survivor write"},
+            }
         if d.spa_path == 1:
             nc = d.n_candidates
             kernels.update({
@@ -460,12 +471,11 @@ def main():
                               "basis": "8 B/survivor key read + per candidate 4 B index "
                                        "+ 16 B point read, 16 B record write",
                               "candidates": nc},
-                "k3_bin_sort": {"ms": t["t_binsort_ms"],
-                                "basis": "bins above 32 candidates sorted in place"},
-                "k4_spa_chunks_emit": {"ms": t["t_spa_kernel_ms"],
-                                       "bytes": 16 * nc + 32 * sum(d.kept_counts),
-                                       "basis": "16 B/candidate read + 16 B/kept scratch "
-                                                "+ 16 B/kept point write"},
+                "k4_chunk_spa": {"ms": t["t_spa_kernel_ms"],
+                                 "bytes": 16 * nc + 32 * sum(d.kept_counts),
+                                 "basis": "k_spa_small + k_spa_finish: 16 B/candidate read "
+                                          "+ 16 B/kept scratch + 16 B/kept point write",
+                                 "of_which_finish_ms": t["t_binsort_ms"]},
             })
         else:
             pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)
@@ -495,7 +505,8 @@ def main():
             "traffic": measured_traffic(dom_name),
             "algorithmic_bytes": f"{dom.get('basis', 'bytes moved')}: {dom['bytes']} B per launch",
             "discard_kernels": {
-                "kernels": "k_extremes_partial (+ last-block merge), k_classify_survivors",
+                "kernels": "k_extremes_partial (+ last-block merge), k_classify_survivors"
+                           + (" (programmatically overlapped)" if d.k1k2_overlapped else ""),
                 "basis": "SURVEY 8(d): 32 B/pt + 16 B/survivor",
                 "bytes": disc_bytes, "ms": disc_ms,
                 "achieved": disc_bytes / (disc_ms * 1e-3) / 1e9,
