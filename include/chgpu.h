@@ -92,6 +92,8 @@ typedef struct {
   double t_binsort_ms;      /* pre-filter: sort of bins above 32 candidates */
   int convex_fast_path;     /* 1: Melkman's all-kept trajectory verified on the GPU (k_convex.cu) */
   int k1k2_overlapped;      /* 1: K2 launched programmatically behind K1; t_k1_ms covers both */
+  double t_host_enqueue_ms; /* host: call entry until the device work is enqueued */
+  double t_host_wait_ms;    /* host: blocked until the counters (and small chains) are back */
 } chgpu_diag;
 
 /* Options (chgpu_ctx_set_option). */

@@ -93,7 +93,8 @@ class _Diag(C.Structure):
                 ("spa_path", C.c_int), ("filter_log2nb", C.c_int), ("n_candidates", C.c_size_t),
                 ("t_binscan_ms", C.c_double), ("t_filter_ms", C.c_double),
                 ("t_binsort_ms", C.c_double), ("convex_fast_path", C.c_int),
-                ("k1k2_overlapped", C.c_int)]
+                ("k1k2_overlapped", C.c_int), ("t_host_enqueue_ms", C.c_double),
+                ("t_host_wait_ms", C.c_double)]
 
 # chgpu_ctx_set_option (include/chgpu.h)
 OPT_SPA_PATH = 1

@@ -1064,7 +1064,11 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   ++ctx->launches;
   CK(cudaGetLastError());
   if (want_filter) CK(cudaEventRecord(ctx->ev[9], st));
+  const auto t_enq = std::chrono::steady_clock::now();
   TRY(sync(ctx));
+  D.t_host_enqueue_ms = std::chrono::duration<double, std::milli>(t_enq - t_wall0).count();
+  D.t_host_wait_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq).count();
   if (want_filter) TRY(ftab_clear_behind(ctx));  // K2 and the filter path are done with them
   // read_points rejects the file before convex_hull runs (io.cpp:38-42)
   if (from_file && ctx->h->ctr[nonfinite_slot])
