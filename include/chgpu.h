@@ -197,6 +197,15 @@ int chgpu_melkman(const double* poly, size_t n, double* out, size_t* n_out);
 int chgpu_finish_chains(const double* chains, const size_t* kept_counts, const double* quad,
                         double* out, size_t* n_out);
 
+/* The hull of the union of several runs of SPA chains against one quad
+ * (a run = one shard's 4 region chains concatenated, kept_counts[4 * k +
+ * r]): each region's runs merged in region order (region_less, spa.cpp:38-52),
+ * then assemble_polygon + melkman as chgpu_finish_chains. The multi-GPU
+ * merge of a non-degenerate frame (every hull vertex of the whole set is in
+ * some shard's chains). Host only. */
+int chgpu_merge_hull(const double* const* runs, const size_t* kept_counts, int nruns,
+                     const double* quad, double* out, size_t* n_out);
+
 /* Counters of the split finisher (finisher.cpp finish_chains_split: chains
  * 1-4 run concurrently and are verified before use): calls that took it,
  * and calls whose checks fell back to the sequential pass. Diagnostics. */

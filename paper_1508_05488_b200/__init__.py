@@ -214,6 +214,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         L.chgpu_hull.argtypes = hull_args
         L.chgpu_hull_device.argtypes = hull_args
         L.chgpu_device_count.argtypes = []
+        L.chgpu_merge_hull.argtypes = [C.POINTER(_dp), _sz, C.c_int, _dp, _dp, _sz]
         L.chgpu_hull_sharded.argtypes = [C.POINTER(vp), C.c_int, C.POINTER(_dp), _sz, C.c_int,
                                          C.c_int, C.c_size_t, C.c_int, C.POINTER(_dp), _sz,
                                          C.POINTER(_Stats)]
@@ -571,6 +572,26 @@ def assemble_polygon(chains, kept_counts, quad) -> np.ndarray:
     st = L.chgpu_assemble_polygon(_p(a), kc, _p(q), _p(out), C.byref(k))
     if st:
         _raise(st, "assemble_polygon: fewer than 3 distinct vertices")
+    return out[:k.value]
+
+
+def merge_hull(runs, quad) -> np.ndarray:
+    """chgpu_merge_hull: the hull of the union of several runs of SPA chains
+    against one (non-degenerate) quad; runs = [(chains (k, 2), kept_counts[4])]."""
+    L = load_library()
+    arrs = [_pts(c) for c, _ in runs]
+    kcs = []
+    for a, (_, kc) in zip(arrs, runs):
+        kcs.extend(list(_kept_counts(kc, len(a))))
+    total = sum(len(a) for a in arrs)
+    parr = (_dp * len(arrs))(*[_p(a) for a in arrs])
+    carr = (C.c_size_t * len(kcs))(*kcs)
+    q = np.ascontiguousarray(np.asarray(quad, np.float64).reshape(8))
+    out = np.empty((total + 4, 2), np.float64)
+    k = C.c_size_t()
+    st = L.chgpu_merge_hull(parr, carr, len(arrs), _p(q), _p(out), C.byref(k))
+    if st:
+        _raise(st, "merge_hull: degenerate polygon")
     return out[:k.value]
 
 

@@ -860,6 +860,65 @@ extern "C" int chgpu_assemble_polygon(const double* chains, const size_t* kept_c
   return st;
 }
 
+namespace chgpu {
+namespace host {
+
+// region_less (spa.cpp:38-52) on points, with == ties (the chains' order).
+static inline bool region_before(int region, const Pt& a, const Pt& b) {
+  switch (region) {
+    case 1: return a.x < b.x || (a.x == b.x && a.y > b.y);  // LL: x asc, y desc
+    case 2: return a.y < b.y || (a.y == b.y && a.x < b.x);  // LR: y asc, x asc
+    case 3: return a.x > b.x || (a.x == b.x && a.y < b.y);  // UR: x desc, y asc
+    default: return a.y > b.y || (a.y == b.y && a.x > b.x); // UL: y desc, x desc
+  }
+}
+
+int merge_chains_hull(const Pt* const* runs, const size_t* counts4, int nruns, const Pt corners[4],
+                      std::vector<Pt>& hull) {
+  // per region, the runs' chains (each sorted in region order) merged into
+  // one sorted chain, ties to the earlier run
+  size_t total[4] = {0, 0, 0, 0};
+  for (int k = 0; k < nruns; ++k)
+    for (int r = 0; r < 4; ++r) total[r] += counts4[4 * k + r];
+  finisher_prewake(total[0] + total[1] + total[2] + total[3]);  // (workers wake during the merge)
+  if (nruns == 1) return finish_chains_split(runs[0], total, corners, hull);
+  std::vector<Pt> merged(total[0] + total[1] + total[2] + total[3]);
+  std::vector<size_t> pos(nruns);
+  std::vector<const Pt*> start(nruns);
+  for (int k = 0; k < nruns; ++k) start[k] = runs[k];
+  Pt* out = merged.data();
+  for (int r = 0; r < 4; ++r) {
+    for (int k = 0; k < nruns; ++k) pos[k] = 0;
+    for (size_t i = 0; i < total[r]; ++i) {
+      int best = -1;
+      for (int k = 0; k < nruns; ++k) {
+        if (pos[k] == counts4[4 * k + r]) continue;
+        if (best < 0 || region_before(r + 1, start[k][pos[k]], start[best][pos[best]])) best = k;
+      }
+      *out++ = start[best][pos[best]++];
+    }
+    for (int k = 0; k < nruns; ++k) start[k] += counts4[4 * k + r];
+  }
+  return finish_chains_split(merged.data(), total, corners, hull);
+}
+
+}  // namespace host
+}  // namespace chgpu
+
+extern "C" int chgpu_merge_hull(const double* const* runs, const size_t* kept_counts, int nruns,
+                                const double* quad, double* out, size_t* n_out) {
+  std::vector<Pt> hull;
+  const int st = chgpu::host::merge_chains_hull(reinterpret_cast<const Pt* const*>(runs), kept_counts,
+                                                nruns, reinterpret_cast<const Pt*>(quad), hull);
+  if (st) {
+    *n_out = 0;
+    return st;
+  }
+  std::memcpy(out, hull.data(), hull.size() * sizeof(Pt));
+  *n_out = hull.size();
+  return 0;
+}
+
 extern "C" int chgpu_finish_chains(const double* chains, const size_t* kept_counts,
                                    const double* quad, double* out, size_t* n_out) {
   std::vector<Pt> hull;

@@ -1931,6 +1931,8 @@ int chgpu_hull_sharded(chgpu_ctx* const* ctxs, int nctx, const double* const* sh
   // (every dropped point lies inside the global quad or inside a triangle
   // of kept points and global anchors, so no hull vertex is lost); each
   // context appends its slices' chains to its device store
+  // (per slice: where its chains sit in its context's store, and its region counts)
+  std::vector<size_t> run_off(slices.size(), 0), run_kc(4 * slices.size(), 0);
   TRY(for_each_ctx(nctx, [&](int i) -> int {
     chgpu_ctx* ctx = ctxs[i];
     cudaSetDevice(ctx->device);
@@ -1946,20 +1948,66 @@ int chgpu_hull_sharded(chgpu_ctx* const* ctxs, int nctx, const double* const* sh
       if (k)
         CK(cudaMemcpyAsync(ctx->d_store + ctx->store_n, ctx->d_kept, k * sizeof(double2),
                            cudaMemcpyDeviceToDevice, ctx->st));
+      run_off[j] = ctx->store_n;
+      for (int r = 0; r < 4; ++r) run_kc[4 * j + r] = kc[r];
       ctx->store_n += k;
     }
     return sync(ctx);
   }));
 
-  // exchange 2: the chains to the first context's device (peer copies over
-  // NVLink), plus the frame; then the single-GPU pipeline over the union:
-  // the hull of the union of chains is the hull of the whole set
-  cudaSetDevice(c0->device);
-  size_t nu = 0;
-  for (int i = 0; i < nctx; ++i) nu += ctxs[i]->store_n;
   Pt fr[4];
   int nf = 0;
   frame_of(quad, fr, &nf);
+  if (nf > 2) {
+    // a proper frame: every hull vertex of the whole set is in some slice's
+    // chains. Each region's runs (one per slice, sorted in region order)
+    // are merged on the host and the ring [L, chain 1, B, ..., chain 4] is
+    // finished with Melkman (chgpu_merge_hull): no second device pipeline.
+    std::vector<std::vector<Pt>> host(nctx);
+    TRY(for_each_ctx(nctx, [&](int i) -> int {
+      chgpu_ctx* ctx = ctxs[i];
+      cudaSetDevice(ctx->device);
+      host[i].resize(ctx->store_n);
+      if (ctx->store_n)
+        CK(cudaMemcpyAsync(host[i].data(), ctx->d_store, ctx->store_n * sizeof(double2),
+                           cudaMemcpyDeviceToHost, ctx->st));
+      return sync(ctx);
+    }));
+    std::vector<const Pt*> runs(slices.size());
+    for (size_t j = 0; j < slices.size(); ++j) runs[j] = host[slices[j].ctx].data() + run_off[j];
+    const auto t_m0 = std::chrono::steady_clock::now();
+    const int mk = chgpu::host::merge_chains_hull(runs.data(), run_kc.data(), (int)slices.size(),
+                                                  reinterpret_cast<const Pt*>(quad), c0->hull);
+    if (mk) return fail(c0, CHGPU_DEGENERATE, "assemble_polygon/melkman: degenerate polygon");
+    c0->hull_ptr = c0->hull.data();
+    c0->hull_n = c0->hull.size();
+    *hull_xy = reinterpret_cast<const double*>(c0->hull_ptr);
+    *n_hull = c0->hull_n;
+    if (stats) {
+      // n_input and n_hull are the whole set's; n_after_spa counts the
+      // shards' chains + frame (a sharded run's stage counters are not
+      // comparable with a single-process run)
+      chgpu_stats S{};
+      S.n_input = total;
+      size_t kept = 0;
+      for (size_t x : run_kc) kept += x;
+      S.n_after_spa = kept + (size_t)nf;
+      S.n_hull = c0->hull_n;
+      const auto t_end = std::chrono::steady_clock::now();
+      S.t_melkman_ms = std::chrono::duration<double, std::milli>(t_end - t_m0).count();
+      S.t_total_ms = std::chrono::duration<double, std::milli>(t_end - t_wall0).count();
+      *stats = S;
+    }
+    return CHGPU_OK;
+  }
+
+  // A degenerate frame (pipeline.cpp:53-71): each slice left its sorted
+  // unique survivors; they go to the first context's device (peer copies
+  // over NVLink) with the frame, and the single-GPU pipeline's degenerate
+  // branch runs over that union
+  cudaSetDevice(c0->device);
+  size_t nu = 0;
+  for (int i = 0; i < nctx; ++i) nu += ctxs[i]->store_n;
   TRY(grow(c0, &c0->d_union, &c0->union_cap, nu + 4, 0));
   size_t off = 0;
   for (int i = 0; i < nctx; ++i) {

@@ -9,9 +9,12 @@ exchanges over torch.distributed (NCCL on GPUs, gloo in the CPU tests):
 2. each rank runs round-1 discard, region sort and SPA of its shard against
    that global quad (every dropped point lies inside the global quad or
    inside a triangle of kept points and global anchors, so no hull vertex is
-   lost), then the chains are gathered on rank 0, which finishes with the
-   single-GPU pipeline over (union of chains) + frame: the hull of the union
-   is the hull of the whole set.
+   lost), then the chains are gathered on rank 0: each region's chains from
+   all ranks merged in region order (they are sorted runs), the ring
+   assembled with the global frame and Melkman run on it on the host
+   (chgpu_merge_hull) — the hull of the union is the hull of the whole set.
+   A degenerate frame (the reference's sort-based branch) finishes with the
+   single-GPU pipeline over (union of the ranks' unique survivors) + frame.
 
 The per-rank compute is behind `ShardOps` so the exchange logic is tested
 with the gloo backend on CPU (tests/test_sharded.py) and runs the sm_100a
@@ -75,8 +78,16 @@ class ShardOps:
     def extremes(self):  # -> (quad (4, 2), global indices (4,))
         raise NotImplementedError
 
-    def chains(self, quad: np.ndarray, chunk_count: int):  # -> (k, 2) kept points
+    def chains(self, quad: np.ndarray, chunk_count: int):
+        """-> ((k, 2) kept points: the 4 region chains concatenated, or on a
+        degenerate frame the sorted unique survivors; kept counts[4])."""
         raise NotImplementedError
+
+    def merge(self, runs, quad: np.ndarray) -> np.ndarray:  # -> hull vertices
+        """Hull of the union of the ranks' chain runs ((chains, counts[4]) on
+        the host), non-degenerate frame."""
+        from . import merge_hull
+        return merge_hull(runs, quad)
 
     def finish(self, points: np.ndarray, chunk_count: int) -> np.ndarray:  # -> hull vertices
         raise NotImplementedError
@@ -102,7 +113,7 @@ class GpuShardOps(ShardOps):
             self.out = torch.empty((max(n, 1), 2), dtype=torch.float64, device=self.t.device)
         kc = self.ctx.shard_chains_device(self.t.data_ptr(), n, quad, chunk_count,
                                           self.out.data_ptr(), self.out.shape[0])
-        return self.out[: sum(kc)]
+        return self.out[: sum(kc)], [int(c) for c in kc]
 
     def finish(self, points, chunk_count):
         from . import PipelineConfig
@@ -116,6 +127,22 @@ class GpuShardOps(ShardOps):
         return self.ctx.convex_hull(points, cfg).hull.vertices
 
 
+_CTRL_GROUPS = {}
+
+
+def _ctrl_group(group):
+    """A gloo group beside an NCCL one for the two small control exchanges
+    (12 doubles, 5 counts per rank): host tensors, no device round trips.
+    Created collectively on first use."""
+    if dist.get_backend(group) != "nccl":
+        return group
+    key = id(group)
+    if key not in _CTRL_GROUPS:
+        ranks = None if group is None else dist.get_process_group_ranks(group)
+        _CTRL_GROUPS[key] = dist.new_group(ranks=ranks, backend="gloo")
+    return _CTRL_GROUPS[key]
+
+
 def _device_for(group) -> torch.device:
     backend = dist.get_backend(group)
     if backend == "nccl":
@@ -127,33 +154,37 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
     """Returns the global hull on rank 0 (None elsewhere)."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = _device_for(group)
+    ctrl = _ctrl_group(group)  # host-side exchanges of the small control data
 
     # exchange 1: extreme candidates (8 coords + 4 indices; indices < 2^53
     # travel exactly as float64)
     q, idx = ops.extremes()
-    mine = torch.tensor(np.concatenate([np.asarray(q, np.float64).reshape(8),
-                                        np.asarray(idx, np.float64)]), dtype=torch.float64,
-                        device=dev)
+    mine = torch.from_numpy(np.concatenate([np.asarray(q, np.float64).reshape(8),
+                                            np.asarray(idx, np.float64)]))
     allq = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(allq, mine, group=group)
-    arr = torch.stack(allq).cpu().numpy()
+    dist.all_gather(allq, mine, group=ctrl)
+    arr = torch.stack(allq).numpy()
     quad = fold_extremes(arr[:, :8], arr[:, 8:].astype(np.int64))
 
     # per-rank discard + sort + SPA against the global quad (a CUDA tensor
     # from GpuShardOps, numpy from the CPU ops of the tests)
-    ch = ops.chains(quad, chunk_count)
+    ch, kc = ops.chains(quad, chunk_count)
     ch = (ch if isinstance(ch, torch.Tensor)
           else torch.from_numpy(np.ascontiguousarray(ch, np.float64))).reshape(-1, 2)
 
-    # exchange 2: chains to rank 0 (sizes first, then padded payloads)
-    cnt = torch.tensor([ch.shape[0]], dtype=torch.int64, device=dev)
+    # exchange 2: chains to rank 0 (sizes and region counts first, then
+    # padded payloads)
+    cnt = torch.tensor([ch.shape[0]] + list(kc), dtype=torch.int64)
     counts = [torch.empty_like(cnt) for _ in range(world)]
-    dist.all_gather(counts, cnt, group=group)
-    counts = [int(c.item()) for c in counts]
-    width = max(max(counts), 1)
-    buf = torch.zeros((width, 2), dtype=torch.float64, device=dev)
-    if ch.shape[0]:
-        buf[: ch.shape[0]] = ch.to(dev)
+    dist.all_gather(counts, cnt, group=ctrl)
+    counts = [[int(x) for x in c.tolist()] for c in counts]
+    width = max(max(c[0] for c in counts), 1)
+    if ch.shape[0] == width and ch.device == dev and ch.is_contiguous():
+        buf = ch  # (the widest rank sends its chains as they are)
+    else:
+        buf = torch.empty((width, 2), dtype=torch.float64, device=dev)  # rows past a rank's count are never read
+        if ch.shape[0]:
+            buf[: ch.shape[0]] = ch.to(dev)
     gathered = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
     if dist.get_backend(group) == "nccl":
         # NCCL gather: emulate with all_gather (the payload is tiny)
@@ -164,6 +195,12 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
         dist.gather(buf, gathered, dst=0, group=group)
     if rank != 0:
         return None
+    if len(frame_vertices(quad)) > 2:
+        # each region's sorted runs merged, the ring closed with the global
+        # frame, Melkman on the host (the chains are ~35K points per rank)
+        runs = [(g[: c[0]].cpu().numpy() if g.is_cuda else g[: c[0]].numpy(), c[1:])
+                for g, c in zip(gathered, counts)]
+        return ops.merge(runs, quad)
     frame = torch.from_numpy(frame_vertices(quad)).to(dev)
-    union = torch.cat([g[:c] for g, c in zip(gathered, counts)] + [frame], dim=0)
+    union = torch.cat([g[: c[0]] for g, c in zip(gathered, counts)] + [frame], dim=0)
     return ops.finish(union.numpy() if dev.type == "cpu" else union, chunk_count)

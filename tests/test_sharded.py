@@ -46,20 +46,25 @@ class OracleShardOps:
         if len(frame_vertices(quad)) <= 2:
             surv = self.p[lab != 0]
             if len(surv) == 0:
-                return surv
+                return surv, [0, 0, 0, 0]
             order = np.lexsort((surv[:, 1], surv[:, 0]))
-            return surv[order]
+            return surv[order], [len(surv), 0, 0, 0]
         out = []
         for r in range(1, 5):
             seg = self.o.sort_region(r, self.p[lab == r])
             anchors = np.array([quad[r - 1], quad[r % 4]])
             out.append(self.o.spa_filter(r, seg, anchors, chunk_count))
-        return np.concatenate(out) if out else np.empty((0, 2))
+        return (np.concatenate(out) if out else np.empty((0, 2))), [len(o) for o in out]
 
     def finish(self, points, chunk_count):
         res = self.o.convex_hull(points, chunk_count)
         assert res.status == 0
         return res.hull
+
+    def merge(self, runs, quad):
+        # the product's host merge (chgpu_merge_hull: no device involved)
+        from paper_1508_05488_b200 import merge_hull
+        return merge_hull(runs, quad)
 
 
 def _worker(rank, world, port, results):
@@ -188,3 +193,22 @@ def test_sharded_hull_nccl_one_rank(oracle):
         for cc in (1, 1024):
             got = np.frombuffer(results[(i, cc)], np.float64).reshape(-1, 2)
             assert np.array_equal(got, want.hull), (dist_name, n, cc)
+
+
+@pytest.mark.parametrize("dist,n", [("uniform_square", 60_000), ("uniform_disk", 50_000),
+                                    ("gaussian", 40_000), ("circle", 3_000)])
+def test_merge_hull_of_shard_chains(oracle, product, dist, n):
+    """chgpu_merge_hull (the rank-0 merge of a non-degenerate frame): each
+    region's runs from 1..8 contiguous shards, SPA'd against the global quad
+    by the reference's stage functions, merged in region order and finished
+    with Melkman = the reference's convex_hull of the whole set."""
+    pts = oracle.generate(dist, n, 3)
+    quad = oracle.find_extremes(pts)
+    for cc in (1, 7, 1024):
+        want = oracle.convex_hull(pts, cc)
+        for k in (1, 2, 5, 8):
+            bounds = np.linspace(0, n, k + 1).astype(int)
+            runs = [OracleShardOps(oracle, pts[bounds[s]:bounds[s + 1]], int(bounds[s])).chains(quad, cc)
+                    for s in range(k)]
+            got = product.merge_hull(runs, quad)
+            assert np.array_equal(got, want.hull), (dist, cc, k)
