@@ -101,8 +101,11 @@ enum {
   CHGPU_OPT_SPA_PATH = 1,   /* value: one of the CHGPU_SPA_* below */
   CHGPU_OPT_CHAINS_TAP = 2, /* value 1: keep each hull call's SPA chains for
                                chgpu_last_chains (a parity tap; costs one D2H) */
-  CHGPU_OPT_PDL = 3         /* value 1 (default): K2 launched programmatically behind
+  CHGPU_OPT_PDL = 3,        /* value 1 (default): K2 launched programmatically behind
                                K1 (overlapped; timed together); 0: separately timed */
+  CHGPU_OPT_STAGE_TIMES = 4 /* value 1: per-kernel CUDA events for chgpu_diag's stage
+                               times (default 0: only the StageStats intervals; each
+                               event query costs ~3 us of host time per call) */
 };
 enum {
   CHGPU_SPA_AUTO = 0,     /* pre-filter when chunks average >= 16 records (default) */

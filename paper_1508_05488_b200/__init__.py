@@ -100,6 +100,7 @@ class _Diag(C.Structure):
 OPT_SPA_PATH = 1
 OPT_CHAINS_TAP = 2
 OPT_PDL = 3
+OPT_STAGE_TIMES = 4
 SPA_AUTO, SPA_SORT, SPA_FILTER, SPA_FILTER_SORTED = 0, 1, 2, 3
 
 
@@ -317,6 +318,11 @@ class Context:
     def set_pdl(self, on: bool = True):
         """CHGPU_OPT_PDL: K2 launched programmatically behind K1 (default)."""
         self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_PDL, int(bool(on))))
+
+    def set_stage_times(self, on: bool = True):
+        """CHGPU_OPT_STAGE_TIMES: per-kernel events for Diag.times_ms (off by
+        default: each event query costs host time on every call)."""
+        self._check(self.lib.chgpu_ctx_set_option(self.h, OPT_STAGE_TIMES, int(bool(on))))
 
     def set_chains_tap(self, on: bool = True):
         """Keep each hull call's SPA chains for last_chains() (parity tap)."""

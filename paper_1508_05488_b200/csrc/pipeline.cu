@@ -153,6 +153,7 @@ struct chgpu_ctx {
   int spa_mode = 0;          // CHGPU_SPA_AUTO / _SORT / _FILTER
   bool chains_tap = false;   // CHGPU_OPT_CHAINS_TAP
   bool pdl = true;           // CHGPU_OPT_PDL: K2 launched programmatically behind K1
+  bool stage_times = false;  // CHGPU_OPT_STAGE_TIMES: per-kernel events (chgpu_diag)
   std::vector<Pt> tap;       // the last call's chains (tap on)
   size_t tap_counts[4] = {0, 0, 0, 0};
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
@@ -766,7 +767,7 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   CK(launch_bin_scan(ctx->d_qinfo, ctx->d_ctr + cnt_slot + 1, chunk_count, log2nb, t.cnt, t.w,
                      ctx->d_plan, ctx->d_fstart, reinterpret_cast<u32*>(ctx->d_fthr), tcoarse,
                      first_bin, aux, ctx->d_ctr + take_ctr(ctx), ctx->d_ctr + *ovf_slot, st));
-  CK(cudaEventRecord(ctx->ev[3], st));
+  if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
   // half of vbuf, each segment's survivor count in its lower part
   launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
@@ -784,13 +785,13 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
                    ctx->d_ck, ctx->d_cv, ctx->d_raw, ctx->d_raw + max_chunks, ctx->d_u64,
                    ctx->d_fdefer, ctx->d_ctr + ndefer_slot,
                    ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ? 0u : kSpaSmallCap, st);
-  CK(cudaEventRecord(ctx->ev[5], st));
+  if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[5], st));
   CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
                        ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
                        ctx->d_ctr + ndefer_slot, ctx->d_ck, ctx->d_cv, ctx->d_raw,
                        ctx->d_raw + max_chunks, ctx->d_u64, ctx->d_kept, ctx->d_ctr + take_ctr(ctx),
                        max_chunks, st));
-  CK(cudaEventRecord(ctx->ev[6], st));
+  if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[6], st));
   ctx->launches += 5;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[8], st));
@@ -1005,7 +1006,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
                                         from_file ? ctx->d_ctr + nonfinite_slot : nullptr, log2nb);
       ++ctx->launches;
     }
-    CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
+    if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[10], ctx->st_copy));
   } else {
     const int blocks = (int)std::min<size_t>(kPartialBlocks, (n + 255) / 256);
     const int ticket = take_ctr(ctx);
@@ -1063,7 +1064,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
                                from_file ? nonfinite_slot : -1, ctx->d_u64, ctx->h);
   ++ctx->launches;
   CK(cudaGetLastError());
-  if (want_filter) CK(cudaEventRecord(ctx->ev[9], st));
+  if (want_filter && ctx->stage_times) CK(cudaEventRecord(ctx->ev[9], st));
   const auto t_enq = std::chrono::steady_clock::now();
   TRY(sync(ctx));
   D.t_host_enqueue_ms = std::chrono::duration<double, std::milli>(t_enq - t_wall0).count();
@@ -1142,16 +1143,18 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
         t_sort_ms = ms_between(ctx->ev[2], ctx->ev[4]);
         t_spa_ms = ms_between(ctx->ev[4], ctx->ev[8]);
         D.t_spa_kernel_ms = t_spa_ms;
-        D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
-        D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
-        D.t_binsort_ms = ms_between(ctx->ev[5], ctx->ev[6]);
+        if (ctx->stage_times) {
+          D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
+          D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
+          D.t_binsort_ms = ms_between(ctx->ev[5], ctx->ev[6]);
+        }
       }
     }
     if (!filtered) {
       // ---- K3: region sort (spa.cpp:59-81) of every survivor.
       CK(cudaEventRecord(ctx->ev[7], st));
       Sorted so{};
-      TRY(sort_regions(ctx, m, qi.q, true, true, &so));
+      TRY(sort_regions(ctx, m, qi.q, ctx->stage_times, true, &so));
       D.sort_passes = so.passes;
       const bool sort_timed = s1 > 0;
       CK(cudaEventRecord(ctx->ev[6], st));
@@ -1183,7 +1186,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       t_sort_ms += ms_between(ctx->ev[7], ctx->ev[6]);
       t_spa_ms = ms_between(ctx->ev[6], ctx->ev[8]);
       D.t_spa_kernel_ms = t_spa_ms;
-      if (sort_timed) {
+      if (sort_timed && ctx->stage_times) {
         D.t_hist_ms = ms_between(ctx->ev[7], ctx->ev[3]);
         D.t_passes_ms = ms_between(ctx->ev[4], ctx->ev[5]);
         D.t_ties_ms = ms_between(ctx->ev[5], ctx->ev[6]);
@@ -1214,7 +1217,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       TRY(convex_finish(ctx, kept_counts, kept, &convex));
       if (convex) {
         D.convex_fast_path = 1;
-        D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
+        if (ctx->stage_times) D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
         goto finished;
       }
     }
@@ -1222,10 +1225,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       TRY(ensure_host_out(ctx, kept + 4));
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, kept * sizeof(double2), cudaMemcpyDeviceToHost,
                          st));
-      CK(cudaEventRecord(ctx->ev[9], st));
+      if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[9], st));
       TRY(sync(ctx));
     }
-    D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
+    if (ctx->stage_times) D.t_d2h_ms = ms_between(ctx->ev[8], ctx->ev[9]);
     const auto t_host0 = std::chrono::steady_clock::now();
     // polygon.cpp:7-29 + melkman.cpp:17-86 in one streaming pass
     // (the four chains concurrently when they are long, verified: finisher.cpp)
@@ -1260,7 +1263,7 @@ finished:
   S.t_total_ms = std::chrono::duration<double, std::milli>(t_end - t_wall0).count();
   D.t_k1_ms = S.t_extremes_ms;  // (K1 + K2 when k1k2_overlapped)
   D.t_k2_ms = S.t_classify_ms;
-  if (h_src || from_file) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
+  if ((h_src || from_file) && ctx->stage_times) D.t_h2d_ms = ms_between(ctx->ev[0], ctx->ev[10]);
   D.launches = ctx->launches;
 
   *hull_xy = reinterpret_cast<const double*>(ctx->hull_ptr);
@@ -1360,6 +1363,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   if (const char* e = std::getenv("CHGPU_PDL")) ctx->pdl = std::atoi(e) != 0;
+  if (const char* e = std::getenv("CHGPU_STAGE_TIMES")) ctx->stage_times = std::atoi(e) != 0;
   if (const char* e = std::getenv("CHGPU_SPA")) {
     if (std::strcmp(e, "sort") == 0) ctx->spa_mode = CHGPU_SPA_SORT;
     if (std::strcmp(e, "filter") == 0) ctx->spa_mode = CHGPU_SPA_FILTER;
@@ -1425,6 +1429,10 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
     case CHGPU_OPT_PDL:
       if (value != 0 && value != 1) break;
       ctx->pdl = value != 0;
+      return CHGPU_OK;
+    case CHGPU_OPT_STAGE_TIMES:
+      if (value != 0 && value != 1) break;
+      ctx->stage_times = value != 0;
       return CHGPU_OK;
     default:
       break;
