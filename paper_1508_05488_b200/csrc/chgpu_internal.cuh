@@ -334,18 +334,19 @@ __host__ __device__ inline void quad_derive(QuadInfo& qi, int log2nb) {
 }
 
 // Bin of a record of region ri + 1 with primary coordinate p:
-// trunc(clamp((p - lo) * scale, 0, top)) in the region's sort direction
-// (NaN -> 0). One dependent multiply: this sits on K2's per-survivor path.
+// min(trunc((p - lo) * scale), top), 0 below the range (rounding
+// stragglers), in the region's sort direction. One dependent multiply: this
+// sits on K2's per-survivor path.
 //
-// The conversion runs on the FP64 pipe, not the (narrow) XU pipe: clamp to
-// [0, top] (fmax maps NaN to 0), then add 2^52 rounding toward zero, which
-// leaves trunc(t) in the low mantissa bits. Same bin as
-// min(__double2uint_rz(t), top) for every t.
-__device__ __forceinline__ u32 bin_of(double lo, double scale, u32 top, double topd, u32 ri,
-                                      double p) {
-  double t = __dmul_rn(__dsub_rn(p, lo), scale);
-  t = fmin(fmax(t, 0.0), topd);  // topd = (double)top, hoisted by the caller
-  const u32 b = (u32)__double_as_longlong(__dadd_rz(t, 4503599627370496.0));
+// The truncation runs on the FP64 pipe, not the (narrow) XU pipe: adding 2^52
+// rounding toward zero leaves trunc(t) in the low mantissa bits for t in
+// [0, 2^51), and below 2^52's bit pattern for t < 0; the clamp is then two
+// integer compares on the bits (a double fmin/fmax pair cost 8% of K2's
+// instructions). Monotone in t, so in the primary coordinate.
+__device__ __forceinline__ u32 bin_of(double lo, double scale, u32 top, u32 ri, double p) {
+  const double t = __dmul_rn(__dsub_rn(p, lo), scale);
+  const long long u = __double_as_longlong(__dadd_rz(t, 4503599627370496.0)) - 0x4330000000000000ll;
+  const u32 b = u < 0 ? 0u : (u > (long long)top ? top : (u32)u);
   return ri >= 2 ? top - b : b;  // UR / UL sort descending
 }
 

@@ -235,8 +235,9 @@ __device__ __forceinline__ int classify(const QuadEdges& e, double px, double py
                 (u32)(cross_edge(e.ax[1], e.ay[1], e.ex[1], e.ey[1], px, py) < 0.0) << 1 |
                 (u32)(cross_edge(e.ax[2], e.ay[2], e.ex[2], e.ey[2], px, py) < 0.0) << 2 |
                 (u32)(cross_edge(e.ax[3], e.ay[3], e.ex[3], e.ey[3], px, py) < 0.0) << 3;
-  // lowest set bit + 1 (0: no edge has the point on its right, Interior)
-  // from a 16-entry table of 3-bit fields: ALU shifts, not the XU pipe's FLO
+  // lowest set bit + 1 (0: no edge has the point on its right, Interior):
+  // an 8-entry table of 3-bit fields for the low three flags (one 32-bit
+  // shift, not the XU pipe's FLO), edge 4 when only it is set
   return (int)((0x28b28c28b288ull >> (3 * m)) & 7u);
 }
 
@@ -515,14 +516,13 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   u64* const out = seg + (u64)base;
   u32* const out_idx = segidx + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
-  const double topd = (double)top;
   for (u32 slot = lane; slot < tot; slot += 32) {
     const double2 q = ss[slot];
     const u32 ri = sr[slot];
     const bool odd = (ri & 1u) == 0;  // LL, UR (ri 0, 2): primary x
     const double prim = odd ? q.x : q.y;
     const double2 bm = s_bmap[warp][ri];
-    const u32 b = (ri << log2nb) | bin_of(bm.x, bm.y, top, topd, ri, prim);
+    const u32 b = (ri << log2nb) | bin_of(bm.x, bm.y, top, ri, prim);
     if (!(CHGPU_K2_ABL & 1)) atomicAdd(bcnt + b, 1u);
     // w = wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
     // complemented for the min-regions LL and UL; kept as w >> kWShift

@@ -1052,7 +1052,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     // (small chains only: a survivor-heavy call reads its result back once
     // it knows the size, or not at all on the convex fast path)
     if (ctx->kept_hint + 4 < kConvexMin)
-      spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 4));
+      spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 16 + 256));
     TRY(ensure_host_out(ctx, spec + 4));
     if (spec)
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
