@@ -584,6 +584,12 @@ def main():
     if sharded:
         dist.barrier()
         dist.destroy_process_group()
+    # torch's tensors (and the pinned-memory events its copies recorded on the
+    # library stream) go before the context that owns that stream
+    torch.cuda.synchronize()
+    del ops, d_pts, h_pin, stream
+    import gc
+    gc.collect()
     ctx.close()
 
 
