@@ -453,10 +453,10 @@ def main():
         s1 = sum(d.region_counts[1:])
         t = dict(d.times_ms)
         t["t_k1_ms"] = statistics.median(disc_steps) if d.k1k2_overlapped else t["t_k1_ms"]
-        # K2 writes each survivor as an 8-byte filter key + a 4-byte input
-        # index on the pre-filtered path, as a 16-byte (k, v) record on the
-        # sort path
-        surv_b = 12 if d.spa_path == 1 else 16
+        # K2 writes each survivor as one 8-byte filter key (bin, segment
+        # position, w >> 32) on the pre-filtered path, as a 16-byte (k, v)
+        # record on the sort path
+        surv_b = 8 if d.spa_path == 1 else 16
         disc_ms = t["t_k1_ms"] + t["t_k2_ms"]
         if d.k1k2_overlapped:
             # K2 launched programmatically behind K1 (its CTAs start while
@@ -480,9 +480,9 @@ def main():
             kernels.update({
                 "k3_bin_scan": {"ms": t["t_binscan_ms"], "bytes": 24 * 4 * (1 << d.filter_log2nb),
                                 "basis": "12 B/bin read + 12 B/bin write"},
-                "k3_filter": {"ms": t["t_filter_ms"], "bytes": 8 * s1 + 36 * nc,
-                              "basis": "8 B/survivor key read + per candidate 4 B index "
-                                       "+ 16 B point read, 16 B record write",
+                "k3_filter": {"ms": t["t_filter_ms"], "bytes": 8 * s1 + 32 * nc,
+                              "basis": "8 B/survivor key read + per candidate 16 B point read, "
+                                       "16 B record write",
                               "candidates": nc},
                 "k4_chunk_spa": {"ms": t["t_spa_kernel_ms"],
                                  "bytes": 16 * nc + 32 * sum(d.kept_counts),

@@ -391,15 +391,21 @@ constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
 #endif
 constexpr int kSegItems = CHGPU_SEG_ITEMS;        // points per lane of the filter path's K2
 constexpr int kSegPts = 32 * kSegItems;           // one K2 warp's survivor segment
-// A survivor's filter key: its global SPA bin (< 4 * 2^18) in the high
-// word, w >> 32 (sign, exponent and 20 mantissa bits of the guarded
-// coordinate) in the low word. w >> 32 is monotone in w, so maxima and
-// threshold tests on it are valid lower bounds / drops (k_filter.cu), and
-// the bin tables of maxima and thresholds are 32-bit.
+// A survivor's filter key: its global SPA bin (< 4 * 2^18) in bits 40-63,
+// its point's position inside its K2 segment in bits 32-39 (the filter
+// recovers the input index from it: no index array), w >> 32 (sign,
+// exponent and 20 mantissa bits of the guarded coordinate) in the low
+// word. w >> 32 is monotone in w, so maxima and threshold tests on it are
+// valid lower bounds / drops (k_filter.cu), and the bin tables of maxima
+// and thresholds are 32-bit.
 constexpr int kWShift = 32;
 constexpr u64 kWMask = 0xFFFFFFFFull;
-__host__ __device__ __forceinline__ u64 filter_key(u32 gbin, u64 w) {
-  return ((u64)gbin << 32) | (w >> kWShift);
+constexpr int kKeyBinShift = 40;
+static_assert(kSegPts <= 256, "a survivor's segment position is 8 bits of its key");
+__host__ __device__ __forceinline__ u64 filter_key(u32 gbin, u32 pos, u64 w) {
+  return ((u64)gbin << kKeyBinShift) | ((u64)pos << 32) | (w >> kWShift);
 }
+__host__ __device__ __forceinline__ u32 key_bin(u64 key) { return (u32)(key >> kKeyBinShift); }
+__host__ __device__ __forceinline__ u32 key_pos(u64 key) { return (u32)(key >> 32) & 255u; }
 
 }  // namespace chgpu

@@ -402,14 +402,13 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
 // stream 1 of (kbuf, vbuf) instead, exactly like k_classify_compact.
 __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivors(
     const double2* __restrict__ pts, u32 n, const QuadInfo* __restrict__ qinfo,
-    u64* __restrict__ seg, u32* __restrict__ segidx, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
+    u64* __restrict__ seg, u64* __restrict__ segcnt, u64* __restrict__ kbuf,
     u64* __restrict__ vbuf, u32* __restrict__ counts_out, int log2nb, u32* __restrict__ bcnt,
     u32* __restrict__ bw, u32 wmask) {
   __shared__ u32 s_segT[kK2Threads / 32];  // (degenerate frame only)
   __shared__ u32 s_base;
   __shared__ __align__(16) double2 s_seg[kK2Threads / 32 * kSegPts];
-  __shared__ u32 s_sidx[kK2Threads / 32 * kSegPts];
-  __shared__ unsigned char s_sreg[kK2Threads / 32 * kSegPts];
+  __shared__ unsigned short s_stag[kK2Threads / 32 * kSegPts];  // segment position << 2 | region
   __shared__ double2 s_bmap[kK2Threads / 32][4];  // (lo, scale) per region, per warp
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -488,13 +487,11 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   // runs in ceil(count / 32) rounds instead of once per item, and the
   // segment's global stores are coalesced.
   double2* const ss = s_seg + warp * kSegPts;
-  u32* const si = s_sidx + warp * kSegPts;
-  unsigned char* const sr = s_sreg + warp * kSegPts;
+  unsigned short* const stg = s_stag + warp * kSegPts;
   {
     // shared-window addresses held in registers and predicated stores:
     // no per-item branch and no re-derived shared base per item
-    const u32 a_pt = (u32)__cvta_generic_to_shared(ss), a_ix = (u32)__cvta_generic_to_shared(si),
-              a_rg = (u32)__cvta_generic_to_shared(sr);
+    const u32 a_pt = (u32)__cvta_generic_to_shared(ss), a_tg = (u32)__cvta_generic_to_shared(stg);
     u32 pos = incl - cnt;
 #pragma unroll
     for (int j = 0; j < kSegItems; ++j) {
@@ -503,10 +500,9 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
           "{\n\t.reg .pred q;\n\t"
           "setp.ne.u32 q, %0, 0;\n\t"
           "@q st.shared.v2.f64 [%1], {%2, %3};\n\t"
-          "@q st.shared.u32 [%4], %5;\n\t"
-          "@q st.shared.u8 [%6], %7;\n\t}" ::"r"(r),
-          "r"(a_pt + 16 * pos), "d"(p[j].x), "d"(p[j].y), "r"(a_ix + 4 * pos), "r"(base + j * 32 + lane),
-          "r"(a_rg + pos), "r"(r - 1)
+          "@q st.shared.u16 [%4], %5;\n\t}" ::"r"(r),
+          "r"(a_pt + 16 * pos), "d"(p[j].x), "d"(p[j].y), "r"(a_tg + 2 * pos),
+          "h"((unsigned short)(((j * 32 + lane) << 2) | (r - 1)))
           : "memory");
       pos += r != 0;
     }
@@ -514,11 +510,11 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
   __syncwarp();
   if (CHGPU_K2_ABL & 8) return;
   u64* const out = seg + (u64)base;
-  u32* const out_idx = segidx + (u64)base;
   const u32 top = (1u << log2nb) - 1u;
   for (u32 slot = lane; slot < tot; slot += 32) {
     const double2 q = ss[slot];
-    const u32 ri = sr[slot];
+    const u32 tg = stg[slot];
+    const u32 ri = tg & 3u;
     const bool odd = (ri & 1u) == 0;  // LL, UR (ri 0, 2): primary x
     const double prim = odd ? q.x : q.y;
     const double2 bm = s_bmap[warp][ri];
@@ -527,13 +523,11 @@ __global__ __launch_bounds__(kK2Threads, CHGPU_K2_MINB) void k_classify_survivor
     // w = wkey(v): the guarded coordinate with -0.0 folded onto +0.0,
     // complemented for the min-regions LL and UL; kept as w >> kWShift
     const double g = odd ? q.y : q.x;
-    const u64 key = filter_key(b, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
+    const u64 key = filter_key(b, tg >> 2, ord_enc_z(g) ^ ((ri == 0 || ri == 3) ? ~0ull : 0ull));
     // any subset of a bin's records gives a valid (lower) max: sample
     if (!(CHGPU_K2_ABL & 2) && (slot & wmask) == 0) atomicMax(bw + b, (u32)key);
-    if (!(CHGPU_K2_ABL & 4)) {
-      out[slot] = key;            // the filter reads 8 B per survivor
-      out_idx[slot] = si[slot];   // ... and the point only for candidates
-    }
+    if (!(CHGPU_K2_ABL & 4)) out[slot] = key;  // the filter reads 8 B per survivor
+
   }
   // (region totals: the bin scan sums the bin counts)
 }
@@ -624,7 +618,7 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
 }
 
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
-                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
                                u32* bcnt, u32* bw, u32 wmask, bool programmatic, cudaStream_t st) {
   constexpr u32 tile = kK2Threads / 32 * kSegPts;  // one segment per warp
   const u32 tiles = (n + tile - 1) / tile;
@@ -638,7 +632,7 @@ void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo,
   attr[0].val.programmaticStreamSerializationAllowed = programmatic ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_classify_survivors, pts, n, qinfo, seg, segidx, segcnt, kbuf, vbuf,
+  cudaLaunchKernelEx(&cfg, k_classify_survivors, pts, n, qinfo, seg, segcnt, kbuf, vbuf,
                      counts_out, log2nb, bcnt, bw, wmask);
 }
 

@@ -423,7 +423,7 @@ size_t filter_smem_bytes(int log2nb) { return ((size_t)4 << log2nb) / kCoarseBin
 // the next slot of its bin and writes its sort record; the bin's 33rd
 // candidate queues it for k_bin_sort_warp, its 257th for k_bin_sort_big.
 __global__ __launch_bounds__(kFilterThreads, 1) void k_filter(
-    const u64* __restrict__ seg, const u32* __restrict__ segidx, const u64* __restrict__ segcnt,
+    const u64* __restrict__ seg, const u64* __restrict__ segcnt,
     u32 nseg, const double2* __restrict__ pts, const FilterPlan* __restrict__ P_p,
     const QuadInfo* __restrict__ qinfo, const u32* __restrict__ bstart,
     const u32* __restrict__ bthr, const u32* __restrict__ tcoarse, u32* __restrict__ bcur,
@@ -463,11 +463,12 @@ __global__ __launch_bounds__(kFilterThreads, 1) void k_filter(
   // One candidate's work (its point, bin slot, sort record, big-bin queue);
   // `at` = its survivor slot in K2's segments.
   auto take = [&](u64 key, u32 at) {
-    const u32 bi = (u32)(key >> 32);
+    const u32 bi = key_bin(key);
     const u32 r = bi >> lg;
     const int reg = (int)r + 1;
     const u32 bs = bstart[bi];
-    const double2 p = __ldg(pts + segidx[at]);
+    // the input index: the segment's first point + the position in the key
+    const double2 p = __ldg(pts + ((at & ~(u32)(kSegPts - 1)) | key_pos(key)));
     const u32 pos = atomicAdd(bcur + bi, 1u);
     if (pos == 0) atomicOr(bmap + (bi >> 5), 1u << (bi & 31));  // k_spa_chunks' index
     const u64 dst = s_off[r] + bs + pos;
@@ -528,7 +529,7 @@ __global__ __launch_bounds__(kFilterThreads, 1) void k_filter(
     push(sl < t && (u32)key >= th, key, g * kSegPts + sl);
   };
   auto coarse = [&](u32 sl, u32 t, u64 key) -> u32 {
-    const u32 bi = (u32)(key >> 32);
+    const u32 bi = key_bin(key);
     const bool pass = sl < t && (u32)key >= s_tc[bi >> kCoarseLog2];
 #if CHGPU_FILTER_ABL & 1  // (diagnostic: count the coarse passes instead of the candidates)
     mine += pass;
@@ -1340,7 +1341,7 @@ cudaError_t launch_bin_scan(const QuadInfo* qinfo, u32* counts, u64 chunk_count,
 
 u32 bin_scan_blocks(int log2nb) { return 4 * std::max(1u, (1u << log2nb) / kBinTile); }
 
-void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
+void launch_filter(const u64* seg, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
                    const u32* bstart, const u32* bthr, const u32* tcoarse, int log2nb, u32* bcur,
                    u32* bmap, u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
@@ -1351,7 +1352,7 @@ void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nse
   const u32 blocks = std::min<u32>((nseg + kFilterThreads / 32 - 1) / (kFilterThreads / 32),
                                    (u32)device_limits().filter_resident);
   k_filter<<<blocks, kFilterThreads, filter_smem_bytes(log2nb), st>>>(
-      seg, segidx, segcnt, nseg, pts, P, qinfo, bstart, bthr, tcoarse, bcur, bmap, kout, vout, big,
+      seg, segcnt, nseg, pts, P, qinfo, bstart, bthr, tcoarse, bcur, bmap, kout, vout, big,
       nbig, ncand, overflow);
 }
 

@@ -52,7 +52,7 @@ void launch_spa_small(const u64* k, const u64* v, const u32* bcur, const u32* bs
                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
                       unsigned long long* kept_counts, u32* defer, u32* ndefer, u32 cap,
                       cudaStream_t st);
-void launch_filter(const u64* seg, const u32* segidx, const u64* segcnt, u32 nseg,
+void launch_filter(const u64* seg, const u64* segcnt, u32 nseg,
                    const double2* pts, const FilterPlan* P, const QuadInfo* qinfo,
                    const u32* bstart, const u32* bthr, const u32* tcoarse, int log2nb, u32* bcur,
                    u32* bmap, u64* kout, u64* vout, u32* big, u32* nbig, unsigned long long* ncand,
@@ -101,7 +101,7 @@ void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              u64 ncap, u32* counts_out, cudaStream_t st);
 // K2 of the pre-filtered path: raw survivor points + bin statistics.
 void launch_classify_survivors(const double2* pts, u32 n, const QuadInfo* qinfo, u64* seg,
-                               u32* segidx, u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
+                               u64* segcnt, u64* kbuf, u64* vbuf, u32* counts_out, int log2nb,
                                u32* bcnt, u32* bw, u32 wmask, bool programmatic, cudaStream_t st);
 void launch_classify_labels(const double2* pts, u64 n, const QuadInfo* qinfo,
                             unsigned char* labels, unsigned long long* counts, int blocks,

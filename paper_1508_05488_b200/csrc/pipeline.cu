@@ -770,7 +770,7 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[3], st));
   // K2's survivor segments: filter keys in kbuf, input indices in the upper
   // half of vbuf, each segment's survivor count in its lower part
-  launch_filter(ctx->d_kbuf, reinterpret_cast<const u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+  launch_filter(ctx->d_kbuf, ctx->d_vbuf,
                 (u32)((n + kSegPts - 1) / kSegPts), pts, P, ctx->d_qinfo, ctx->d_fstart,
                 reinterpret_cast<const u32*>(ctx->d_fthr), tcoarse, log2nb,
                 t.cur, t.bmap, ctx->d_ka, ctx->d_va, ctx->d_fbig, ctx->d_ctr + nbig_slot,
@@ -1030,8 +1030,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   if (want_filter) {
     // raw survivor points + bin statistics (a degenerate frame writes the
     // LEX records of stream 1 instead)
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
-                              reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), pdl,
                               st);
@@ -1752,8 +1751,7 @@ int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double
     const FilterTabs ftabs = filter_tabs(ctx, log2nb);
     const int cnt_slot = ctx->ctr_used;
     ctx->ctr_used += 5;
-    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf,
-                              reinterpret_cast<u32*>(ctx->d_vbuf + ctx->cap), ctx->d_vbuf,
+    launch_classify_survivors(pts, (u32)n, ctx->d_qinfo, ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_kbuf, ctx->d_vbuf,
                               ctx->d_ctr + cnt_slot, log2nb, ftabs.cnt, ftabs.w, filter_wmask(), false,
                               st);
