@@ -1296,7 +1296,7 @@ __global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
     u32* __restrict__ overflow, const u32* __restrict__ defer, const u32* __restrict__ ndefer_p,
     u64* __restrict__ sk, u64* __restrict__ sv, u32* __restrict__ chunk_kept,
     u32* __restrict__ group_kept, unsigned long long* __restrict__ kept_counts,
-    double2* __restrict__ out, u32* __restrict__ bar) {
+    double2* __restrict__ out, u32* __restrict__ bar, ReadbackArgs rb) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const u32 nwarps = gridDim.x * (kFinishThreads / 32);
@@ -1319,6 +1319,10 @@ __global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
   }
   const u32 total = P_p->spa.total_chunks;
   for (u32 c = gw; c < total; c += nwarps) spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out);
+  // every CTA is done with the counters: CTA 0 hands them to the host and
+  // clears them (no separate read-back launch)
+  grid_barrier(bar, nd ? 2u : 0u);
+  if (blockIdx.x == 0) readback_block(rb);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -1375,14 +1379,15 @@ cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart
                               const u32* nbig, u32* overflow, const u32* defer, const u32* ndefer,
                               u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
                               unsigned long long* kept_counts, double2* out, u32* bar,
-                              u32 max_chunks, cudaStream_t st) {
+                              u32 max_chunks, const ReadbackArgs& rb_in, cudaStream_t st) {
+  ReadbackArgs rb = rb_in;
   if (max_chunks == 0) return cudaSuccess;
   const u32 blocks = std::max(1u, std::min<u32>((u32)device_limits().finish_coop,
                                                 (max_chunks + 7) / 8));
   void* args[] = {(void*)&k, (void*)&v, (void*)&bcur, (void*)&bstart, (void*)&bmap,
                   (void*)&first_bin, (void*)&P, (void*)&big, (void*)&nbig, (void*)&overflow,
                   (void*)&defer, (void*)&ndefer, (void*)&sk, (void*)&sv, (void*)&chunk_kept,
-                  (void*)&group_kept, (void*)&kept_counts, (void*)&out, (void*)&bar};
+                  (void*)&group_kept, (void*)&kept_counts, (void*)&out, (void*)&bar, (void*)&rb};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_spa_finish, dim3(blocks),
                                                     dim3(kFinishThreads), args, kFinishSmem, st);
 #if CHGPU_SPA_CLOCKS

@@ -29,6 +29,34 @@ struct FilterPlan {
   int log2nb;           // bins per region = 2^log2nb
 };
 // Small per-call scratch of the pre-filter (<= 512 bin tiles).
+// The counters the host reads after the filter path, written straight into
+// pinned, device-mapped host memory by the last kernel of the path, which
+// then clears them for the next call (pipeline.cu k_readback does the same
+// for the other paths).
+struct ReadbackArgs {
+  const QuadInfo* qinfo;
+  u32* ctr;                      // device counters [nctr]
+  int nctr, cnt_slot, ovf_slot, nonfinite_slot;
+  unsigned long long* u64s;      // device 64-bit counters [16]: kept [0, 4), candidates [11]
+  u32* h_qi;                     // host (mapped): QuadInfo words
+  u32* h_ctr;                    // host (mapped): counters
+  unsigned long long* h_kept;    // host (mapped): kept [4]
+  unsigned long long* h_ncand;   // host (mapped): candidates
+};
+__device__ __forceinline__ void readback_block(const ReadbackArgs& a) {
+  const int t = threadIdx.x;
+  const u32* q = reinterpret_cast<const u32*>(a.qinfo);
+  for (int i = t; i < (int)(sizeof(QuadInfo) / 4); i += blockDim.x) a.h_qi[i] = q[i];
+  if (t < 5) a.h_ctr[a.cnt_slot + t] = a.ctr[a.cnt_slot + t];
+  if (t == 5 && a.ovf_slot >= 0) a.h_ctr[a.ovf_slot] = a.ctr[a.ovf_slot];
+  if (t == 6 && a.nonfinite_slot >= 0) a.h_ctr[a.nonfinite_slot] = a.ctr[a.nonfinite_slot];
+  if (t >= 8 && t < 12) a.h_kept[t - 8] = a.u64s[t - 8];
+  if (t == 12) *a.h_ncand = a.u64s[11];
+  __syncthreads();
+  for (int i = t; i < a.nctr; i += blockDim.x) a.ctr[i] = 0;
+  if (t < 16) a.u64s[t] = 0;
+}
+
 struct FilterAux {
   u32* tsum;        // records per bin tile
   u32* agg_seg;     // tile aggregates of the segmented max
@@ -46,7 +74,7 @@ cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart
                               const u32* nbig, u32* overflow, const u32* defer, const u32* ndefer,
                               u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,
                               unsigned long long* kept_counts, double2* out, u32* bar,
-                              u32 max_chunks, cudaStream_t st);
+                              u32 max_chunks, const ReadbackArgs& rb, cudaStream_t st);
 void launch_spa_small(const u64* k, const u64* v, const u32* bcur, const u32* bstart,
                       const u32* bmap, const u32* first_bin, const FilterPlan* P, u32 max_chunks,
                       u64* sk, u64* sv, u32* chunk_kept, u32* group_kept,

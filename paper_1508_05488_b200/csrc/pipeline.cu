@@ -739,7 +739,7 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
 // Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
 // *ovf_slot / *ncand land in the counters for the caller's read-back.
 int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chunk_count,
-                       int log2nb, int cnt_slot, int* ovf_slot) {
+                       int log2nb, int cnt_slot, int* ovf_slot, int nonfinite_slot = -1) {
   cudaStream_t st = ctx->st;
   const FilterPlan* P = ctx->d_plan;
   const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
@@ -786,11 +786,25 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
                    ctx->d_fdefer, ctx->d_ctr + ndefer_slot,
                    ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ? 0u : kSpaSmallCap, st);
   if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[5], st));
+  // the finish kernel also hands the call's counters to the host and
+  // clears them (what k_readback does on the other paths)
+  ReadbackArgs rb;
+  rb.qinfo = ctx->d_qinfo;
+  rb.ctr = ctx->d_ctr;
+  rb.nctr = kCtrSlots;
+  rb.cnt_slot = cnt_slot;
+  rb.ovf_slot = *ovf_slot;
+  rb.nonfinite_slot = nonfinite_slot;
+  rb.u64s = ctx->d_u64;
+  rb.h_qi = reinterpret_cast<u32*>(&ctx->h->qi);
+  rb.h_ctr = ctx->h->ctr;
+  rb.h_kept = ctx->h->kept;
+  rb.h_ncand = &ctx->h->ncand;
   CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
                        ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
                        ctx->d_ctr + ndefer_slot, ctx->d_ck, ctx->d_cv, ctx->d_raw,
                        ctx->d_raw + max_chunks, ctx->d_u64, ctx->d_kept, ctx->d_ctr + take_ctr(ctx),
-                       max_chunks, st));
+                       max_chunks, rb, st));
   if (ctx->stage_times) CK(cudaEventRecord(ctx->ev[6], st));
   ctx->launches += 5;
   CK(cudaGetLastError());
@@ -1047,7 +1061,8 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   int ovf_slot = -1;
   size_t spec = 0;
   if (want_filter) {
-    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
+    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot,
+                           from_file ? nonfinite_slot : -1));
     // (small chains only: a survivor-heavy call reads its result back once
     // it knows the size, or not at all on the convex fast path)
     if (ctx->kept_hint + 4 < kConvexMin)
@@ -1058,11 +1073,14 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
                          st));
   }
   // every counter the host needs, in one launch straight into the pinned
-  // (device-mapped) host block instead of one DMA per value
-  k_readback<<<1, 64, 0, st>>>(ctx->d_qinfo, ctx->d_ctr, cnt_slot, ovf_slot,
-                               from_file ? nonfinite_slot : -1, ctx->d_u64, ctx->h);
-  ++ctx->launches;
-  CK(cudaGetLastError());
+  // (device-mapped) host block instead of one DMA per value (the filter
+  // path's k_spa_finish did it already)
+  if (!want_filter) {
+    k_readback<<<1, 64, 0, st>>>(ctx->d_qinfo, ctx->d_ctr, cnt_slot, ovf_slot,
+                                 from_file ? nonfinite_slot : -1, ctx->d_u64, ctx->h);
+    ++ctx->launches;
+    CK(cudaGetLastError());
+  }
   if (want_filter && ctx->stage_times) CK(cudaEventRecord(ctx->ev[9], st));
   const auto t_enq = std::chrono::steady_clock::now();
   TRY(sync(ctx));
@@ -1757,11 +1775,8 @@ int shard_chains_impl(chgpu_ctx* ctx, const double* d_xy, size_t n, const double
                               st);
     CK(cudaGetLastError());
     int ovf_slot = -1;
+    // (k_spa_finish hands the kept counts and the overflow flag to ctx->h)
     TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot));
-    CK(cudaMemcpyAsync(ctx->h->kept, ctx->d_u64, 4 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ctx->h->ctr[ovf_slot], ctx->d_ctr + ovf_slot, sizeof(u32),
-                       cudaMemcpyDeviceToHost, st));
     TRY(sync(ctx));
     TRY(ftab_clear_behind(ctx));  // (for the next call, while the host exchanges)
     if (!ctx->h->ctr[ovf_slot]) {
