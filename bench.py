@@ -461,12 +461,16 @@ def main():
         if d.k1k2_overlapped:
             # K2 launched programmatically behind K1 (its CTAs start while
             # K1's last block merges the quad): one CUDA-event interval for
-            # the discard stage
+            # the discard stage. Algorithmic bytes on SURVEY §8(d)'s basis
+            # (K1 16 B/pt; K2 16 B/pt + 16 B/survivor); K2 actually writes
+            # surv_b B per survivor (bytes_moved).
             kernels = {
-                "k1k2_discard": {"ms": t["t_k1_ms"], "bytes": 32 * n + surv_b * s1,
-                                 "basis": f"K1 16 B/pt read + K2 16 B/pt read + {surv_b} B/survivor "
-                                          "write (k_extremes_partial + k_classify_survivors, "
-                                          "programmatically overlapped)"},
+                "k1k2_discard": {"ms": t["t_k1_ms"], "bytes": 32 * n + 16 * s1,
+                                 "bytes_moved": 32 * n + surv_b * s1,
+                                 "basis": "SURVEY 8(d): K1 16 B/pt read + K2 16 B/pt read + 16 B/"
+                                          f"survivor write (moved: {surv_b} B/survivor); "
+                                          "k_extremes_partial + k_classify_survivors, "
+                                          "programmatically overlapped"},
             }
         else:
             kernels = {
