@@ -213,6 +213,10 @@ int chgpu_merge_hull(const double* const* runs, const size_t* kept_counts, int n
  * 1-4 run concurrently and are verified before use): calls that took it,
  * and calls whose checks fell back to the sequential pass. Diagnostics. */
 void chgpu_finish_split_stats(unsigned long long* taken, unsigned long long* fallback);
+/* The last split finisher call's timings in µs from the segments' submit:
+ * segment A (calling thread), B, C, D done; all joined; result written.
+ * Diagnostics. */
+void chgpu_finish_split_times(double* out6);
 /* canonicalize_ring (melkman.hpp:20), in place. */
 void chgpu_canonicalize_ring(double* ring, size_t n);
 /* hull_oracle (pipeline.hpp:62): host reference hull; out capacity n. */

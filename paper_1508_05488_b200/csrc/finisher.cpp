@@ -696,6 +696,9 @@ WorkerPool* worker_pool() {  // nullptr if threads cannot be made here
 }
 
 std::atomic<unsigned long long> g_split_taken{0}, g_split_fallback{0};
+// the last split call's segment times (µs from the submit: A, B, C, D, all
+// joined) and its total (set after the merge)
+double g_seg_us[6] = {0, 0, 0, 0, 0, 0};
 
 size_t split_min() {
   static const size_t v = [] {
@@ -755,16 +758,24 @@ int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt 
   // onto corner 0 (finish_chains' closing logic; a repeat of the previous
   // ring point drops as a consecutive duplicate)
   const bool drop_last = same(last_pt, corners[0]);
-  pool->b.submit([&] { sb.run(c[1], kept_counts[1], corners[2]); });
-  pool->c.submit([&] { sc.run(c[2], kept_counts[2], corners[3]); });
-  pool->d.submit([&] { sd.run(c[3], cut, last_pt, !drop_last); });
+  const auto t_sub = Clock::now();
+  double seg_us[4] = {0, 0, 0, 0};
+  auto us_since = [&](Clock::time_point a) {
+    return std::chrono::duration<double, std::micro>(Clock::now() - a).count();
+  };
+  pool->b.submit([&] { sb.run(c[1], kept_counts[1], corners[2]); seg_us[1] = us_since(t_sub); });
+  pool->c.submit([&] { sc.run(c[2], kept_counts[2], corners[3]); seg_us[2] = us_since(t_sub); });
+  pool->d.submit([&] { sd.run(c[3], cut, last_pt, !drop_last); seg_us[3] = us_since(t_sub); });
   double qx = 0, qy = 0;
   const Pt* sp[3] = {&corners[0], c[0], &corners[1]};
   const size_t sl[3] = {1, kept_counts[0], 1};
   const bool seeded = run_prefix(sp, sl, 3, head, tail, qx, qy);
+  seg_us[0] = us_since(t_sub);
   pool->b.wait();
   pool->c.wait();
   pool->d.wait();
+  for (int q = 0; q < 4; ++q) g_seg_us[q] = seg_us[q];  // (diagnostics: chgpu_finish_split_times)
+  g_seg_us[4] = us_since(t_sub);
 
   // handover checks: A ends as [B, L, X, ..., Y, B]; B as [R, L, ..., R]; C as [T, L, ..., T]
   bool ok = seeded && sb.ok && sc.ok && sd.ok && tail - head >= 5 && same(head[0], corners[1]) &&
@@ -801,6 +812,7 @@ int finish_chains_split(const Pt* chains, const size_t kept_counts[4], const Pt 
   hull.resize(m);
   std::memcpy(hull.data(), head + lo_i, (m - lo_i) * sizeof(Pt));
   std::memcpy(hull.data() + (m - lo_i), head, lo_i * sizeof(Pt));
+  g_seg_us[5] = us_since(t_sub);
   return kOk;
 }
 
@@ -935,6 +947,10 @@ extern "C" int chgpu_finish_chains(const double* chains, const size_t* kept_coun
 
 // Split-finisher counters (tests): calls that took the concurrent path, and
 // calls whose checks sent them to the sequential pass.
+extern "C" void chgpu_finish_split_times(double* out6) {
+  for (int q = 0; q < 6; ++q) out6[q] = chgpu::host::g_seg_us[q];
+}
+
 extern "C" void chgpu_finish_split_stats(unsigned long long* taken, unsigned long long* fallback) {
   *taken = chgpu::host::g_split_taken.load();
   *fallback = chgpu::host::g_split_fallback.load();
