@@ -13,9 +13,12 @@
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <chrono>
@@ -868,55 +871,149 @@ int begin_call(chgpu_ctx* ctx) {
 
 // Core of chgpu_hull / chgpu_hull_device. h_src != nullptr: the input is on
 // the host and is staged in chunks on a copy stream, overlapped with K1.
+// memcpy into the pinned staging slot with non-temporal stores: the slot is
+// read next by the copy engine, not by this core, so a cached store only
+// adds a read-for-ownership of every destination line to the host memory
+// traffic. dst is 16-byte aligned (slot offsets are multiples of 4 KB).
+void copy_stream(unsigned char* dst, const unsigned char* src, size_t len) {
+  static const bool nt = [] {
+    const char* e = std::getenv("CHGPU_STAGE_NT");  // A/B knob
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!nt || (reinterpret_cast<uintptr_t>(dst) & 15)) {
+    std::memcpy(dst, src, len);
+    return;
+  }
+  size_t i = 0;
+  for (; i + 64 <= len; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  _mm_sfence();
+  if (i < len) std::memcpy(dst + i, src + i, len - i);
+}
+
+// Copies bytes [off, off + len) of the source into dst with up to
+// `threads` parallel workers: pread from fd (>= 0), else memcpy from the
+// pageable host array src (page-cache reads and pageable copies are
+// memcpy-bound on one core). false on a read error.
+// Host threads that stage pageable or file input into the pinned ring: one
+// process-wide pool, started on first use (a chunk used to spawn its own
+// threads: 15 thread creations per 32 MB chunk cost more than the copy).
+// A job is cut into parts, taken from an atomic counter by the caller and
+// the workers. Workers spin briefly after a job (the next chunk follows
+// within a millisecond), then park. Serves one job at a time (a mutex).
+class StagePool {
+ public:
+  static StagePool& get() {
+    static StagePool* p = new StagePool();  // (never destroyed: its threads live with the process)
+    return *p;
+  }
+  // f(part) for every part in [0, parts), parts handed out through an
+  // atomic counter to the caller and the workers; false if any part
+  // returned false
+  bool run(int parts, const std::function<bool(int)>& f) {
+    std::lock_guard<std::mutex> busy(busy_);
+    start(parts - 1);
+    if (th_.empty() || parts <= 1) {
+      bool ok = true;
+      for (int i = 0; i < parts; ++i) ok = f(i) && ok;
+      return ok;
+    }
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &f;
+      nparts_ = parts;
+      next_.store(0);
+      ok_.store(true);
+      active_.store((int)th_.size());
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    work();
+    while (active_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+    return ok_.load();
+  }
+
+ private:
+  void work() {
+    for (int i = next_.fetch_add(1); i < nparts_; i = next_.fetch_add(1))
+      if (!(*job_)(i)) ok_.store(false);
+  }
+  void start(int want) {
+    const pid_t me = getpid();
+    if (pid_ != me) {  // (a forked child has no threads: it starts its own)
+      th_.clear();
+      pid_ = me;
+    }
+    while ((int)th_.size() < want && !failed_) {
+      try {
+        th_.emplace_back([this, g = gen_.load()] { loop(g); });
+      } catch (...) {
+        failed_ = true;  // run with the threads that did start
+      }
+    }
+  }
+  // seen = the generation when the thread was created: a thread that is
+  // first scheduled after the job was posted still takes part in it
+  void loop(unsigned seen) {
+    for (;;) {
+      // spin ~200 us for the next job, then park
+      const auto until = std::chrono::steady_clock::now() + std::chrono::microseconds(200);
+      while (gen_.load(std::memory_order_acquire) == seen && std::chrono::steady_clock::now() < until)
+        std::this_thread::yield();
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+      }
+      seen = gen_.load(std::memory_order_acquire);
+      work();
+      active_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::mutex busy_, m_;
+  std::condition_variable cv_;
+  std::vector<std::thread> th_;
+  pid_t pid_ = 0;
+  bool failed_ = false;
+  const std::function<bool(int)>* job_ = nullptr;
+  int nparts_ = 0;
+  std::atomic<unsigned> gen_{0};
+  std::atomic<int> next_{0}, active_{0};
+  std::atomic<bool> ok_{true};
+};
+
 // Copies bytes [off, off + len) of the source into dst with up to
 // `threads` parallel workers: pread from fd (>= 0), else memcpy from the
 // pageable host array src (page-cache reads and pageable copies are
 // memcpy-bound on one core). false on a read error.
 bool stage_bytes(int fd, const unsigned char* src, unsigned char* dst, size_t off, size_t len,
                  int threads) {
-  auto part = [&](size_t a, size_t b, bool* ok) {
+  auto part = [&](size_t a, size_t b) -> bool {
     if (fd < 0) {
-      std::memcpy(dst + (a - off), src + a, b - a);
-      *ok = true;
-      return;
+      copy_stream(dst + (a - off), src + a, b - a);
+      return true;
     }
     while (a < b) {
       const ssize_t r = pread(fd, dst + (a - off), b - a, (off_t)a);
-      if (r <= 0) {
-        *ok = false;
-        return;
-      }
+      if (r <= 0) return false;
       a += (size_t)r;
     }
-    *ok = true;
+    return true;
   };
-  if (threads <= 1 || len < (size_t(4) << 20)) {
-    bool ok = false;
-    part(off, off + len, &ok);
-    return ok;
-  }
-  std::vector<std::thread> th;
-  std::vector<char> oks(threads, 0);
+  if (threads <= 1 || len < (size_t(1) << 20)) return part(off, off + len);
   const size_t step = ((len + threads - 1) / threads + 4095) & ~size_t(4095);
-  for (int t = 1; t < threads; ++t) {
-    const size_t a = off + t * step, b = std::min(off + len, a + step);
-    if (a >= b) {
-      oks[t] = 1;
-      continue;
-    }
-    th.emplace_back([&, a, b, t] {
-      bool ok = false;
-      part(a, b, &ok);
-      oks[t] = ok;
-    });
-  }
-  bool ok0 = false;
-  part(off, std::min(off + len, off + step), &ok0);
-  for (auto& x : th) x.join();
-  oks[0] = ok0;
-  for (char o : oks)
-    if (!o) return false;
-  return true;
+  const int parts = (int)((len + step - 1) / step);
+  return StagePool::get().run(parts, [&](int t) -> bool {
+    const size_t a = off + (size_t)t * step, b = std::min(off + len, a + step);
+    return a >= b ? true : part(a, b);
+  });
 }
 
 // Core of chgpu_hull / chgpu_hull_device / chgpu_hull_xy_binary. h_src !=
@@ -969,7 +1066,15 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   }
   const bool staged = from_file || pageable;
   if (h_src || from_file) {
-    const size_t nchunks = (n + kH2DChunk - 1) / kH2DChunk;
+    // staged input moves in smaller chunks through more slots (the same
+    // pinned ring): the first chunk's host copy is not overlapped
+    static const int stage_split = [] {
+      const char* e = std::getenv("CHGPU_STAGE_SPLIT");  // tuning knob (log2)
+      return e ? std::max(0, std::min(4, std::atoi(e))) : 2;
+    }();
+    const size_t chunk = staged ? kH2DChunk >> stage_split : kH2DChunk;
+    const size_t slots = staged ? kFileSlots << stage_split : kFileSlots;
+    const size_t nchunks = (n + chunk - 1) / chunk;
     const int per = std::max(1, std::min(kPartialBlocks, kMaxPartials / (int)nchunks));
     if (ctx->ev_copy.size() < nchunks) {
       size_t old = ctx->ev_copy.size();
@@ -982,7 +1087,7 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     // the last partial block of the call merges the quad (no final launch)
     u32 total_parts = 0;
     for (size_t c = 0; c < nchunks; ++c) {
-      const size_t cnt = std::min(kH2DChunk, n - c * kH2DChunk);
+      const size_t cnt = std::min(chunk, n - c * chunk);
       total_parts += (u32)extremes_blocks((int)std::min<size_t>(per, (cnt + 255) / 256));
     }
     const int ticket = take_ctr(ctx);
@@ -995,12 +1100,12 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       return std::max(1, e ? std::atoi(e) : std::min(16, hw));
     }();
     for (size_t c = 0; c < nchunks; ++c) {
-      const size_t off = c * kH2DChunk, cnt = std::min(kH2DChunk, n - off);
+      const size_t off = c * chunk, cnt = std::min(chunk, n - off);
       const double* src = h_src ? h_src + 2 * off : nullptr;
       if (staged) {
         // the slot's previous chunk must have reached the device
-        if (c >= kFileSlots) CK(cudaEventSynchronize(ctx->ev_copy[c - kFileSlots]));
-        double2* slot = ctx->h_fslots + (c % kFileSlots) * kH2DChunk;
+        if (c >= slots) CK(cudaEventSynchronize(ctx->ev_copy[c - slots]));
+        double2* slot = ctx->h_fslots + (c % slots) * chunk;
         if (!stage_bytes(fd, reinterpret_cast<const unsigned char*>(h_src),
                          reinterpret_cast<unsigned char*>(slot), off * sizeof(double2),
                          cnt * sizeof(double2), readers)) {
