@@ -47,15 +47,18 @@ struct RingMap {
   u64 chain_off[4];  // chain r's offset in the chains array
 };
 
+// (constant indices only: a dynamically indexed parameter or QuadInfo copy
+// would live in local memory)
 __device__ __forceinline__ double2 ring_at(const RingMap& M, const double2* __restrict__ chains,
                                            const QuadInfo& qi, u64 i) {
-  int r = 0;
-  r += i >= M.seg_begin[1];
-  r += i >= M.seg_begin[2];
-  r += i >= M.seg_begin[3];
-  const u64 j = i - M.seg_begin[r];
-  if (j == 0) return make_double2(qi.q[2 * r], qi.q[2 * r + 1]);
-  return chains[M.chain_off[r] + j - 1];
+  u64 sb = M.seg_begin[0], co = M.chain_off[0];
+  double cx = qi.q[0], cy = qi.q[1];
+  if (i >= M.seg_begin[1]) sb = M.seg_begin[1], co = M.chain_off[1], cx = qi.q[2], cy = qi.q[3];
+  if (i >= M.seg_begin[2]) sb = M.seg_begin[2], co = M.chain_off[2], cx = qi.q[4], cy = qi.q[5];
+  if (i >= M.seg_begin[3]) sb = M.seg_begin[3], co = M.chain_off[3], cx = qi.q[6], cy = qi.q[7];
+  const u64 j = i - sb;
+  if (j == 0) return make_double2(cx, cy);
+  return chains[co + j - 1];
 }
 
 __device__ __forceinline__ bool same2(double2 a, double2 b) { return a.x == b.x && a.y == b.y; }
@@ -80,24 +83,46 @@ __global__ __launch_bounds__(256) void k_convex_check(const double2* __restrict_
   bool good = true;
   u64 best = ~0ull;  // hull position of this thread's best candidate
   double2 bestp = make_double2(0.0, 0.0);
-  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (u64)gridDim.x * blockDim.x) {
-    const double2 rk = ring_at(M, chains, qi, k);
-    const double2 rp = ring_at(M, chains, qi, k == 0 ? N - 1 : k - 1);
+  // A warp covers 32 consecutive ring indices. Inside a chain (no corner in
+  // [base - 2, base + 32)) ring index i of segment r is chains[i - r - 1]:
+  // three plain loads, the two shifted ones L1 hits.
+  const int lane = threadIdx.x & 31;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 base = (u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < N; base += stride) {
+    const u64 k = base + lane;
+    const bool valid = k < N;
+    u64 sb = M.seg_begin[0], nx = M.seg_begin[1];
+    int r = 0;
+    if (base >= M.seg_begin[1]) r = 1, sb = M.seg_begin[1], nx = M.seg_begin[2];
+    if (base >= M.seg_begin[2]) r = 2, sb = M.seg_begin[2], nx = M.seg_begin[3];
+    if (base >= M.seg_begin[3]) r = 3, sb = M.seg_begin[3], nx = N;
+    double2 rk, rp, rpp;
+    if (base >= sb + 3 && base + 32 <= nx) {
+      const double2* p = chains + (base - (u64)r - 1) + lane;
+      rk = p[0];
+      rp = p[-1];
+      rpp = p[-2];
+    } else {
+      rk = ring_at(M, chains, qi, valid ? k : N - 1);
+      rp = ring_at(M, chains, qi, !valid || k == 0 ? N - 1 : k - 1);
+      rpp = valid && k >= 2 ? ring_at(M, chains, qi, k - 2) : rk;
+    }
+    if (!valid) continue;
     if (same2(rk, rp)) good = false;  // consecutive or wrap duplicate
     if (k == 2) {
       const double2 lo = lex_lt(r1, r0) ? r1 : r0, hi = lex_lt(r1, r0) ? r0 : r1;
       if (!(turn_val(lo.x, lo.y, hi.x, hi.y, rk.x, rk.y) != 0.0)) good = false;
       if (!(turn_val(r0.x, r0.y, r1.x, r1.y, rk.x, rk.y) > 0.0)) good = false;
     } else if (k >= 3) {
-      const double2 rpp = ring_at(M, chains, qi, k - 2);
       if (!(turn_val(rpp.x, rpp.y, rp.x, rp.y, rk.x, rk.y) > 0.0)) good = false;   // A_k
       if (turn_val(rp.x, rp.y, r0.x, r0.y, rk.x, rk.y) > 0.0) good = false;        // B_k
       if (turn_val(rk.x, rk.y, rp.x, rp.y, r0.x, r0.y) > 0.0) good = false;        // C_k
       if (!(turn_val(rk.x, rk.y, r0.x, r0.y, r1.x, r1.y) > 0.0)) good = false;    // D_k
     }
-    const u64 hp = k + 1 == N ? 0 : k + 1;
-    if (best == ~0ull || lex_lt(rk, bestp) || (same2(rk, bestp) && hp < best)) {
-      best = hp;
+    // a thread visits increasing k, so its hull positions k + 1 increase
+    // except the last ring index (hull position 0), which wins ties
+    if (best == ~0ull || lex_lt(rk, bestp) || (k + 1 == N && same2(rk, bestp))) {
+      best = k + 1 == N ? 0 : k + 1;
       bestp = rk;
     }
   }
@@ -136,21 +161,42 @@ __global__ __launch_bounds__(256) void k_convex_emit(const double2* __restrict__
                                                      int nblocks, double2* __restrict__ out) {
   const QuadInfo qi = *qinfo;
   const u64 N = M.seg_begin[4];
+  // block-wide (point, hull position) minimum over the block winners
+  __shared__ double sx[256], sy[256];
+  __shared__ u64 sp[256];
   __shared__ u64 s_start;
-  if (threadIdx.x == 0) {
-    u64 best = ~0ull;
-    double2 bp = make_double2(0.0, 0.0);
-    for (int b = 0; b < nblocks; ++b) {
-      const u64 hp = block_best[b];
-      if (hp == ~0ull) continue;
-      const double2 p = ring_at(M, chains, qi, hp == 0 ? N - 1 : hp - 1);
-      if (best == ~0ull || lex_lt(p, bp) || (same2(p, bp) && hp < best)) {
-        best = hp;
-        bp = p;
+  u64 best = ~0ull;
+  double2 bp = make_double2(0.0, 0.0);
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+    const u64 hp = block_best[b];
+    if (hp == ~0ull) continue;
+    const double2 p = ring_at(M, chains, qi, hp == 0 ? N - 1 : hp - 1);
+    if (best == ~0ull || lex_lt(p, bp) || (same2(p, bp) && hp < best)) {
+      best = hp;
+      bp = p;
+    }
+  }
+  sx[threadIdx.x] = bp.x;
+  sy[threadIdx.x] = bp.y;
+  sp[threadIdx.x] = best;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      const int o = threadIdx.x + s;
+      const double2 a = make_double2(sx[threadIdx.x], sy[threadIdx.x]);
+      const double2 b = make_double2(sx[o], sy[o]);
+      const bool take = sp[o] != ~0ull &&
+                        (sp[threadIdx.x] == ~0ull || lex_lt(b, a) ||
+                         (same2(a, b) && sp[o] < sp[threadIdx.x]));
+      if (take) {
+        sx[threadIdx.x] = b.x;
+        sy[threadIdx.x] = b.y;
+        sp[threadIdx.x] = sp[o];
       }
     }
-    s_start = best;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) s_start = sp[0];
   __syncthreads();
   const u64 start = s_start;
   for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < N; j += (u64)gridDim.x * blockDim.x) {
@@ -160,7 +206,7 @@ __global__ __launch_bounds__(256) void k_convex_emit(const double2* __restrict__
   }
 }
 
-int convex_blocks() { return device_limits().sms * 4; }
+int convex_blocks() { return device_limits().sms * 8; }
 
 void launch_convex_check(const double2* chains, const u64 kept[4], const QuadInfo* qinfo, u32* ok,
                          u64* block_best, cudaStream_t st) {

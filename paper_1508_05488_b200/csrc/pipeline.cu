@@ -161,6 +161,12 @@ struct chgpu_ctx {
   size_t tap_counts[4] = {0, 0, 0, 0};
   FilterPlan* d_plan = nullptr;  // device-side plan (FilterPlan; .spa alone on the sort path)
   size_t kept_hint = 0;          // chain points of the previous call (speculative D2H size)
+  // AUTO mode: the previous call of about this size overflowed the
+  // pre-filter (or, sent to the sort by this hint, kept a dense chain set),
+  // so this one goes straight to the full region sort instead of running
+  // K2 twice. Performance only: both paths give the same hull.
+  bool sort_hint = false;
+  size_t sort_hint_n = 0;
   // Pinned staging arena for host->device uploads of small host-built
   // tables (segments, plans, quads): every upload gets its own slice, so a
   // host buffer can be rewritten while earlier copies are still queued.
@@ -1039,6 +1045,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       chunk_count >= 1 &&
       (ctx->spa_mode == CHGPU_SPA_FILTER || ctx->spa_mode == CHGPU_SPA_FILTER_SORTED ||
        (ctx->spa_mode == CHGPU_SPA_AUTO && chunk_count <= n / 64));
+  const bool hinted = want_filter && ctx->spa_mode == CHGPU_SPA_AUTO && ctx->sort_hint &&
+                      n >= ctx->sort_hint_n / 2 && n / 2 <= ctx->sort_hint_n;
+  if (hinted) want_filter = false;
   int log2nb = want_filter ? filter_bits(n, chunk_count) : 0;
   // the bin scan is one cooperative launch: every CTA must be resident
   if (want_filter && bin_scan_blocks(log2nb) > (u32)device_limits().binscan_coop) {
@@ -1332,6 +1341,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     // ---- D2H of the chains, then polygon.cpp + melkman.cpp on the host.
     t_fin0 = std::chrono::steady_clock::now();
     ctx->kept_hint = kept;
+    // (a filter-path call that fit clears the sort hint; an overflow sets
+    // it; a hinted sort keeps it while the chains stay dense)
+    ctx->sort_hint = overflow || (hinted && kept > n / 64);
+    ctx->sort_hint_n = n;
     if (kept + 4 >= kConvexMin) {
       // Survivor-heavy: try Melkman's convex-position trajectory on the
       // device (k_convex.cu); on success the hull comes back canonical.
@@ -1543,6 +1556,7 @@ int chgpu_ctx_set_option(chgpu_ctx* ctx, int option, long long value) {
     case CHGPU_OPT_SPA_PATH:
       if (value < CHGPU_SPA_AUTO || value > CHGPU_SPA_FILTER_SORTED) break;
       ctx->spa_mode = (int)value;
+      ctx->sort_hint = false;
       return CHGPU_OK;
     case CHGPU_OPT_CHAINS_TAP:
       if (value != 0 && value != 1) break;

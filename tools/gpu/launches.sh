@@ -2,7 +2,7 @@
 # timeline; prints name + microseconds for the last N launches.
 N=${N:-12}
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c ${C:-80} --csv \
-  --log-file gpurun_out/launches_tl.csv python tools/gpu/timeline.py > /dev/null 2>&1
+  --log-file gpurun_out/launches_tl.csv python tools/gpu/timeline.py ${ARGS:-} > /dev/null 2>&1
 python - <<'PY'
 import csv, os
 rows = list(csv.reader(open("gpurun_out/launches_tl.csv")))

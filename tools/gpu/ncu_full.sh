@@ -4,7 +4,7 @@ TAG=$1; shift
 mkdir -p gpurun_out
 for K in "$@"; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 \
-    -o gpurun_out/full_${TAG}_$K python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-pageable \
+    -o gpurun_out/full_${TAG}_$K python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-pageable ${BENCH_ARGS:-} \
     > gpurun_out/ncu_${TAG}_$K.log 2>&1
   echo "$K rc=$?"
 done
