@@ -378,7 +378,10 @@ enum : int { kDigitK = 0, kDigitV = 1, kDigitQ = 2 };
 enum : int { kEqQ = 0, kEqPrim = 1 };
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 12;
+#ifndef CHGPU_SORT_ITEMS
+#define CHGPU_SORT_ITEMS 12
+#endif
+constexpr int kSortItems = CHGPU_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 3072
 constexpr int kDigits = 256;
 constexpr int kPasses = 8;

@@ -164,7 +164,10 @@ struct OnesweepSmem {
 // reduce-then-scan pass, reading those offsets from tile_prefix (written by
 // k_upsweep + k_colscan), so tiles never wait on each other.
 template <int kMode, bool kScan>
-__global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
+#ifndef CHGPU_SORT_MINB
+#define CHGPU_SORT_MINB 3
+#endif
+__global__ __launch_bounds__(kSortThreads, CHGPU_SORT_MINB) void k_onesweep(
     const u64* __restrict__ kin, const u64* __restrict__ vin, u64* __restrict__ kout,
     u64* __restrict__ vout, const SegDesc* __restrict__ segs, int nseg, int use_src,
     const u32* __restrict__ digit_excl, int pass, u64* __restrict__ status, u32 tag,
@@ -173,6 +176,9 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // reduce-then-scan: this (tile, digit)'s offset from k_colscan (digit-
+  // major), loaded now so its latency hides behind the tile load and ranking
+  const u32 scan_before = kScan ? __ldcg(rows + (size_t)tid * total_tiles + blockIdx.x) : 0u;
   if (tid == 0) {
     const u32 t = kScan ? blockIdx.x : atomicAdd(tile_ctr, 1u);
     S.tile = t;
@@ -273,7 +279,7 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
   // fence.acq_rel.gpu + flag store"; readers acquire the flag in one warp
   // and bar.sync before touching rows.
   if (kScan) {
-    before = rows[(size_t)tile * kDigits + b];
+    before = scan_before;
   } else if (tile == sd.tile_begin) {
     __stcg(inc + (size_t)tile * kDigits + b, tile_cnt);
     __syncthreads();
@@ -328,8 +334,24 @@ __global__ __launch_bounds__(kSortThreads, 3) void k_onesweep(
       store_status(status + tile, make_status(tag, kFlagPrefix, 0));
     }
   }
-  S.bin_base[b] =
-      sd.dst_off + digit_excl[((size_t)segi * kPasses + pass) * kDigits + b] + before - bexcl;
+  u32 dex = digit_excl[((size_t)segi * kPasses + pass) * kDigits + b];
+  if (kScan) {
+    // reduce-then-scan: k_colscan left the segment's raw digit totals of
+    // this pass there; their exclusive scan over digits is the digit base
+    u32 incl = dex;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();  // (S.wsum was read above for the tile's bin offsets)
+    if (lane == 31) S.wsum[warp] = incl;
+    __syncthreads();
+    u32 wp = 0;
+    for (int w = 0; w < warp; ++w) wp += S.wsum[w];
+    dex = wp + incl - dex;
+  }
+  S.bin_base[b] = sd.dst_off + dex + before - bexcl;
   __syncthreads();
 
   // Tile-sorted staging: keys, load positions and digits.
@@ -621,31 +643,42 @@ __global__ __launch_bounds__(kSortThreads) void k_upsweep(const u64* __restrict_
     if (i < cnt) atomicAdd(&h[digit_of<kMode>(sd, kk[j], kk[j], pass)], 1u);
   }
   __syncthreads();
-  counts[(size_t)tile * kDigits + threadIdx.x] = h[threadIdx.x];
+  counts[(size_t)threadIdx.x * gridDim.x + tile] = h[threadIdx.x];  // column-major: [digit][tile]
 }
 
-// Column scan: for digit d (one block each), the exclusive prefix of
-// counts[t][d] over the tiles of each segment, in place.
-__global__ __launch_bounds__(1024) void k_colscan(u32* __restrict__ counts,
-                                                  const SegDesc* __restrict__ segs, int nseg,
-                                                  u32 total_tiles) {
-  const u32 d = blockIdx.x;
+// Column scan: for digit d and segment s (one block each), the exclusive
+// prefix of counts[d][t] over the segment's tiles, in place, and the
+// segment's digit total (into totals, slot [s][pass][d]). The column is
+// contiguous (k_upsweep writes digit-major) and each thread scans kColItems
+// consecutive tiles, so a segment of up to 2048 tiles is one block scan.
+constexpr int kColItems = 8;
+__global__ __launch_bounds__(256) void k_colscan(u32* __restrict__ counts,
+                                                 const SegDesc* __restrict__ segs, int nseg,
+                                                 u32 total_tiles, u32* __restrict__ totals,
+                                                 int pass) {
+  u32* const col = counts + (size_t)blockIdx.x * total_tiles;
   __shared__ u32 wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int s = 0; s < nseg; ++s) {
+  for (int s = blockIdx.y; s < nseg; s += gridDim.y) {
     const u32 tb = segs[s].tile_begin;
     const u32 te = (s + 1 < nseg) ? segs[s + 1].tile_begin : total_tiles;
     u32 carry = 0;
-    for (u32 t0 = tb; t0 < te; t0 += blockDim.x) {
-      const u32 t = t0 + threadIdx.x;
-      const u32 x0 = t < te ? counts[(size_t)t * kDigits + d] : 0u;
-      u32 x = x0;
+    for (u32 t0 = tb; t0 < te; t0 += blockDim.x * kColItems) {
+      const u32 t = t0 + threadIdx.x * kColItems;
+      u32 x[kColItems];
+      u32 sum = 0;
+#pragma unroll
+      for (int j = 0; j < kColItems; ++j) {
+        x[j] = t + j < te ? col[t + j] : 0u;
+        sum += x[j];
+      }
+      u32 incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      if (lane == 31) wsum[warp] = x;
+      if (lane == 31) wsum[warp] = incl;
       __syncthreads();
       u32 pre = 0, tot = 0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
@@ -653,10 +686,16 @@ __global__ __launch_bounds__(1024) void k_colscan(u32* __restrict__ counts,
         pre += (w < warp) ? ws : 0u;
         tot += ws;
       }
-      if (t < te) counts[(size_t)t * kDigits + d] = carry + pre + x - x0;
+      u32 run = carry + pre + incl - sum;
+#pragma unroll
+      for (int j = 0; j < kColItems; ++j) {
+        if (t + j < te) col[t + j] = run;
+        run += x[j];
+      }
       carry += tot;
       __syncthreads();
     }
+    if (threadIdx.x == 0) totals[((size_t)s * kPasses + pass) * kDigits + blockIdx.x] = carry;
   }
 }
 
@@ -666,7 +705,9 @@ static void lsd_pass_launch(const u64* kin, const u64* vin, u64* kout, u64* vout
                             const u32* digit_excl, int pass, u32* counts, cudaStream_t st) {
   k_upsweep<kMode><<<total_tiles, kSortThreads, 0, st>>>(kin, vin, segs, nseg, use_src, pass,
                                                          counts);
-  k_colscan<<<kDigits, 1024, 0, st>>>(counts, segs, nseg, total_tiles);
+  // (the segment totals go where the downsweep reads its digit bases)
+  k_colscan<<<dim3(kDigits, (unsigned)nseg), 256, 0, st>>>(counts, segs, nseg, total_tiles,
+                                                           const_cast<u32*>(digit_excl), pass);
   onesweep_launch<kMode, true>(kin, vin, kout, vout, segs, nseg, total_tiles, use_src, digit_excl,
                                pass, nullptr, 0, nullptr, counts, st);
 }

@@ -302,6 +302,315 @@ __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ 
 }
 
 
+// ------------------------------------------------------------------ SPA, tile scan
+//
+// The same filter as one pass over the sorted records, whatever the chunk
+// sizes: a CTA takes 4096 consecutive records (16 per thread), and the
+// running threshold is a segmented prefix-max over the guarded key w
+// (wkey: every region's SPA is a running MAX of w, steps_back <=> w < t),
+// reset at every chunk head to the chunk's seed. Across tiles it is carried
+// by a decoupled look-back over (any head, max w) pairs; a second look-back
+// over the kept counts places the tile's kept points, which are decoded,
+// staged in shared memory and written once, coalesced, to their final,
+// region-ordered place: no scratch copy and no gather pass.
+
+#ifndef CHGPU_SPA_NOLB
+#define CHGPU_SPA_NOLB 0
+#endif
+constexpr int kTileThreads = 256;
+constexpr int kTileItems = 16;
+constexpr int kTileRecs = kTileThreads * kTileItems;
+
+struct SpaTileSmem {
+  double2 out[kTileRecs];   // the tile's kept points, in order
+  u64 wx[kTileThreads / 32];
+  u32 wf[kTileThreads / 32];
+  u32 wk[kTileThreads / 32];
+  u64 carry_x;
+  u64 rend[4], cs[4], wseed[4];  // region ends, chunk sizes, seeds as w
+  u32 tile, kept_excl, last;
+};
+
+// Staging index swizzle: a thread's kept points are consecutive, so the
+// lanes of one store are 16 records apart; the XOR spreads them over the
+// banks (the copy-out reads with the same map, conflict-free).
+__device__ __forceinline__ u32 stage_slot(u32 i) { return i ^ ((i >> 4) & 7u); }
+
+// (F, X) pairs: F = a chunk head was seen, X = max w since the last head.
+__device__ __forceinline__ void seg_max(u32& fa, u64& xa, u32 fb, u64 xb) {
+  xa = fb ? xb : (xb > xa ? xb : xa);
+  fa |= fb;
+}
+
+__device__ __forceinline__ u64 ld_cg_u64(const u64* p) { return __ldcg(p); }
+
+__global__ __launch_bounds__(kTileThreads) void k_spa_tile(
+    const u64* __restrict__ k, const u64* __restrict__ v, const SpaPlan plan, u64 total,
+    u64* __restrict__ status, u32 tag, u32 ntiles, u64* __restrict__ pay, u32* __restrict__ ticket,
+    double2* __restrict__ out, unsigned long long* __restrict__ kept_counts) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SpaTileSmem& S = *reinterpret_cast<SpaTileSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) S.tile = atomicAdd(ticket, 1u);
+  if (tid < 4) {
+    S.rend[tid] = plan.off[tid] + plan.m[tid];
+    S.cs[tid] = plan.chunk_size[tid];
+    S.wseed[tid] = wkey(tid + 1, (tid == 0 || tid == 3) ? ~ord_enc(plan.seed[tid])
+                                                         : ord_enc(plan.seed[tid]));
+  }
+  __syncthreads();
+  u64* const pay_agg = pay;
+  u64* const pay_inc = pay + ntiles;
+  // tiles in ticket order: a tile only waits on lower tickets, all taken by
+  // CTAs that are already running
+  const u32 tile = S.tile;
+  const u64 i0 = (u64)tile * kTileRecs + (u64)tid * kTileItems;
+
+  // region (0-based) and chunk position of the thread's first record
+  int r = 0;
+  while (r < 3 && i0 >= S.rend[r]) ++r;
+  u64 cs = S.cs[r], rend = S.rend[r];
+  const u64 roff = r ? S.rend[r - 1] : 0;
+  const u64 rel = i0 >= roff ? i0 - roff : 0;
+  u64 pos = rel % cs;
+  bool first_chunk = rel < cs;
+
+  u64 w[kTileItems];
+  if (i0 + kTileItems <= total) {
+    const ulonglong2* vp = reinterpret_cast<const ulonglong2*>(v + i0);
+#pragma unroll
+    for (int j = 0; j < kTileItems / 2; ++j) {
+      const ulonglong2 t = vp[j];
+      w[2 * j] = t.x;
+      w[2 * j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) w[j] = i0 + j < total ? v[i0 + j] : 0ull;
+  }
+  // per record: head bit, first-chunk bit, region (2 bits)
+  u32 heads = 0, firsts = 0, regs = 0, F = 0;
+  u64 X = 0;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) {
+    const u64 i = i0 + j;
+    if (i < total) {
+      if (i == rend) {  // next non-empty region
+        while (r < 3 && i >= S.rend[r]) ++r;
+        cs = S.cs[r];
+        rend = S.rend[r];
+        pos = 0;
+        first_chunk = true;
+      } else if (pos == cs) {
+        pos = 0;
+        first_chunk = false;
+      }
+      w[j] = wkey(r + 1, w[j]);
+      regs |= (u32)r << (2 * j);
+      if (pos == 0) {
+        heads |= 1u << j;
+        if (first_chunk) firsts |= 1u << j;
+        const u64 seed = first_chunk ? S.wseed[r] : 0ull;
+        X = w[j] > seed ? w[j] : seed;
+        F = 1;
+      } else {
+        X = w[j] > X ? w[j] : X;
+      }
+      ++pos;
+    }
+  }
+  // block scan of the (F, X) pairs: warp shuffles, then the warp totals
+  u32 fi = F;
+  u64 xi = X;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 fy = __shfl_up_sync(0xffffffffu, fi, o);
+    const u64 xy = __shfl_up_sync(0xffffffffu, xi, o);
+    if (lane >= o) {
+      u32 f2 = fy;
+      u64 x2 = xy;
+      seg_max(f2, x2, fi, xi);
+      fi = f2;
+      xi = x2;
+    }
+  }
+  if (lane == 31) {
+    S.wf[warp] = fi;
+    S.wx[warp] = xi;
+  }
+  u32 fe = __shfl_up_sync(0xffffffffu, fi, 1);  // warp-exclusive
+  u64 xe = __shfl_up_sync(0xffffffffu, xi, 1);
+  if (lane == 0) fe = 0, xe = 0;
+  __syncthreads();
+  u32 fw = 0, ft = 0;  // block-exclusive for this warp; tile aggregate
+  u64 xw = 0, xt = 0;
+  for (int q = 0; q < kTileThreads / 32; ++q) {
+    if (q == warp) fw = ft, xw = xt;
+    seg_max(ft, xt, S.wf[q], S.wx[q]);
+  }
+  seg_max(fw, xw, fe, xe);  // this thread's block-exclusive prefix
+
+  // look-back 1: the carry into the tile
+  if (warp == 0) {
+    u64 carry = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        __stcg(pay_inc, xt);
+        fence_acq_rel_gpu();
+        store_status(status, make_status(tag, kFlagPrefix, ft));
+      }
+    } else {
+      if (lane == 0) {
+        __stcg(pay_agg + tile, xt);
+        fence_acq_rel_gpu();
+        store_status(status + tile, make_status(tag, kFlagAgg, ft));
+      }
+      int base = CHGPU_SPA_NOLB ? -1 : (int)tile - 1;  // (NOLB: timing experiment only)
+      while (true) {
+        const int j = base - lane;
+        u32 flag = kFlagPrefix, fj = 1;
+        if (j >= 0) {
+          u64 st;
+          do {
+            st = load_status(status + j);
+            flag = status_flag(st, tag);
+          } while (flag == kFlagNone);
+          fj = (u32)st;
+        }
+        const unsigned stopm = __ballot_sync(0xffffffffu, flag == kFlagPrefix || fj != 0);
+        const int stop = stopm ? __ffs(stopm) - 1 : 31;
+        fence_acq_rel_gpu();  // acquire for the payloads of the flags seen
+        u64 xj = 0;
+        if (j >= 0 && lane <= stop) xj = ld_cg_u64((flag == kFlagPrefix ? pay_inc : pay_agg) + j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const u64 y = __shfl_xor_sync(0xffffffffu, xj, o);
+          xj = y > xj ? y : xj;
+        }
+        carry = xj > carry ? xj : carry;
+        if (stopm) break;
+        base -= 32;
+      }
+      if (lane == 0) {
+        u32 fin = 1;
+        u64 xin = carry;
+        seg_max(fin, xin, ft, xt);
+        __stcg(pay_inc + tile, xin);
+        fence_acq_rel_gpu();
+        store_status(status + tile, make_status(tag, kFlagPrefix, 1));
+      }
+    }
+    if (lane == 0) S.carry_x = carry;
+  }
+  __syncthreads();
+  // the thread's exclusive threshold, then the keep test per record
+  u64 t = fw ? xw : (xw > S.carry_x ? xw : S.carry_x);
+  u32 kmask = 0;
+#pragma unroll
+  for (int j = 0; j < kTileItems; ++j) {
+    if (i0 + j < total) {
+      if (heads & (1u << j)) {
+        const int rj = (regs >> (2 * j)) & 3;
+        t = (firsts & (1u << j)) ? S.wseed[rj] : 0ull;
+      }
+      if (w[j] >= t) kmask |= 1u << j;
+      t = w[j] > t ? w[j] : t;
+    }
+  }
+  // block-exclusive kept positions
+  const u32 nk = __popc(kmask);
+  u32 ki = nk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, ki, o);
+    if (lane >= o) ki += y;
+  }
+  if (lane == 31) S.wk[warp] = ki;
+  __syncthreads();
+  u32 kw = 0, kt = 0;
+  for (int q = 0; q < kTileThreads / 32; ++q) {
+    if (q == warp) kw = kt;
+    kt += S.wk[q];
+  }
+  const u32 kex = kw + ki - nk;
+  // the kept records' k words, loaded before look-back 2 so their latency
+  // hides behind it
+  u64 kk[kTileItems];
+  if (nk) {
+    if (i0 + kTileItems <= total) {
+      const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(k + i0);
+#pragma unroll
+      for (int j = 0; j < kTileItems / 2; ++j) {
+        const ulonglong2 q = kp[j];
+        kk[2 * j] = q.x;
+        kk[2 * j + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kTileItems; ++j) kk[j] = i0 + j < total ? k[i0 + j] : 0ull;
+    }
+  }
+  // look-back 2: the kept points before the tile
+  if (warp == 0) {
+    u64* const col = status + ntiles;
+    u32 excl = 0;
+    if (tile == 0) {
+      if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, kt));
+    } else {
+      if (lane == 0) store_status(col + tile, make_status(tag, kFlagAgg, kt));
+      excl = CHGPU_SPA_NOLB ? 0u : warp_lookback(col, 1, (int)tile, 0, tag);
+      if (lane == 0) store_status(col + tile, make_status(tag, kFlagPrefix, excl + kt));
+    }
+    if (lane == 0) S.kept_excl = excl;
+  }
+  // decode the kept records into the staging area. v is w except where
+  // wkey folded -0.0 onto +0.0 (the target value is ambiguous there: the
+  // reference keeps the original bits, so those are re-read)
+  if (nk) {
+    u32 o = kex;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      if (kmask & (1u << j)) {
+        const int rj = (regs >> (2 * j)) & 3;
+        const u64 fold = (rj == 0 || rj == 3) ? 0x7FFFFFFFFFFFFFFFull : 0x8000000000000000ull;
+        const u64 vj = w[j] == fold ? v[i0 + j] : w[j];
+        double px, py;
+        decode_point(rj + 1, kk[j], vj, px, py);
+        S.out[stage_slot(o++)] = make_double2(px, py);
+      }
+    }
+  }
+  __syncthreads();
+  const u64 gbase = S.kept_excl;
+  // per-region kept counts: + the kept position after the region's last
+  // record, - the one before its first (kept_counts starts at zero)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (!plan.m[q]) continue;
+    const u64 a = plan.off[q], e = S.rend[q] - 1;
+    if (a >= i0 && a < i0 + kTileItems)
+      atomicAdd(kept_counts + q,
+                0ull - (gbase + kex + __popc(kmask & ((1u << (int)(a - i0)) - 1u))));
+    if (e >= i0 && e < i0 + kTileItems)
+      atomicAdd(kept_counts + q, gbase + kex + __popc(kmask & ((2u << (int)(e - i0)) - 1u)));
+  }
+  for (u32 i = tid; i < kt; i += kTileThreads) out[gbase + i] = S.out[stage_slot(i)];
+}
+
+void launch_spa_tile(const u64* k, const u64* v, const SpaPlan& plan, u64 total, u64* status,
+                     u32 tag, u64* pay, u32* ticket, double2* out,
+                     unsigned long long* kept_counts, cudaStream_t st) {
+  const u64 tiles = (total + kTileRecs - 1) / kTileRecs;
+  if (tiles == 0) return;
+  k_spa_tile<<<(unsigned)tiles, kTileThreads, sizeof(SpaTileSmem), st>>>(
+      k, v, plan, total, status, tag, (u32)tiles, pay, ticket, out, kept_counts);
+}
+
+cudaError_t configure_spa_kernels() {
+  return cudaFuncSetAttribute((const void*)k_spa_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(SpaTileSmem));
+}
+
 void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
                      double2* scratch, u32* chunk_kept, u32* offs,
                      unsigned long long* kept_counts, double2* out, cudaStream_t st) {

@@ -108,6 +108,7 @@ struct DeviceLimits {
 };
 const DeviceLimits& device_limits();
 cudaError_t configure_sort_kernels();
+cudaError_t configure_spa_kernels();
 cudaError_t configure_filter_kernels(DeviceLimits* lim);
 
 // K1
@@ -158,6 +159,9 @@ size_t group_run_bytes();
 void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
                      double2* scratch, u32* chunk_kept, u32* offs,
                      unsigned long long* kept_counts, double2* out, cudaStream_t st);
+void launch_spa_tile(const u64* k, const u64* v, const SpaPlan& plan, u64 total, u64* status,
+                     u32 tag, u64* pay, u32* ticket, double2* out,
+                     unsigned long long* kept_counts, cudaStream_t st);
 void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status, u32 tag,
                    u32* tile_ctr, unsigned long long* total, cudaStream_t st);
 

@@ -432,11 +432,16 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
   if (tiles == 0) return CHGPU_OK;
   const int mask_slot = take_ctr(ctx);
   TRY(upload(ctx, ctx->d_segs, ctx->h_segs, nseg * sizeof(SegDesc)));
-  CK(cudaMemsetAsync(ctx->d_hist, 0, (size_t)nseg * kPasses * kDigits * sizeof(u32), ctx->st));
-  launch_hist(ksrc, vsrc, ctx->d_segs, nseg, tiles, mode, npasses, 1, ctx->d_hist, ctx->st);
-  launch_hist_scan(ctx->d_hist, ctx->d_segs, nseg, npasses, ctx->d_digit_excl,
-                   ctx->d_ctr + mask_slot, ctx->st);
-  ctx->launches += 2;
+  // reduce-then-scan passes take their digit bases from the column scan:
+  // the global histogram only tells which passes a full-key sort may skip
+  const bool scan_passes = lsd_scan_passes() && nseg <= 64;
+  if (!(scan_passes && all_passes)) {
+    CK(cudaMemsetAsync(ctx->d_hist, 0, (size_t)nseg * kPasses * kDigits * sizeof(u32), ctx->st));
+    launch_hist(ksrc, vsrc, ctx->d_segs, nseg, tiles, mode, npasses, 1, ctx->d_hist, ctx->st);
+    launch_hist_scan(ctx->d_hist, ctx->d_segs, nseg, npasses, ctx->d_digit_excl,
+                     ctx->d_ctr + mask_slot, ctx->st);
+    ctx->launches += 2;
+  }
   if (timed) CK(cudaEventRecord(ctx->ev[3], ctx->st));
   // Bucket passes always move data; a full-key sort skips digit positions
   // that are constant in every segment (one host round trip).
@@ -450,7 +455,7 @@ int radix_sort(chgpu_ctx* ctx, int nseg, const u64* ksrc, const u64* vsrc, u64* 
     if (!(mask & (1u << p))) continue;
     u64* ko = (done % 2 == 0) ? kA : kB;
     u64* vo = (done % 2 == 0) ? vA : vB;
-    if (lsd_scan_passes() && nseg <= 64) {
+    if (scan_passes) {
       // reduce-then-scan: no inter-tile waiting (3 launches per pass)
       launch_lsd_pass(kin, vin, ko, vo, ctx->d_segs, nseg, tiles, use_src, mode,
                       ctx->d_digit_excl, p, ctx->d_raw, ctx->st);
@@ -620,13 +625,23 @@ int sort_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, bool timed,
   return sort_segments(ctx, 4, qbits, timed, defer, out);
 }
 
+// Largest region (log2 records) sorted on a 24-bit quantized primary (3
+// passes) instead of 32 bits (4): more equal-q groups for the fix-up.
+int q24_log2() {
+  static const int v = [] {
+    const char* e = std::getenv("CHGPU_Q24_LOG2");  // tuning knob
+    return e ? std::max(0, std::min(30, std::atoi(e))) : 22;
+  }();
+  return v;
+}
+
 // Region segments of the K2 two-ended layout, with quantizers.
 int plan_regions(chgpu_ctx* ctx, const u64 m[4], const double* quad, int* qbits) {
   TRY(ensure_segs(ctx, 4));
   const u64 cap = ctx->cap;
   const u64 src_off[4] = {0, cap - m[1], cap, 2 * cap - m[3]};
   const u64 mmax = std::max(std::max(m[0], m[1]), std::max(m[2], m[3]));
-  *qbits = mmax <= (u64(1) << 22) ? 24 : 32;
+  *qbits = mmax <= (u64(1) << q24_log2()) ? 24 : 32;
   u64 dst = 0;
   for (int s = 0; s < 4; ++s) {
     ctx->h_segs[s] = make_seg(src_off[s], dst, m[s], s + 1);
@@ -687,13 +702,28 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
 // d_kept (region order) and per-region counts in d_u64[0..3]. The input
 // copy d_pts is dead by now and serves as the per-chunk scratch.
 int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
-  u32* chunk_kept = ctx->d_raw;
-  u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
+  static const bool warp_spa = [] {
+    const char* e = std::getenv("CHGPU_SPA_WARP");  // A/B knob: warp per chunk + gather
+    return e && std::atoi(e) != 0;
+  }();
   SpaPlan* d_splan = &ctx->d_plan->spa;
   TRY(upload(ctx, d_splan, &plan, sizeof(SpaPlan)));
-  launch_spa_warp(kF, vF, d_splan, plan.total_chunks, ctx->d_pts, chunk_kept, offs, ctx->d_u64,
-                  ctx->d_kept, ctx->st);
-  if (plan.total_chunks) ctx->launches += 3;
+  if (warp_spa) {
+    u32* chunk_kept = ctx->d_raw;
+    u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
+    launch_spa_warp(kF, vF, d_splan, plan.total_chunks, ctx->d_pts, chunk_kept, offs, ctx->d_u64,
+                    ctx->d_kept, ctx->st);
+    if (plan.total_chunks) ctx->launches += 3;
+  } else {
+    const u64 total = plan.m[0] + plan.m[1] + plan.m[2] + plan.m[3];
+    const int ticket = take_ctr(ctx);
+    // (the kept counts are accumulated: + region end, - region start)
+    CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), ctx->st));
+    launch_spa_tile(kF, vF, plan, total, ctx->d_status, next_tag(ctx),
+                    reinterpret_cast<u64*>(ctx->d_raw), ctx->d_ctr + ticket, ctx->d_kept,
+                    ctx->d_u64, ctx->st);
+    if (total) ctx->launches += 1;
+  }
   CK(cudaGetLastError());
   return CHGPU_OK;
 }
@@ -1447,6 +1477,7 @@ const DeviceLimits& device_limits() {
     DeviceLimits& d = lim[dev];
     cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = configure_sort_kernels();
+    if (e == cudaSuccess) e = configure_spa_kernels();
     if (e == cudaSuccess) e = configure_filter_kernels(&d);
     if (e == cudaSuccess) d.k1_wave = extremes_wave(d.sms);
     d.status = e;
