@@ -1111,7 +1111,11 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       const char* e = std::getenv("CHGPU_STAGE_SPLIT");  // tuning knob (log2)
       return e ? std::max(0, std::min(4, std::atoi(e))) : 2;
     }();
-    const size_t chunk = staged ? kH2DChunk >> stage_split : kH2DChunk;
+    static const size_t pinned_chunk = [] {
+      const char* e = std::getenv("CHGPU_H2D_CHUNK_LOG2");  // tuning knob (points, log2)
+      return e ? size_t(1) << std::max(16, std::min(30, std::atoi(e))) : kH2DChunk;
+    }();
+    const size_t chunk = staged ? kH2DChunk >> stage_split : pinned_chunk;
     const size_t slots = staged ? kFileSlots << stage_split : kFileSlots;
     const size_t nchunks = (n + chunk - 1) / chunk;
     const int per = std::max(1, std::min(kPartialBlocks, kMaxPartials / (int)nchunks));

@@ -143,6 +143,41 @@ def _ctrl_group(group):
     return _CTRL_GROUPS[key]
 
 
+_PINNED = {}
+
+
+def _pinned(dev, key, rows):
+    """A reused pinned host buffer of at least `rows` points."""
+    buf = _PINNED.get((dev, key))
+    if buf is None or buf.shape[0] < rows:
+        buf = torch.empty((max(rows, 1 << 16), 2), dtype=torch.float64, pin_memory=True)
+        _PINNED[(dev, key)] = buf
+    return buf
+
+
+def _pinned_copy(t, key):
+    """Starts the copy of device points t into a pinned buffer (on the
+    current stream); the caller synchronises before reading it."""
+    out = _pinned(t.device, key, t.shape[0])[: t.shape[0]]
+    out.copy_(t, non_blocking=True)
+    return out
+
+
+def _to_host(gathered, counts):
+    """The gathered chains on the host: device runs go through one reused
+    pinned buffer (a pageable .cpu() per run stages every byte twice)."""
+    if not gathered or not gathered[0].is_cuda:
+        return gathered
+    buf = _pinned(gathered[0].device, "peers", sum(c[0] for c in counts))
+    out, off = [], 0
+    for g, c in zip(gathered, counts):
+        out.append(buf[off: off + c[0]])
+        out[-1].copy_(g[: c[0]], non_blocking=True)
+        off += c[0]
+    torch.cuda.current_stream(dev).synchronize()
+    return out
+
+
 def _device_for(group) -> torch.device:
     backend = dist.get_backend(group)
     if backend == "nccl":
@@ -171,6 +206,9 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
     ch, kc = ops.chains(quad, chunk_count)
     ch = (ch if isinstance(ch, torch.Tensor)
           else torch.from_numpy(np.ascontiguousarray(ch, np.float64))).reshape(-1, 2)
+    # rank 0's own chains never need the exchange: their copy to the host
+    # starts now and overlaps it
+    own = _pinned_copy(ch, "own") if rank == 0 and ch.is_cuda else None
 
     # exchange 2: chains to rank 0 (sizes and region counts first, then
     # padded payloads)
@@ -187,10 +225,11 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
             buf[: ch.shape[0]] = ch.to(dev)
     gathered = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
     if dist.get_backend(group) == "nccl":
-        # NCCL gather: emulate with all_gather (the payload is tiny)
-        tmp = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(tmp, buf, group=group)
-        gathered = tmp if rank == 0 else None
+        # NCCL gather: emulate with all_gather (the payload is tiny), into
+        # one flat tensor (one launch, no per-rank output list)
+        flat = torch.empty((world * width, 2), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(flat, buf, group=group)
+        gathered = list(flat.view(world, width, 2)) if rank == 0 else None
     else:
         dist.gather(buf, gathered, dst=0, group=group)
     if rank != 0:
@@ -198,8 +237,14 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
     if len(frame_vertices(quad)) > 2:
         # each region's sorted runs merged, the ring closed with the global
         # frame, Melkman on the host (the chains are ~35K points per rank)
-        runs = [(g[: c[0]].cpu().numpy() if g.is_cuda else g[: c[0]].numpy(), c[1:])
-                for g, c in zip(gathered, counts)]
+        peers = _to_host(gathered[1:], counts[1:])
+        if own is not None:
+            torch.cuda.current_stream(ch.device).synchronize()
+            mine_host = own.numpy()
+        else:
+            mine_host = gathered[0][: counts[0][0]].numpy()
+        runs = [(mine_host, counts[0][1:])] + [(g[: c[0]].numpy(), c[1:])
+                                              for g, c in zip(peers, counts[1:])]
         return ops.merge(runs, quad)
     frame = torch.from_numpy(frame_vertices(quad)).to(dev)
     union = torch.cat([g[: c[0]] for g, c in zip(gathered, counts)] + [frame], dim=0)
