@@ -22,6 +22,12 @@ for K in k_extremes_partial k_classify_survivors k_bin_scan k_filter k_spa_small
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 -o $O/full_$K \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-pageable > $O/ncu_$K.log 2>&1
 done
+# the sort path (20M circle: every point survives and is kept)
+for K in k_classify_compact k_upsweep k_colscan k_onesweep k_group_scan k_spa_tile k_convex_check k_convex_emit; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 -o $O/circle_$K \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-pageable --dist circle > $O/ncu_circle_$K.log 2>&1
+done
+python tools/ncu_summary.py $O/circle_*.ncu-rep > $O/ncu_circle_summary.txt 2>&1
 python tools/ncu_summary.py $O/full_*.ncu-rep > $O/ncu_full_summary.txt 2>&1
 python tools/make_traffic.py $O/traffic.json $O/full_*.ncu-rep > /dev/null 2>&1
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -c "
@@ -30,7 +36,13 @@ import paper_1508_05488_b200 as P
 c=P.Context(0)
 for d,n in (('uniform_square',300000),('uniform_disk',100000),('duplicates_heavy',20000),('circle',100000),('gaussian',200000)):
     r=c.convex_hull(P.generate(d,n,1)); print(d, r.stats.n_hull, r.diag.spa_path, r.diag.convex_fast_path)
+r=c.convex_hull(P.generate('circle',100000,1)); print('circle again (sort hint)', r.stats.n_hull, r.diag.spa_path)
 c.set_spa_path(P.SPA_FILTER_SORTED)
 r=c.convex_hull(P.generate('uniform_square',300000,2)); print('filter_sorted', r.stats.n_hull)
+c.set_spa_path(P.SPA_SORT)
+for cc in (1, 7, 1024):
+    r=c.convex_hull(P.generate('uniform_disk',300000,3), P.PipelineConfig(chunk_count=cc)); print('sort path cc', cc, r.stats.n_hull, r.diag.spa_path)
 " > $O/memcheck.log 2>&1; echo memcheck=$? >> $O/memcheck.log
+# bench lines: the JSON line only (NCCL prints its version first)
+for f in $O/*.json; do grep '^{' $f | tail -1 > $f.tmp && mv $f.tmp $f; done
 echo done
