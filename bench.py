@@ -496,14 +496,18 @@ def main():
             })
         else:
             pass_ms = t["t_passes_ms"] / max(d.sort_passes, 1)
+            kept = sum(d.kept_counts)
             kernels.update({
-                "k3_hist": {"ms": t["t_hist_ms"], "bytes": 8 * s1, "basis": "8 B/record read"},
-                "k3_radix_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": 32 * s1,
-                                  "basis": "16 B/record read + 16 B/record write"},
+                # (the bucket passes take their digit bases from the column
+                # scans: no global histogram, this interval is the setup)
+                "k3_setup": {"ms": t["t_hist_ms"]},
+                "k3_radix_pass": {"ms": pass_ms, "launches": d.sort_passes, "bytes": 40 * s1,
+                                  "basis": "per pass: k_upsweep 8 B/record read + k_colscan + "
+                                           "k_onesweep 16 B/record read + 16 B/record write"},
                 "k3_ties": {"ms": t["t_ties_ms"]},
-                "k4_spa": {"ms": t["t_spa_kernel_ms"],
-                           "bytes": 8 * s1 + 2 * s1 + 16 * sum(d.kept_counts),
-                           "basis": "8 B/record read + 16 B/kept write (+ flags)"},
+                "k4_spa": {"ms": t["t_spa_kernel_ms"], "bytes": 8 * s1 + 24 * kept,
+                           "basis": "k_spa_tile: 8 B/record read (v) + per kept record 8 B read "
+                                    "(k) + 16 B point write"},
             })
         for kv in kernels.values():
             if kv.get("bytes") and kv.get("ms"):

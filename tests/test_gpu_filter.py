@@ -119,6 +119,40 @@ def _ring_points(n, seed, r=1.0):
     return np.stack([r * np.cos(t), r * np.sin(t)], 1)
 
 
+def test_auto_sort_hint(product):
+    """AUTO mode: after a call that overflowed the pre-filter (20M on a
+    circle), a call of about the same size goes straight to the full sort
+    (one K2); the hint holds while the chains stay dense and clears after a
+    sparse one. Every call gives the reference's hull and counters."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    big = load_golden("big.json")
+    circ_case, uni_case = big[4], big[1]
+    assert circ_case["dist"] == "circle" and uni_case["dist"] == "uniform_square"
+    circ = product.generate("circle", circ_case["n"], circ_case["seed"])
+    uni = product.generate("uniform_square", uni_case["n"], uni_case["seed"])
+    ctx = product.Context(0)
+    paths = []
+    for pts, case in ((circ, circ_case), (circ, circ_case), (circ, circ_case), (uni, uni_case),
+                      (uni, uni_case)):
+        r = ctx.convex_hull(pts)
+        assert _counts(r) == case["counts"]
+        assert sha(r.hull.vertices) == case["hull_sha"]
+        paths.append(r.diag.spa_path)
+    # overflow, hinted sort twice, hinted sort (sparse chains: clears), filter
+    assert paths == [2, 0, 0, 0, 1], paths
+    r = ctx.convex_hull(circ)  # overflows again, sets the hint
+    assert r.diag.spa_path == 2
+    small = product.generate("circle", 2_000_000, 3)  # outside 2x of the hinted size
+    assert ctx.convex_hull(small).diag.spa_path != 0
+    r = ctx.convex_hull(circ)
+    assert r.diag.spa_path == 2  # (the hint, if any, now describes the small call)
+    ctx.set_spa_path(product.SPA_AUTO)  # setting the mode clears the hint
+    assert ctx.convex_hull(circ).diag.spa_path == 2
+    ctx.close()
+
+
 @pytest.mark.parametrize("case", ["circle", "circle_noisy", "square_edges", "duplicates",
                                   "near_flat_arc"])
 def test_convex_fast_path(gpu_ctx, product, oracle, case):
