@@ -234,6 +234,13 @@ int chgpu_generate(int dist, size_t n, uint64_t seed, double* out_xy);
 int chgpu_generate_range(int dist, size_t n, uint64_t seed, size_t begin, size_t count,
                          double* out_xy);
 
+/* Touches every page of [p, p + bytes) from the library's host staging
+ * threads, so that a fresh allocation (the C++ API's result vector of a
+ * survivor-heavy hull: 320 MB for 20M points) takes its first-touch page
+ * faults in parallel instead of inside a single-threaded copy. The bytes'
+ * contents are unspecified afterwards (the caller overwrites them). */
+void chgpu_host_prefault(void* p, size_t bytes);
+
 /* ---- sharded path (multi-GPU, one rank per GPU) ------------------------- */
 
 /* Local extremes of a device-resident shard with global tie-break indices:

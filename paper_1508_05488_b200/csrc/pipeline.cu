@@ -2042,6 +2042,19 @@ size_t slice_max() {
 
 extern "C" {
 
+void chgpu_host_prefault(void* p, size_t bytes) {
+  unsigned char* const b = static_cast<unsigned char*>(p);
+  if (!b || bytes == 0) return;
+  const size_t step = size_t(4) << 20;  // 4 MB per part
+  const int parts = (int)((bytes + step - 1) / step);
+  StagePool::get().run(parts, [&](int t) -> bool {
+    const size_t a = (size_t)t * step, e = std::min(bytes, a + step);
+    for (size_t o = a; o < e; o += 4096) b[o] = 0;
+    b[e - 1] = 0;
+    return true;
+  });
+}
+
 int chgpu_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
