@@ -238,6 +238,7 @@ __global__ __launch_bounds__(kSortThreads, CHGPU_SORT_MINB) void k_onesweep(
     }
     old = __shfl_sync(0xffffffffu, old, leader);
     code[j] = d | ((old + __popc(peers[j] & lanemask_lt())) << 8);
+    __syncwarp();  // (orders this leader's counter write before the next item's leader reads it)
   }
   __syncthreads();
 
