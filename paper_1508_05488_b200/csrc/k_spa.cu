@@ -314,15 +314,12 @@ __global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ 
 // staged in shared memory and written once, coalesced, to their final,
 // region-ordered place: no scratch copy and no gather pass.
 
-#ifndef CHGPU_SPA_NOLB
-#define CHGPU_SPA_NOLB 0
-#endif
 constexpr int kTileThreads = 256;
 constexpr int kTileItems = 16;
 constexpr int kTileRecs = kTileThreads * kTileItems;
 
 struct SpaTileSmem {
-  double2 out[kTileRecs];   // the tile's kept points, in order
+  unsigned short kidx[kTileRecs];  // the tile's kept records (tile offsets), in order
   u64 wx[kTileThreads / 32];
   u32 wf[kTileThreads / 32];
   u32 wk[kTileThreads / 32];
@@ -330,11 +327,6 @@ struct SpaTileSmem {
   u64 rend[4], cs[4], wseed[4];  // region ends, chunk sizes, seeds as w
   u32 tile, kept_excl, last;
 };
-
-// Staging index swizzle: a thread's kept points are consecutive, so the
-// lanes of one store are 16 records apart; the XOR spreads them over the
-// banks (the copy-out reads with the same map, conflict-free).
-__device__ __forceinline__ u32 stage_slot(u32 i) { return i ^ ((i >> 4) & 7u); }
 
 // (F, X) pairs: F = a chunk head was seen, X = max w since the last head.
 __device__ __forceinline__ void seg_max(u32& fa, u64& xa, u32 fb, u64 xb) {
@@ -344,7 +336,7 @@ __device__ __forceinline__ void seg_max(u32& fa, u64& xa, u32 fb, u64 xb) {
 
 __device__ __forceinline__ u64 ld_cg_u64(const u64* p) { return __ldcg(p); }
 
-__global__ __launch_bounds__(kTileThreads) void k_spa_tile(
+__global__ __launch_bounds__(kTileThreads, 4) void k_spa_tile(
     const u64* __restrict__ k, const u64* __restrict__ v, const SpaPlan plan, u64 total,
     u64* __restrict__ status, u32 tag, u32 ntiles, u64* __restrict__ pay, u32* __restrict__ ticket,
     double2* __restrict__ out, unsigned long long* __restrict__ kept_counts) {
@@ -465,7 +457,7 @@ __global__ __launch_bounds__(kTileThreads) void k_spa_tile(
         fence_acq_rel_gpu();
         store_status(status + tile, make_status(tag, kFlagAgg, ft));
       }
-      int base = CHGPU_SPA_NOLB ? -1 : (int)tile - 1;  // (NOLB: timing experiment only)
+      int base = (int)tile - 1;
       while (true) {
         const int j = base - lane;
         u32 flag = kFlagPrefix, fj = 1;
@@ -533,23 +525,6 @@ __global__ __launch_bounds__(kTileThreads) void k_spa_tile(
     kt += S.wk[q];
   }
   const u32 kex = kw + ki - nk;
-  // the kept records' k words, loaded before look-back 2 so their latency
-  // hides behind it
-  u64 kk[kTileItems];
-  if (nk) {
-    if (i0 + kTileItems <= total) {
-      const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(k + i0);
-#pragma unroll
-      for (int j = 0; j < kTileItems / 2; ++j) {
-        const ulonglong2 q = kp[j];
-        kk[2 * j] = q.x;
-        kk[2 * j + 1] = q.y;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kTileItems; ++j) kk[j] = i0 + j < total ? k[i0 + j] : 0ull;
-    }
-  }
   // look-back 2: the kept points before the tile
   if (warp == 0) {
     u64* const col = status + ntiles;
@@ -558,27 +533,17 @@ __global__ __launch_bounds__(kTileThreads) void k_spa_tile(
       if (lane == 0) store_status(col, make_status(tag, kFlagPrefix, kt));
     } else {
       if (lane == 0) store_status(col + tile, make_status(tag, kFlagAgg, kt));
-      excl = CHGPU_SPA_NOLB ? 0u : warp_lookback(col, 1, (int)tile, 0, tag);
+      excl = warp_lookback(col, 1, (int)tile, 0, tag);
       if (lane == 0) store_status(col + tile, make_status(tag, kFlagPrefix, excl + kt));
     }
     if (lane == 0) S.kept_excl = excl;
   }
-  // decode the kept records into the staging area. v is w except where
-  // wkey folded -0.0 onto +0.0 (the target value is ambiguous there: the
-  // reference keeps the original bits, so those are re-read)
-  if (nk) {
+  // the kept records' tile offsets, in order
+  {
     u32 o = kex;
 #pragma unroll
-    for (int j = 0; j < kTileItems; ++j) {
-      if (kmask & (1u << j)) {
-        const int rj = (regs >> (2 * j)) & 3;
-        const u64 fold = (rj == 0 || rj == 3) ? 0x7FFFFFFFFFFFFFFFull : 0x8000000000000000ull;
-        const u64 vj = w[j] == fold ? v[i0 + j] : w[j];
-        double px, py;
-        decode_point(rj + 1, kk[j], vj, px, py);
-        S.out[stage_slot(o++)] = make_double2(px, py);
-      }
-    }
+    for (int j = 0; j < kTileItems; ++j)
+      if (kmask & (1u << j)) S.kidx[o++] = (unsigned short)(tid * kTileItems + j);
   }
   __syncthreads();
   const u64 gbase = S.kept_excl;
@@ -594,7 +559,35 @@ __global__ __launch_bounds__(kTileThreads) void k_spa_tile(
     if (e >= i0 && e < i0 + kTileItems)
       atomicAdd(kept_counts + q, gbase + kex + __popc(kmask & ((2u << (int)(e - i0)) - 1u)));
   }
-  for (u32 i = tid; i < kt; i += kTileThreads) out[gbase + i] = S.out[stage_slot(i)];
+  // decoded and written in order, coalesced: consecutive threads take
+  // consecutive kept records (their k and v words re-read: L1/L2 hits)
+  // (four records per thread in flight: the loads are the latency here)
+  const u64 tbase = (u64)tile * kTileRecs;
+  for (u32 i0c = tid; i0c < kt; i0c += 4 * kTileThreads) {
+    u64 rec[4], kw[4], vw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const u32 i = i0c + q * kTileThreads;
+      rec[q] = tbase + (i < kt ? S.kidx[i] : 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = i0c + q * kTileThreads < kt;
+      kw[q] = ok ? k[rec[q]] : 0ull;
+      vw[q] = ok ? v[rec[q]] : 0ull;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const u32 i = i0c + q * kTileThreads;
+      if (i < kt) {
+        int rq = 0;
+        while (rq < 3 && rec[q] >= S.rend[rq]) ++rq;
+        double px, py;
+        decode_point(rq + 1, kw[q], vw[q], px, py);
+        out[gbase + i] = make_double2(px, py);
+      }
+    }
+  }
 }
 
 void launch_spa_tile(const u64* k, const u64* v, const SpaPlan& plan, u64 total, u64* status,
