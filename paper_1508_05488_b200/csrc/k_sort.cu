@@ -425,15 +425,14 @@ __device__ __forceinline__ u64 group_key(int eqmode, const SegDesc& s, u64 k) {
   return eqmode == kEqQ ? (u64)quantize(s, k) : canon_k(s.region, k);
 }
 
-// Detects group starts tile by tile and fixes each group on the spot, all
-// in shared memory: the tile's records plus a kSmallGroup halo are loaded
-// once (coalesced), the thread owning a group start insertion-sorts it in
-// shared memory when it holds at most kSmallGroup records and writes only
-// that group back; longer groups are queued for k_group_fix_medium.
+// Detects group starts tile by tile and fixes each group on the spot: the
+// group keys of the tile's records plus a kSmallGroup halo are computed
+// once (coalesced k reads) into shared memory, the thread owning a group
+// start insertion-sorts it in registers when it holds at most kSmallGroup
+// records (reading and writing only that group's k and v); longer groups
+// are queued for k_group_fix_medium.
 constexpr int kGroupWin = kSortTile + kSmallGroup + 1;
 struct GroupSmem {
-  u64 k[kGroupWin];
-  u64 v[kGroupWin];
   u64 g[kGroupWin + 1];  // g[0]: group key of the record before the tile
 };
 
@@ -457,12 +456,7 @@ __global__ __launch_bounds__(256) void k_group_scan(u64* __restrict__ k, u64* __
     s_found = 0;
     S.g[0] = e0 > 0 ? group_key(eqmode, sd, k[base - 1]) : ~0ull;
   }
-  for (u32 i = threadIdx.x; i < win; i += blockDim.x) {
-    const u64 kx = k[base + i];
-    S.k[i] = kx;
-    S.v[i] = v[base + i];
-    S.g[i + 1] = group_key(eqmode, sd, kx);
-  }
+  for (u32 i = threadIdx.x; i < win; i += blockDim.x) S.g[i + 1] = group_key(eqmode, sd, k[base + i]);
   __syncthreads();
   u32 found = 0;
   for (u32 i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -480,22 +474,26 @@ __global__ __launch_bounds__(256) void k_group_scan(u64* __restrict__ k, u64* __
       medium[atomicAdd(nmedium, 1u)] = GroupRun{a, len, s};
       continue;
     }
-  small:
-    for (u32 j = 1; j < len; ++j) {
-      const u64 kx = S.k[i + j], vx = S.v[i + j];
+  small : {
+    // (a few percent of the records: the group is sorted in registers,
+    // read and written back in global memory)
+    u64 gk[kSmallGroup], gv[kSmallGroup];
+    for (u32 j = 0; j < len; ++j) {
+      const u64 kx = k[base + i + j], vx = v[base + i + j];
       u32 t = j;
-      while (t > 0 && rec_less(sd.region, kx, vx, S.k[i + t - 1], S.v[i + t - 1])) {
-        S.k[i + t] = S.k[i + t - 1];
-        S.v[i + t] = S.v[i + t - 1];
+      while (t > 0 && rec_less(sd.region, kx, vx, gk[t - 1], gv[t - 1])) {
+        gk[t] = gk[t - 1];
+        gv[t] = gv[t - 1];
         --t;
       }
-      S.k[i + t] = kx;
-      S.v[i + t] = vx;
+      gk[t] = kx;
+      gv[t] = vx;
     }
     for (u32 j = 0; j < len; ++j) {
-      k[base + i + j] = S.k[i + j];
-      v[base + i + j] = S.v[i + j];
+      k[base + i + j] = gk[j];
+      v[base + i + j] = gv[j];
     }
+  }
   }
   if (found) atomicAdd(&s_found, found);
   __syncthreads();
