@@ -1246,7 +1246,8 @@ __global__ void k_spa_clocks_report() {
 // those of the earlier chunks of its own group. Decoded to points.
 __device__ void spa_emit_warp(u32 c, const FilterPlan* __restrict__ P_p, const u64* __restrict__ sk,
                               const u64* __restrict__ sv, const u32* __restrict__ chunk_kept,
-                              const u32* __restrict__ group_kept, double2* __restrict__ out) {
+                              const u32* __restrict__ group_kept, double2* __restrict__ out,
+                              double2* hout, u32 hcap) {
   const SpaPlan& plan = P_p->spa;
   const int lane = threadIdx.x & 31;
   if (c >= plan.total_chunks) return;
@@ -1267,6 +1268,8 @@ __device__ void spa_emit_warp(u32 c, const FilterPlan* __restrict__ P_p, const u
     double px, py;
     decode_point(region, sk[src + i], sv[src + i], px, py);
     out[x + i] = make_double2(px, py);
+    // (the host's copy, straight over PCIe while the emit runs)
+    if (x + i < hcap) hout[x + i] = make_double2(px, py);
   }
 }
 
@@ -1318,7 +1321,8 @@ __global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
     grid_barrier(bar, 1);
   }
   const u32 total = P_p->spa.total_chunks;
-  for (u32 c = gw; c < total; c += nwarps) spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out);
+  for (u32 c = gw; c < total; c += nwarps)
+    spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out, rb.h_chains, rb.h_chains_cap);
   // every CTA is done with the counters: CTA 0 hands them to the host and
   // clears them (no separate read-back launch)
   grid_barrier(bar, nd ? 2u : 0u);

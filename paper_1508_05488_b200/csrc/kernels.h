@@ -42,6 +42,8 @@ struct ReadbackArgs {
   u32* h_ctr;                    // host (mapped): counters
   unsigned long long* h_kept;    // host (mapped): kept [4]
   unsigned long long* h_ncand;   // host (mapped): candidates
+  double2* h_chains = nullptr;   // host (mapped): the emit also writes the first
+  u32 h_chains_cap = 0;          // h_chains_cap kept points here (no D2H copy)
 };
 __device__ __forceinline__ void readback_block(const ReadbackArgs& a) {
   const int t = threadIdx.x;

@@ -778,7 +778,8 @@ FilterTabs filter_tabs(chgpu_ctx* ctx, int log2nb) {
 // Bounds the host knows (n records, min(4 C, n) chunks) size the grids.
 // *ovf_slot / *ncand land in the counters for the caller's read-back.
 int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chunk_count,
-                       int log2nb, int cnt_slot, int* ovf_slot, int nonfinite_slot = -1) {
+                       int log2nb, int cnt_slot, int* ovf_slot, int nonfinite_slot = -1,
+                       size_t host_chains = 0) {
   cudaStream_t st = ctx->st;
   const FilterPlan* P = ctx->d_plan;
   const u32 max_chunks = (u32)(chunk_count > n / 4 ? n : std::min<size_t>(4 * chunk_count, n));
@@ -839,6 +840,9 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   rb.h_ctr = ctx->h->ctr;
   rb.h_kept = ctx->h->kept;
   rb.h_ncand = &ctx->h->ncand;
+  // the first host_chains kept points also go to the pinned h_out (mapped)
+  rb.h_chains = host_chains ? ctx->h_out : nullptr;
+  rb.h_chains_cap = (u32)host_chains;
   CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
                        ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
                        ctx->d_ctr + ndefer_slot, ctx->d_ck, ctx->d_cv, ctx->d_raw,
@@ -1209,14 +1213,19 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   int ovf_slot = -1;
   size_t spec = 0;
   if (want_filter) {
-    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot,
-                           from_file ? nonfinite_slot : -1));
     // (small chains only: a survivor-heavy call reads its result back once
-    // it knows the size, or not at all on the convex fast path)
+    // it knows the size, or not at all on the convex fast path). The emit
+    // writes up to `spec` kept points straight into the pinned h_out.
     if (ctx->kept_hint + 4 < kConvexMin)
       spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 16 + 256));
     TRY(ensure_host_out(ctx, spec + 4));
-    if (spec)
+    static const bool mapped_emit = [] {
+      const char* e = std::getenv("CHGPU_EMIT_MAPPED");  // A/B knob: 0 = DMA read-back
+      return !e || std::atoi(e) != 0;
+    }();
+    TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot,
+                           from_file ? nonfinite_slot : -1, mapped_emit ? spec : 0));
+    if (spec && !mapped_emit)
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
                          st));
   }
