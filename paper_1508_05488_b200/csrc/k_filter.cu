@@ -1323,10 +1323,18 @@ __global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
   const u32 total = P_p->spa.total_chunks;
   for (u32 c = gw; c < total; c += nwarps)
     spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out, rb.h_chains, rb.h_chains_cap);
+  if (rb.h_done) __threadfence_system();  // this CTA's host chain writes, before the flag
   // every CTA is done with the counters: CTA 0 hands them to the host and
-  // clears them (no separate read-back launch)
+  // clears them (no separate read-back launch), then raises the call's flag
   grid_barrier(bar, nd ? 2u : 0u);
-  if (blockIdx.x == 0) readback_block(rb);
+  if (blockIdx.x == 0) {
+    readback_block(rb);
+    if (rb.h_done) {
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0) *reinterpret_cast<volatile u32*>(rb.h_done) = rb.seq;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ launchers

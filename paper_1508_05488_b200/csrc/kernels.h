@@ -44,6 +44,8 @@ struct ReadbackArgs {
   unsigned long long* h_ncand;   // host (mapped): candidates
   double2* h_chains = nullptr;   // host (mapped): the emit also writes the first
   u32 h_chains_cap = 0;          // h_chains_cap kept points here (no D2H copy)
+  u32* h_done = nullptr;         // host (mapped): set to `seq` once all of the above is
+  u32 seq = 0;                   // visible (the host starts on it before the stream drains)
 };
 __device__ __forceinline__ void readback_block(const ReadbackArgs& a) {
   const int t = threadIdx.x;

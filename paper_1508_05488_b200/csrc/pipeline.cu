@@ -52,6 +52,7 @@ struct Pinned {
   unsigned long long uniq;
   unsigned long long counts5[5];
   unsigned long long ncand;
+  u32 done;  // k_spa_finish's completion flag (the call's sequence number)
 };
 
 // The per-call counters the host reads after K2 and the filter path: the
@@ -167,6 +168,7 @@ struct chgpu_ctx {
   // K2 twice. Performance only: both paths give the same hull.
   bool sort_hint = false;
   size_t sort_hint_n = 0;
+  u32 call_seq = 0;  // the filter path's completion flag value (Pinned::done)
   // Pinned staging arena for host->device uploads of small host-built
   // tables (segments, plans, quads): every upload gets its own slice, so a
   // host buffer can be rewritten while earlier copies are still queued.
@@ -331,6 +333,33 @@ int ensure_cap(chgpu_ctx* ctx, size_t n) {
 
 int sync(chgpu_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->st));
+  return CHGPU_OK;
+}
+
+// The filter path's results are in host memory once k_spa_finish raises
+// the call's flag (its last act): the host starts on them without waiting
+// for the stream to drain. The stream is polled now and then, so a failed
+// launch ends the wait (sync() then reports it).
+int wait_filter_flag(chgpu_ctx* ctx) {
+  static const bool on = [] {
+    const char* e = std::getenv("CHGPU_FLAG_WAIT");  // A/B knob: 0 = stream sync
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on) return sync(ctx);
+  const volatile u32* f = &ctx->h->done;
+  for (unsigned i = 1; *f != ctx->call_seq; ++i) {
+    if ((i & 255) == 0) {
+      const cudaError_t q = cudaStreamQuery(ctx->st);
+      if (q != cudaErrorNotReady) {
+        if (*f == ctx->call_seq) break;
+        return sync(ctx);  // done without the flag (an error, or a path that skips it)
+      }
+    }
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   return CHGPU_OK;
 }
 
@@ -843,6 +872,14 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   // the first host_chains kept points also go to the pinned h_out (mapped)
   rb.h_chains = host_chains ? ctx->h_out : nullptr;
   rb.h_chains_cap = (u32)host_chains;
+  // (process-wide sequence: pinned memory recycled from a destroyed context
+  // may still hold that context's last flag value)
+  static std::atomic<u32> g_seq{0};
+  u32 seq = g_seq.fetch_add(1, std::memory_order_relaxed) + 1;
+  if (seq == 0) seq = g_seq.fetch_add(1, std::memory_order_relaxed) + 1;
+  ctx->h->done = 0;
+  rb.h_done = &ctx->h->done;
+  rb.seq = ctx->call_seq = seq;
   CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
                        ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
                        ctx->d_ctr + ndefer_slot, ctx->d_ck, ctx->d_cv, ctx->d_raw,
@@ -1240,7 +1277,10 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   }
   if (want_filter && ctx->stage_times) CK(cudaEventRecord(ctx->ev[9], st));
   const auto t_enq = std::chrono::steady_clock::now();
-  TRY(sync(ctx));
+  if (want_filter && !ctx->stage_times)  // (per-kernel events want a drained stream)
+    TRY(wait_filter_flag(ctx));
+  else
+    TRY(sync(ctx));
   D.t_host_enqueue_ms = std::chrono::duration<double, std::milli>(t_enq - t_wall0).count();
   D.t_host_wait_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq).count();
@@ -1310,19 +1350,12 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
       D.filter_log2nb = log2nb;
       D.spa_path = overflow ? 2 : 1;
       filtered = !overflow;
-      if (!filtered) t_sort_ms = ms_between(ctx->ev[2], ctx->ev[8]);  // the attempt
-      if (filtered) {
-        // sort = bin scan + filter (what replaces sort_region); spa = the
-        // chunk SPA (k_spa_small, deferred bin sorts + k_spa_chunks, emit)
-        t_sort_ms = ms_between(ctx->ev[2], ctx->ev[4]);
-        t_spa_ms = ms_between(ctx->ev[4], ctx->ev[8]);
-        D.t_spa_kernel_ms = t_spa_ms;
-        if (ctx->stage_times) {
-          D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
-          D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
-          D.t_binsort_ms = ms_between(ctx->ev[5], ctx->ev[6]);
-        }
+      if (!filtered) {  // the attempt
+        CK(cudaEventSynchronize(ctx->ev[8]));
+        t_sort_ms = ms_between(ctx->ev[2], ctx->ev[8]);
       }
+      // (a filtered call's stage times are read after the finisher: the
+      // host may be here before the stream has drained, see wait_filter_flag)
     }
     if (!filtered) {
       // ---- K3: region sort (spa.cpp:59-81) of every survivor.
@@ -1422,6 +1455,21 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   }
 finished:
   const auto t_end = std::chrono::steady_clock::now();
+  if (want_filter) {
+    CK(cudaEventSynchronize(ctx->ev[8]));  // (drained long ago: the finisher ran since)
+    if (D.spa_path == 1) {
+      // sort = bin scan + filter (what replaces sort_region); spa = the
+      // chunk SPA (k_spa_small, deferred bin sorts + k_spa_chunks, emit)
+      t_sort_ms = ms_between(ctx->ev[2], ctx->ev[4]);
+      t_spa_ms = ms_between(ctx->ev[4], ctx->ev[8]);
+      D.t_spa_kernel_ms = t_spa_ms;
+      if (ctx->stage_times) {
+        D.t_binscan_ms = ms_between(ctx->ev[2], ctx->ev[3]);
+        D.t_filter_ms = ms_between(ctx->ev[3], ctx->ev[4]);
+        D.t_binsort_ms = ms_between(ctx->ev[5], ctx->ev[6]);
+      }
+    }
+  }
 
   S.n_hull = ctx->hull_n;
   if (pdl) {
@@ -1540,6 +1588,7 @@ int chgpu_ctx_create(int device, chgpu_ctx** out) {
     chgpu_ctx_destroy(ctx);
     return CHGPU_CUDA_ERR;
   }
+  std::memset(ctx->h, 0, sizeof(Pinned));
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   if (const char* e = std::getenv("CHGPU_PDL")) ctx->pdl = std::atoi(e) != 0;
   if (const char* e = std::getenv("CHGPU_STAGE_TIMES")) ctx->stage_times = std::atoi(e) != 0;

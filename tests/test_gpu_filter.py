@@ -234,3 +234,23 @@ def test_filter_tables_across_sizes(product, oracle):
         assert _counts(r) == want.counts.tolist(), (dist, n, cc)
         assert np.array_equal(r.hull.vertices, want.hull), (dist, n, cc)
     ctx.close()
+
+
+def test_fresh_contexts_after_destroyed_ones(product, oracle):
+    """The filter path's completion flag lives in pinned memory that a new
+    context may recycle from a destroyed one: a stale flag value must never
+    end the new call's wait (each call draws a process-wide sequence number)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    inputs = [product.generate(d, n, s) for d, n, s in
+              (("circle", 300_000, 1), ("uniform_square", 400_000, 2), ("uniform_disk", 300_000, 3),
+               ("gaussian", 300_000, 4))]
+    wants = [oracle.convex_hull(p, 1024) for p in inputs]
+    for rep in range(3):
+        for p, want in zip(inputs, wants):
+            ctx = product.Context(0)
+            r = ctx.convex_hull(p)
+            assert _counts(r) == want.counts.tolist(), rep
+            assert np.array_equal(r.hull.vertices, want.hull)
+            ctx.close()
