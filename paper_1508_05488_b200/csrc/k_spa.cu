@@ -143,165 +143,6 @@ void launch_unique(const u64* k, const u64* v, u64 n, double2* out, u64* status,
 
 namespace chgpu {
 
-// ------------------------------------------------------------------ SPA, warp per chunk
-//
-// One warp scans one chunk, 256 records per step (8 coalesced rows of 32),
-// with a shuffle scan per row and the carry in a register: no block
-// barriers and no inter-chunk dependency. Kept records are written,
-// decoded, compactly at the start of the chunk's own range of a scratch
-// array (ranges never overlap); k_spa_offsets scans the per-chunk counts and
-// k_spa_gather moves each chunk's run to its final, region-ordered place.
-
-constexpr int kSpaPer = 8;                  // consecutive records per lane and step
-constexpr int kSpaStep = 32 * kSpaPer;      // records per warp step
-
-// Lane L of a step owns records [t0 + 8L, t0 + 8L + 8): it folds them
-// sequentially, one warp scan combines the 32 lane aggregates, and the lane
-// replays its 8 records against the exclusive prefix. The next step's loads
-// are issued before the current step is scanned.
-__global__ __launch_bounds__(256) void k_spa_warp(const u64* __restrict__ k,
-                                                  const u64* __restrict__ v,
-                                                  const SpaPlan* __restrict__ plan_p,
-                                                  double2* __restrict__ scratch,
-                                                  u32* __restrict__ chunk_kept) {
-  const SpaPlan& plan = *plan_p;
-  const int lane = threadIdx.x & 31;
-  const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= plan.total_chunks) return;
-  int r = 0;
-  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
-  const int region = r + 1;
-  const u64 cl = c - plan.chunk_begin[r];
-  const u64 begin = plan.off[r] + cl * plan.chunk_size[r];
-  const u64 len = min((u64)plan.chunk_size[r], (u64)plan.m[r] - cl * plan.chunk_size[r]);
-  const bool is_min = (region == 1 || region == 4);
-  const double ident = is_min ? INFINITY : -INFINITY;
-  double carry = (cl == 0) ? plan.seed[r] : ident;
-  u32 kept = 0;
-
-  u64 nv[kSpaPer];
-  auto fetch = [&](u64 t0) {
-#pragma unroll
-    for (int j = 0; j < kSpaPer; ++j) {
-      const u64 idx = t0 + (u64)lane * kSpaPer + j;
-      nv[j] = idx < len ? v[begin + idx] : 0ull;
-    }
-  };
-  fetch(0);
-  for (u64 t0 = 0; t0 < len; t0 += kSpaStep) {
-    double g[kSpaPer];
-    double agg = ident;
-#pragma unroll
-    for (int j = 0; j < kSpaPer; ++j) {
-      const u64 idx = t0 + (u64)lane * kSpaPer + j;
-      g[j] = idx < len ? guarded_of(region, nv[j]) : ident;
-      agg = op_ext(is_min, agg, g[j]);
-    }
-    if (t0 + kSpaStep < len) fetch(t0 + kSpaStep);
-    double x = agg;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x = op_ext(is_min, y, x);
-    }
-    double ex = __shfl_up_sync(0xffffffffu, x, 1);
-    if (lane == 0) ex = ident;
-    double t = op_ext(is_min, carry, ex);
-    carry = op_ext(is_min, carry, __shfl_sync(0xffffffffu, x, 31));
-    u32 kmask = 0;
-#pragma unroll
-    for (int j = 0; j < kSpaPer; ++j) {
-      const u64 idx = t0 + (u64)lane * kSpaPer + j;
-      if (idx < len && !steps_back(is_min, g[j], t)) kmask |= 1u << j;
-      t = op_ext(is_min, t, g[j]);
-    }
-    const u32 nk = __popc(kmask);
-    u32 pre = nk;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += y;
-    }
-    u32 pos = kept + pre - nk;
-    kept += __shfl_sync(0xffffffffu, pre, 31);
-    while (kmask) {
-      const int j = __ffs(kmask) - 1;
-      kmask &= kmask - 1;
-      const u64 a = begin + t0 + (u64)lane * kSpaPer + j;
-      double px, py;
-      decode_point(region, k[a], v[a], px, py);
-      scratch[begin + pos++] = make_double2(px, py);
-    }
-  }
-  if (lane == 0) chunk_kept[c] = kept;
-}
-
-// Exclusive scan of the per-chunk kept counts (one block); per-region
-// totals follow from the offsets at the region boundaries.
-__global__ __launch_bounds__(1024) void k_spa_offsets(const u32* __restrict__ chunk_kept,
-                                                      const SpaPlan* __restrict__ plan_p,
-                                                      u32* __restrict__ offs,
-                                                      unsigned long long* __restrict__ kept_counts) {
-  const SpaPlan& plan = *plan_p;
-  __shared__ u32 wsum[32];
-  __shared__ u32 carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const u32 total = plan.total_chunks;
-  for (u32 c0 = 0; c0 < total; c0 += blockDim.x) {
-    const u32 c = c0 + threadIdx.x;
-    const u32 x0 = c < total ? chunk_kept[c] : 0u;
-    u32 x = x0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    u32 pre = 0, tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      const u32 ws = wsum[w];
-      pre += (w < warp) ? ws : 0u;
-      tot += ws;
-    }
-    if (c < total) offs[c] = carry + pre + x - x0;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const u32 grand = carry;
-    for (int r = 0; r < 4; ++r) {
-      const u32 a = plan.chunk_begin[r];
-      const u32 b = r < 3 ? plan.chunk_begin[r + 1] : total;
-      const u32 oa = a < total ? offs[a] : grand;
-      const u32 ob = b < total ? offs[b] : grand;
-      kept_counts[r] = (unsigned long long)(ob - oa);
-    }
-  }
-}
-
-__global__ __launch_bounds__(256) void k_spa_gather(const double2* __restrict__ scratch,
-                                                    const SpaPlan* __restrict__ plan_p,
-                                                    const u32* __restrict__ chunk_kept,
-                                                    const u32* __restrict__ offs,
-                                                    double2* __restrict__ out) {
-  const SpaPlan& plan = *plan_p;
-  const int lane = threadIdx.x & 31;
-  const u32 c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= plan.total_chunks) return;
-  const u32 kc = chunk_kept[c];
-  if (!kc) return;
-  int r = 0;
-  while (r < 3 && c >= plan.chunk_begin[r + 1]) ++r;
-  const u64 begin = plan.off[r] + (u64)(c - plan.chunk_begin[r]) * plan.chunk_size[r];
-  const u32 o = offs[c];
-  for (u32 i = lane; i < kc; i += 32) out[o + i] = scratch[begin + i];
-}
-
-
 // ------------------------------------------------------------------ SPA, tile scan
 //
 // The same filter as one pass over the sorted records, whatever the chunk
@@ -604,14 +445,5 @@ cudaError_t configure_spa_kernels() {
                               (int)sizeof(SpaTileSmem));
 }
 
-void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
-                     double2* scratch, u32* chunk_kept, u32* offs,
-                     unsigned long long* kept_counts, double2* out, cudaStream_t st) {
-  if (max_chunks == 0) return;
-  const u32 blocks = (max_chunks + 7) / 8;
-  k_spa_warp<<<blocks, 256, 0, st>>>(k, v, plan, scratch, chunk_kept);
-  k_spa_offsets<<<1, 1024, 0, st>>>(chunk_kept, plan, offs, kept_counts);
-  k_spa_gather<<<blocks, 256, 0, st>>>(scratch, plan, chunk_kept, offs, out);
-}
 
 }  // namespace chgpu

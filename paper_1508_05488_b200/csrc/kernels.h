@@ -160,9 +160,6 @@ void launch_group_fix_medium(u64* k, u64* v, const SegDesc* segs, const void* me
                              const u32* nmedium, void* longr, u32* nlong, cudaStream_t st);
 size_t group_run_bytes();
 // K4/K5
-void launch_spa_warp(const u64* k, const u64* v, const SpaPlan* plan, u32 max_chunks,
-                     double2* scratch, u32* chunk_kept, u32* offs,
-                     unsigned long long* kept_counts, double2* out, cudaStream_t st);
 void launch_spa_tile(const u64* k, const u64* v, const SpaPlan& plan, u64 total, u64* status,
                      u32 tag, u64* pay, u32* ticket, double2* out,
                      unsigned long long* kept_counts, cudaStream_t st);

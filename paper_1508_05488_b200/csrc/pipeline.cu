@@ -731,28 +731,14 @@ int sorted_unique_survivors(chgpu_ctx* ctx, u64 s1, const double* quad, size_t* 
 // d_kept (region order) and per-region counts in d_u64[0..3]. The input
 // copy d_pts is dead by now and serves as the per-chunk scratch.
 int run_spa(chgpu_ctx* ctx, const u64* kF, const u64* vF, const SpaPlan& plan) {
-  static const bool warp_spa = [] {
-    const char* e = std::getenv("CHGPU_SPA_WARP");  // A/B knob: warp per chunk + gather
-    return e && std::atoi(e) != 0;
-  }();
-  SpaPlan* d_splan = &ctx->d_plan->spa;
-  TRY(upload(ctx, d_splan, &plan, sizeof(SpaPlan)));
-  if (warp_spa) {
-    u32* chunk_kept = ctx->d_raw;
-    u32* offs = chunk_kept + ((plan.total_chunks + 31) & ~31u);
-    launch_spa_warp(kF, vF, d_splan, plan.total_chunks, ctx->d_pts, chunk_kept, offs, ctx->d_u64,
-                    ctx->d_kept, ctx->st);
-    if (plan.total_chunks) ctx->launches += 3;
-  } else {
-    const u64 total = plan.m[0] + plan.m[1] + plan.m[2] + plan.m[3];
-    const int ticket = take_ctr(ctx);
-    // (the kept counts are accumulated: + region end, - region start)
-    CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), ctx->st));
-    launch_spa_tile(kF, vF, plan, total, ctx->d_status, next_tag(ctx),
-                    reinterpret_cast<u64*>(ctx->d_raw), ctx->d_ctr + ticket, ctx->d_kept,
-                    ctx->d_u64, ctx->st);
-    if (total) ctx->launches += 1;
-  }
+  const u64 total = plan.m[0] + plan.m[1] + plan.m[2] + plan.m[3];
+  const int ticket = take_ctr(ctx);
+  // (the kept counts are accumulated: + region end, - region start)
+  CK(cudaMemsetAsync(ctx->d_u64, 0, 4 * sizeof(unsigned long long), ctx->st));
+  launch_spa_tile(kF, vF, plan, total, ctx->d_status, next_tag(ctx),
+                  reinterpret_cast<u64*>(ctx->d_raw), ctx->d_ctr + ticket, ctx->d_kept,
+                  ctx->d_u64, ctx->st);
+  if (total) ctx->launches += 1;
   CK(cudaGetLastError());
   return CHGPU_OK;
 }
