@@ -336,6 +336,19 @@ int sync(chgpu_ctx* ctx) {
   return CHGPU_OK;
 }
 
+// Whether the filter path's emit writes the chains straight into pinned
+// host memory (CHGPU_EMIT_MAPPED=1) instead of a DMA read-back after it.
+// Off by default: the saving (~13 µs) depends on the host. On some B200
+// hosts the finisher reads PCIe-written lines far slower than DMA-written
+// ones (its worker segments 50 -> 95 µs), a net loss of ~30 µs.
+bool emit_mapped() {
+  static const bool on = [] {
+    const char* e = std::getenv("CHGPU_EMIT_MAPPED");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // The filter path's results are in host memory once k_spa_finish raises
 // the call's flag (its last act): the host starts on them without waiting
 // for the stream to drain. The stream is polled now and then, so a failed
@@ -1242,13 +1255,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
     if (ctx->kept_hint + 4 < kConvexMin)
       spec = std::min<size_t>(ctx->cap, std::max<size_t>(4096, ctx->kept_hint + ctx->kept_hint / 16 + 256));
     TRY(ensure_host_out(ctx, spec + 4));
-    static const bool mapped_emit = [] {
-      const char* e = std::getenv("CHGPU_EMIT_MAPPED");  // A/B knob: 0 = DMA read-back
-      return !e || std::atoi(e) != 0;
-    }();
     TRY(enqueue_filter_spa(ctx, pts, n, chunk_count, log2nb, cnt_slot, &ovf_slot,
-                           from_file ? nonfinite_slot : -1, mapped_emit ? spec : 0));
-    if (spec && !mapped_emit)
+                           from_file ? nonfinite_slot : -1, emit_mapped() ? spec : 0));
+    if (spec && !emit_mapped())
       CK(cudaMemcpyAsync(ctx->h_out, ctx->d_kept, spec * sizeof(double2), cudaMemcpyDeviceToHost,
                          st));
   }
@@ -1263,7 +1272,9 @@ int run_pipeline(chgpu_ctx* ctx, const double* h_src, const double2* pts_dev, si
   }
   if (want_filter && ctx->stage_times) CK(cudaEventRecord(ctx->ev[9], st));
   const auto t_enq = std::chrono::steady_clock::now();
-  if (want_filter && !ctx->stage_times)  // (per-kernel events want a drained stream)
+  // (per-kernel events want a drained stream; a DMA read-back of the chains
+  // comes after the flag)
+  if (want_filter && !ctx->stage_times && emit_mapped() && spec)
     TRY(wait_filter_flag(ctx));
   else
     TRY(sync(ctx));
