@@ -3,6 +3,8 @@ the full-sort path it replaces, forced per context, against the reference's
 golden outputs and the C oracle. Both paths must give the reference's hull
 and every stage counter (n_after_spa counts the kept chains, so the kept set
 itself is pinned)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -254,3 +256,48 @@ def test_fresh_contexts_after_destroyed_ones(product, oracle):
             assert _counts(r) == want.counts.tolist(), rep
             assert np.array_equal(r.hull.vertices, want.hull)
             ctx.close()
+
+
+def test_mapped_emit_and_flag_wait(product):
+    """CHGPU_EMIT_MAPPED=1 (chains written into pinned host memory by the
+    emit, the host waiting on k_spa_finish's flag): the same hulls and
+    counters as the default DMA read-back, across fresh contexts that may
+    recycle a destroyed one's pinned memory (a separate process: the knob is
+    read once per process)."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from conftest import ROOT
+    cases = [("uniform_square", 2_000_000, 1), ("uniform_disk", 1_000_000, 2), ("gaussian", 800_000, 3),
+             ("circle", 300_000, 4), ("uniform_square", 20_000, 5)]
+    code = r'''
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_1508_05488_b200 as P
+out = []
+for rep in range(2):
+    for d, n, s in json.loads(sys.argv[2]):
+        ctx = P.Context(0)
+        for _ in range(2):  # the second call reads back through the mapped buffer
+            r = ctx.convex_hull(P.generate(d, n, s))
+        st = r.stats
+        out.append([hashlib.sha256(r.hull.vertices.tobytes()).hexdigest(),
+                    [st.n_input, st.n_after_round1, st.n_after_spa, st.n_hull]])
+        ctx.close()
+print(json.dumps(out))
+'''
+    env = dict(os.environ, CHGPU_EMIT_MAPPED="1")
+    res = subprocess.run([sys.executable, "-c", code, ROOT, json.dumps(cases)], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    ctx = product.Context(0)
+    want = []
+    for d, n, s in cases:
+        r = ctx.convex_hull(product.generate(d, n, s))
+        want.append([sha(r.hull.vertices), _counts(r)])
+    ctx.close()
+    assert got == want + want
