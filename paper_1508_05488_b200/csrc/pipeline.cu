@@ -987,6 +987,16 @@ void copy_stream(unsigned char* dst, const unsigned char* src, size_t len) {
 // within a millisecond), then park. Serves one job at a time (a mutex).
 class StagePool {
  public:
+  // the staging threads besides the caller: CHGPU_STAGE_THREADS - 1
+  // (default min(16, cores) - 1)
+  static int max_threads() {
+    static const int m = [] {
+      const char* e = std::getenv("CHGPU_STAGE_THREADS");
+      const int hw = (int)std::thread::hardware_concurrency();
+      return std::max(0, (e ? std::atoi(e) : std::min(16, std::max(1, hw))) - 1);
+    }();
+    return m;
+  }
   static StagePool& get() {
     static StagePool* p = new StagePool();  // (never destroyed: its threads live with the process)
     return *p;
@@ -1024,10 +1034,16 @@ class StagePool {
   }
   void start(int want) {
     const pid_t me = getpid();
-    if (pid_ != me) {  // (a forked child has no threads: it starts its own)
+    if (pid_ != me) {
+      // a forked child has none of these threads: it starts its own (the
+      // parent's std::thread objects are moved out of the way, never
+      // destroyed: destroying a joinable std::thread terminates)
+      if (!th_.empty()) new std::vector<std::thread>(std::move(th_));
       th_.clear();
       pid_ = me;
+      failed_ = false;
     }
+    want = std::min(want, max_threads());
     while ((int)th_.size() < want && !failed_) {
       try {
         th_.emplace_back([this, g = gen_.load()] { loop(g); });

@@ -220,3 +220,26 @@ def test_split_finisher(product):
     assert out.returncode == 0, out.stdout + out.stderr
     taken = int(out.stdout.split("taken=")[1].split()[0])
     assert taken > 0, out.stdout
+
+
+def test_host_prefault_pool_and_fork(product):
+    """chgpu_host_prefault (the C++ API's result-vector prefault) runs on the
+    library's staging threads: every page of the range is touched, a range
+    far larger than the pool is split among its threads, and a forked child
+    (which has none of the parent's threads) starts its own pool."""
+    L = product.load_library()
+    L.chgpu_host_prefault.argtypes = [C.c_void_p, C.c_size_t]
+    L.chgpu_host_prefault.restype = None
+    a = np.full(64 << 20, 7, np.uint8)  # 64 MB: 16 parts of 4 MB
+    L.chgpu_host_prefault(a.ctypes.data, a.nbytes)
+    assert a[::4096].max() == 0 and a[-1] == 0  # (the touched bytes are zeroed)
+    pid = os.fork()
+    if pid == 0:  # child: the pool must start fresh, not inherit dead threads
+        try:
+            b = np.full(32 << 20, 7, np.uint8)
+            L.chgpu_host_prefault(b.ctypes.data, b.nbytes)
+            os._exit(0 if b[::4096].max() == 0 else 3)
+        except BaseException:
+            os._exit(4)
+    _, status = os.waitpid(pid, 0)
+    assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0, status
