@@ -877,7 +877,8 @@ int enqueue_filter_spa(chgpu_ctx* ctx, const double2* pts, size_t n, size_t chun
   u32 seq = g_seq.fetch_add(1, std::memory_order_relaxed) + 1;
   if (seq == 0) seq = g_seq.fetch_add(1, std::memory_order_relaxed) + 1;
   ctx->h->done = 0;
-  rb.h_done = &ctx->h->done;
+  // (the flag and its system-scope fences only serve the mapped emit)
+  rb.h_done = host_chains ? &ctx->h->done : nullptr;
   rb.seq = ctx->call_seq = seq;
   CK(launch_spa_finish(ctx->d_ka, ctx->d_va, t.cur, ctx->d_fstart, t.bmap, first_bin, P, ctx->d_fbig,
                        ctx->d_ctr + nbig_slot, ctx->d_ctr + *ovf_slot, ctx->d_fdefer,
