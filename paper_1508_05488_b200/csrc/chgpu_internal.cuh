@@ -387,7 +387,10 @@ constexpr int kDigits = 256;
 constexpr int kPasses = 8;
 
 constexpr int kK2Threads = 256;
-constexpr int kK2Items = 8;
+#ifndef CHGPU_K2C_ITEMS
+#define CHGPU_K2C_ITEMS 8
+#endif
+constexpr int kK2Items = CHGPU_K2C_ITEMS;
 constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
 #ifndef CHGPU_SEG_ITEMS
 #define CHGPU_SEG_ITEMS 8

@@ -308,7 +308,7 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
   const QuadEdges e = s_edges;
   cp_async_wait<0>();  // each thread reads back only its own copies
 
-  u32 codes = 0;  // 3 bits of stream id per item
+  u64 codes = 0;  // 3 bits of stream id per item
   u32 cnt[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int j = 0; j < kK2Items; ++j) {
@@ -323,7 +323,7 @@ __global__ __launch_bounds__(kK2Threads, 3) void k_classify_compact(
       }
       if (lex && r != 0) r = 1;
     }
-    codes |= (u32)r << (3 * j);
+    codes |= (u64)r << (3 * j);
 #pragma unroll
     for (int s = 0; s < 4; ++s) cnt[s] += (r == s + 1);
   }
