@@ -388,10 +388,10 @@ constexpr int kPasses = 8;
 
 constexpr int kK2Threads = 256;
 #ifndef CHGPU_K2C_ITEMS
-#define CHGPU_K2C_ITEMS 8
+#define CHGPU_K2C_ITEMS 6
 #endif
 constexpr int kK2Items = CHGPU_K2C_ITEMS;
-constexpr int kK2Tile = kK2Threads * kK2Items;  // 2048
+constexpr int kK2Tile = kK2Threads * kK2Items;  // 1536
 #ifndef CHGPU_SEG_ITEMS
 #define CHGPU_SEG_ITEMS 8
 #endif

@@ -603,6 +603,17 @@ void launch_extremes_final(const QuadCand* partials, int nparts, QuadInfo* out,
   k_extremes_final<<<1, 1024, 0, st>>>(partials, nparts, out, raw_out);
 }
 
+// Dynamic shared memory opt-in of the record-writing K2 (its point tile).
+cudaError_t configure_k2_kernels() {
+  const int smem = (int)(kK2Tile * sizeof(double2));
+  cudaError_t e = cudaFuncSetAttribute((const void*)k_classify_compact<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void*)k_classify_compact<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
+}
+
 void launch_classify_compact(const double2* pts, u32 n, const QuadInfo* qinfo,
                              const unsigned char* given_labels, int force_lex, u64* kbuf,
                              u64* vbuf, u64 ncap, u32* counts_out, cudaStream_t st) {

@@ -113,6 +113,7 @@ struct DeviceLimits {
 const DeviceLimits& device_limits();
 cudaError_t configure_sort_kernels();
 cudaError_t configure_spa_kernels();
+cudaError_t configure_k2_kernels();
 cudaError_t configure_filter_kernels(DeviceLimits* lim);
 
 // K1

@@ -1553,6 +1553,7 @@ const DeviceLimits& device_limits() {
     cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = configure_sort_kernels();
     if (e == cudaSuccess) e = configure_spa_kernels();
+    if (e == cudaSuccess) e = configure_k2_kernels();
     if (e == cudaSuccess) e = configure_filter_kernels(&d);
     if (e == cudaSuccess) d.k1_wave = extremes_wave(d.sms);
     d.status = e;
