@@ -397,6 +397,19 @@ __global__ __launch_bounds__(kBinThreads, 4) void k_bin_scan(
 #ifndef CHGPU_SPA_CLOCKS
 #define CHGPU_SPA_CLOCKS 0
 #endif
+#ifndef CHGPU_FINISH_CLOCKS
+#define CHGPU_FINISH_CLOCKS 0
+#endif
+#if CHGPU_FINISH_CLOCKS  // (diagnostic build: phase clocks of k_spa_finish)
+__device__ unsigned long long g_fin_clk[9];
+__global__ void k_fin_clocks_report() {
+  printf("spa_finish max clocks: warp sorts %llu | big sorts %llu | barrier %llu | chunk SPA %llu | "
+         "barrier %llu ; lists: warp %llu big %llu deferred %llu\n",
+         g_fin_clk[1], g_fin_clk[2], g_fin_clk[3], g_fin_clk[4], g_fin_clk[5], g_fin_clk[6],
+         g_fin_clk[7], g_fin_clk[8]);
+  for (int i = 0; i < 9; ++i) g_fin_clk[i] = 0;
+}
+#endif
 #if CHGPU_SPA_CLOCKS  // (diagnostic build: per-chunk clocks of k_spa_chunks)
 __device__ unsigned long long g_spa_clk[40];
 #endif
@@ -593,10 +606,14 @@ __device__ __forceinline__ bool key_gt(u64 ci, u64 vi, u64 ki, u64 cj, u64 vj, u
 }
 
 // Bitonic network over sc/sv/sk[0, Pn) executed by `nthreads` threads
-// (index `me`); `sync` separates the stages.
-template <typename Sync>
+// (index `me`); `sync` separates the stages. A stage of stride <= 32 keeps
+// every warp inside its own 64-element blocks (thread t's pair starts at
+// 2t - (t & (stride - 1))), so two such stages in a row need only `wsync`
+// (a warp barrier) between them; `sync` runs where a stride >= 64 ends or
+// begins.
+template <typename Sync, typename WSync>
 __device__ __forceinline__ void bitonic_smem(u64* sc, u64* sv, u64* sk, u32 Pn, u32 me, u32 nthreads,
-                                             Sync sync) {
+                                             Sync sync, WSync wsync) {
   for (u32 size = 2; size <= Pn; size <<= 1) {
     for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
       for (u32 t = me; t < Pn / 2; t += nthreads) {
@@ -610,7 +627,11 @@ __device__ __forceinline__ void bitonic_smem(u64* sc, u64* sv, u64* sk, u32 Pn, 
           sk[i] = kj; sk[jx] = ki;
         }
       }
-      sync();
+      const u32 next = stride > 1 ? stride >> 1 : size;  // the next stage's stride
+      if (stride >= 64 || next >= 64)
+        sync();
+      else
+        wsync();
     }
   }
 }
@@ -646,7 +667,7 @@ __device__ void bin_sort_warp_body(u64* __restrict__ k, u64* __restrict__ v, con
       }
     }
     __syncwarp();
-    bitonic_smem(sc, sv, sk, Pn, lane, 32, [] { __syncwarp(); });
+    bitonic_smem(sc, sv, sk, Pn, lane, 32, [] { __syncwarp(); }, [] { __syncwarp(); });
     for (u32 i = lane; i < len; i += 32) {
       k[base + i] = sk[i];
       v[base + i] = sv[i];
@@ -689,7 +710,8 @@ __device__ void bin_sort_big_body(u64* __restrict__ k, u64* __restrict__ v, cons
       }
     }
     __syncthreads();
-    bitonic_smem(S.c, S.v, S.k, Pn, threadIdx.x, kBigThreads, [] { __syncthreads(); });
+    bitonic_smem(S.c, S.v, S.k, Pn, threadIdx.x, kBigThreads, [] { __syncthreads(); },
+                 [] { __syncwarp(); });
     for (u32 i = threadIdx.x; i < len; i += kBigThreads) {
       k[base + i] = S.k[i];
       v[base + i] = S.v[i];
@@ -1305,21 +1327,47 @@ __global__ __launch_bounds__(kFinishThreads) void k_spa_finish(
   const u32 nwarps = gridDim.x * (kFinishThreads / 32);
   const u32 gw = blockIdx.x * (kFinishThreads / 32) + warp;
   const u32 nd = *ndefer_p;
+#if CHGPU_FINISH_CLOCKS
+  long long fc[6] = {clock64(), 0, 0, 0, 0, 0};
+#endif
   if (nd) {
     const FilterPlan& P = *P_p;
     bin_sort_warp_body(k, v, P, bstart, bcur, big, nbig_p[0],
                        reinterpret_cast<u64*>(smem) + (size_t)warp * 3 * kWarpSortMax, blockIdx.x,
                        gridDim.x);
     __syncthreads();
+#if CHGPU_FINISH_CLOCKS
+    fc[1] = clock64();
+#endif
     bin_sort_big_body(k, v, P, bstart, bcur, big + kBigListB, nbig_p[1], overflow,
                       *reinterpret_cast<BigSmem*>(smem), blockIdx.x, gridDim.x);
+#if CHGPU_FINISH_CLOCKS
+    fc[2] = clock64();
+#endif
     grid_barrier(bar, 0);
+#if CHGPU_FINISH_CLOCKS
+    fc[3] = clock64();
+#endif
     SpaWarpSmem& W = reinterpret_cast<SpaWarpSmem*>(smem)[warp];
     for (u32 i = gw; i < nd; i += nwarps)
       spa_chunk_warp(defer[i], k, v, bcur, bstart, bmap, first_bin, P_p, sk, sv, chunk_kept,
                      group_kept, kept_counts, W);
+#if CHGPU_FINISH_CLOCKS
+    fc[4] = clock64();
+#endif
     grid_barrier(bar, 1);
   }
+#if CHGPU_FINISH_CLOCKS
+  fc[5] = clock64();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 6; ++q) atomicMax(&g_fin_clk[q], (u64)(fc[q] - fc[q - 1]));
+    if (blockIdx.x == 0) {
+      g_fin_clk[6] = nbig_p[0];
+      g_fin_clk[7] = nbig_p[1];
+      g_fin_clk[8] = nd;
+    }
+  }
+#endif
   const u32 total = P_p->spa.total_chunks;
   for (u32 c = gw; c < total; c += nwarps)
     spa_emit_warp(c, P_p, sk, sv, chunk_kept, group_kept, out, rb.h_chains, rb.h_chains_cap);
@@ -1404,6 +1452,9 @@ cudaError_t launch_spa_finish(u64* k, u64* v, const u32* bcur, const u32* bstart
                                                     dim3(kFinishThreads), args, kFinishSmem, st);
 #if CHGPU_SPA_CLOCKS
   k_spa_clocks_report<<<1, 1, 0, st>>>();
+#endif
+#if CHGPU_FINISH_CLOCKS
+  k_fin_clocks_report<<<1, 1, 0, st>>>();
 #endif
   return e;
 }
