@@ -72,6 +72,9 @@ class PipelineConfig:
     degenerate_fallback: bool = True
 
 
+_DEFAULT_CONFIG = PipelineConfig()
+
+
 class _Stats(C.Structure):
     _fields_ = [("n_input", C.c_size_t), ("n_after_round1", C.c_size_t),
                 ("n_after_spa", C.c_size_t), ("n_hull", C.c_size_t),
@@ -341,18 +344,25 @@ class Context:
         return a, counts
 
     def _hull(self, fn, ptr, n, config, copy=True):
-        config = config or PipelineConfig()
+        config = config or _DEFAULT_CONFIG
         out = _dp()
         k = C.c_size_t()
         s = _Stats()
         d = _Diag()
-        st = fn(self.h, ptr, n, config.chunk_count, int(bool(config.degenerate_fallback)),
+        st = fn(self.h, ptr, n, config.chunk_count, 1 if config.degenerate_fallback else 0,
                 C.byref(out), C.byref(k), C.byref(s), C.byref(d))
-        self._check(st)
-        verts = np.ctypeslib.as_array(out, shape=(k.value * 2,)).reshape(-1, 2) \
-            if k.value else np.empty((0, 2))
-        if copy:
-            verts = verts.copy()
+        if st:
+            self._check(st)
+        kv = k.value
+        if kv:
+            # (a view of the C ABI's result buffer: frombuffer over a sized
+            # ctypes array is several times cheaper than np.ctypeslib.as_array)
+            addr = C.cast(out, C.c_void_p).value
+            verts = np.frombuffer((C.c_double * (2 * kv)).from_address(addr), np.float64).reshape(kv, 2)
+            if copy:
+                verts = verts.copy()
+        else:
+            verts = np.empty((0, 2))
         return HullResult(Hull(verts), raw=d, raw_stats=s)
 
     def convex_hull(self, points, config: PipelineConfig | None = None,
