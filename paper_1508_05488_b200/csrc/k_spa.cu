@@ -156,7 +156,10 @@ namespace chgpu {
 // region-ordered place: no scratch copy and no gather pass.
 
 constexpr int kTileThreads = 256;
-constexpr int kTileItems = 16;
+#ifndef CHGPU_SPA_TILE_ITEMS
+#define CHGPU_SPA_TILE_ITEMS 16
+#endif
+constexpr int kTileItems = CHGPU_SPA_TILE_ITEMS;
 constexpr int kTileRecs = kTileThreads * kTileItems;
 
 struct SpaTileSmem {
@@ -177,7 +180,10 @@ __device__ __forceinline__ void seg_max(u32& fa, u64& xa, u32 fb, u64 xb) {
 
 __device__ __forceinline__ u64 ld_cg_u64(const u64* p) { return __ldcg(p); }
 
-__global__ __launch_bounds__(kTileThreads, 4) void k_spa_tile(
+#ifndef CHGPU_SPA_TILE_MINB
+#define CHGPU_SPA_TILE_MINB 4
+#endif
+__global__ __launch_bounds__(kTileThreads, CHGPU_SPA_TILE_MINB) void k_spa_tile(
     const u64* __restrict__ k, const u64* __restrict__ v, const SpaPlan plan, u64 total,
     u64* __restrict__ status, u32 tag, u32 ntiles, u64* __restrict__ pay, u32* __restrict__ ticket,
     double2* __restrict__ out, unsigned long long* __restrict__ kept_counts) {
