@@ -121,3 +121,28 @@ def test_cpp_drop_in_routes_through_shards(product, monkeypatch):
         assert cnt[0] == len(pts) and cnt[3] == len(h.hull)
         if k == "0":
             assert list(cnt) == [int(c) for c in h.counts]
+
+
+def test_cpp_drop_in_large_hull(product, oracle):
+    """chainhull::convex_hull returning a hull of 2^16 vertices or more (its
+    result vector is prefaulted from the library's staging threads before
+    the copy): the reference's hull, from pageable input."""
+    from conftest import ROOT
+    L = ctypes.CDLL(os.path.join(ROOT, "paper_1508_05488_b200", "libchainhull.so"))
+    L.chainhull_capi_convex_hull.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
+                                            ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(ctypes.c_size_t)]
+    for dist, n, seed in (("circle", 300_000, 31), ("circle", 70_000, 32)):
+        pts = oracle.generate(dist, n, seed)
+        want = oracle.convex_hull(pts, 1024)
+        out = np.empty((len(want.hull) + 16, 2))
+        nh = ctypes.c_size_t()
+        cnt = (ctypes.c_size_t * 4)()
+        for _ in range(2):
+            st = L.chainhull_capi_convex_hull(pts.ctypes.data, len(pts), 1024, 0, 1, out.ctypes.data,
+                                              len(out), ctypes.byref(nh), cnt)
+            assert st == 0
+            assert nh.value == len(want.hull) >= (1 << 16)
+            assert out[: nh.value].tobytes() == want.hull.tobytes()
+            assert list(cnt) == [int(c) for c in want.counts]
