@@ -301,3 +301,34 @@ print(json.dumps(out))
         want.append([sha(r.hull.vertices), _counts(r)])
     ctx.close()
     assert got == want + want
+
+
+@pytest.mark.parametrize("mode", ["sort", "filter", "auto"])
+def test_tile_and_chunk_boundaries(product, oracle, mode):
+    """Sizes around the sort path's SPA tile (4096 records) and the sort
+    tiles, odd chunk counts (1 record per chunk, chunks straddling tiles and
+    region ends): counters and hull equal the oracle's on every path."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = product.Context(0)
+    ctx.set_spa_path({"sort": product.SPA_SORT, "filter": product.SPA_FILTER,
+                      "auto": product.SPA_AUTO}[mode])
+    sizes = [3, 17, 257, 4095, 4096, 4097, 8193, 12289, 30001]
+    dists = ["uniform_square", "uniform_disk", "circle", "gaussian", "duplicates_heavy"]
+    for i, n in enumerate(sizes):
+        d = dists[i % len(dists)]
+        pts = product.generate(d, n, 100 + i)
+        for cc in (1, 3, 64, 1024, n // 2 + 1, n + 5):
+            want = oracle.convex_hull(pts, cc)
+            r = ctx.convex_hull(pts, product.PipelineConfig(chunk_count=cc))
+            assert _counts(r) == want.counts.tolist(), (mode, d, n, cc)
+            assert np.array_equal(r.hull.vertices, want.hull), (mode, d, n, cc)
+        # a circle of the same size: every point kept (the convex fast path
+        # from 2^16 ring points, the host loop below)
+        pts = product.generate("circle", n, 200 + i)
+        want = oracle.convex_hull(pts, 7)
+        r = ctx.convex_hull(pts, product.PipelineConfig(chunk_count=7))
+        assert _counts(r) == want.counts.tolist(), (mode, "circle", n)
+        assert np.array_equal(r.hull.vertices, want.hull)
+    ctx.close()
