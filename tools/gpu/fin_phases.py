@@ -1,3 +1,6 @@
+"""A few hulls of N uniform points (seed 42), device-resident: run under a
+library built with -DCHGPU_FINISH_CLOCKS=1 (CHGPU_LIB) to print k_spa_finish's
+phase clocks. usage: fin_phases.py N"""
 import sys, torch
 sys.path.insert(0, ".")
 import paper_1508_05488_b200 as P
