@@ -83,6 +83,11 @@ class ShardOps:
         degenerate frame the sorted unique survivors; kept counts[4])."""
         raise NotImplementedError
 
+    def fold(self, quads: np.ndarray, idxs: np.ndarray) -> np.ndarray:  # -> quad (4, 2)
+        """The global quad from every rank's corner candidates (rank order,
+        lowest global index on ties)."""
+        return fold_extremes(quads, idxs)
+
     def merge(self, runs, quad: np.ndarray) -> np.ndarray:  # -> hull vertices
         """Hull of the union of the ranks' chain runs ((chains, counts[4]) on
         the host), non-degenerate frame."""
@@ -104,6 +109,19 @@ class GpuShardOps(ShardOps):
     def extremes(self):
         q, idx = self.ctx.shard_extremes(self.t.data_ptr(), self.t.shape[0], self.base)
         return q.reshape(4, 2), idx.astype(np.int64)
+
+    def fold(self, quads, idxs):
+        # chgpu_fold_extremes: the same fold in C (tests/test_sharded.py pins
+        # it to fold_extremes)
+        import ctypes as C
+        from . import load_library
+        q = np.ascontiguousarray(np.asarray(quads, np.float64).reshape(-1))
+        ix = np.ascontiguousarray(np.asarray(idxs, np.uint64).reshape(-1))
+        out = np.empty(8, np.float64)
+        load_library().chgpu_fold_extremes(q.ctypes.data_as(C.POINTER(C.c_double)),
+                                           ix.ctypes.data_as(C.POINTER(C.c_uint64)), len(q) // 8,
+                                           out.ctypes.data_as(C.POINTER(C.c_double)))
+        return out.reshape(4, 2)
 
     def chains(self, quad, chunk_count):
         # device-resident chains (a shard never keeps more than its points):
@@ -199,7 +217,8 @@ def sharded_convex_hull(ops: ShardOps, chunk_count: int = 1024, group=None):
     allq = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(allq, mine, group=ctrl)
     arr = torch.stack(allq).numpy()
-    quad = fold_extremes(arr[:, :8], arr[:, 8:].astype(np.int64))
+    fold = getattr(ops, "fold", None) or fold_extremes  # (duck-typed ops may not have one)
+    quad = fold(arr[:, :8], arr[:, 8:].astype(np.int64))
 
     # per-rank discard + sort + SPA against the global quad (a CUDA tensor
     # from GpuShardOps, numpy from the CPU ops of the tests)

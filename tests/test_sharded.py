@@ -127,6 +127,9 @@ def test_fold_extremes_python_and_c_agree(product):
                                 ix.ctypes.data_as(C.POINTER(C.c_uint64)), k,
                                 out.ctypes.data_as(C.POINTER(C.c_double)))
         assert np.array_equal(out.reshape(4, 2), want)
+        # (the GPU ranks' fold goes through it)
+        from paper_1508_05488_b200.sharded import GpuShardOps
+        assert np.array_equal(GpuShardOps.fold(None, quads, idxs.astype(np.int64)), want)
 
 
 def _gpu_worker(rank, world, port, results, mode=0, backend="gloo"):
