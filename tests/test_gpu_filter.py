@@ -332,3 +332,44 @@ def test_tile_and_chunk_boundaries(product, oracle, mode):
         assert _counts(r) == want.counts.tolist(), (mode, "circle", n)
         assert np.array_equal(r.hull.vertices, want.hull)
     ctx.close()
+
+
+def test_concurrent_contexts_in_threads(product):
+    """Reentrancy (pipeline.hpp:53: concurrent calls on independent inputs):
+    three host threads, one context each, hulls from pageable memory (the
+    shared staging pool), device memory and the sort path, interleaved; each
+    result equals the same call made alone."""
+    import threading
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    inputs = [product.generate("uniform_square", 3_000_000, 41), product.generate("uniform_disk", 2_000_000, 42),
+              product.generate("circle", 400_000, 43)]
+    solo = []
+    ctx = product.Context(0)
+    for p in inputs:
+        r = ctx.convex_hull(p)
+        solo.append((sha(r.hull.vertices), _counts(r)))
+    ctx.close()
+    errors = []
+
+    def worker(t):
+        try:
+            c = product.Context(0)
+            if t == 2:
+                c.set_spa_path(product.SPA_SORT)
+            for rep in range(4):
+                i = (t + rep) % len(inputs)
+                r = c.convex_hull(inputs[i])
+                if (sha(r.hull.vertices), _counts(r)) != solo[i]:
+                    errors.append((t, rep, i))
+            c.close()
+        except Exception as e:  # surfaced below
+            errors.append((t, repr(e)))
+
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errors, errors

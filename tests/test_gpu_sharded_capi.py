@@ -146,3 +146,41 @@ def test_cpp_drop_in_large_hull(product, oracle):
             assert nh.value == len(want.hull) >= (1 << 16)
             assert out[: nh.value].tobytes() == want.hull.tobytes()
             assert list(cnt) == [int(c) for c in want.counts]
+
+
+def test_cpp_drop_in_concurrent_callers(product, oracle):
+    """chainhull::convex_hull from several host threads at once (the C++ API
+    pools contexts per device): every call returns the reference's hull."""
+    import threading
+    from conftest import ROOT
+    L = ctypes.CDLL(os.path.join(ROOT, "paper_1508_05488_b200", "libchainhull.so"))
+    L.chainhull_capi_convex_hull.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t,
+                                            ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(ctypes.c_size_t)]
+    cases = [("uniform_square", 1_500_000, 51), ("gaussian", 1_000_000, 52), ("uniform_disk", 800_000, 53),
+             ("circle", 100_000, 54)]
+    data = []
+    for dist, n, seed in cases:
+        pts = oracle.generate(dist, n, seed)
+        want = oracle.convex_hull(pts, 1024)
+        data.append((pts, want))
+    errors = []
+
+    def worker(t):
+        for rep in range(3):
+            pts, want = data[(t + rep) % len(data)]
+            out = np.empty((len(want.hull) + 16, 2))
+            nh = ctypes.c_size_t()
+            cnt = (ctypes.c_size_t * 4)()
+            st = L.chainhull_capi_convex_hull(pts.ctypes.data, len(pts), 1024, 0, 1, out.ctypes.data,
+                                              len(out), ctypes.byref(nh), cnt)
+            if st or out[: nh.value].tobytes() != want.hull.tobytes():
+                errors.append((t, rep, st))
+
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errors, errors
